@@ -1,0 +1,338 @@
+"""CPU oracle for the PQ ADC scan path -- TEST INFRASTRUCTURE ONLY.
+
+This module is a plain-numpy restatement of the reference package `pqscan`
+(arxiv/paper_1712_02912, `/root/reference/pkg/src/pqscan/`) for exactly the
+functions on the hot path.  Every function cites the
+reference file:line it follows.
+
+Only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s CPU-baseline leg
+(`--impl reference` / `cpu_baseline`) may import this module, and only as the
+checker or as the timed CPU baseline.  The product package
+(`paper_1712_02912_b200`) never imports it: the product path runs on the GPU
+through `libpqs.so` and fails loudly when that library is missing.
+
+Parity pin: `tests/golden/*.npz` were produced by running the real reference
+(`tests/golden/make_golden.py`, imported from /root/reference in the build
+container); `tests/test_oracle_golden.py` checks this restatement against
+every fixture bit-for-bit.
+
+Third-party arithmetic (not vendored in the reference):
+  * scipy.spatial.distance.cdist(.., 'sqeuclidean') (scipy>=1.10, unpinned) --
+    restated as fp64 direct differences (`_dist.py:13-21`); the golden
+    fixtures pin the bitwise fp32 result of `compute_tables`.
+  * numpy partition/lexsort/floor/clip/minimum (numpy>=1.24) -- restated with
+    the same semantics; ties are pinned by the sorted-oracle fixtures.
+"""
+
+from __future__ import annotations
+
+import heapq
+
+import numpy as np
+
+BINS = 127          # fastscan.py:23
+BLOCK = 16          # scan.py:206
+DEFAULT_INIT_COUNT = 200            # quickadc.py:28
+DEFAULT_INIT_COUNT_BILLION = 1000   # quickadc.py:29
+
+
+# --------------------------------------------------------------------------
+# tables  (scan.py:45-56, _dist.py:13-21, quantizer.py:85-89)
+# --------------------------------------------------------------------------
+
+def compute_tables(codebooks: np.ndarray, query: np.ndarray) -> np.ndarray:
+    """D[j, i] = fp32(sum_t (fp64(y_j[t]) - fp64(C_j[i, t]))^2).
+
+    scan.py:45-56 calls `sqdist_matrix` (_dist.py:13-21, scipy cdist
+    'sqeuclidean' in fp64) per sub-space on the fp64-cast query
+    (quantizer.py:85-89, identity rotation) and stores the row as fp32.
+    """
+    codebooks = np.asarray(codebooks, dtype=np.float32)
+    m, k, dsub = codebooks.shape
+    y = np.asarray(query, dtype=np.float64).reshape(m, 1, dsub)
+    diff = y - codebooks.astype(np.float64)
+    out = np.zeros((m, k), dtype=np.float64)
+    for t in range(dsub):  # scipy cdist 'sqeuclidean': sequential fp64 sum
+        out += diff[:, :, t] * diff[:, :, t]
+    return out.astype(np.float32)
+
+
+def compute_tables_batch(codebooks: np.ndarray, queries: np.ndarray) -> np.ndarray:
+    """compute_tables for a (Q, d) batch -> (Q, m, k) float32."""
+    queries = np.asarray(queries)
+    return np.stack([compute_tables(codebooks, q) for q in queries])
+
+
+# --------------------------------------------------------------------------
+# float ADC  (scan.py:59-81)
+# --------------------------------------------------------------------------
+
+def adc_distance(tables: np.ndarray, code) -> float:
+    """scan.py:59-65: fp64 sum of fp32 entries, sub-space order."""
+    acc = 0.0
+    for j in range(tables.shape[0]):
+        acc += float(tables[j, int(code[j])])
+    return acc
+
+
+def scan_distances(tables: np.ndarray, codes: np.ndarray) -> np.ndarray:
+    """scan.py:68-81: acc(fp64) += T64[j][codes[:, j]] for j = 0..m-1."""
+    t64 = np.asarray(tables, dtype=np.float32).astype(np.float64)
+    codes = np.asarray(codes)
+    acc = np.zeros(codes.shape[0], dtype=np.float64)
+    for j in range(t64.shape[0]):
+        acc += t64[j][codes[:, j].astype(np.int64)]
+    return acc
+
+
+# --------------------------------------------------------------------------
+# selection  (scan.py:84-154)
+# --------------------------------------------------------------------------
+
+def select_best(dists: np.ndarray, ids: np.ndarray, r: int):
+    """scan.py:142-154: the r smallest (distance, id) pairs, ascending."""
+    n = dists.shape[0]
+    r_eff = min(r, n)
+    if r_eff == 0:
+        return np.empty(0, np.float64), np.empty(0, np.int64)
+    kth = np.partition(dists, r_eff - 1)[r_eff - 1]
+    cand = np.flatnonzero(dists <= kth)
+    order = np.lexsort((ids[cand], dists[cand]))[:r_eff]
+    pick = cand[order]
+    return dists[pick], ids[pick]
+
+
+class NeighborMerge:
+    """Bounded (distance, id) set with the NeighborSet.push semantics of
+    scan.py:109-118: keeps the r smallest by (distance, id)."""
+
+    def __init__(self, r: int):
+        if r < 1:
+            raise ValueError("r must be >= 1")
+        self.r = r
+        self._heap: list = []
+
+    def push(self, distance: float, ident: int) -> None:
+        entry = (-float(distance), -int(ident))
+        if len(self._heap) < self.r:
+            heapq.heappush(self._heap, entry)
+        elif entry > self._heap[0]:
+            heapq.heappushpop(self._heap, entry)
+
+    def items(self):
+        return sorted((-d, -i) for d, i in self._heap)
+
+
+def scan(codes: np.ndarray, ids: np.ndarray, tables: np.ndarray, r: int):
+    """scan.py:197-203 -> (dists fp64, ids int64) ascending by (d, id)."""
+    if r < 1:
+        raise ValueError("r must be >= 1")
+    d = scan_distances(tables, codes)
+    return select_best(d, np.asarray(ids, dtype=np.int64), r)
+
+
+# --------------------------------------------------------------------------
+# 16-code block layout  (scan.py:206-287)
+# --------------------------------------------------------------------------
+
+def transpose_blocks(codes: np.ndarray, b: int) -> np.ndarray:
+    """scan.py:248-274 -> blocks (nblocks, rows, 16) uint8."""
+    codes = np.asarray(codes)
+    n, m = codes.shape
+    if b == 4:
+        if m % 2:
+            raise ValueError("b=4 transposition needs even m")
+        if np.any(codes >= 16):
+            raise ValueError("component out of range for b=4")
+    elif b == 8:
+        if np.any(codes.astype(np.int64) >= 256):
+            raise ValueError("component out of range for b=8")
+    else:
+        raise ValueError(f"block transposition supports b in (4, 8), got b={b}")
+    nblocks = (n + BLOCK - 1) // BLOCK
+    padded = np.zeros((nblocks * BLOCK, m), dtype=np.uint8)
+    padded[:n] = codes.astype(np.uint8)
+    per_block = padded.reshape(nblocks, BLOCK, m)
+    if b == 4:
+        blocks = (per_block[:, :, 0::2] | (per_block[:, :, 1::2] << 4)).transpose(0, 2, 1)
+    else:
+        blocks = per_block.transpose(0, 2, 1)
+    return np.ascontiguousarray(blocks)
+
+
+def detranspose_blocks(blocks: np.ndarray, n: int, m: int, b: int) -> np.ndarray:
+    """scan.py:277-287 -> codes (n, m) uint8."""
+    nblocks = blocks.shape[0]
+    if b == 4:
+        flat = blocks.transpose(0, 2, 1).reshape(-1, m // 2)
+        codes = np.empty((nblocks * BLOCK, m), dtype=np.uint8)
+        codes[:, 0::2] = flat & 0x0F
+        codes[:, 1::2] = flat >> 4
+    else:
+        codes = blocks.transpose(0, 2, 1).reshape(-1, m)
+    return np.ascontiguousarray(codes[:n])
+
+
+# --------------------------------------------------------------------------
+# 127-bin quantization  (fastscan.py:28-57, quickadc.py:32-141)
+# --------------------------------------------------------------------------
+
+def quant_scale(qmin: float, qmax: float) -> float:
+    """fastscan.py:42-45."""
+    span = qmax - qmin
+    return BINS / span if span > 0.0 else 0.0
+
+
+def quantize(qmin: float, qmax: float, values) -> np.ndarray:
+    """fastscan.py:48-57: 127 at or above qmax, else floor-scaled, clamped
+    to [0, 126]; all-zero when the span is empty.  fp64 arithmetic."""
+    v = np.asarray(values, dtype=np.float64)
+    scale = quant_scale(qmin, qmax)
+    if scale == 0.0:
+        return np.zeros(v.shape, dtype=np.uint8)
+    bins = np.clip(np.floor((v - qmin) * scale), 0, BINS - 1)
+    return np.where(v >= qmax, BINS, bins).astype(np.uint8)
+
+
+def qadc_block(block: np.ndarray, qtables: np.ndarray) -> np.ndarray:
+    """quickadc.py:66-84: one transposed 16-code block, clamp after each add."""
+    block = np.asarray(block, dtype=np.uint8)
+    acc = np.zeros(BLOCK, dtype=np.int16)
+    for j in range(block.shape[0]):
+        row = block[j]
+        acc = np.minimum(acc + qtables[2 * j][row & 0x0F], BINS)
+        acc = np.minimum(acc + qtables[2 * j + 1][row >> 4], BINS)
+    return acc.astype(np.uint8)
+
+
+def quantized_distances(codes: np.ndarray, qtables: np.ndarray) -> np.ndarray:
+    """quickadc.py:87-101: int16 acc = min(acc + t[j][c_j], 127)."""
+    codes = np.asarray(codes)
+    acc = np.zeros(codes.shape[0], dtype=np.int16)
+    for j in range(qtables.shape[0]):
+        acc = np.minimum(acc + qtables[j][codes[:, j].astype(np.int64)], BINS)
+    return acc.astype(np.uint8)
+
+
+def qadc_params(tables: np.ndarray, codes: np.ndarray, init_count: int, r: int):
+    """quickadc.py:129-137 -> (qmin, qmax) fp64.
+
+    qmax = r-th smallest fp64 ADC distance of the first min(init_count, n)
+    codes in storage order (largest if fewer than r); qmin = global fp32
+    table minimum; qmax = max(qmax, qmin)."""
+    n_init = min(init_count, codes.shape[0])
+    prefix_d = scan_distances(tables, codes[:n_init])
+    if n_init >= r:
+        qmax = float(np.partition(prefix_d, r - 1)[r - 1])
+    else:
+        qmax = float(prefix_d.max())
+    qmin = float(np.asarray(tables, dtype=np.float32).min())
+    return qmin, max(qmax, qmin)
+
+
+def qadc_scan(codes: np.ndarray, ids: np.ndarray, tables: np.ndarray,
+              init_count: int, r: int):
+    """quickadc.py:104-141 on the detransposed codes.
+
+    Returns (bins float64 ascending, ids int64, qtables uint8 (m,16), qmin, qmax).
+    """
+    tables = np.asarray(tables, dtype=np.float32)
+    if tables.shape[1] != 16:
+        raise ValueError("tables do not match the code list shape")
+    if tables.shape[0] % 2:
+        raise ValueError("quick scan needs even m")
+    if init_count < 1:
+        raise ValueError("init_count must be >= 1")
+    if r < 1:
+        raise ValueError("r must be >= 1")
+    if codes.shape[0] == 0:
+        raise ValueError("empty code list")
+    qmin, qmax = qadc_params(tables, codes, init_count, r)
+    qt = quantize(qmin, qmax, tables)
+    dq = quantized_distances(codes, qt).astype(np.float64)
+    best_d, best_i = select_best(dq, np.asarray(ids, dtype=np.int64), r)
+    return best_d, best_i, qt, qmin, qmax
+
+
+def rescale(bins, qmin: float, qmax: float):
+    """quickadc.py:50-54."""
+    return np.asarray(bins, dtype=np.float64) * (qmax - qmin) / BINS + qmin
+
+
+# --------------------------------------------------------------------------
+# IVFADC  (_dist.py:42-67, ivf.py:148-196)
+# --------------------------------------------------------------------------
+
+def sqdist_matrix(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """_dist.py:13-21: fp64 all-pairs squared distances, direct form,
+    summed sequentially over t (bit-identical to scipy 1.18 cdist)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    out = np.empty((a.shape[0], b.shape[0]), dtype=np.float64)
+    for lo in range(0, a.shape[0], 64):
+        d = a[lo:lo + 64, None, :] - b[None, :, :]
+        acc = np.zeros(d.shape[:2], dtype=np.float64)
+        for t in range(d.shape[2]):  # sequential order, as scipy's cdist
+            acc += d[:, :, t] * d[:, :, t]
+        out[lo:lo + 64] = acc
+    return out
+
+
+def nearest_k(points: np.ndarray, centroids: np.ndarray, k: int):
+    """_dist.py:42-67: k nearest by (fp64 distance, index), ascending."""
+    points = np.atleast_2d(np.asarray(points))
+    n = points.shape[0]
+    idx = np.empty((n, k), dtype=np.int64)
+    dist = np.empty((n, k), dtype=np.float64)
+    ncent = centroids.shape[0]
+    cent_ids = np.arange(ncent)
+    dm_all = sqdist_matrix(points, centroids)
+    for row in range(n):
+        d = dm_all[row]
+        if k < ncent:
+            kth = np.partition(d, k - 1)[k - 1]
+            cand = np.flatnonzero(d <= kth)
+        else:
+            cand = cent_ids
+        order = np.lexsort((cand, d[cand]))[:k]
+        sel = cand[order]
+        idx[row] = sel
+        dist[row] = d[sel]
+    return idx, dist
+
+
+def query_ivf(coarse: np.ndarray, codebooks: np.ndarray, lists_codes, lists_ids,
+              query: np.ndarray, ma: int, r: int):
+    """ivf.py:148-196, kernel='adc': probe the ma nearest cells, scan each
+    list against the fp64 residual's tables, merge by (distance, id)."""
+    K = coarse.shape[0]
+    if not 1 <= ma <= K:
+        raise ValueError(f"ma must be in [1, {K}]")
+    if r < 1:
+        raise ValueError("r must be >= 1")
+    q64 = np.asarray(query, dtype=np.float64)
+    cells, _ = nearest_k(q64[None, :], np.asarray(coarse, np.float32).astype(np.float64), ma)
+    merged = NeighborMerge(r)
+    for cell in cells[0]:
+        codes = lists_codes[int(cell)]
+        if codes.shape[0] == 0:
+            continue
+        residual = q64 - np.asarray(coarse[int(cell)], np.float32).astype(np.float64)
+        tables = compute_tables(codebooks, residual)
+        d, ids = scan(codes, lists_ids[int(cell)], tables, r)
+        for dist, ident in zip(d.tolist(), ids.tolist()):
+            merged.push(dist, ident)
+    items = merged.items()
+    return (np.array([p[0] for p in items], dtype=np.float64),
+            np.array([p[1] for p in items], dtype=np.int64))
+
+
+# --------------------------------------------------------------------------
+# sharded merge  (scan.py:109-118 semantics; no reference counterpart)
+# --------------------------------------------------------------------------
+
+def merge_shards(dists_list, ids_list, r: int):
+    """Top-r of the union of per-shard top-r lists by (distance, id)."""
+    d = np.concatenate([np.asarray(x, np.float64) for x in dists_list])
+    i = np.concatenate([np.asarray(x, np.int64) for x in ids_list])
+    return select_best(d, i, r)

@@ -1,0 +1,214 @@
+"""Generate golden fixtures by running the REAL reference package.
+
+Run in the build container (the reference is mounted read-only):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+It imports `pqscan` from /root/reference, runs the hot-path functions on small
+seeded inputs and stores inputs + outputs as .npz files next to this script.
+The fixtures are committed; nothing on the GPU box reads /root/reference.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+if REF not in sys.path:
+    sys.path.insert(0, REF)
+
+import pqscan  # noqa: E402
+from pqscan import (  # noqa: E402
+    CodeList,
+    LookupTables,
+    QuantParams,
+    QuantizedTables4,
+    TrainConfig,
+    build_ivf,
+    compute_tables,
+    encode,
+    generate_synthetic,
+    qadc_block,
+    qadc_scan,
+    quantize,
+    quantized_distances,
+    query_ivf,
+    scan,
+    scan_distances,
+    train_pq,
+    transpose_blocks,
+)
+from pqscan._dist import nearest_k  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def save(name, **arrays):
+    path = os.path.join(OUT, name)
+    np.savez_compressed(path, **arrays)
+    print("wrote", path, {k: v.shape for k, v in arrays.items()})
+
+
+def items_arrays(nset, r):
+    items = nset.items()
+    d = np.full(r, np.nan)
+    i = np.full(r, -1, dtype=np.int64)
+    for p, (dist, ident) in enumerate(items):
+        d[p] = dist
+        i[p] = ident
+    return d, i, len(items)
+
+
+def mixture(rng, n, d, comps, hi, sigma, clip_lo=None, clip_hi=None):
+    centers = rng.uniform(0.0, hi, size=(comps, d))
+    lab = rng.integers(0, comps, size=n)
+    x = centers[lab] + rng.normal(0.0, sigma, size=(n, d))
+    if clip_lo is not None or clip_hi is not None:
+        x = np.clip(x, clip_lo, clip_hi)
+    return x.astype(np.float32)
+
+
+def g_tables():
+    """compute_tables bitwise, for three table shapes (cfg0/1/2-like)."""
+    rng = np.random.default_rng(101)
+    out = {}
+    for tag, (d, m, b, hi, sigma) in {
+        "c0": (128, 8, 8, 128.0, 16.0),
+        "c1": (128, 16, 4, 128.0, 16.0),
+        "c2": (960, 64, 8, 1.0, 0.05),
+    }.items():
+        x = mixture(rng, 3000, d, 16, hi, sigma, 0.0, 255.0)
+        pq = train_pq(x[:2000], m, b, TrainConfig(kmeans_iters=4, seed=7))
+        qs = x[2000:2006] + rng.normal(0, sigma / 2, (6, d)).astype(np.float32)
+        tabs = np.stack([compute_tables(pq, q).tables for q in qs])
+        out[f"{tag}_codebooks"] = pq.codebooks
+        out[f"{tag}_queries"] = qs
+        out[f"{tag}_tables"] = tabs
+        codes = encode(pq, x[:500])
+        out[f"{tag}_codes"] = codes
+        out[f"{tag}_dist"] = np.stack([scan_distances(compute_tables(pq, q), codes) for q in qs])
+    save("tables.npz", **out)
+
+
+def g_scan():
+    """scan() on random instances (criterion-9 style) incl. ties and r > n."""
+    rng = np.random.default_rng(202)
+    cases = []
+    for trial in range(40):
+        n = int(rng.integers(1, 600))
+        m = int(rng.integers(1, 9))
+        k = int(rng.integers(2, 257))
+        r = int(rng.integers(1, n + 5))
+        if trial % 5 == 0:
+            # coarse tables -> many exact distance ties
+            tables = rng.integers(0, 4, (m, k)).astype(np.float32)
+        else:
+            tables = (rng.random((m, k)) * 100).astype(np.float32)
+        codes = rng.integers(0, k, (n, m)).astype(np.uint8)
+        ids = rng.permutation(n * 3)[:n].astype(np.int64)
+        nset = scan(CodeList(codes, ids), LookupTables(tables), r)
+        d, i, cnt = items_arrays(nset, r)
+        cases.append(dict(tables=tables, codes=codes, ids=ids, r=np.int64(r),
+                          dist=d, out_ids=i, count=np.int64(cnt)))
+    flat = {}
+    for c, case in enumerate(cases):
+        for key, val in case.items():
+            flat[f"{c}_{key}"] = np.asarray(val)
+    flat["ncases"] = np.int64(len(cases))
+    save("scan.npz", **flat)
+
+
+def g_quick_adc():
+    """qadc_scan on trained 4-bit PQ data, several init_count / r."""
+    rng = np.random.default_rng(303)
+    x = mixture(rng, 6000, 64, 32, 128.0, 16.0, 0.0, 255.0)
+    pq = train_pq(x[:3000], 16, 4, TrainConfig(kmeans_iters=6, seed=1))
+    codes = encode(pq, x[:5000])
+    ids = np.arange(5000, dtype=np.int64)
+    tlist = transpose_blocks(CodeList(codes, ids), 4)
+    qs = x[5000:5012] + rng.normal(0, 8, (12, 64)).astype(np.float32)
+    out = dict(codebooks=pq.codebooks, codes=codes, queries=qs, blocks=tlist.blocks)
+    settings = [(200, 100), (200, 10), (50, 100), (5000, 20), (1, 1), (7, 300)]
+    for s, (init, r) in enumerate(settings):
+        bins = np.full((len(qs), r), np.nan)
+        oids = np.full((len(qs), r), -1, dtype=np.int64)
+        qts = np.zeros((len(qs), 16, 16), dtype=np.uint8)
+        qmm = np.zeros((len(qs), 2))
+        for qi, q in enumerate(qs):
+            tables = compute_tables(pq, q)
+            nset, qt = qadc_scan(tlist, tables, init, r)
+            d, i, _ = items_arrays(nset, r)
+            bins[qi], oids[qi] = d, i
+            qts[qi] = qt.tables
+            qmm[qi] = (qt.params.qmin, qt.params.qmax)
+        out[f"s{s}_init"] = np.int64(init)
+        out[f"s{s}_r"] = np.int64(r)
+        out[f"s{s}_bins"] = bins
+        out[f"s{s}_ids"] = oids
+        out[f"s{s}_qtables"] = qts
+        out[f"s{s}_qminmax"] = qmm
+    # permuted ids + tail padding (n not a multiple of 16)
+    n2 = 1237
+    ids2 = rng.permutation(10 * n2)[:n2].astype(np.int64)
+    tl2 = transpose_blocks(CodeList(codes[:n2], ids2), 4)
+    q = qs[0]
+    nset, qt = qadc_scan(tl2, compute_tables(pq, q), 200, 64)
+    d, i, _ = items_arrays(nset, 64)
+    out.update(p_ids=ids2, p_bins=d, p_out_ids=i, p_qtables=qt.tables,
+               p_qminmax=np.array([qt.params.qmin, qt.params.qmax]))
+    save("quick_adc.npz", **out)
+
+
+def g_quantize():
+    """quantize boundaries + quantized_distances + qadc_block known answers."""
+    rng = np.random.default_rng(404)
+    vals = np.concatenate([
+        np.array([0.0, 2.0, 7.9999, 8.0, 100.0, 1e-9, 3.99999]),
+        rng.random(200) * 10,
+    ])
+    params = [(0.0, 8.0), (2.0, 10.0), (1.0, 1.0), (0.5, 9.75)]
+    q = np.stack([quantize(QuantParams(a, b), vals) for a, b in params])
+    qt = rng.integers(0, 128, (8, 16)).astype(np.uint8)
+    codes = rng.integers(0, 16, (333, 8)).astype(np.uint8)
+    qd = quantized_distances(codes, QuantizedTables4(qt, QuantParams(0.0, 127.0)))
+    blocks = rng.integers(0, 256, (200, 4, 16)).astype(np.uint8)
+    qb = np.stack([qadc_block(b, QuantizedTables4(qt, QuantParams(0.0, 127.0))) for b in blocks])
+    save("quantize.npz", values=vals, params=np.array(params), bins=q,
+         qtables=qt, codes=codes, qdist=qd, blocks=blocks, qblock=qb)
+
+
+def g_ivf():
+    """query_ivf (kernel='adc') on a small built index, ma in {1,4,16}."""
+    rng = np.random.default_rng(505)
+    base = mixture(rng, 4000, 32, 24, 128.0, 16.0, 0.0, 255.0)
+    idx = build_ivf(base, K=32, m=4, b=8, cfg=TrainConfig(kmeans_iters=6, seed=2))
+    qs = base[rng.choice(4000, 8, replace=False)] + rng.normal(0, 6, (8, 32)).astype(np.float32)
+    out = dict(coarse=idx.coarse, codebooks=idx.pq.codebooks, queries=qs)
+    sizes = np.array([lst.n for lst in idx.lists], dtype=np.int64)
+    out["list_sizes"] = sizes
+    out["list_codes"] = np.concatenate([lst.codes for lst in idx.lists])
+    out["list_ids"] = np.concatenate([lst.ids for lst in idx.lists])
+    for ma, r in [(1, 20), (4, 50), (16, 100), (32, 10)]:
+        d = np.full((len(qs), r), np.nan)
+        i = np.full((len(qs), r), -1, dtype=np.int64)
+        for qi, q in enumerate(qs):
+            dd, ii, _ = items_arrays(query_ivf(idx, q, ma=ma, r=r), r)
+            d[qi], i[qi] = dd, ii
+        out[f"ma{ma}_r{r}_dist"] = d
+        out[f"ma{ma}_r{r}_ids"] = i
+    cells, cd = nearest_k(qs.astype(np.float64), idx.coarse.astype(np.float64), 8)
+    out["probe_cells"] = cells
+    out["probe_dist"] = cd
+    save("ivf.npz", **out)
+
+
+if __name__ == "__main__":
+    print("pqscan from", pqscan.__file__)
+    g_tables()
+    g_scan()
+    g_quick_adc()
+    g_quantize()
+    g_ivf()

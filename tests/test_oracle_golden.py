@@ -1,0 +1,108 @@
+"""Pin the CPU oracle (oracle/pqscan_oracle.py) to fixtures produced by the
+real reference (tests/golden/make_golden.py).  CPU only."""
+
+import numpy as np
+import pytest
+
+from oracle import pqscan_oracle as O
+
+
+@pytest.mark.parametrize("tag", ["c0", "c1", "c2"])
+def test_tables_bitwise(golden, tag):
+    g = golden("tables.npz")
+    books, qs, tabs = g[f"{tag}_codebooks"], g[f"{tag}_queries"], g[f"{tag}_tables"]
+    got = O.compute_tables_batch(books, qs)
+    assert got.dtype == np.float32
+    np.testing.assert_array_equal(got.view(np.uint32), tabs.view(np.uint32))
+
+
+@pytest.mark.parametrize("tag", ["c0", "c1", "c2"])
+def test_scan_distances_bitwise(golden, tag):
+    g = golden("tables.npz")
+    for qi in range(g[f"{tag}_tables"].shape[0]):
+        got = O.scan_distances(g[f"{tag}_tables"][qi], g[f"{tag}_codes"])
+        np.testing.assert_array_equal(got, g[f"{tag}_dist"][qi])
+
+
+def test_scan_cases(golden):
+    g = golden("scan.npz")
+    for c in range(int(g["ncases"])):
+        r = int(g[f"{c}_r"])
+        d, i = O.scan(g[f"{c}_codes"], g[f"{c}_ids"], g[f"{c}_tables"], r)
+        cnt = int(g[f"{c}_count"])
+        assert len(d) == cnt
+        np.testing.assert_array_equal(d, g[f"{c}_dist"][:cnt])
+        np.testing.assert_array_equal(i, g[f"{c}_out_ids"][:cnt])
+
+
+def test_quick_adc_settings(golden):
+    g = golden("quick_adc.npz")
+    codes, books, qs = g["codes"], g["codebooks"], g["queries"]
+    ids = np.arange(codes.shape[0], dtype=np.int64)
+    for s in range(6):
+        init, r = int(g[f"s{s}_init"]), int(g[f"s{s}_r"])
+        for qi, q in enumerate(qs):
+            t = O.compute_tables(books, q)
+            bins, oid, qt, qmin, qmax = O.qadc_scan(codes, ids, t, init, r)
+            n = len(bins)
+            np.testing.assert_array_equal(bins, g[f"s{s}_bins"][qi][:n])
+            np.testing.assert_array_equal(oid, g[f"s{s}_ids"][qi][:n])
+            np.testing.assert_array_equal(qt, g[f"s{s}_qtables"][qi])
+            assert (qmin, qmax) == tuple(g[f"s{s}_qminmax"][qi])
+
+
+def test_quick_adc_permuted_ids(golden):
+    g = golden("quick_adc.npz")
+    n2 = g["p_ids"].shape[0]
+    t = O.compute_tables(g["codebooks"], g["queries"][0])
+    bins, oid, qt, qmin, qmax = O.qadc_scan(g["codes"][:n2], g["p_ids"], t, 200, 64)
+    np.testing.assert_array_equal(bins, g["p_bins"])
+    np.testing.assert_array_equal(oid, g["p_out_ids"])
+    np.testing.assert_array_equal(qt, g["p_qtables"])
+
+
+def test_transpose_layout(golden):
+    g = golden("quick_adc.npz")
+    blocks = O.transpose_blocks(g["codes"], 4)
+    np.testing.assert_array_equal(blocks, g["blocks"])
+    back = O.detranspose_blocks(blocks, g["codes"].shape[0], 16, 4)
+    np.testing.assert_array_equal(back, g["codes"])
+
+
+def test_quantize_known_answers(golden):
+    g = golden("quantize.npz")
+    for p, (a, b) in enumerate(g["params"]):
+        np.testing.assert_array_equal(O.quantize(a, b, g["values"]), g["bins"][p])
+    np.testing.assert_array_equal(O.quantized_distances(g["codes"], g["qtables"]), g["qdist"])
+    for bi, blk in enumerate(g["blocks"]):
+        np.testing.assert_array_equal(O.qadc_block(blk, g["qtables"]), g["qblock"][bi])
+    # test_fastscan.py:67-79 boundaries
+    assert int(O.quantize(0.0, 8.0, 7.9999)) == 126
+    assert int(O.quantize(0.0, 8.0, 8.0)) == 127
+
+
+def _lists(g):
+    sizes = g["list_sizes"]
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    codes = [g["list_codes"][offs[c]:offs[c + 1]] for c in range(len(sizes))]
+    ids = [g["list_ids"][offs[c]:offs[c + 1]] for c in range(len(sizes))]
+    return codes, ids
+
+
+def test_ivf_probes(golden):
+    g = golden("ivf.npz")
+    cells, dist = O.nearest_k(g["queries"].astype(np.float64), g["coarse"].astype(np.float64), 8)
+    np.testing.assert_array_equal(cells, g["probe_cells"])
+    np.testing.assert_array_equal(dist, g["probe_dist"])
+
+
+@pytest.mark.parametrize("ma,r", [(1, 20), (4, 50), (16, 100), (32, 10)])
+def test_ivf_query(golden, ma, r):
+    g = golden("ivf.npz")
+    codes, ids = _lists(g)
+    for qi, q in enumerate(g["queries"]):
+        d, i = O.query_ivf(g["coarse"], g["codebooks"], codes, ids, q, ma, r)
+        n = len(d)
+        np.testing.assert_array_equal(d, g[f"ma{ma}_r{r}_dist"][qi][:n])
+        np.testing.assert_array_equal(i, g[f"ma{ma}_r{r}_ids"][qi][:n])
+        assert np.all(g[f"ma{ma}_r{r}_ids"][qi][n:] == -1)
