@@ -1,0 +1,164 @@
+/*
+ * pqs.h -- C ABI of libpqs.so, the B200 (sm_100a) ADC-scan engine.
+ *
+ * This is the drop-in boundary for the PQ ADC scan path of the reference
+ * package `pqscan` (arxiv/paper_1712_02912, /root/reference/pkg/src/pqscan).
+ * The reference has no FFI of its own (it is pure NumPy/SciPy); its
+ * "operator API" is the Python function surface listed in SURVEY.md 8(b).
+ * Each entry point below names the reference function it replaces; the
+ * Python package `paper_1712_02912_b200` binds these through ctypes and
+ * re-exports the reference names (see INTEGRATION.md for the binding a
+ * reference maintainer would add).
+ *
+ * Conventions
+ *   - Plain pointers and sizes, no framework types.  Every call returns an
+ *     int status (PQS_OK == 0); on failure pqs_last_error(ctx) holds a
+ *     message.  Argument errors the reference raises as ValueError map to
+ *     PQS_ERR_INVALID.
+ *   - `io` says where the per-call arrays (queries/tables in, results out)
+ *     live: PQS_IO_HOST (host memory; copies happen inside the call) or
+ *     PQS_IO_DEVICE (device pointers, e.g. torch.Tensor.data_ptr()).
+ *     Quantizer / code-list / index handles always own device copies made
+ *     from host arrays at creation time.
+ *   - All work of a context is issued on one CUDA stream (its own, or the
+ *     one set with pqs_ctx_set_stream).  A context is single-writer, like
+ *     the reference NeighborSet; separate contexts may run
+ *     concurrently.
+ *   - Results are (nq, r) row-major arrays ascending by (distance, id);
+ *     out_count[q] = number of valid entries (min(r, candidates)); unused
+ *     slots hold distance +inf (bins 255) and id -1.
+ */
+#ifndef PQS_H
+#define PQS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PQS_API_VERSION 1
+
+typedef struct pqs_ctx pqs_ctx;
+typedef struct pqs_pq pqs_pq;
+typedef struct pqs_db pqs_db;
+typedef struct pqs_ivf pqs_ivf;
+
+enum pqs_status {
+  PQS_OK = 0,
+  PQS_ERR_INVALID = 1,     /* the reference raises ValueError here */
+  PQS_ERR_CUDA = 2,
+  PQS_ERR_NOMEM = 3,
+  PQS_ERR_UNSUPPORTED = 4  /* valid for the reference, outside this engine's limits */
+};
+
+enum pqs_io { PQS_IO_HOST = 0, PQS_IO_DEVICE = 1 };
+
+enum pqs_option {
+  PQS_OPT_CAND_CAP = 1,     /* candidate slots per query in a filtered scan (default 32768) */
+  PQS_OPT_SAMPLE_DIV = 2,   /* threshold sample = 1/SAMPLE_DIV of the code tiles (default 32) */
+  PQS_OPT_FORCE_FALLBACK = 3/* 1: run the exact dense fallback for every query (testing) */
+};
+
+enum pqs_stat {
+  PQS_STAT_LAUNCHES = 1,       /* kernels launched by this context since creation */
+  PQS_STAT_LAST_MAX_CAND = 2,  /* largest per-query candidate count of the last search */
+  PQS_STAT_LAST_OVERFLOW = 3,  /* queries that took the dense fallback in the last search */
+  PQS_STAT_LAST_EVALS = 4      /* (query, code) evaluations of the last search (IVF: exact count) */
+};
+
+int pqs_api_version(void);
+
+/* ---- context --------------------------------------------------------- */
+int pqs_ctx_create(int device, pqs_ctx** out);
+void pqs_ctx_destroy(pqs_ctx* ctx);
+int pqs_ctx_set_stream(pqs_ctx* ctx, void* cuda_stream); /* NULL -> context's own stream */
+int pqs_ctx_synchronize(pqs_ctx* ctx);
+int pqs_ctx_set_option(pqs_ctx* ctx, int option, int64_t value);
+int pqs_ctx_get_stat(pqs_ctx* ctx, int stat, int64_t* out);
+const char* pqs_last_error(const pqs_ctx* ctx);
+
+/* ---- quantizer: ProductQuantizer (quantizer.py:38-89, identity rotation) */
+/* codebooks: host float32 (m, 2^b, d/m) C-contiguous. */
+int pqs_pq_create(pqs_ctx* ctx, int m, int b, int d, const float* codebooks, pqs_pq** out);
+void pqs_pq_destroy(pqs_pq* pq);
+
+/* ---- code lists: CodeList (scan.py:157-194) / TransposedCodeList (scan.py:209-245)
+ * codes: host uint8 (n, m) row-major component values (< 2^b).
+ * b == 8: float-ADC layout (scan8), any m >= 1, 2 <= k <= 256.
+ * b == 4: Quick ADC layout (scan4, 4-code PRMT-selector quads), even m <= 32.
+ * ids:  host int64 (n,) or NULL for implicit ids id_base + i (CodeList default
+ *       ids = arange(n), scan.py:170-171).                                 */
+int pqs_db_create(pqs_ctx* ctx, const uint8_t* codes, int64_t n, int m, int b,
+                  const int64_t* ids, int64_t id_base, pqs_db** out);
+/* Quick ADC under sharding: qmax must come from the first init_count codes of
+ * the GLOBAL list (quickadc.py:130-137).  Supplies them (host uint8 (n_prefix, m)). */
+int pqs_db_set_prefix(pqs_ctx* ctx, pqs_db* db, const uint8_t* prefix_codes, int64_t n_prefix);
+void pqs_db_destroy(pqs_db* db);
+
+/* ---- tables: compute_tables (scan.py:45-56; sqdist_matrix _dist.py:13-21)
+ * queries (nq, d) float32 -> out_tables (nq, m, k) float32, bit-identical. */
+int pqs_compute_tables(pqs_ctx* ctx, const pqs_pq* pq, const float* queries, int64_t nq,
+                       float* out_tables, int io);
+
+/* ---- dense fp64 ADC: scan_distances (scan.py:68-81), b == 8 list
+ * tables (nq, m, k) float32 (k <= 256, every code < k) -> out (nq, n)
+ * float64, bit-identical.                                                 */
+int pqs_scan_distances(pqs_ctx* ctx, const pqs_db* db, const float* tables, int64_t nq,
+                       int k, double* out, int io);
+
+/* ---- float ADC top-r: scan (scan.py:197-203), b == 8 list, given tables. */
+int pqs_adc_scan(pqs_ctx* ctx, const pqs_db* db, const float* tables, int64_t nq, int k,
+                 int r, double* out_dist, int64_t* out_ids, int32_t* out_count, int io);
+/* batched search from queries: compute_tables + scan for every query.     */
+int pqs_adc_search(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* pq, const float* queries,
+                   int64_t nq, int r, double* out_dist, int64_t* out_ids, int32_t* out_count,
+                   int io);
+
+/* ---- Quick ADC: qadc_scan (quickadc.py:104-141), b == 4 list, given tables
+ * (nq, m, 16) float32.  Outputs bins (nq, r) uint8 ascending by (bin, id),
+ * ids, counts, the quantized tables (nq, m, 16) uint8 and (qmin, qmax)
+ * (nq, 2) float64 -- QuantizedTables4 (quickadc.py:32-54).  Output pointers
+ * out_qtables / out_qminmax may be NULL.                                   */
+int pqs_qadc_scan(pqs_ctx* ctx, const pqs_db* db, const float* tables, int64_t nq,
+                  int init_count, int r, uint8_t* out_bins, int64_t* out_ids,
+                  int32_t* out_count, uint8_t* out_qtables, double* out_qminmax, int io);
+int pqs_qadc_search(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* pq, const float* queries,
+                    int64_t nq, int init_count, int r, uint8_t* out_bins, int64_t* out_ids,
+                    int32_t* out_count, uint8_t* out_qtables, double* out_qminmax, int io);
+
+/* ---- quantize (fastscan.py:48-57): 127-bin fp64 quantization of values
+ * (n,) float64 with QuantParams(qmin, qmax) -> out (n,) uint8.            */
+int pqs_quantize(pqs_ctx* ctx, double qmin, double qmax, const double* values, int64_t n,
+                 uint8_t* out, int io);
+
+/* ---- quantized_distances (quickadc.py:87-101), b == 4 list:
+ * qtables (nq, m, 16) uint8 (entries <= 127) -> out (nq, n) uint8.          */
+int pqs_quantized_distances(pqs_ctx* ctx, const pqs_db* db, const uint8_t* qtables,
+                            int64_t nq, uint8_t* out, int io);
+
+/* ---- IVFADC: IvfIndex (ivf.py:58-86) + query_ivf kernel='adc' (ivf.py:148-196)
+ * coarse (K, d) float32; lists concatenated in cell order: list_sizes (K,),
+ * codes (sum, m) uint8 (b == 8), ids (sum,) int64.  All host arrays.       */
+int pqs_ivf_create(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t K,
+                   const int64_t* list_sizes, const uint8_t* codes, const int64_t* ids,
+                   pqs_ivf** out);
+void pqs_ivf_destroy(pqs_ivf* ivf);
+/* probes only: nearest_k (_dist.py:42-67) -> out_cells (nq, ma) int64,
+ * out_dist (nq, ma) float64 (may be NULL), ascending by (distance, cell).  */
+int pqs_ivf_probe(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_t nq, int ma,
+                  int64_t* out_cells, double* out_dist, int io);
+int pqs_ivf_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_t nq, int ma,
+                   int r, double* out_dist, int64_t* out_ids, int32_t* out_count, int io);
+
+/* ---- sharded merge: top-r of the union of G per-shard top-r lists by
+ * (distance, id) -- NeighborSet.push semantics (scan.py:109-118).
+ * dists (G, nq, r_in) float64, ids (G, nq, r_in), counts (G, nq).          */
+int pqs_merge_topr(pqs_ctx* ctx, int G, const double* dists, const int64_t* ids,
+                   const int32_t* counts, int64_t nq, int r_in, int r, double* out_dist,
+                   int64_t* out_ids, int32_t* out_count, int io);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PQS_H */

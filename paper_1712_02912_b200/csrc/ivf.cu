@@ -1,0 +1,740 @@
+// ivf.cu -- IVFADC query (K7 probes, K8 list-major scan).
+//
+// Reference: query_ivf kernel='adc' (ivf.py:148-196): probe the ma nearest
+// coarse cells by fp64 (distance, index) (nearest_k, _dist.py:42-67), scan
+// each cell's list against the tables of the fp64 residual q - coarse[c]
+// (ivf.py:179-183), merge all per-list top-r by (distance, id).
+//
+// B200 design:
+//  K7  probe distances: ||c||^2 - 2 q.c with the q.c products from one fp32
+//      GEMM (cuBLAS, pedantic fp32 math = no TF32); a per-query radix select
+//      finds the ma-th approximate distance, every cell within a certified
+//      fp32 error bound of it is re-scored in exact fp64 (scipy's sequential
+//      order) and the ma best by (distance, cell) are kept -> identical probe
+//      sets and order to nearest_k.
+//  K8  the residual tables are never materialised per (query, list): with
+//      PQ sub-spaces disjoint, sum_j T_j = ||q-c||^2 + sum_j U_q[j][code_j]
+//      + V[code] where U_q[j][i] = ||C_ji||^2 - 2<q_j, C_ji> (per query) and
+//      V = 2 sum_j <c_j, C_j[code_j]> (per stored code, at index build).
+//      The list-major kernel (one CTA per inverted list, all queries probing
+//      it) adds those in fp32 as a certified filter; survivors are re-scored
+//      exactly (residual tables in fp64, scan.py:45-56 + 77-81 order) in the
+//      select kernel.  The filter threshold per query comes from a sample
+//      (the first 64 codes of every probed list).
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "pqs_common.cuh"
+#include "select_dev.cuh"
+
+namespace {
+
+using namespace seldev;
+
+constexpr int SAMPLE_PER_LIST = 64;
+
+// ------------------------------------------------------------ index build
+__global__ void cnorm_kernel(const float* __restrict__ coarse, int64_t K, int d, double* __restrict__ cnorm,
+                             float* __restrict__ gnorm) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= K) return;
+  double s = 0.0;
+  for (int t = 0; t < d; ++t) {
+    const double v = (double)coarse[c * d + t];
+    s = __dadd_rn(s, __dmul_rn(v, v));
+  }
+  cnorm[c] = s;
+  gnorm[c] = (float)sqrt(s);
+}
+
+// V[pos] = 2 sum_j <g_cj, C_j[code_j]>, fp64 -> fp32; one CTA per list
+__global__ void v_kernel(const float* __restrict__ coarse, const float* __restrict__ books,
+                         const int64_t* __restrict__ offsets, const uint8_t* __restrict__ codes, int m, int k,
+                         int dsub, int d, float* __restrict__ V, float* __restrict__ vmax_out) {
+  const int64_t c = blockIdx.x;
+  const int64_t b = offsets[c], e = offsets[c + 1];
+  const float* g = coarse + c * (int64_t)d;
+  float vmax = 0.f;
+  for (int64_t p = b + threadIdx.x; p < e; p += blockDim.x) {
+    double s = 0.0;
+    for (int j = 0; j < m; ++j) {
+      const float* cb = books + ((int64_t)j * k + codes[p * m + j]) * dsub;
+      for (int t = 0; t < dsub; ++t) s += (double)g[j * dsub + t] * (double)cb[t];
+    }
+    const float v = (float)(2.0 * s);
+    V[p] = v;
+    vmax = fmaxf(vmax, fabsf(v));
+  }
+  for (int o = 16; o > 0; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+  if ((threadIdx.x & 31) == 0) atomicMax((int*)vmax_out, __float_as_int(vmax));
+}
+
+// per-query tables U[q][j][i] = ||C_ji||^2 - 2 <q_j, C_ji> (fp64 -> fp32)
+__global__ void utables_kernel(const float* __restrict__ queries, const float* __restrict__ books, int64_t nq, int m,
+                               int k, int dsub, float* __restrict__ U) {
+  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gid >= nq * m * (int64_t)k) return;
+  const int i = (int)(gid % k);
+  const int64_t t = gid / k;
+  const int j = (int)(t % m);
+  const int64_t q = t / m;
+  const float* qv = queries + q * (int64_t)m * dsub + (int64_t)j * dsub;
+  const float* cb = books + ((int64_t)j * k + i) * dsub;
+  double nn = 0.0, dot = 0.0;
+  for (int s = 0; s < dsub; ++s) {
+    const double cv = (double)cb[s];
+    nn += cv * cv;
+    dot += (double)qv[s] * cv;
+  }
+  U[gid] = (float)(nn - 2.0 * dot);
+}
+
+// per query: E_q = certified bound of |filter distance - exact distance|
+__global__ void ivf_bound_kernel(const float* __restrict__ U, const double* __restrict__ pdist, int64_t nq, int ma,
+                                 int m, int k, const float* __restrict__ vmax, float* __restrict__ aerr) {
+  const int64_t q = blockIdx.x;
+  __shared__ double part[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double s = 0.0;
+  for (int j = warp; j < m; j += nw) {
+    float mx = 0.f;
+    for (int i = lane; i < k; i += 32) mx = fmaxf(mx, fabsf(U[(q * m + j) * (int64_t)k + i]));
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    s += (double)mx;
+  }
+  if (lane == 0) part[warp] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double usum = 0.0;
+    for (int i = 0; i < nw; ++i) usum += part[i];
+    double amax = 0.0;
+    for (int p = 0; p < ma; ++p) amax = fmax(amax, pdist[q * ma + p]);
+    const double B = amax + (double)vmax[0] + usum;
+    const double u = 5.9604644775390625e-08;
+    aerr[q] = (float)((m + 6) * u * 1.05 * B + 1e-30);
+  }
+}
+
+// ------------------------------------------------------------ K7 probes
+struct ProbeArgs {
+  const float* dots;     // (nqb, K) fp32 q.c
+  const double* cnorm;   // (K,)
+  const float* gnorm;    // (K,) ||c|| fp32
+  float gmax;
+  const float* queries;  // (nq, d), batch-offset applied
+  const float* coarse;   // (K, d)
+  int64_t K;
+  int d, ma;
+  int64_t q0;            // global index of batch row 0
+  int64_t* out_cells;    // (nq, ma)
+  double* out_dist;      // (nq, ma)
+  uint64_t* gkeys;       // (nqb, K) scratch
+  int64_t* gids;
+};
+
+constexpr int PROBE_THREADS = 512;
+constexpr int PROBE_SMEM_CAP = 4096;
+
+__global__ void __launch_bounds__(PROBE_THREADS) probe_select_kernel(ProbeArgs a, int sortP) {
+  extern __shared__ __align__(16) unsigned char psm[];
+  __shared__ SelShared sh;
+  __shared__ int s_cnt;
+  __shared__ double s_qn;
+  uint64_t* ck = (uint64_t*)psm;                 // candidates (PROBE_SMEM_CAP)
+  int64_t* ci = (int64_t*)(ck + PROBE_SMEM_CAP);
+  uint64_t* ok = (uint64_t*)(ci + PROBE_SMEM_CAP);
+  int64_t* oi = (int64_t*)(ok + sortP);
+  const int64_t ql = blockIdx.x;
+  const int64_t q = a.q0 + ql;
+  const float* dots = a.dots + ql * a.K;
+  const float* qv = a.queries + ql * (int64_t)a.d;
+  const int64_t K = a.K;
+  const int ma = a.ma;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int t = 0; t < a.d; ++t) s += (double)qv[t] * (double)qv[t];
+    s_qn = sqrt(s);
+    s_cnt = 0;
+  }
+  __syncthreads();
+  // certified bound on |approx - exact|: fp32 dot (any order) error <= gamma_d ||q|| ||c||
+  const double u = 5.9604644775390625e-08;
+  const double gam = a.d * u / (1.0 - a.d * u);
+  const double eps = 2.0 * gam * s_qn * (double)a.gmax * 1.01 + 1e-9 * (s_qn * s_qn + (double)a.gmax * a.gmax);
+  auto approx = [&](int64_t c) { return a.cnorm[c] - 2.0 * (double)dots[c]; };
+  double thr = 1e300;
+  if (ma < K) {
+    auto getk = [&](int64_t c, uint64_t& v) {
+      v = dkey(approx(c));
+      return true;
+    };
+    block_radix_select(K, getk, (unsigned long long)(ma - 1), sh);
+    thr = dkey_inv(sh.prefix) + 2.0 * eps;
+    __syncthreads();
+  }
+  // gather candidates, exact fp64 distance (sequential, as scipy cdist)
+  const bool use_global = false;
+  (void)use_global;
+  for (int64_t c = threadIdx.x; c < K; c += blockDim.x) {
+    if (approx(c) <= thr) {
+      const int p = atomicAdd(&s_cnt, 1);
+      const float* g = a.coarse + c * (int64_t)a.d;
+      double s = 0.0;
+      for (int t = 0; t < a.d; ++t) {
+        const double df = __dsub_rn((double)qv[t], (double)g[t]);
+        s = __dadd_rn(s, __dmul_rn(df, df));
+      }
+      if (p < PROBE_SMEM_CAP) {
+        ck[p] = dkey(s);
+        ci[p] = c;
+      } else {
+        a.gkeys[ql * K + p] = dkey(s);
+        a.gids[ql * K + p] = c;
+      }
+    }
+  }
+  __syncthreads();
+  const int64_t M = s_cnt;
+  const uint64_t* KK = M <= PROBE_SMEM_CAP ? ck : a.gkeys + ql * K;
+  const int64_t* II = M <= PROBE_SMEM_CAP ? ci : a.gids + ql * K;
+  if (M > PROBE_SMEM_CAP) {
+    // move the shared part to global so that one array holds all
+    for (int p = threadIdx.x; p < PROBE_SMEM_CAP; p += blockDim.x) {
+      a.gkeys[ql * K + p] = ck[p];
+      a.gids[ql * K + p] = ci[p];
+    }
+    __syncthreads();
+  }
+  unsigned long long kstar = ~0ull;
+  long long istar = 0x7FFFFFFFFFFFFFFFll;
+  bool all_ties = true;
+  const int64_t r_eff = ma < M ? ma : M;
+  if (r_eff < M) {
+    auto getk = [&](int64_t i, uint64_t& v) {
+      v = KK[i];
+      return true;
+    };
+    block_radix_select(M, getk, (unsigned long long)(r_eff - 1), sh);
+    kstar = sh.prefix;
+    const unsigned long long less = sh.less, eq = sh.eq, need = r_eff - less;
+    __syncthreads();
+    if (eq > need) {
+      all_ties = false;
+      auto geti = [&](int64_t i, uint64_t& v) {
+        v = (uint64_t)II[i] ^ 0x8000000000000000ull;
+        return KK[i] == kstar;
+      };
+      block_radix_select(M, geti, need - 1, sh);
+      istar = (long long)(sh.prefix ^ 0x8000000000000000ull);
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+    const uint64_t key = KK[i];
+    const int64_t id = II[i];
+    if (key < kstar || (key == kstar && (all_ties || id <= istar))) {
+      const int p = atomicAdd(&s_cnt, 1);
+      if (p < sortP) {
+        ok[p] = key;
+        oi[p] = id;
+      }
+    }
+  }
+  __syncthreads();
+  for (int p = (int)r_eff + threadIdx.x; p < sortP; p += blockDim.x) {
+    ok[p] = ~0ull;
+    oi[p] = 0x7FFFFFFFFFFFFFFFll;
+  }
+  __syncthreads();
+  bitonic_sort(ok, oi, sortP);
+  for (int p = threadIdx.x; p < ma; p += blockDim.x) {
+    a.out_cells[q * ma + p] = p < r_eff ? oi[p] : -1;
+    if (a.out_dist) a.out_dist[q * ma + p] = p < r_eff ? dkey_inv(ok[p]) : __longlong_as_double(0x7FF0000000000000ll);
+  }
+}
+
+// ------------------------------------------------------------ K8 helpers
+// sample: the first SAMPLE_PER_LIST codes of every probed list, query-major
+__global__ void ivf_sample_kernel(const float* __restrict__ U, const int64_t* __restrict__ cells,
+                                  const double* __restrict__ pdist, const int64_t* __restrict__ offsets,
+                                  const uint8_t* __restrict__ codes, const float* __restrict__ V, int ma, int m, int k,
+                                  float* __restrict__ sample) {
+  extern __shared__ float su[];
+  const int64_t q = blockIdx.x;
+  for (int i = threadIdx.x; i < m * k; i += blockDim.x) su[i] = U[q * (int64_t)m * k + i];
+  __syncthreads();
+  const int64_t ns = (int64_t)ma * SAMPLE_PER_LIST;
+  for (int64_t s = threadIdx.x; s < ns; s += blockDim.x) {
+    const int p = (int)(s / SAMPLE_PER_LIST);
+    const int i = (int)(s % SAMPLE_PER_LIST);
+    const int64_t c = cells[q * ma + p];
+    float out = __int_as_float(0x7f800000);
+    if (c >= 0) {
+      const int64_t b = offsets[c], e = offsets[c + 1];
+      if (b + i < e) {
+        const int64_t pos = b + i;
+        float acc = (float)pdist[q * ma + p] + V[pos];
+        for (int j = 0; j < m; ++j) acc += su[j * k + codes[pos * m + j]];
+        out = acc;
+      }
+    }
+    sample[q * ns + s] = out;
+  }
+}
+
+__global__ void pair_count_kernel(const int64_t* __restrict__ cells, int64_t npairs, int* __restrict__ cnt) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < npairs && cells[i] >= 0) atomicAdd(cnt + cells[i], 1);
+}
+
+// exclusive scan of K ints (single CTA, K up to a few million)
+__global__ void scan_kernel(const int* __restrict__ in, int64_t K, int64_t* __restrict__ out) {
+  __shared__ int64_t part[1024];
+  const int64_t per = cdiv(K, blockDim.x);
+  const int64_t b = threadIdx.x * per, e = min(b + per, K);
+  int64_t s = 0;
+  for (int64_t i = b; i < e; ++i) s += in[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int i = 0; i < (int)blockDim.x; ++i) {
+      const int64_t t = part[i];
+      part[i] = acc;
+      acc += t;
+    }
+  }
+  __syncthreads();
+  int64_t acc = part[threadIdx.x];
+  for (int64_t i = b; i < e; ++i) {
+    out[i] = acc;
+    acc += in[i];
+  }
+  if (threadIdx.x == blockDim.x - 1) out[K] = acc;
+}
+
+__global__ void pair_fill_kernel(const int64_t* __restrict__ cells, const double* __restrict__ pdist, int64_t nq, int ma,
+                                 const int64_t* __restrict__ starts, int* __restrict__ fill, int* __restrict__ pq,
+                                 float* __restrict__ pa) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nq * ma) return;
+  const int64_t c = cells[i];
+  if (c < 0) return;
+  const int slot = atomicAdd(fill + c, 1);
+  const int64_t o = starts[c] + slot;
+  pq[o] = (int)(i / ma);
+  pa[o] = (float)pdist[i];
+}
+
+// one CTA per inverted list: every probing query scans the list's codes
+__global__ void __launch_bounds__(256) ivf_list_kernel(const float* __restrict__ U, const int64_t* __restrict__ starts,
+                                                       const int* __restrict__ pq, const float* __restrict__ pa,
+                                                       const int64_t* __restrict__ offsets,
+                                                       const uint8_t* __restrict__ codes, const float* __restrict__ V,
+                                                       int m, int k, const float* __restrict__ theta,
+                                                       uint64_t* __restrict__ cand, int* __restrict__ cand_cnt,
+                                                       int64_t cap, int LIST_CHUNK) {
+  extern __shared__ __align__(16) unsigned char lsm[];
+  const int64_t c = blockIdx.x;
+  const int64_t p0 = starts[c], p1 = starts[c + 1];
+  if (p0 == p1) return;
+  const int64_t b = offsets[c], e = offsets[c + 1];
+  if (b == e) return;
+  float* su = (float*)lsm;                              // m*k
+  uint8_t* sc = lsm + (size_t)m * k * 4;                // chunk codes
+  float* sv = (float*)(sc + ((size_t)LIST_CHUNK * m + 15) / 16 * 16);
+  for (int64_t cb = b; cb < e; cb += LIST_CHUNK) {
+    const int64_t ce = min(cb + (int64_t)LIST_CHUNK, e);
+    const int nc = (int)(ce - cb);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nc * m; i += blockDim.x) sc[i] = codes[cb * m + i];
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) sv[i] = V[cb + i];
+    for (int64_t pp = p0; pp < p1; ++pp) {
+      const int q = pq[pp];
+      const float A = pa[pp];
+      const float th = theta[q];
+      __syncthreads();
+      for (int i = threadIdx.x; i < m * k; i += blockDim.x) su[i] = U[(int64_t)q * m * k + i];
+      __syncthreads();
+      for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+        float acc = A + sv[i];
+        const uint8_t* cd = sc + i * m;
+        for (int j = 0; j < m; ++j) acc += su[j * k + cd[j]];
+        if (acc <= th) {
+          const int pos = atomicAdd(cand_cnt + q, 1);
+          if (pos < cap) cand[(int64_t)q * cap + pos] = ((uint64_t)c << 32) | (uint64_t)(uint32_t)(cb + i);
+        }
+      }
+    }
+  }
+}
+
+// fallback: every code of the query's probed lists becomes a candidate
+__global__ void ivf_all_kernel(const int64_t* __restrict__ cells_row, int ma, const int64_t* __restrict__ offsets,
+                               uint64_t* __restrict__ cand, int* __restrict__ cnt, int64_t cap) {
+  for (int p = 0; p < ma; ++p) {
+    const int64_t c = cells_row[p];
+    if (c < 0) continue;
+    const int64_t b = offsets[c], e = offsets[c + 1];
+    for (int64_t pos = b + threadIdx.x; pos < e; pos += blockDim.x) {
+      const int s = atomicAdd(cnt, 1);
+      if (s < cap) cand[s] = ((uint64_t)c << 32) | (uint64_t)(uint32_t)pos;
+    }
+  }
+}
+
+__global__ void theta_ivf_kernel(const float* __restrict__ sample, int64_t ns, int r, const float* __restrict__ aerr,
+                                 float* __restrict__ theta) {
+  __shared__ unsigned int hist[256];
+  __shared__ unsigned int s_prefix, s_k, s_valid;
+  const int64_t q = blockIdx.x;
+  const float* row = sample + q * ns;
+  if (threadIdx.x == 0) {
+    s_prefix = 0;
+    s_k = (unsigned)(r - 1);
+    s_valid = 0;
+  }
+  __syncthreads();
+  unsigned int valid = 0;
+  for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) valid += isfinite(row[i]) ? 1u : 0u;
+  atomicAdd(&s_valid, valid);
+  __syncthreads();
+  if (s_valid < (unsigned)r) {
+    if (threadIdx.x == 0) theta[q] = __int_as_float(0x7f800000);
+    return;
+  }
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const unsigned prefix = s_prefix;
+    for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
+      const float v = row[i];
+      if (!isfinite(v)) continue;
+      const unsigned key = fkey(v);
+      const bool match = (shift == 24) ? true : ((key ^ prefix) >> (shift + 8)) == 0;
+      if (match) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned cc = 0, kk = s_k;
+      int d = 0;
+      for (; d < 256; ++d) {
+        if (kk < cc + hist[d]) break;
+        cc += hist[d];
+      }
+      s_k = kk - cc;
+      s_prefix = prefix | ((unsigned)d << shift);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double t = (double)fkey_inv(s_prefix) + 2.0 * (double)aerr[q];
+    float f = (float)t;
+    if ((double)f < t) f = nextafterf(f, __int_as_float(0x7f800000));
+    theta[q] = nextafterf(f, __int_as_float(0x7f800000));
+  }
+}
+
+struct Cublas {
+  cublasHandle_t h = nullptr;
+  int device = -1;
+};
+Cublas g_cublas[16];
+
+int get_cublas(pqs_ctx* ctx, cublasHandle_t* out) {
+  Cublas& c = g_cublas[ctx->device & 15];
+  if (!c.h) {
+    if (cublasCreate(&c.h) != CUBLAS_STATUS_SUCCESS) return set_err(ctx, PQS_ERR_CUDA, "cublasCreate failed");
+    cublasSetMathMode(c.h, CUBLAS_PEDANTIC_MATH);  // true fp32, no TF32
+    c.device = ctx->device;
+  }
+  cublasSetStream(c.h, ctx->stream);
+  *out = c.h;
+  return PQS_OK;
+}
+
+}  // namespace
+
+void ivf_destroy_impl(pqs_ivf* iv);
+
+// ---------------------------------------------------------------------------
+int ivf_create_impl(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t K, const int64_t* list_sizes,
+                    const uint8_t* codes, const int64_t* ids, pqs_ivf** out) {
+  *out = nullptr;
+  PQS_CHECK(ctx, K >= 1, "need at least one coarse centroid");
+  PQS_CHECK(ctx, pq->k <= 256, "IVF lists need b <= 8");
+  std::vector<int64_t> offs(K + 1, 0);
+  int64_t mx = 0;
+  for (int64_t c = 0; c < K; ++c) {
+    PQS_CHECK(ctx, list_sizes[c] >= 0, "list sizes must be >= 0");
+    offs[c + 1] = offs[c] + list_sizes[c];
+    mx = std::max(mx, list_sizes[c]);
+  }
+  const int64_t n = offs[K];
+  PQS_CHECK(ctx, n < (1ll << 32), "an IVF shard holds at most 2^32 - 1 codes");
+  PQS_CHECK(ctx, K < (1ll << 31), "K must be < 2^31");
+  for (int64_t i = 0; i < n * pq->m; ++i) PQS_CHECK(ctx, codes[i] < pq->k, "code component out of range");
+  pqs_ivf* iv = new pqs_ivf();
+  iv->K = K;
+  iv->n = n;
+  iv->m = pq->m;
+  iv->k = pq->k;
+  iv->d = pq->d;
+  iv->dsub = pq->dsub;
+  iv->h_offsets = offs;
+  iv->max_list = mx;
+  const int d = pq->d;
+  auto al = [&](void** p, size_t bytes) { return cudaMalloc(p, std::max<size_t>(bytes, 16)) == cudaSuccess; };
+  bool ok = al((void**)&iv->coarse, (size_t)K * d * 4) && al((void**)&iv->cnorm, (size_t)K * 8) &&
+            al((void**)&iv->books, (size_t)pq->m * pq->k * pq->dsub * 4) && al((void**)&iv->offsets, (size_t)(K + 1) * 8) &&
+            al((void**)&iv->codes, (size_t)n * pq->m) && al((void**)&iv->ids, (size_t)n * 8) &&
+            al((void**)&iv->gnorm, (size_t)K * 4 /* gnorm */ + 16) && al((void**)&iv->vtab, (size_t)n * 4) &&
+            al((void**)&iv->vmax, 16);
+  if (!ok) {
+    cudaGetLastError();
+    ivf_destroy_impl(iv);
+    return set_err(ctx, PQS_ERR_NOMEM, "IVF allocation failed");
+  }
+  PQS_CUDA(ctx, cudaMemcpy(iv->coarse, coarse, (size_t)K * d * 4, cudaMemcpyHostToDevice));
+  PQS_CUDA(ctx, cudaMemcpy(iv->books, pq->books, (size_t)pq->m * pq->k * pq->dsub * 4, cudaMemcpyDeviceToDevice));
+  PQS_CUDA(ctx, cudaMemcpy(iv->offsets, offs.data(), (size_t)(K + 1) * 8, cudaMemcpyHostToDevice));
+  if (n) {
+    PQS_CUDA(ctx, cudaMemcpy(iv->codes, codes, (size_t)n * pq->m, cudaMemcpyHostToDevice));
+    PQS_CUDA(ctx, cudaMemcpy(iv->ids, ids, (size_t)n * 8, cudaMemcpyHostToDevice));
+  }
+  PQS_CUDA(ctx, cudaMemset(iv->vmax, 0, 16));
+  cnorm_kernel<<<(unsigned)cdiv(K, 256), 256, 0, ctx->stream>>>(iv->coarse, K, d, iv->cnorm, iv->gnorm);
+  PQS_LAUNCHED(ctx);
+  v_kernel<<<(unsigned)K, 256, 0, ctx->stream>>>(iv->coarse, iv->books, iv->offsets, iv->codes, iv->m, iv->k, iv->dsub,
+                                                 d, iv->vtab, iv->vmax);
+  PQS_LAUNCHED(ctx);
+  PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  // gmax on host
+  std::vector<float> gn(K);
+  PQS_CUDA(ctx, cudaMemcpy(gn.data(), iv->gnorm, (size_t)K * 4, cudaMemcpyDeviceToHost));
+  float gm = 0.f;
+  for (float v : gn) gm = std::max(gm, v);
+  iv->gmax = gm;
+  *out = iv;
+  return PQS_OK;
+}
+
+void ivf_destroy_impl(pqs_ivf* iv) {
+  if (!iv) return;
+  cudaFree(iv->coarse);
+  cudaFree(iv->gnorm);
+  cudaFree(iv->cnorm);
+  cudaFree(iv->books);
+  cudaFree(iv->offsets);
+  cudaFree(iv->codes);
+  cudaFree(iv->ids);
+  cudaFree(iv->vtab);
+  cudaFree(iv->vmax);
+  delete iv;
+}
+
+int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int64_t nq, int ma, int64_t* d_cells,
+                  double* d_dist) {
+  const int64_t K = iv->K;
+  const int d = iv->d;
+  const int64_t QB = std::max<int64_t>(1, std::min<int64_t>(nq, (int64_t)(256ll << 20) / (K * 4)));
+  float* dots = nullptr;
+  uint64_t* gk = nullptr;
+  int64_t* gi = nullptr;
+  PQS_TRY(scratch(ctx, S_IVF_WORK, (size_t)(QB * K), &dots));
+  PQS_TRY(scratch(ctx, S_KEYS, (size_t)(QB * K), &gk));
+  PQS_TRY(scratch(ctx, S_IDS, (size_t)(QB * K), &gi));
+  cublasHandle_t h;
+  PQS_TRY(get_cublas(ctx, &h));
+  int P = 1;
+  while (P < ma) P <<= 1;
+  if (P < 2) P = 2;
+  PQS_CHECK(ctx, P <= 4096, "ma too large for the device probe select (<= 4096)");
+  const size_t smem = (size_t)PROBE_SMEM_CAP * 16 + (size_t)P * 16;
+  PQS_CUDA(ctx, cudaFuncSetAttribute(probe_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)((size_t)PROBE_SMEM_CAP * 16 + 4096 * 16)));
+  for (int64_t q0 = 0; q0 < nq; q0 += QB) {
+    const int64_t nb = std::min(QB, nq - q0);
+    // dots (nb, K) row-major = queries (nb, d) x coarse^T; column-major view:
+    // dots^T (K x nb) = coarse (K x d, col-major = coarse^T row-major...) use
+    // C(K, nb) = A(K, d) * B(d, nb) with A = coarse row-major seen as (d x K)
+    // col-major transposed, B = queries row-major seen as (d x nb) col-major.
+    const float alpha = 1.f, beta = 0.f;
+    if (cublasSgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)K, (int)nb, d, &alpha, iv->coarse, d, d_queries + q0 * d, d,
+                    &beta, dots, (int)K) != CUBLAS_STATUS_SUCCESS)
+      return set_err(ctx, PQS_ERR_CUDA, "cublasSgemm failed");
+    ctx->launches++;
+    ProbeArgs a{};
+    a.dots = dots;
+    a.cnorm = iv->cnorm;
+    a.gnorm = iv->gnorm;
+    a.gmax = iv->gmax;
+    a.queries = d_queries + q0 * d;
+    a.coarse = iv->coarse;
+    a.K = K;
+    a.d = d;
+    a.ma = ma;
+    a.q0 = q0;
+    a.out_cells = d_cells;
+    a.out_dist = d_dist;
+    a.gkeys = gk;
+    a.gids = gi;
+    probe_select_kernel<<<(unsigned)nb, PROBE_THREADS, smem, ctx->stream>>>(a, P);
+    PQS_LAUNCHED(ctx);
+  }
+  return PQS_OK;
+}
+
+int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int64_t nq, int ma, int r, double* d_dist,
+                   int64_t* d_ids, int32_t* d_count) {
+  const int64_t K = iv->K;
+  const int m = iv->m, k = iv->k;
+  // probes
+  int64_t* cells = nullptr;
+  double* pdist = nullptr;
+  PQS_TRY(scratch(ctx, S_PROBE, (size_t)(nq * ma), &cells));
+  PQS_TRY(scratch(ctx, S_PROBE_D, (size_t)(nq * ma), &pdist));
+  PQS_TRY(run_ivf_probe(ctx, iv, d_queries, nq, ma, cells, pdist));
+  // per-query tables + bound
+  float* U = nullptr;
+  float* aerr = nullptr;
+  PQS_TRY(scratch(ctx, S_TABLES, (size_t)(nq * m * k), &U));
+  PQS_TRY(scratch(ctx, S_AERR, (size_t)nq, &aerr));
+  utables_kernel<<<(unsigned)cdiv(nq * m * k, 256), 256, 0, ctx->stream>>>(d_queries, iv->books, nq, m, k, iv->dsub, U);
+  PQS_LAUNCHED(ctx);
+  ivf_bound_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(U, pdist, nq, ma, m, k, iv->vmax, aerr);
+  PQS_LAUNCHED(ctx);
+  // threshold from the sample
+  const int64_t ns = (int64_t)ma * SAMPLE_PER_LIST;
+  float* sample = nullptr;
+  float* theta = nullptr;
+  PQS_TRY(scratch(ctx, S_SAMPLE, (size_t)(nq * ns) * 4, (uint8_t**)&sample));
+  PQS_TRY(scratch(ctx, S_THETA, (size_t)nq * 4, (uint8_t**)&theta));
+  const size_t usm = (size_t)m * k * 4;
+  PQS_CUDA(ctx, cudaFuncSetAttribute(ivf_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
+  ivf_sample_kernel<<<(unsigned)nq, 256, usm, ctx->stream>>>(U, cells, pdist, iv->offsets, iv->codes, iv->vtab, ma, m, k,
+                                                            sample);
+  PQS_LAUNCHED(ctx);
+  theta_ivf_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(sample, ns, r, aerr, theta);
+  PQS_LAUNCHED(ctx);
+  // bucket (query, probe) pairs by list
+  int* lcnt = nullptr;
+  int64_t* starts = nullptr;
+  int* pq_ = nullptr;
+  float* pa = nullptr;
+  PQS_TRY(scratch(ctx, S_IVF_WORK2, (size_t)(K + 1), &lcnt));
+  PQS_TRY(scratch(ctx, S_IVF_WORK3, (size_t)(K + 1), &starts));
+  PQS_TRY(scratch(ctx, S_MISC, (size_t)(nq * ma) * 2, &pq_));
+  pa = (float*)(pq_ + nq * ma);
+  PQS_CUDA(ctx, cudaMemsetAsync(lcnt, 0, sizeof(int) * (K + 1), ctx->stream));
+  pair_count_kernel<<<(unsigned)cdiv(nq * ma, 256), 256, 0, ctx->stream>>>(cells, nq * ma, lcnt);
+  PQS_LAUNCHED(ctx);
+  scan_kernel<<<1, 1024, 0, ctx->stream>>>(lcnt, K, starts);
+  PQS_LAUNCHED(ctx);
+  PQS_CUDA(ctx, cudaMemsetAsync(lcnt, 0, sizeof(int) * (K + 1), ctx->stream));
+  pair_fill_kernel<<<(unsigned)cdiv(nq * ma, 256), 256, 0, ctx->stream>>>(cells, pdist, nq, ma, starts, lcnt, pq_, pa);
+  PQS_LAUNCHED(ctx);
+  // list-major filtered scan
+  const int64_t cap = ctx->cand_cap;
+  uint64_t* cand = nullptr;
+  int* cnt = nullptr;
+  PQS_TRY(scratch(ctx, S_CAND, (size_t)(nq * cap), &cand));
+  PQS_TRY(scratch(ctx, S_CAND_CNT, (size_t)nq, &cnt));
+  PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nq, ctx->stream));
+  const int LIST_CHUNK = std::max(64, std::min(4096, 65536 / m));
+  const size_t lsm = usm + ((size_t)LIST_CHUNK * m + 15) / 16 * 16 + (size_t)LIST_CHUNK * 4;
+  PQS_CUDA(ctx, cudaFuncSetAttribute(ivf_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+  ivf_list_kernel<<<(unsigned)K, 256, lsm, ctx->stream>>>(U, starts, pq_, pa, iv->offsets, iv->codes, iv->vtab, m, k,
+                                                         theta, cand, cnt, cap, LIST_CHUNK);
+  PQS_LAUNCHED(ctx);
+  // exact rerank + select
+  uint64_t* gk = nullptr;
+  int64_t* gi = nullptr;
+  PQS_TRY(scratch(ctx, S_KEYS, (size_t)(nq * cap), &gk));
+  PQS_TRY(scratch(ctx, S_IDS, (size_t)(nq * cap), &gi));
+  SelArgs s{};
+  s.src = SEL_CAND_IVF;
+  s.nq = nq;
+  s.r = r;
+  s.cand = cand;
+  s.cand_cnt = cnt;
+  s.cap = cap;
+  s.ids = iv->ids;
+  s.ivf_q = d_queries;
+  s.ivf_coarse = iv->coarse;
+  s.ivf_books = iv->books;
+  s.ivf_codes = iv->codes;
+  s.m = m;
+  s.k = k;
+  s.d = iv->d;
+  s.dsub = iv->dsub;
+  s.out_d = d_dist;
+  s.out_i = d_ids;
+  s.out_c = d_count;
+  s.gkeys = gk;
+  s.gids = gi;
+  s.gcap = cap;
+  PQS_TRY(launch_select(ctx, s));
+  // overflow / sanity check against the exact probed totals
+  std::vector<int> hcnt(nq);
+  std::vector<int64_t> hcells(nq * ma);
+  PQS_CUDA(ctx, cudaMemcpyAsync(hcnt.data(), cnt, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
+  PQS_CUDA(ctx, cudaMemcpyAsync(hcells.data(), cells, sizeof(int64_t) * nq * ma, cudaMemcpyDeviceToHost, ctx->stream));
+  PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  std::vector<int> over;
+  int64_t mx = 0, total_evals = 0, worst_total = 0;
+  for (int64_t q = 0; q < nq; ++q) {
+    int64_t tot = 0;
+    for (int p = 0; p < ma; ++p) {
+      const int64_t c = hcells[q * ma + p];
+      if (c >= 0) tot += iv->h_offsets[c + 1] - iv->h_offsets[c];
+    }
+    total_evals += tot;
+    mx = std::max<int64_t>(mx, hcnt[q]);
+    const int64_t r_eff = std::min<int64_t>(r, tot);
+    if (hcnt[q] > cap || hcnt[q] < r_eff || ctx->force_fallback) {
+      over.push_back((int)q);
+      worst_total = std::max(worst_total, tot);
+    }
+  }
+  ctx->last_evals = total_evals;
+  ctx->last_max_cand = mx;
+  ctx->last_overflow = (int64_t)over.size();
+  if (!over.empty()) {
+    const int64_t fcap = std::max<int64_t>(worst_total, 1);
+    uint64_t* fc = nullptr;
+    int* fcnt = nullptr;
+    for (size_t i = 0; i < over.size(); ++i) {
+      // one query at a time: its whole probed set is the candidate list
+      PQS_TRY(scratch(ctx, S_DENSE, (size_t)fcap * (nq > 0 ? 1 : 1) * 2 + 2, &fc));
+      fcnt = (int*)(fc + fcap);
+      PQS_TRY(scratch(ctx, S_KEYS, (size_t)fcap, &gk));
+      PQS_TRY(scratch(ctx, S_IDS, (size_t)fcap, &gi));
+      PQS_CUDA(ctx, cudaMemsetAsync(fcnt, 0, sizeof(int) * 1, ctx->stream));
+      // candidates are indexed by the global query id; use a 1-row view
+      const int qg = over[i];
+      ivf_all_kernel<<<1, 256, 0, ctx->stream>>>(cells + (int64_t)qg * ma, ma, iv->offsets, fc, fcnt, fcap);
+      PQS_LAUNCHED(ctx);
+      SelArgs f = s;
+      f.nq = 1;
+      f.cand = fc;
+      f.cand_cnt = fcnt;
+      f.cap = fcap;
+      f.ivf_q = d_queries + (int64_t)qg * iv->d;
+      f.out_d = d_dist + (int64_t)qg * r;
+      f.out_i = d_ids + (int64_t)qg * r;
+      f.out_c = d_count + qg;
+      f.gkeys = gk;
+      f.gids = gi;
+      f.gcap = fcap;
+      PQS_TRY(launch_select(ctx, f));
+    }
+  }
+  return PQS_OK;
+}

@@ -1,0 +1,606 @@
+// scan4.cu -- Quick ADC over 4-bit codes (K2 layout, K9 params, K4 scan).
+//
+// Reference: qadc_scan (quickadc.py:104-141), quantize (fastscan.py:42-57),
+// quantized_distances / qadc_block (quickadc.py:66-101).
+//
+// K4 design: one thread per query holds that query's m
+// quantized 16-entry tables in registers (4 x u32 per component).  Codes are
+// stored as 4-code quads: one u32 per (quad, component pair) whose low/high
+// 16 bits are PRMT selectors for components 2p / 2p+1.  Each tile of 1024
+// codes is expanded once per CTA into shared memory as (s, s^0x8888, s>>16,
+// (s^0x8888)>>16) and read by every thread with a broadcast LDS.128.  A
+// 16-entry lookup of 4 codes is two PRMTs: entries 0-7 with the raw selector
+// (a set nibble msb sign-replicates a byte <= 127 -> 0), entries 8-15 with
+// the msb-flipped selector.  Two components are summed in byte lanes (<= 254)
+// and widened into 16-bit lanes; min(sum,127) equals the reference's clamp
+// after every add because entries are non-negative (quickadc.py:87-92).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "pqs_common.cuh"
+
+namespace {
+
+constexpr int SCAN4_THREADS = 256;
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
+  return d;
+}
+
+// ---------------------------------------------------------------- K2 layout
+// codes (n, m) row-major -> words[(tile*QUADS4 + g) * (mp/2) + p]
+__global__ void build_words4_kernel(const uint8_t* __restrict__ codes, int64_t n, int m, int mp,
+                                    int64_t nquads, uint32_t* __restrict__ words) {
+  const int hp = mp / 2;
+  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (gid >= nquads * hp) return;
+  const int p = (int)(gid % hp);
+  const int64_t g = gid / hp;
+  uint32_t w = 0;
+  for (int i = 0; i < 4; ++i) {
+    const int64_t c = g * 4 + i;
+    if (c >= n) continue;
+    const int j0 = 2 * p, j1 = 2 * p + 1;
+    const uint32_t v0 = j0 < m ? (codes[c * m + j0] & 15u) : 0u;
+    const uint32_t v1 = j1 < m ? (codes[c * m + j1] & 15u) : 0u;
+    w |= v0 << (4 * i);
+    w |= v1 << (16 + 4 * i);
+  }
+  words[gid] = w;
+}
+
+__device__ __forceinline__ int code4_at(const pqs_db& db, const uint32_t* __restrict__ words, int64_t i,
+                                        int j) {
+  const int hp = db.mp / 2;
+  const uint32_t w = words[(i >> 2) * hp + (j >> 1)];
+  const uint32_t sel = (j & 1) ? (w >> 16) : (w & 0xFFFFu);
+  return (int)((sel >> (4 * (i & 3))) & 15u);
+}
+
+// fastscan.py:48-57 in fp64: 127 at or above qmax, else floor((v-qmin)*scale)
+// clamped to [0, 126]; 0 everywhere when the span is empty.
+__device__ __forceinline__ uint8_t quantize1(double v, double qmin, double qmax, double scale) {
+  if (scale == 0.0) return 0;
+  if (v >= qmax) return 127;
+  double f = floor(__dmul_rn(__dsub_rn(v, qmin), scale));
+  f = f < 0.0 ? 0.0 : (f > 126.0 ? 126.0 : f);
+  return (uint8_t)f;
+}
+
+__global__ void quantize_kernel(const double* __restrict__ v, int64_t n, double qmin, double qmax, double scale,
+                                uint8_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = quantize1(v[i], qmin, qmax, scale);
+}
+
+// ---------------------------------------------------------------- K9 params
+// One CTA per query.  qmin = global fp32 table min; qmax = r-th smallest fp64
+// ADC over the first n_init codes in storage order (max if n_init < r);
+// qmax = max(qmax, qmin); quantize with fp64 scale = 127/span (0 if span==0).
+struct ParamShared {
+  unsigned int hist[256];
+  unsigned long long red[SCAN4_THREADS / 32];
+  float fred[SCAN4_THREADS / 32];
+  unsigned long long prefix, k, vmin, vmax;
+  double qmin, qmax;
+};
+
+__device__ __forceinline__ bool match_above4(uint64_t v, uint64_t prefix, int s) {
+  return s >= 64 ? true : ((v ^ prefix) >> s) == 0;
+}
+
+// k-th smallest (0-based) of M keys in keys[] (block-wide), small helper
+__device__ unsigned long long kth_smallest(const unsigned long long* keys, int64_t M, unsigned long long k,
+                                           ParamShared& sh) {
+  // min / max
+  unsigned long long lo = ~0ull, hi = 0;
+  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+    lo = min(lo, keys[i]);
+    hi = max(hi, keys[i]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) sh.red[threadIdx.x >> 5] = lo;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long a = ~0ull;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) a = min(a, sh.red[i]);
+    sh.vmin = a;
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh.red[threadIdx.x >> 5] = hi;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long b = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) b = max(b, sh.red[i]);
+    sh.vmax = b;
+  }
+  __syncthreads();
+  const unsigned long long vmin = sh.vmin, vmax = sh.vmax;
+  if (vmin == vmax) return vmin;
+  const int hib = 63 - __clzll((long long)(vmin ^ vmax));
+  int shift = (hib / 8) * 8;
+  if (threadIdx.x == 0) {
+    const int s = shift + 8;
+    sh.prefix = s >= 64 ? 0ull : (vmin >> s) << s;
+    sh.k = k;
+  }
+  __syncthreads();
+  for (; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sh.hist[i] = 0;
+    __syncthreads();
+    const unsigned long long prefix = sh.prefix;
+    for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+      const unsigned long long v = keys[i];
+      if (match_above4(v, prefix, shift + 8)) atomicAdd(&sh.hist[(v >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long c = 0, kk = sh.k;
+      int d = 0;
+      for (; d < 256; ++d) {
+        if (kk < c + sh.hist[d]) break;
+        c += sh.hist[d];
+      }
+      sh.k = kk - c;
+      sh.prefix = prefix | ((unsigned long long)d << shift);
+    }
+    __syncthreads();
+  }
+  return sh.prefix;
+}
+
+__global__ void __launch_bounds__(SCAN4_THREADS) qadc_params_kernel(
+    pqs_db db, const float* __restrict__ tables, int64_t nq, int init_count, int r,
+    unsigned long long* __restrict__ gscratch, int64_t gscratch_ld, uint8_t* __restrict__ qt_out,
+    double* __restrict__ qmm_out) {
+  __shared__ ParamShared sh;
+  __shared__ unsigned long long s_keys[2048];
+  const int64_t q = blockIdx.x;
+  const int m = db.m;
+  const float* T = tables + q * (int64_t)m * 16;
+  // qmin
+  float mn = __int_as_float(0x7f800000);
+  for (int i = threadIdx.x; i < m * 16; i += blockDim.x) mn = fminf(mn, T[i]);
+  for (int o = 16; o > 0; o >>= 1) mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  if ((threadIdx.x & 31) == 0) sh.fred[threadIdx.x >> 5] = mn;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float a = sh.fred[0];
+    for (int i = 1; i < (int)(blockDim.x >> 5); ++i) a = fminf(a, sh.fred[i]);
+    sh.qmin = (double)a;
+  }
+  __syncthreads();
+  // prefix distances
+  const int64_t n_src = db.prefix ? db.n_prefix : db.n;
+  const int64_t n_init = min((int64_t)init_count, n_src);
+  unsigned long long* keys = n_init <= 2048 ? s_keys : gscratch + q * gscratch_ld;
+  for (int64_t i = threadIdx.x; i < n_init; i += blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < m; ++j) {
+      const int c = db.prefix ? db.prefix[i * m + j] : code4_at(db, db.words4, i, j);
+      acc = __dadd_rn(acc, (double)T[j * 16 + c]);
+    }
+    keys[i] = dkey(acc);
+  }
+  __syncthreads();
+  double qmax;
+  if (n_init >= r) {
+    qmax = dkey_inv(kth_smallest(keys, n_init, (unsigned long long)(r - 1), sh));
+  } else {
+    qmax = dkey_inv(kth_smallest(keys, n_init, (unsigned long long)(n_init - 1), sh));
+  }
+  const double qmin = sh.qmin;
+  qmax = qmax > qmin ? qmax : qmin;
+  const double span = __dsub_rn(qmax, qmin);
+  const double scale = span > 0.0 ? __ddiv_rn(127.0, span) : 0.0;
+  for (int i = threadIdx.x; i < m * 16; i += blockDim.x)
+    qt_out[q * (int64_t)m * 16 + i] = quantize1((double)T[i], qmin, qmax, scale);
+  if (threadIdx.x == 0) {
+    qmm_out[2 * q] = qmin;
+    qmm_out[2 * q + 1] = qmax;
+  }
+}
+
+// ---------------------------------------------------------------- K4 scan
+enum { MODE_DENSE = 0, MODE_FILTER = 1 };
+
+struct Scan4Args {
+  const uint32_t* words;
+  int64_t n;
+  int m;
+  const uint8_t* qt;       // (nq, m, 16)
+  int64_t nq;
+  // virtual tiles: tile(i) = tile_off + i * tile_step, i in [0, nvt)
+  int64_t nvt, tile_off, tile_step, per_cta;
+  // dense
+  uint8_t* out;
+  int64_t ld;
+  // filter
+  const uint8_t* theta;
+  uint64_t* cand;
+  int* cand_cnt;
+  int64_t cap;
+};
+
+template <int MP>
+__device__ __forceinline__ void load_tile_raw(const uint32_t* __restrict__ words, int64_t tile, uint4* regs,
+                                              int nthreads) {
+  constexpr int HP = MP / 2;
+  constexpr int WORDS = QUADS4 * HP;            // words per tile
+  constexpr int V4 = WORDS / 4;                 // uint4 per tile
+  const uint4* src = reinterpret_cast<const uint4*>(words + tile * (int64_t)WORDS);
+  constexpr int PER = (V4 + SCAN4_THREADS - 1) / SCAN4_THREADS;
+#pragma unroll
+  for (int v = 0; v < PER; ++v) {
+    const int i = threadIdx.x + v * nthreads;
+    if (i < V4) regs[v] = __ldg(src + i);
+  }
+}
+
+template <int MP>
+__device__ __forceinline__ void store_tile_pred(const uint4* regs, uint4* __restrict__ buf, int nthreads) {
+  constexpr int HP = MP / 2;
+  constexpr int WORDS = QUADS4 * HP;
+  constexpr int V4 = WORDS / 4;
+  constexpr int PER = (V4 + SCAN4_THREADS - 1) / SCAN4_THREADS;
+#pragma unroll
+  for (int v = 0; v < PER; ++v) {
+    const int i = threadIdx.x + v * nthreads;
+    if (i < V4) {
+      const uint32_t w4[4] = {regs[v].x, regs[v].y, regs[v].z, regs[v].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t w = w4[e];
+        const uint32_t x = w ^ 0x88888888u;
+        buf[i * 4 + e] = make_uint4(w, x, w >> 16, x >> 16);
+      }
+    }
+  }
+}
+
+template <int MP, int MODE>
+__global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kernel(Scan4Args a) {
+  constexpr int HP = MP / 2;
+  constexpr int WORDS = QUADS4 * HP;
+  constexpr int V4 = WORDS / 4;
+  constexpr int PER = (V4 + SCAN4_THREADS - 1) / SCAN4_THREADS;
+  extern __shared__ __align__(16) uint4 s_pred[];  // 2 buffers of WORDS uint4
+  const int nthreads = blockDim.x;
+
+  const int64_t q = blockIdx.y * (int64_t)blockDim.x + threadIdx.x;
+  const bool qvalid = q < a.nq;
+
+  // query tables -> registers (components >= m are zero)
+  uint32_t T[MP][4];
+#pragma unroll
+  for (int j = 0; j < MP; ++j) {
+    if (qvalid && j < a.m) {
+      const uint4 t = __ldg(reinterpret_cast<const uint4*>(a.qt + (q * a.m + j) * 16));
+      T[j][0] = t.x;
+      T[j][1] = t.y;
+      T[j][2] = t.z;
+      T[j][3] = t.w;
+    } else {
+      T[j][0] = T[j][1] = T[j][2] = T[j][3] = 0u;
+    }
+  }
+  uint32_t theta = 0;
+  if (MODE == MODE_FILTER) theta = qvalid ? a.theta[q] : 0u;
+  const uint32_t bias = (0x7FFFu - theta) * 0x00010001u;
+
+  const int64_t i0 = blockIdx.x * a.per_cta;
+  const int64_t i1 = min(i0 + a.per_cta, a.nvt);
+  if (i0 >= i1) return;
+
+  uint4 regs[PER];
+  load_tile_raw<MP>(a.words, a.tile_off + i0 * a.tile_step, regs, nthreads);
+  store_tile_pred<MP>(regs, s_pred, nthreads);
+  __syncthreads();
+
+  int cur = 0;
+  for (int64_t i = i0; i < i1; ++i) {
+    const bool has_next = (i + 1 < i1);
+    if (has_next) load_tile_raw<MP>(a.words, a.tile_off + (i + 1) * a.tile_step, regs, nthreads);
+    const uint4* buf = s_pred + cur * WORDS;
+    const int64_t tile = a.tile_off + i * a.tile_step;
+    const int64_t code0 = tile * TILE4;
+#pragma unroll 2
+    for (int g = 0; g < QUADS4; ++g) {
+      uint32_t ae = 0, ao = 0;
+#pragma unroll
+      for (int p = 0; p < HP; ++p) {
+        const uint4 s = buf[g * HP + p];
+        const uint32_t lo0 = prmt(T[2 * p][0], T[2 * p][1], s.x);
+        const uint32_t hi0 = prmt(T[2 * p][2], T[2 * p][3], s.y);
+        const uint32_t lo1 = prmt(T[2 * p + 1][0], T[2 * p + 1][1], s.z);
+        const uint32_t hi1 = prmt(T[2 * p + 1][2], T[2 * p + 1][3], s.w);
+        const uint32_t v = lo0 + hi0 + lo1 + hi1;
+        ae += v & 0x00FF00FFu;
+        ao += (v >> 8) & 0x00FF00FFu;
+      }
+      const int64_t c = code0 + 4 * g;
+      if (MODE == MODE_FILTER) {
+        const uint32_t t = (ae + bias) & (ao + bias) & 0x80008000u;
+        if (t != 0x80008000u && qvalid) {
+          const uint32_t S[4] = {ae & 0xFFFFu, ao & 0xFFFFu, ae >> 16, ao >> 16};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if (S[e] <= theta && c + e < a.n) {
+              const int pos = atomicAdd(a.cand_cnt + q, 1);
+              if (pos < a.cap)
+                a.cand[q * a.cap + pos] = ((uint64_t)S[e] << 32) | (uint64_t)(uint32_t)(c + e);
+            }
+          }
+        }
+      } else {
+        if (qvalid) {
+          const uint32_t S[4] = {ae & 0xFFFFu, ao & 0xFFFFu, ae >> 16, ao >> 16};
+          const int64_t col = i * TILE4 + 4 * g;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t b = S[e] < 127u ? S[e] : 127u;
+            if (col + e < a.ld) a.out[q * a.ld + col + e] = (c + e < a.n) ? (uint8_t)b : (uint8_t)255;
+          }
+        }
+      }
+    }
+    if (has_next) {
+      store_tile_pred<MP>(regs, s_pred + (cur ^ 1) * WORDS, nthreads);
+      cur ^= 1;
+    }
+    __syncthreads();
+  }
+}
+
+template <int MP, int MODE>
+int launch_scan4_t(pqs_ctx* ctx, Scan4Args a, int64_t nq) {
+  constexpr int HP = MP / 2;
+  const size_t smem = 2 * (size_t)QUADS4 * HP * sizeof(uint4);
+  PQS_CUDA(ctx, cudaFuncSetAttribute(scan4_kernel<MP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+  const int threads = SCAN4_THREADS;  // the tile loader assumes a full CTA
+  const int64_t qgroups = cdiv(nq, threads);
+  // split the tiles so that the grid covers the SMs a few times over
+  const int64_t target = (int64_t)ctx->sm_count * 2 * 4;
+  int64_t splits = std::max<int64_t>(1, cdiv(target, qgroups));
+  splits = std::min<int64_t>(splits, a.nvt);
+  a.per_cta = cdiv(a.nvt, splits);
+  splits = cdiv(a.nvt, a.per_cta);
+  if (splits <= 0) return PQS_OK;
+  dim3 grid((unsigned)splits, (unsigned)qgroups);
+  scan4_kernel<MP, MODE><<<grid, threads, smem, ctx->stream>>>(a);
+  PQS_LAUNCHED(ctx);
+  return PQS_OK;
+}
+
+template <int MODE>
+int launch_scan4(pqs_ctx* ctx, int mp, const Scan4Args& a, int64_t nq) {
+  switch (mp) {
+    case 2: return launch_scan4_t<2, MODE>(ctx, a, nq);
+    case 4: return launch_scan4_t<4, MODE>(ctx, a, nq);
+    case 8: return launch_scan4_t<8, MODE>(ctx, a, nq);
+    case 16: return launch_scan4_t<16, MODE>(ctx, a, nq);
+    case 32: return launch_scan4_t<32, MODE>(ctx, a, nq);
+  }
+  return set_err(ctx, PQS_ERR_UNSUPPORTED, "scan4: unsupported padded m");
+}
+
+// per-query threshold bin from the dense sample: r-th smallest valid bin
+__global__ void theta4_kernel(const uint8_t* __restrict__ sample, int64_t ns, int64_t nq, int r,
+                              uint8_t* __restrict__ theta) {
+  __shared__ unsigned int hist[128];
+  const int64_t q = blockIdx.x;
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
+    const uint8_t b = sample[q * ns + i];
+    if (b < 128) atomicAdd(&hist[b], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long c = 0;
+    int t = 127;
+    for (int b = 0; b < 128; ++b) {
+      c += hist[b];
+      if (c >= (unsigned long long)r) {
+        t = b;
+        break;
+      }
+    }
+    theta[q] = (uint8_t)t;
+  }
+}
+
+__global__ void fill_u8_kernel(uint8_t* p, int64_t n, uint8_t v) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+__global__ void gather_rows_u8_kernel(const uint8_t* __restrict__ src, const int* __restrict__ qmap, int64_t rows,
+                                      int64_t width, uint8_t* __restrict__ dst) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows * width) return;
+  const int64_t r = i / width, c = i % width;
+  dst[i] = src[(int64_t)qmap[r] * width + c];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+int build_db4(pqs_ctx* ctx, pqs_db* db, const uint8_t* d_codes) {
+  const int hp = db->mp / 2;
+  const int64_t nquads = db->ntiles * QUADS4;
+  const int64_t total = nquads * hp;
+  build_words4_kernel<<<(unsigned)cdiv(total, 256), 256, 0, ctx->stream>>>(d_codes, db->n, db->m, db->mp,
+                                                                           nquads, db->words4);
+  PQS_LAUNCHED(ctx);
+  return PQS_OK;
+}
+
+int launch_quantize(pqs_ctx* ctx, double qmin, double qmax, const double* d_v, int64_t n, uint8_t* d_out) {
+  if (n == 0) return PQS_OK;
+  const double span = qmax - qmin;
+  const double scale = span > 0.0 ? 127.0 / span : 0.0;
+  quantize_kernel<<<(unsigned)cdiv(n, 256), 256, 0, ctx->stream>>>(d_v, n, qmin, qmax, scale, d_out);
+  PQS_LAUNCHED(ctx);
+  return PQS_OK;
+}
+
+int launch_scan4_dense(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qtables, int64_t nq, uint8_t* d_out,
+                       int64_t ld_out) {
+  Scan4Args a{};
+  a.words = db->words4;
+  a.n = db->n;
+  a.m = db->m;
+  a.qt = d_qtables;
+  a.nq = nq;
+  a.nvt = db->ntiles;
+  a.tile_off = 0;
+  a.tile_step = 1;
+  a.out = d_out;
+  a.ld = ld_out;
+  return launch_scan4<MODE_DENSE>(ctx, db->mp, a, nq);
+}
+
+int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t nq, int init_count, int r,
+                  uint8_t* d_bins, int64_t* d_ids, int32_t* d_count, uint8_t* d_qt, double* d_qmm) {
+  const int64_t n = db->n;
+  const int m = db->m;
+  // ---- K9: params + quantized tables
+  const int64_t n_src = db->prefix ? db->n_prefix : n;
+  const int64_t n_init = std::min<int64_t>(init_count, n_src);
+  unsigned long long* pscratch = nullptr;
+  if (n_init > 2048) PQS_TRY(scratch(ctx, S_PREFIX, (size_t)(nq * n_init), &pscratch));
+  qadc_params_kernel<<<(unsigned)nq, SCAN4_THREADS, 0, ctx->stream>>>(*db, d_tables, nq, init_count, r, pscratch,
+                                                                     n_init, d_qt, d_qmm);
+  PQS_LAUNCHED(ctx);
+
+  // ---- threshold: exact when every code fits the candidate buffer
+  uint8_t* theta = nullptr;
+  PQS_TRY(scratch(ctx, S_THETA, (size_t)nq, &theta));
+  const int64_t cap = std::min<int64_t>(ctx->cand_cap, std::max<int64_t>(n, 1));
+  const int64_t r_eff = std::min<int64_t>(r, n);
+  if (n <= cap) {
+    fill_u8_kernel<<<(unsigned)cdiv(nq, 256), 256, 0, ctx->stream>>>(theta, nq, 127);
+    PQS_LAUNCHED(ctx);
+  } else {
+    // strided sample of whole tiles
+    int64_t st = std::max<int64_t>(cdiv(db->ntiles, ctx->sample_div), cdiv(16 * r_eff, TILE4));
+    st = std::min<int64_t>(st, db->ntiles);
+    const int64_t step = std::max<int64_t>(1, db->ntiles / st);
+    const int64_t ns = st * TILE4;
+    uint8_t* sample = nullptr;
+    PQS_TRY(scratch(ctx, S_SAMPLE, (size_t)(nq * ns), &sample));
+    Scan4Args a{};
+    a.words = db->words4;
+    a.n = n;
+    a.m = m;
+    a.qt = d_qt;
+    a.nq = nq;
+    a.nvt = st;
+    a.tile_off = 0;
+    a.tile_step = step;
+    a.out = sample;
+    a.ld = ns;
+    PQS_TRY(launch_scan4<MODE_DENSE>(ctx, db->mp, a, nq));
+    theta4_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(sample, ns, nq, (int)r_eff, theta);
+    PQS_LAUNCHED(ctx);
+  }
+
+  // ---- K4 filtered scan
+  uint64_t* cand = nullptr;
+  int* cnt = nullptr;
+  PQS_TRY(scratch(ctx, S_CAND, (size_t)(nq * cap), &cand));
+  PQS_TRY(scratch(ctx, S_CAND_CNT, (size_t)nq, &cnt));
+  PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nq, ctx->stream));
+  {
+    Scan4Args a{};
+    a.words = db->words4;
+    a.n = n;
+    a.m = m;
+    a.qt = d_qt;
+    a.nq = nq;
+    a.nvt = db->ntiles;
+    a.tile_off = 0;
+    a.tile_step = 1;
+    a.theta = theta;
+    a.cand = cand;
+    a.cand_cnt = cnt;
+    a.cap = cap;
+    PQS_TRY(launch_scan4<MODE_FILTER>(ctx, db->mp, a, nq));
+  }
+  ctx->last_evals = nq * n;
+
+  // ---- K5 select
+  uint64_t* gk = nullptr;
+  int64_t* gi = nullptr;
+  PQS_TRY(scratch(ctx, S_KEYS, (size_t)(nq * cap), &gk));
+  PQS_TRY(scratch(ctx, S_IDS, (size_t)(nq * cap), &gi));
+  SelArgs s{};
+  s.src = SEL_CAND_BIN;
+  s.nq = nq;
+  s.r = r;
+  s.cand = cand;
+  s.cand_cnt = cnt;
+  s.cap = cap;
+  s.ids = db->ids;
+  s.id_base = db->id_base;
+  s.out_b = d_bins;
+  s.out_i = d_ids;
+  s.out_c = d_count;
+  s.gkeys = gk;
+  s.gids = gi;
+  s.gcap = cap;
+  PQS_TRY(launch_select(ctx, s));
+
+  // ---- overflow check -> exact dense fallback for those queries
+  std::vector<int> hcnt(nq);
+  PQS_CUDA(ctx, cudaMemcpyAsync(hcnt.data(), cnt, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
+  PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  std::vector<int> over;
+  int64_t mx = 0;
+  for (int64_t q = 0; q < nq; ++q) {
+    mx = std::max<int64_t>(mx, hcnt[q]);
+    if (hcnt[q] > cap || hcnt[q] < r_eff || ctx->force_fallback) over.push_back((int)q);
+  }
+  ctx->last_max_cand = mx;
+  ctx->last_overflow = (int64_t)over.size();
+  if (!over.empty()) {
+    const int64_t B = std::max<int64_t>(1, std::min<int64_t>((int64_t)over.size(), (int64_t)(1ll << 30) / std::max<int64_t>(n, 1)));
+    int* d_qmap = nullptr;
+    uint8_t* qt_sub = nullptr;
+    uint8_t* dense = nullptr;
+    PQS_TRY(scratch(ctx, S_MISC, (size_t)over.size(), &d_qmap));
+    PQS_TRY(scratch(ctx, S_QTABLES, (size_t)(B * m * 16), &qt_sub));
+    PQS_TRY(scratch(ctx, S_DENSE, (size_t)(B * n), &dense));
+    PQS_CUDA(ctx, cudaMemcpyAsync(d_qmap, over.data(), sizeof(int) * over.size(), cudaMemcpyHostToDevice, ctx->stream));
+    for (int64_t b0 = 0; b0 < (int64_t)over.size(); b0 += B) {
+      const int64_t nb = std::min<int64_t>(B, (int64_t)over.size() - b0);
+      gather_rows_u8_kernel<<<(unsigned)cdiv(nb * m * 16, 256), 256, 0, ctx->stream>>>(d_qt, d_qmap + b0, nb,
+                                                                                     (int64_t)m * 16, qt_sub);
+      PQS_LAUNCHED(ctx);
+      PQS_TRY(launch_scan4_dense(ctx, db, qt_sub, nb, dense, n));
+      SelArgs f{};
+      f.src = SEL_DENSE_U8;
+      f.nq = nb;
+      f.r = r;
+      f.dense = dense;
+      f.n = n;
+      f.ids = db->ids;
+      f.id_base = db->id_base;
+      f.qmap = d_qmap + b0;
+      f.out_b = d_bins;
+      f.out_i = d_ids;
+      f.out_c = d_count;
+      PQS_TRY(launch_select(ctx, f));
+    }
+  }
+  return PQS_OK;
+}

@@ -1,0 +1,274 @@
+"""Device handles and the batched search API over libpqs.so.
+
+The reference (`pqscan`) searches one query per call; the GPU needs batches.
+These classes own device copies of a quantizer / code list / inverted index
+and search many queries per call.  Arrays may be numpy (host; copies happen
+inside the call) or CUDA torch tensors (device; zero-copy, same stream rules
+as the context).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import IO_DEVICE, IO_HOST, default_context, ptr
+
+
+def _is_device(x) -> bool:
+    return not isinstance(x, np.ndarray) and getattr(x, "is_cuda", False)
+
+
+def _io_of(*arrays) -> int:
+    dev = [_is_device(a) for a in arrays if a is not None]
+    if dev and all(dev):
+        return IO_DEVICE
+    if any(dev):
+        raise ValueError("mix of host and device arrays in one call")
+    return IO_HOST
+
+
+def _empty(shape, dtype, like):
+    if _is_device(like):
+        import torch
+
+        tmap = {np.float64: torch.float64, np.int64: torch.int64, np.int32: torch.int32,
+                np.uint8: torch.uint8, np.float32: torch.float32}
+        return torch.empty(shape, dtype=tmap[dtype], device=like.device)
+    return np.empty(shape, dtype=dtype)
+
+
+def _host_f32(a, ndim, what):
+    if _is_device(a):
+        if a.dtype.__str__() != "torch.float32" or not a.is_contiguous():
+            raise ValueError(f"{what} must be a contiguous float32 tensor")
+        if a.dim() != ndim:
+            raise ValueError(f"{what} must be {ndim}-D")
+        return a
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    if a.ndim != ndim:
+        raise ValueError(f"{what} must be {ndim}-D")
+    return a
+
+
+class DeviceQuantizer:
+    """pqs_pq: device copy of a ProductQuantizer's codebooks (no rotation)."""
+
+    def __init__(self, pq, ctx=None):
+        if pq.rotation is not None:
+            raise NotImplementedError("rotated (OPQ) quantizers are outside the device scan path")
+        if pq.b > 8:
+            raise NotImplementedError("device tables support b <= 8")
+        self.ctx = ctx or default_context()
+        self.m, self.b, self.d, self.k = pq.m, pq.b, pq.d, pq.k
+        books = np.ascontiguousarray(pq.codebooks, dtype=np.float32)
+        h = ctypes.c_void_p()
+        self.ctx.check(self.ctx.lib.pqs_pq_create(self.ctx.handle, pq.m, pq.b, pq.d, ptr(books), ctypes.byref(h)),
+                       "pq_create")
+        self.handle = h
+
+    def compute_tables(self, queries):
+        """Batched compute_tables (scan.py:45-56): (nq, d) -> (nq, m, k) fp32."""
+        q = _host_f32(queries, 2, "queries")
+        if q.shape[1] != self.d:
+            raise ValueError(f"queries must have shape (nq, {self.d})")
+        out = _empty((q.shape[0], self.m, self.k), np.float32, q)
+        self.ctx.check(self.ctx.lib.pqs_compute_tables(self.ctx.handle, self.handle, ptr(q), q.shape[0], ptr(out),
+                                                       _io_of(q, out)), "compute_tables")
+        return out
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self.ctx.lib.pqs_pq_destroy(self.handle)
+        except Exception:
+            pass
+
+
+class DeviceCodes:
+    """pqs_db: a device-resident code list (b=8 float ADC or b=4 Quick ADC)."""
+
+    def __init__(self, codes, b: int, ids=None, id_base: int = 0, ctx=None):
+        self.ctx = ctx or default_context()
+        codes = np.asarray(codes)
+        if codes.ndim != 2:
+            raise ValueError("codes must be 2-D (n, m)")
+        if codes.size and int(codes.max()) > 255:
+            raise NotImplementedError("device code lists hold components < 256")
+        codes = np.ascontiguousarray(codes, dtype=np.uint8)
+        self.n, self.m, self.b = codes.shape[0], codes.shape[1], b
+        ids_arr = None if ids is None else np.ascontiguousarray(ids, dtype=np.int64)
+        h = ctypes.c_void_p()
+        self.ctx.check(self.ctx.lib.pqs_db_create(self.ctx.handle, ptr(codes), self.n, self.m, b, ptr(ids_arr),
+                                                  int(id_base), ctypes.byref(h)), "db_create")
+        self.handle = h
+
+    def set_prefix(self, prefix_codes):
+        """Global Quick ADC prefix for a shard (quickadc.py:130-137)."""
+        p = np.ascontiguousarray(prefix_codes, dtype=np.uint8)
+        self.ctx.check(self.ctx.lib.pqs_db_set_prefix(self.ctx.handle, self.handle, ptr(p), p.shape[0]), "set_prefix")
+
+    # -- float ADC (b=8) --------------------------------------------------
+    def scan_distances(self, tables):
+        t = _host_f32(tables, 3, "tables")
+        out = _empty((t.shape[0], self.n), np.float64, t)
+        self.ctx.check(self.ctx.lib.pqs_scan_distances(self.ctx.handle, self.handle, ptr(t), t.shape[0], t.shape[2],
+                                                       ptr(out), _io_of(t, out)), "scan_distances")
+        return out
+
+    def adc_scan(self, tables, r: int):
+        """scan() for a batch of tables (nq, m, k) -> (dist, ids, count)."""
+        t = _host_f32(tables, 3, "tables")
+        if t.shape[1] != self.m:
+            raise ValueError(f"codes must have shape (n, {t.shape[1]})")
+        nq = t.shape[0]
+        d = _empty((nq, r), np.float64, t)
+        i = _empty((nq, r), np.int64, t)
+        c = _empty((nq,), np.int32, t)
+        self.ctx.check(self.ctx.lib.pqs_adc_scan(self.ctx.handle, self.handle, ptr(t), nq, t.shape[2], int(r), ptr(d),
+                                                 ptr(i), ptr(c), _io_of(t, d)), "adc_scan")
+        return d, i, c
+
+    def adc_search(self, dq: DeviceQuantizer, queries, r: int):
+        """Batched compute_tables + scan: (nq, d) queries -> (dist, ids, count)."""
+        q = _host_f32(queries, 2, "queries")
+        nq = q.shape[0]
+        d = _empty((nq, r), np.float64, q)
+        i = _empty((nq, r), np.int64, q)
+        c = _empty((nq,), np.int32, q)
+        self.ctx.check(self.ctx.lib.pqs_adc_search(self.ctx.handle, self.handle, dq.handle, ptr(q), nq, int(r), ptr(d),
+                                                   ptr(i), ptr(c), _io_of(q, d)), "adc_search")
+        return d, i, c
+
+    # -- Quick ADC (b=4) ---------------------------------------------------
+    def qadc_scan(self, tables, init_count: int, r: int):
+        """qadc_scan for a batch of tables (nq, m, 16) ->
+        (bins uint8, ids, count, qtables (nq,m,16) uint8, qminmax (nq,2))."""
+        t = _host_f32(tables, 3, "tables")
+        if t.shape[2] != 16 or t.shape[1] != self.m:
+            raise ValueError("tables do not match the code list shape")
+        nq = t.shape[0]
+        bins = _empty((nq, r), np.uint8, t)
+        i = _empty((nq, r), np.int64, t)
+        c = _empty((nq,), np.int32, t)
+        qt = _empty((nq, self.m, 16), np.uint8, t)
+        qmm = _empty((nq, 2), np.float64, t)
+        self.ctx.check(self.ctx.lib.pqs_qadc_scan(self.ctx.handle, self.handle, ptr(t), nq, int(init_count), int(r),
+                                                  ptr(bins), ptr(i), ptr(c), ptr(qt), ptr(qmm), _io_of(t, bins)),
+                       "qadc_scan")
+        return bins, i, c, qt, qmm
+
+    def qadc_search(self, dq: DeviceQuantizer, queries, init_count: int, r: int, want_tables: bool = False):
+        q = _host_f32(queries, 2, "queries")
+        nq = q.shape[0]
+        bins = _empty((nq, r), np.uint8, q)
+        i = _empty((nq, r), np.int64, q)
+        c = _empty((nq,), np.int32, q)
+        qt = _empty((nq, self.m, 16), np.uint8, q) if want_tables else None
+        qmm = _empty((nq, 2), np.float64, q) if want_tables else None
+        self.ctx.check(self.ctx.lib.pqs_qadc_search(self.ctx.handle, self.handle, dq.handle, ptr(q), nq,
+                                                    int(init_count), int(r), ptr(bins), ptr(i), ptr(c), ptr(qt),
+                                                    ptr(qmm), _io_of(q, bins)), "qadc_search")
+        return bins, i, c, qt, qmm
+
+    def quantized_distances(self, qtables):
+        qt = qtables if _is_device(qtables) else np.ascontiguousarray(qtables, dtype=np.uint8)
+        if qt.ndim != 3 or qt.shape[1] != self.m or qt.shape[2] != 16:
+            raise ValueError(f"codes must have shape (n, {qt.shape[1]})")
+        out = _empty((qt.shape[0], self.n), np.uint8, qt)
+        self.ctx.check(self.ctx.lib.pqs_quantized_distances(self.ctx.handle, self.handle, ptr(qt), qt.shape[0],
+                                                            ptr(out), _io_of(qt, out)), "quantized_distances")
+        return out
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self.ctx.lib.pqs_db_destroy(self.handle)
+        except Exception:
+            pass
+
+
+class DeviceIvf:
+    """pqs_ivf: device-resident IVFADC index (coarse + residual PQ + lists)."""
+
+    def __init__(self, index, ctx=None):
+        self.ctx = ctx or default_context()
+        self.dq = DeviceQuantizer(index.pq, self.ctx)
+        sizes = np.array([lst.n for lst in index.lists], dtype=np.int64)
+        m = index.pq.m
+        if sizes.sum():
+            codes = np.ascontiguousarray(np.concatenate([np.asarray(l.codes).reshape(-1, m) for l in index.lists]),
+                                         dtype=np.uint8)
+            ids = np.ascontiguousarray(np.concatenate([l.ids for l in index.lists]), dtype=np.int64)
+        else:
+            codes = np.zeros((0, m), np.uint8)
+            ids = np.zeros(0, np.int64)
+        coarse = np.ascontiguousarray(index.coarse, dtype=np.float32)
+        self.K, self.d = coarse.shape
+        h = ctypes.c_void_p()
+        self.ctx.check(self.ctx.lib.pqs_ivf_create(self.ctx.handle, self.dq.handle, ptr(coarse), self.K, ptr(sizes),
+                                                   ptr(codes), ptr(ids), ctypes.byref(h)), "ivf_create")
+        self.handle = h
+
+    def probe(self, queries, ma: int):
+        q = _host_f32(queries, 2, "queries")
+        nq = q.shape[0]
+        cells = _empty((nq, ma), np.int64, q)
+        dist = _empty((nq, ma), np.float64, q)
+        self.ctx.check(self.ctx.lib.pqs_ivf_probe(self.ctx.handle, self.handle, ptr(q), nq, int(ma), ptr(cells),
+                                                  ptr(dist), _io_of(q, cells)), "ivf_probe")
+        return cells, dist
+
+    def search(self, queries, ma: int, r: int):
+        q = _host_f32(queries, 2, "queries")
+        if q.shape[1] != self.d:
+            raise ValueError(f"query must have shape ({self.d},)")
+        nq = q.shape[0]
+        d = _empty((nq, r), np.float64, q)
+        i = _empty((nq, r), np.int64, q)
+        c = _empty((nq,), np.int32, q)
+        self.ctx.check(self.ctx.lib.pqs_ivf_search(self.ctx.handle, self.handle, ptr(q), nq, int(ma), int(r), ptr(d),
+                                                   ptr(i), ptr(c), _io_of(q, d)), "ivf_search")
+        return d, i, c
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self.ctx.lib.pqs_ivf_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def merge_topr(dists, ids, counts, r: int, ctx=None):
+    """Top-r of G per-shard lists by (distance, id): dists/ids (G, nq, r_in),
+    counts (G, nq) -> (dist (nq, r), ids, count)."""
+    ctx = ctx or default_context()
+    if _is_device(dists):
+        G, nq, r_in = dists.shape
+    else:
+        dists = np.ascontiguousarray(dists, dtype=np.float64)
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        counts = np.ascontiguousarray(counts, dtype=np.int32)
+        G, nq, r_in = dists.shape
+    od = _empty((nq, r), np.float64, dists)
+    oi = _empty((nq, r), np.int64, dists)
+    oc = _empty((nq,), np.int32, dists)
+    ctx.check(ctx.lib.pqs_merge_topr(ctx.handle, G, ptr(dists), ptr(ids), ptr(counts), nq, r_in, int(r), ptr(od),
+                                     ptr(oi), ptr(oc), _io_of(dists, od)), "merge_topr")
+    return od, oi, oc
+
+
+def quantize_device(qmin: float, qmax: float, values, ctx=None):
+    """fastscan.quantize (fastscan.py:48-57) on the GPU, fp64."""
+    ctx = ctx or default_context()
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    flat = v.reshape(-1)
+    out = np.empty(flat.shape, dtype=np.uint8)
+    ctx.check(ctx.lib.pqs_quantize(ctx.handle, float(qmin), float(qmax), ptr(flat), flat.shape[0], ptr(out), IO_HOST),
+              "quantize")
+    return out.reshape(v.shape)
+
+
+__all__ = ["DeviceQuantizer", "DeviceCodes", "DeviceIvf", "merge_topr", "quantize_device", "_lib"]

@@ -1,0 +1,63 @@
+"""Drop-in for `pqscan.ivf.query_ivf` (ivf.py:148-196), kernel='adc', on the GPU.
+
+Probes (nearest_k, _dist.py:42-67) and the list scans run in libpqs.so
+(K7 probe GEMM + exact fp64 re-score, K8 list-major filtered scan, K6 exact
+residual-table rerank, K5 select).  The index is uploaded once and cached on
+the IvfIndex object.  The 'quick-adc' and 'derived' kernels are outside the
+device scan path (not in any BASELINE config).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .engine import DeviceIvf
+from .types import IvfIndex, NeighborSet
+
+KERNELS = ("adc", "quick-adc", "derived")   # ivf.py:46
+DEFAULT_R2_SMALL = 9000                     # ivf.py:47
+DEFAULT_R2_LARGE = 120000                   # ivf.py:48
+
+
+def default_r2(r: int) -> int:
+    """ivf.py:51-53."""
+    return DEFAULT_R2_SMALL if r <= 100 else DEFAULT_R2_LARGE
+
+
+def device_index(index: IvfIndex) -> DeviceIvf:
+    key = (index.coarse.ctypes.data, index.coarse.shape, len(index.lists), index.n)
+    cached = index._device.get("ivf")
+    if cached is None or cached[0] != key:
+        cached = (key, DeviceIvf(index))
+        index._device["ivf"] = cached
+    return cached[1]
+
+
+def query_ivf(index: IvfIndex, query: np.ndarray, ma: int, r: int, kernel: str = "adc",
+              init_count: int = 200, r2: int | None = None) -> NeighborSet:
+    """ivf.py:148-196 with kernel='adc'."""
+    kernel = kernel.replace("_", "-")
+    if kernel not in KERNELS:
+        raise ValueError(f"kernel must be one of {KERNELS}")
+    if not 1 <= ma <= index.K:
+        raise ValueError(f"ma must be in [1, {index.K}]")
+    if r < 1:
+        raise ValueError("r must be >= 1")
+    if kernel == "quick-adc" and (index.pq.b != 4 or index.pq.m % 2):
+        raise ValueError("quick-adc kernel requires b=4 and even m")
+    if kernel == "derived" and index.dpq is None:
+        raise ValueError("index has no derived quantizer")
+    query = np.asarray(query, dtype=np.float64)
+    if query.shape != (index.d,):
+        raise ValueError(f"query must have shape ({index.d},)")
+    if kernel != "adc":
+        raise NotImplementedError(f"kernel={kernel!r} is outside the device ADC scan path")
+    dev = device_index(index)
+    d, i, c = dev.search(query.astype(np.float32)[None, :], int(ma), int(r))
+    n = int(c[0])
+    return NeighborSet.from_pairs(r, d[0, :n], i[0, :n])
+
+
+def query_ivf_batch(index: IvfIndex, queries: np.ndarray, ma: int, r: int):
+    """Batched query_ivf: (nq, d) -> (dist (nq, r), ids (nq, r), count (nq,))."""
+    return device_index(index).search(queries, int(ma), int(r))
