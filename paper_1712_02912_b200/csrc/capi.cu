@@ -49,6 +49,20 @@ int scratch_get(pqs_ctx* ctx, int slot, size_t bytes, void** out) {
   return PQS_OK;
 }
 
+int upload(pqs_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return PQS_OK;
+  PQS_CUDA(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
+  PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return PQS_OK;
+}
+
+int download(pqs_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return PQS_OK;
+  PQS_CUDA(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
+  PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return PQS_OK;
+}
+
 namespace {
 
 // input staging: device pointer as-is, host pointer copied into a scratch slot
@@ -199,7 +213,7 @@ int pqs_pq_create(pqs_ctx* ctx, int m, int b, int d, const float* codebooks, pqs
     delete pq;
     return set_err(ctx, PQS_ERR_NOMEM, "codebook allocation failed");
   }
-  PQS_CUDA(ctx, cudaMemcpy(pq->books, codebooks, bytes, cudaMemcpyHostToDevice));
+  PQS_TRY(upload(ctx, pq->books, codebooks, bytes));
   *out = pq;
   return PQS_OK;
 }
@@ -260,8 +274,8 @@ int pqs_db_create(pqs_ctx* ctx, const uint8_t* codes, int64_t n, int m, int b, c
       if (cudaMalloc(&db->words4, words * 4) != cudaSuccess) return fail(PQS_ERR_NOMEM, "code allocation failed");
       uint8_t* d_codes = nullptr;
       if (cudaMalloc(&d_codes, (size_t)n * m) != cudaSuccess) return fail(PQS_ERR_NOMEM, "staging allocation failed");
-      cudaMemcpy(d_codes, codes, (size_t)n * m, cudaMemcpyHostToDevice);
-      int s = build_db4(ctx, db, d_codes);
+      int s = upload(ctx, d_codes, codes, (size_t)n * m);
+      if (s == PQS_OK) s = build_db4(ctx, db, d_codes);
       cudaStreamSynchronize(ctx->stream);
       cudaFree(d_codes);
       if (s != PQS_OK) return fail(s, ctx->err.c_str());
@@ -269,8 +283,7 @@ int pqs_db_create(pqs_ctx* ctx, const uint8_t* codes, int64_t n, int m, int b, c
   }
   if (ids && n) {
     if (cudaMalloc(&db->ids, (size_t)n * 8) != cudaSuccess) return fail(PQS_ERR_NOMEM, "id allocation failed");
-    if (cudaMemcpy(db->ids, ids, (size_t)n * 8, cudaMemcpyHostToDevice) != cudaSuccess)
-      return fail(PQS_ERR_CUDA, "id upload failed");
+    if (upload(ctx, db->ids, ids, (size_t)n * 8) != PQS_OK) return fail(PQS_ERR_CUDA, "id upload failed");
   }
   PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   *out = db;
@@ -285,7 +298,7 @@ int pqs_db_set_prefix(pqs_ctx* ctx, pqs_db* db, const uint8_t* prefix, int64_t n
   if (db->prefix) cudaFree(db->prefix);
   db->prefix = nullptr;
   PQS_CUDA(ctx, cudaMalloc(&db->prefix, (size_t)n_prefix * db->m));
-  PQS_CUDA(ctx, cudaMemcpy(db->prefix, prefix, (size_t)n_prefix * db->m, cudaMemcpyHostToDevice));
+  PQS_TRY(upload(ctx, db->prefix, prefix, (size_t)n_prefix * db->m));
   db->n_prefix = n_prefix;
   return PQS_OK;
 }

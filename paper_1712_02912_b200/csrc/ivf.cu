@@ -501,14 +501,14 @@ int ivf_create_impl(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t
     ivf_destroy_impl(iv);
     return set_err(ctx, PQS_ERR_NOMEM, "IVF allocation failed");
   }
-  PQS_CUDA(ctx, cudaMemcpy(iv->coarse, coarse, (size_t)K * d * 4, cudaMemcpyHostToDevice));
-  PQS_CUDA(ctx, cudaMemcpy(iv->books, pq->books, (size_t)pq->m * pq->k * pq->dsub * 4, cudaMemcpyDeviceToDevice));
-  PQS_CUDA(ctx, cudaMemcpy(iv->offsets, offs.data(), (size_t)(K + 1) * 8, cudaMemcpyHostToDevice));
+  PQS_TRY(upload(ctx, iv->coarse, coarse, (size_t)K * d * 4));
+  PQS_TRY(upload(ctx, iv->books, pq->books, (size_t)pq->m * pq->k * pq->dsub * 4));
+  PQS_TRY(upload(ctx, iv->offsets, offs.data(), (size_t)(K + 1) * 8));
   if (n) {
-    PQS_CUDA(ctx, cudaMemcpy(iv->codes, codes, (size_t)n * pq->m, cudaMemcpyHostToDevice));
-    PQS_CUDA(ctx, cudaMemcpy(iv->ids, ids, (size_t)n * 8, cudaMemcpyHostToDevice));
+    PQS_TRY(upload(ctx, iv->codes, codes, (size_t)n * pq->m));
+    PQS_TRY(upload(ctx, iv->ids, ids, (size_t)n * 8));
   }
-  PQS_CUDA(ctx, cudaMemset(iv->vmax, 0, 16));
+  PQS_CUDA(ctx, cudaMemsetAsync(iv->vmax, 0, 16, ctx->stream));
   cnorm_kernel<<<(unsigned)cdiv(K, 256), 256, 0, ctx->stream>>>(iv->coarse, K, d, iv->cnorm, iv->gnorm);
   PQS_LAUNCHED(ctx);
   v_kernel<<<(unsigned)K, 256, 0, ctx->stream>>>(iv->coarse, iv->books, iv->offsets, iv->codes, iv->m, iv->k, iv->dsub,
@@ -517,7 +517,7 @@ int ivf_create_impl(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t
   PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   // gmax on host
   std::vector<float> gn(K);
-  PQS_CUDA(ctx, cudaMemcpy(gn.data(), iv->gnorm, (size_t)K * 4, cudaMemcpyDeviceToHost));
+  PQS_TRY(download(ctx, gn.data(), iv->gnorm, (size_t)K * 4));
   float gm = 0.f;
   for (float v : gn) gm = std::max(gm, v);
   iv->gmax = gm;

@@ -143,6 +143,9 @@ int set_err(pqs_ctx* ctx, int code, const std::string& msg);
   } while (0)
 
 int scratch_get(pqs_ctx* ctx, int slot, size_t bytes, void** out);
+// host <-> device copies ordered on the context stream and completed on return
+int upload(pqs_ctx* ctx, void* dst, const void* src, size_t bytes);
+int download(pqs_ctx* ctx, void* dst, const void* src, size_t bytes);
 template <class T>
 inline int scratch(pqs_ctx* ctx, int slot, size_t count, T** out) {
   void* p = nullptr;
