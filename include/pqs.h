@@ -64,7 +64,9 @@ enum pqs_stat {
   PQS_STAT_LAUNCHES = 1,       /* kernels launched by this context since creation */
   PQS_STAT_LAST_MAX_CAND = 2,  /* largest per-query candidate count of the last search */
   PQS_STAT_LAST_OVERFLOW = 3,  /* queries that took the dense fallback in the last search */
-  PQS_STAT_LAST_EVALS = 4      /* (query, code) evaluations of the last search (IVF: exact count) */
+  PQS_STAT_LAST_EVALS = 4,     /* (query, code) evaluations of the last search (IVF: exact count) */
+  PQS_STAT_LAST_SCAN_NS = 5,   /* device time of the last search's main scan kernel (CUDA events) */
+  PQS_STAT_LAST_SCAN_LAUNCHES = 6 /* launches of that kernel in the last search */
 };
 
 int pqs_api_version(void);

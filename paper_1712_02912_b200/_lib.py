@@ -31,6 +31,8 @@ STAT_LAUNCHES = 1
 STAT_LAST_MAX_CAND = 2
 STAT_LAST_OVERFLOW = 3
 STAT_LAST_EVALS = 4
+STAT_LAST_SCAN_NS = 5
+STAT_LAST_SCAN_LAUNCHES = 6
 
 _p = ctypes.c_void_p
 _i = ctypes.c_int

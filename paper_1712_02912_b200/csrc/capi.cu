@@ -49,6 +49,27 @@ int scratch_get(pqs_ctx* ctx, int slot, size_t bytes, void** out) {
   return PQS_OK;
 }
 
+int scan_timer_begin(pqs_ctx* ctx) {
+  if (!ctx->scan_ev[0]) {
+    PQS_CUDA(ctx, cudaEventCreate(&ctx->scan_ev[0]));
+    PQS_CUDA(ctx, cudaEventCreate(&ctx->scan_ev[1]));
+  }
+  PQS_CUDA(ctx, cudaEventRecord(ctx->scan_ev[0], ctx->stream));
+  return PQS_OK;
+}
+
+int scan_timer_end(pqs_ctx* ctx) {
+  PQS_CUDA(ctx, cudaEventRecord(ctx->scan_ev[1], ctx->stream));
+  return PQS_OK;
+}
+
+int scan_timer_collect(pqs_ctx* ctx) {
+  float ms = 0.f;
+  PQS_CUDA(ctx, cudaEventElapsedTime(&ms, ctx->scan_ev[0], ctx->scan_ev[1]));
+  ctx->last_scan_ns = (int64_t)((double)ms * 1e6);
+  return PQS_OK;
+}
+
 int upload(pqs_ctx* ctx, void* dst, const void* src, size_t bytes) {
   if (bytes == 0) return PQS_OK;
   PQS_CUDA(ctx, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->stream));
@@ -148,6 +169,8 @@ void pqs_ctx_destroy(pqs_ctx* ctx) {
   for (auto& s : ctx->scratch)
     if (s.p) cudaFree(s.p);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  for (auto& e : ctx->scan_ev)
+    if (e) cudaEventDestroy(e);
   delete ctx;
 }
 
@@ -188,6 +211,8 @@ int pqs_ctx_get_stat(pqs_ctx* ctx, int stat, int64_t* out) {
     case PQS_STAT_LAST_MAX_CAND: *out = ctx->last_max_cand; return PQS_OK;
     case PQS_STAT_LAST_OVERFLOW: *out = ctx->last_overflow; return PQS_OK;
     case PQS_STAT_LAST_EVALS: *out = ctx->last_evals; return PQS_OK;
+    case PQS_STAT_LAST_SCAN_NS: *out = ctx->last_scan_ns; return PQS_OK;
+    case PQS_STAT_LAST_SCAN_LAUNCHES: *out = ctx->last_scan_launches; return PQS_OK;
   }
   return set_err(ctx, PQS_ERR_INVALID, "unknown stat");
 }

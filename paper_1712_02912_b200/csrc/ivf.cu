@@ -650,9 +650,12 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
   const int LIST_CHUNK = std::max(64, std::min(4096, 65536 / m));
   const size_t lsm = usm + ((size_t)LIST_CHUNK * m + 15) / 16 * 16 + (size_t)LIST_CHUNK * 4;
   PQS_CUDA(ctx, cudaFuncSetAttribute(ivf_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+  PQS_TRY(scan_timer_begin(ctx));
   ivf_list_kernel<<<(unsigned)K, 256, lsm, ctx->stream>>>(U, starts, pq_, pa, iv->offsets, iv->codes, iv->vtab, m, k,
                                                          theta, cand, cnt, cap, LIST_CHUNK);
   PQS_LAUNCHED(ctx);
+  PQS_TRY(scan_timer_end(ctx));
+  ctx->last_scan_launches = 1;
   // exact rerank + select
   uint64_t* gk = nullptr;
   int64_t* gi = nullptr;
@@ -687,6 +690,7 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
   PQS_CUDA(ctx, cudaMemcpyAsync(hcnt.data(), cnt, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
   PQS_CUDA(ctx, cudaMemcpyAsync(hcells.data(), cells, sizeof(int64_t) * nq * ma, cudaMemcpyDeviceToHost, ctx->stream));
   PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  PQS_TRY(scan_timer_collect(ctx));
   std::vector<int> over;
   int64_t mx = 0, total_evals = 0, worst_total = 0;
   for (int64_t q = 0; q < nq; ++q) {

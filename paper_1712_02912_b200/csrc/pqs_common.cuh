@@ -69,6 +69,9 @@ struct pqs_ctx {
   int64_t last_max_cand = 0;
   int64_t last_overflow = 0;
   int64_t last_evals = 0;
+  int64_t last_scan_ns = 0;
+  int64_t last_scan_launches = 0;
+  cudaEvent_t scan_ev[2] = {nullptr, nullptr};
   Scratch scratch[S_NSLOTS];
   int* host_flag = nullptr;  // pinned
 };
@@ -143,6 +146,10 @@ int set_err(pqs_ctx* ctx, int code, const std::string& msg);
   } while (0)
 
 int scratch_get(pqs_ctx* ctx, int slot, size_t bytes, void** out);
+// CUDA events around the main scan kernel of a search (PQS_STAT_LAST_SCAN_NS)
+int scan_timer_begin(pqs_ctx* ctx);
+int scan_timer_end(pqs_ctx* ctx);
+int scan_timer_collect(pqs_ctx* ctx);  // after a stream sync
 // host <-> device copies ordered on the context stream and completed on return
 int upload(pqs_ctx* ctx, void* dst, const void* src, size_t bytes);
 int download(pqs_ctx* ctx, void* dst, const void* src, size_t bytes);

@@ -442,7 +442,10 @@ int run_adc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t 
     a.cand = cand;
     a.cand_cnt = cnt;
     a.cap = cap;
+    PQS_TRY(scan_timer_begin(ctx));
     PQS_TRY(launch_scan8<MODE8_FILTER>(ctx, a));
+    PQS_TRY(scan_timer_end(ctx));
+    ctx->last_scan_launches = 1;
   }
   ctx->last_evals = nq * n;
 
@@ -474,6 +477,7 @@ int run_adc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t 
   std::vector<int> hcnt(nq);
   PQS_CUDA(ctx, cudaMemcpyAsync(hcnt.data(), cnt, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
   PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  PQS_TRY(scan_timer_collect(ctx));
   std::vector<int> over;
   int64_t mx = 0;
   for (int64_t q = 0; q < nq; ++q) {
