@@ -31,6 +31,21 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
   return d;
 }
 
+// FMA-pipe integer ops.  The multiplier comes from a kernel argument (runtime
+// value 1 or 2^24) so ptxas cannot strength-reduce them into ALU-pipe
+// IADD3/SHF: the PRMT lookups keep the ALU pipe busy, the byte-lane sums and
+// the widening shift run on the otherwise idle FMA pipe (IMAD / IMAD.HI).
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t imulhi(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
 // ---------------------------------------------------------------- K2 layout
 // codes (n, m) row-major -> words[(tile*QUADS4 + g) * (mp/2) + p]
 __global__ void build_words4_kernel(const uint8_t* __restrict__ codes, int64_t n, int m, int mp,
@@ -222,6 +237,9 @@ struct Scan4Args {
   // dense
   uint8_t* out;
   int64_t ld;
+  uint32_t one;            // runtime 1 (see imad)
+  uint32_t k24;            // runtime 2^24 (v >> 8 as a high multiply)
+  int tout;                // dense output transposed: u32 [col/4][nq] (4 packed bins)
   // filter
   const uint8_t* theta;
   uint64_t* cand;
@@ -265,14 +283,28 @@ __device__ __forceinline__ void store_tile_pred(const uint4* regs, uint4* __rest
   }
 }
 
+// Candidates are staged per thread in shared memory ([slot][thread], no
+// atomics) and flushed to the query's global list CSTAGE at a time with one
+// global atomicAdd, so the scan never waits on an atomic's return value.
+constexpr int CSTAGE = 16;
+
+__device__ __forceinline__ void flush_cands(const uint64_t* stage, int cnt, int64_t q, uint64_t* cand,
+                                            int* cand_cnt, int64_t cap) {
+  const int pos = atomicAdd(cand_cnt + q, cnt);
+  for (int i = 0; i < cnt; ++i)
+    if (pos + i < cap) cand[q * cap + pos + i] = stage[i * SCAN4_THREADS];
+}
+
 template <int MP, int MODE>
 __global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kernel(Scan4Args a) {
   constexpr int HP = MP / 2;
   constexpr int WORDS = QUADS4 * HP;
   constexpr int V4 = WORDS / 4;
   constexpr int PER = (V4 + SCAN4_THREADS - 1) / SCAN4_THREADS;
-  extern __shared__ __align__(16) uint4 s_pred[];  // 2 buffers of WORDS uint4
+  extern __shared__ __align__(16) uint4 s_pred[];  // 2 buffers of WORDS uint4 (+ candidate stage)
   const int nthreads = blockDim.x;
+  uint64_t* stage = reinterpret_cast<uint64_t*>(s_pred + 2 * WORDS) + threadIdx.x;
+  int ncand = 0;
 
   const int64_t q = blockIdx.y * (int64_t)blockDim.x + threadIdx.x;
   const bool qvalid = q < a.nq;
@@ -294,6 +326,7 @@ __global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kerne
   uint32_t theta = 0;
   if (MODE == MODE_FILTER) theta = qvalid ? a.theta[q] : 0u;
   const uint32_t bias = (0x7FFFu - theta) * 0x00010001u;
+  const uint32_t one = a.one, k24 = a.k24;
 
   const int64_t i0 = blockIdx.x * a.per_cta;
   const int64_t i1 = min(i0 + a.per_cta, a.nvt);
@@ -321,21 +354,24 @@ __global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kerne
         const uint32_t hi0 = prmt(T[2 * p][2], T[2 * p][3], s.y);
         const uint32_t lo1 = prmt(T[2 * p + 1][0], T[2 * p + 1][1], s.z);
         const uint32_t hi1 = prmt(T[2 * p + 1][2], T[2 * p + 1][3], s.w);
-        const uint32_t v = lo0 + hi0 + lo1 + hi1;
-        ae += v & 0x00FF00FFu;
-        ao += (v >> 8) & 0x00FF00FFu;
+        // two components per byte lane (each entry <= 127, sum <= 254)
+        const uint32_t v = imad(imad(lo0, one, hi0), one, imad(lo1, one, hi1));
+        ae = imad(v & 0x00FF00FFu, one, ae);
+        ao = imad(imulhi(v, k24) & 0x00FF00FFu, one, ao);
       }
       const int64_t c = code0 + 4 * g;
       if (MODE == MODE_FILTER) {
-        const uint32_t t = (ae + bias) & (ao + bias) & 0x80008000u;
+        const uint32_t t = imad(ae, one, bias) & imad(ao, one, bias) & 0x80008000u;
         if (t != 0x80008000u && qvalid) {
           const uint32_t S[4] = {ae & 0xFFFFu, ao & 0xFFFFu, ae >> 16, ao >> 16};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             if (S[e] <= theta && c + e < a.n) {
-              const int pos = atomicAdd(a.cand_cnt + q, 1);
-              if (pos < a.cap)
-                a.cand[q * a.cap + pos] = ((uint64_t)S[e] << 32) | (uint64_t)(uint32_t)(c + e);
+              stage[ncand * SCAN4_THREADS] = ((uint64_t)S[e] << 32) | (uint64_t)(uint32_t)(c + e);
+              if (++ncand == CSTAGE) {
+                flush_cands(stage, ncand, q, a.cand, a.cand_cnt, a.cap);
+                ncand = 0;
+              }
             }
           }
         }
@@ -343,10 +379,20 @@ __global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kerne
         if (qvalid) {
           const uint32_t S[4] = {ae & 0xFFFFu, ao & 0xFFFFu, ae >> 16, ao >> 16};
           const int64_t col = i * TILE4 + 4 * g;
+          if (a.tout) {
+            uint32_t packed = 0;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const uint32_t b = S[e] < 127u ? S[e] : 127u;
-            if (col + e < a.ld) a.out[q * a.ld + col + e] = (c + e < a.n) ? (uint8_t)b : (uint8_t)255;
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t b = (c + e < a.n) ? (S[e] < 127u ? S[e] : 127u) : 255u;
+              packed |= b << (8 * e);
+            }
+            reinterpret_cast<uint32_t*>(a.out)[(col >> 2) * a.nq + q] = packed;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t b = S[e] < 127u ? S[e] : 127u;
+              if (col + e < a.ld) a.out[q * a.ld + col + e] = (c + e < a.n) ? (uint8_t)b : (uint8_t)255;
+            }
           }
         }
       }
@@ -357,12 +403,14 @@ __global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kerne
     }
     __syncthreads();
   }
+  if (MODE == MODE_FILTER && ncand > 0) flush_cands(stage, ncand, q, a.cand, a.cand_cnt, a.cap);
 }
 
 template <int MP, int MODE>
 int launch_scan4_t(pqs_ctx* ctx, Scan4Args a, int64_t nq) {
   constexpr int HP = MP / 2;
-  const size_t smem = 2 * (size_t)QUADS4 * HP * sizeof(uint4);
+  const size_t smem = 2 * (size_t)QUADS4 * HP * sizeof(uint4) +
+                      (MODE == MODE_FILTER ? (size_t)CSTAGE * SCAN4_THREADS * sizeof(uint64_t) : 0);
   PQS_CUDA(ctx, cudaFuncSetAttribute(scan4_kernel<MP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
   const int threads = SCAN4_THREADS;  // the tile loader assumes a full CTA
@@ -374,6 +422,8 @@ int launch_scan4_t(pqs_ctx* ctx, Scan4Args a, int64_t nq) {
   a.per_cta = cdiv(a.nvt, splits);
   splits = cdiv(a.nvt, a.per_cta);
   if (splits <= 0) return PQS_OK;
+  a.one = 1u;
+  a.k24 = 1u << 24;
   dim3 grid((unsigned)splits, (unsigned)qgroups);
   scan4_kernel<MP, MODE><<<grid, threads, smem, ctx->stream>>>(a);
   PQS_LAUNCHED(ctx);
@@ -392,23 +442,31 @@ int launch_scan4(pqs_ctx* ctx, int mp, const Scan4Args& a, int64_t nq) {
   return set_err(ctx, PQS_ERR_UNSUPPORTED, "scan4: unsupported padded m");
 }
 
-// per-query threshold bin from the dense sample: r-th smallest valid bin
-__global__ void theta4_kernel(const uint8_t* __restrict__ sample, int64_t ns, int64_t nq, int r,
+// per-query threshold bin from the transposed dense sample (u32 [ns/4][nq],
+// 4 packed bins): r-th smallest valid bin.  One CTA per 32 queries.
+__global__ void theta4_kernel(const uint32_t* __restrict__ sample, int64_t rows, int64_t nq, int r,
                               uint8_t* __restrict__ theta) {
-  __shared__ unsigned int hist[128];
-  const int64_t q = blockIdx.x;
-  for (int i = threadIdx.x; i < 128; i += blockDim.x) hist[i] = 0;
+  __shared__ unsigned int hist[32][129];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t q = blockIdx.x * 32 + lane;
+  for (int i = threadIdx.x; i < 32 * 129; i += blockDim.x) (&hist[0][0])[i] = 0;
   __syncthreads();
-  for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
-    const uint8_t b = sample[q * ns + i];
-    if (b < 128) atomicAdd(&hist[b], 1u);
+  if (q < nq) {
+    for (int64_t row = warp; row < rows; row += nw) {
+      const uint32_t w = sample[row * nq + q];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t b = (w >> (8 * e)) & 255u;
+        if (b < 128) atomicAdd(&hist[lane][b], 1u);
+      }
+    }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (warp == 0 && q < nq) {
     unsigned long long c = 0;
     int t = 127;
     for (int b = 0; b < 128; ++b) {
-      c += hist[b];
+      c += hist[lane][b];
       if (c >= (unsigned long long)r) {
         t = b;
         break;
@@ -499,6 +557,7 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
     uint8_t* sample = nullptr;
     PQS_TRY(scratch(ctx, S_SAMPLE, (size_t)(nq * ns), &sample));
     Scan4Args a{};
+    a.tout = 1;
     a.words = db->words4;
     a.n = n;
     a.m = m;
@@ -510,7 +569,8 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
     a.out = sample;
     a.ld = ns;
     PQS_TRY(launch_scan4<MODE_DENSE>(ctx, db->mp, a, nq));
-    theta4_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(sample, ns, nq, (int)r_eff, theta);
+    theta4_kernel<<<(unsigned)cdiv(nq, 32), 256, 0, ctx->stream>>>((const uint32_t*)sample, ns / 4, nq,
+                                                                   (int)r_eff, theta);
     PQS_LAUNCHED(ctx);
   }
 
