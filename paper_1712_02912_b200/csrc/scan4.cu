@@ -442,38 +442,51 @@ int launch_scan4(pqs_ctx* ctx, int mp, const Scan4Args& a, int64_t nq) {
   return set_err(ctx, PQS_ERR_UNSUPPORTED, "scan4: unsupported padded m");
 }
 
-// per-query threshold bin from the transposed dense sample (u32 [ns/4][nq],
-// 4 packed bins): r-th smallest valid bin.  One CTA per 32 queries.
-__global__ void theta4_kernel(const uint32_t* __restrict__ sample, int64_t rows, int64_t nq, int r,
-                              uint8_t* __restrict__ theta) {
-  __shared__ unsigned int hist[32][129];
+// per-query threshold bin from the transposed dense sample (u32 [rows][nq],
+// 4 packed bins per word): the r-th smallest valid bin.  theta4_hist_kernel:
+// one CTA per (32 queries, row slice); a conflict-free [bin][lane] shared
+// histogram, then one global atomicAdd per non-zero bin.
+__global__ void theta4_hist_kernel(const uint32_t* __restrict__ sample, int64_t rows, int64_t nq, int64_t rows_per,
+                                   unsigned int* __restrict__ ghist) {
+  __shared__ unsigned int hist[128][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int64_t q = blockIdx.x * 32 + lane;
-  for (int i = threadIdx.x; i < 32 * 129; i += blockDim.x) (&hist[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < 128 * 32; i += blockDim.x) (&hist[0][0])[i] = 0;
   __syncthreads();
+  const int64_t r0 = blockIdx.y * rows_per, r1 = min(rows, r0 + rows_per);
   if (q < nq) {
-    for (int64_t row = warp; row < rows; row += nw) {
+    for (int64_t row = r0 + warp; row < r1; row += nw) {
       const uint32_t w = sample[row * nq + q];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const uint32_t b = (w >> (8 * e)) & 255u;
-        if (b < 128) atomicAdd(&hist[lane][b], 1u);
+        if (b < 128) atomicAdd(&hist[b][lane], 1u);
       }
     }
   }
   __syncthreads();
-  if (warp == 0 && q < nq) {
-    unsigned long long c = 0;
-    int t = 127;
-    for (int b = 0; b < 128; ++b) {
-      c += hist[lane][b];
-      if (c >= (unsigned long long)r) {
-        t = b;
-        break;
-      }
-    }
-    theta[q] = (uint8_t)t;
+  for (int i = threadIdx.x; i < 128 * 32; i += blockDim.x) {
+    const int b = i >> 5, l = i & 31;
+    const int64_t qq = blockIdx.x * 32 + l;
+    const unsigned int v = hist[b][l];
+    if (v && qq < nq) atomicAdd(ghist + qq * 128 + b, v);
   }
+}
+
+__global__ void theta4_final_kernel(const unsigned int* __restrict__ ghist, int64_t nq, int r,
+                                    uint8_t* __restrict__ theta) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  unsigned long long c = 0;
+  int t = 127;
+  for (int b = 0; b < 128; ++b) {
+    c += ghist[q * 128 + b];
+    if (c >= (unsigned long long)r) {
+      t = b;
+      break;
+    }
+  }
+  theta[q] = (uint8_t)t;
 }
 
 __global__ void fill_u8_kernel(uint8_t* p, int64_t n, uint8_t v) {
@@ -569,8 +582,16 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
     a.out = sample;
     a.ld = ns;
     PQS_TRY(launch_scan4<MODE_DENSE>(ctx, db->mp, a, nq));
-    theta4_kernel<<<(unsigned)cdiv(nq, 32), 256, 0, ctx->stream>>>((const uint32_t*)sample, ns / 4, nq,
-                                                                   (int)r_eff, theta);
+    unsigned int* ghist = nullptr;
+    PQS_TRY(scratch(ctx, S_IVF_WORK3, (size_t)(nq * 128), &ghist));
+    PQS_CUDA(ctx, cudaMemsetAsync(ghist, 0, sizeof(unsigned int) * nq * 128, ctx->stream));
+    const int64_t rows = ns / 4;
+    const int64_t qg = cdiv(nq, 32);
+    const int64_t rs = std::max<int64_t>(1, std::min<int64_t>(cdiv(rows, 256), cdiv(4 * ctx->sm_count, qg)));
+    dim3 tgrid((unsigned)qg, (unsigned)rs);
+    theta4_hist_kernel<<<tgrid, 256, 0, ctx->stream>>>((const uint32_t*)sample, rows, nq, cdiv(rows, rs), ghist);
+    PQS_LAUNCHED(ctx);
+    theta4_final_kernel<<<(unsigned)cdiv(nq, 128), 128, 0, ctx->stream>>>(ghist, nq, (int)r_eff, theta);
     PQS_LAUNCHED(ctx);
   }
 

@@ -66,11 +66,24 @@ CONFIGS = {
 
 
 def rows(cfg: dict, seed: int, lo: int, hi_row: int, stream: int = 0) -> np.ndarray:
-    if cfg["kind"] == "mix":
-        cl = cfg["clip"]
-        return mixture_rows(seed, lo, hi_row, cfg["d"], cfg["comps"], cfg["center_hi"], cfg["sigma"], cl[0], cl[1],
-                            stream)
-    return decay_gaussian_rows(seed, lo, hi_row, cfg["d"], stream)
+    """Rows [lo, hi_row); chunks are generated in parallel (each has its own seed)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    step = CHUNK * 4
+    parts = [(a, min(a + step, hi_row)) for a in range(lo, hi_row, step)]
+
+    def one(ab):
+        a, b = ab
+        if cfg["kind"] == "mix":
+            cl = cfg["clip"]
+            return mixture_rows(seed, a, b, cfg["d"], cfg["comps"], cfg["center_hi"], cfg["sigma"], cl[0], cl[1],
+                                stream)
+        return decay_gaussian_rows(seed, a, b, cfg["d"], stream)
+
+    if len(parts) <= 1:
+        return one((lo, hi_row))
+    with ThreadPoolExecutor(max_workers=8) as ex:
+        return np.concatenate(list(ex.map(one, parts)))
 
 
 def kmeans(x: np.ndarray, k: int, iters: int, seed: int) -> np.ndarray:
@@ -80,33 +93,45 @@ def kmeans(x: np.ndarray, k: int, iters: int, seed: int) -> np.ndarray:
     c = x[rng.choice(x.shape[0], k, replace=False)].copy()
     xx = (x * x).sum(1)
     for _ in range(iters):
-        dd = xx[:, None] - 2.0 * (x @ c.T) + (c * c).sum(1)[None]
+        dd = (c * c).sum(1)[None] - 2.0 * (x @ c.T)
         a = dd.argmin(1)
+        order = np.argsort(a, kind="stable")
         cnt = np.bincount(a, minlength=k)
-        s = np.stack([np.bincount(a, weights=x[:, t], minlength=k) for t in range(x.shape[1])], axis=1)
-        nz = cnt > 0
-        c[nz] = (s[nz] / cnt[nz, None]).astype(np.float32)
+        nz = np.flatnonzero(cnt)
+        starts = np.concatenate([[0], np.cumsum(cnt)[:-1]])[nz]
+        sums = np.add.reduceat(x[order].astype(np.float64), starts, axis=0)
+        c[nz] = (sums / cnt[nz, None]).astype(np.float32)
     return c
 
 
 def train_pq(x: np.ndarray, m: int, b: int, iters: int = 20, seed: int = 0) -> np.ndarray:
+    from concurrent.futures import ThreadPoolExecutor
+
     d = x.shape[1]
     dsub = d // m
     k = 1 << b
-    return np.stack([kmeans(x[:, j * dsub:(j + 1) * dsub], k, iters, seed + j) for j in range(m)])
+    with ThreadPoolExecutor(max_workers=min(m, 16)) as ex:
+        books = list(ex.map(lambda j: kmeans(x[:, j * dsub:(j + 1) * dsub], k, iters, seed + j), range(m)))
+    return np.stack(books)
 
 
 def encode(books: np.ndarray, x: np.ndarray, chunk: int = 1 << 16) -> np.ndarray:
     """Nearest centroid per sub-space (fp32 matmul expansion; data prep only)."""
+    from concurrent.futures import ThreadPoolExecutor
+
     m, k, dsub = books.shape
     out = np.empty((x.shape[0], m), dtype=np.uint8)
     cn = (books * books).sum(2)
-    for lo in range(0, x.shape[0], chunk):
+
+    def work(lo):
         xs = x[lo:lo + chunk]
         for j in range(m):
             sub = xs[:, j * dsub:(j + 1) * dsub]
             dd = cn[j][None] - 2.0 * (sub @ books[j].T)
             out[lo:lo + chunk, j] = dd.argmin(1)
+
+    with ThreadPoolExecutor(max_workers=8) as ex:
+        list(ex.map(work, range(0, x.shape[0], chunk)))
     return out
 
 
