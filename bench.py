@@ -58,8 +58,9 @@ def make_data(cfg_name: str, rank: int):
     cfg = G.CONFIGS[cfg_name]
     books, codes, queries = G.make_exhaustive(cfg_name, shard=rank)
     prefix = None
-    if cfg["b"] == 4 and rank > 0:
-        prefix = G.encode(books, G.rows(cfg, 1712, 0, cfg.get("init_count", 200), stream=1))
+    if cfg["b"] == 4:
+        prefix = codes[:cfg["init_count"]] if rank == 0 else \
+            G.encode(books, G.rows(cfg, 1712, 0, cfg["init_count"], stream=1))
     return cfg, books, codes, queries, prefix
 
 
@@ -183,7 +184,8 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": metric_name(args.config), "value": value, "unit": "evals/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8" if cfg["b"] == 4 else "f64",
+        "ms_per_step": codes.shape[0] * queries.shape[0] / value * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8" if cfg["b"] == 4 else "f64",
         "data": "synthetic (seeded stand-in for the BASELINE config; see DESIGN.md)",
         "config": config_dict(args.config, cfg, world),
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": base["cores"], "kind": "port",
@@ -228,30 +230,20 @@ def main():
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
     pq = P.ProductQuantizer(cfg["m"], cfg["b"], cfg["d"], books)
-    dq = P.DeviceQuantizer(pq, ctx)
-    db = P.DeviceCodes(codes, cfg["b"], id_base=rank * n, ctx=ctx)
-    if prefix is not None:
-        db.set_prefix(prefix)
+    from paper_1712_02912_b200.sharded import ShardedSearch
+
+    n_total = n * world
+    if cfg["b"] == 4:
+        if prefix is None:
+            prefix = codes[:cfg["init_count"]]
+        searcher = ShardedSearch.quick_adc(codes, rank, world, n_total, prefix, pq, cfg["init_count"], ctx=ctx)
+    else:
+        searcher = ShardedSearch.float_adc(codes, rank, world, n_total, pq, ctx=ctx)
     q_dev = torch.from_numpy(queries).to(dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
     def step_device():
-        if cfg["b"] == 4:
-            bins, ids, cnt, _, _ = db.qadc_search(dq, q_dev, cfg["init_count"], r)
-            dist_ = bins.to(torch.float64)
-        else:
-            dist_, ids, cnt = db.adc_search(dq, q_dev, r)
-        if world > 1:
-            import torch.distributed as dist
-
-            gd = [torch.empty_like(dist_) for _ in range(world)]
-            gi = [torch.empty_like(ids) for _ in range(world)]
-            gc = [torch.empty_like(cnt) for _ in range(world)]
-            dist.all_gather(gd, dist_)
-            dist.all_gather(gi, ids)
-            dist.all_gather(gc, cnt)
-            P.merge_topr(torch.stack(gd), torch.stack(gi), torch.stack(gc), r, ctx=ctx)
-        return ids
+        return searcher.search(q_dev, r)
 
     def barrier():
         if world > 1:
@@ -294,32 +286,22 @@ def main():
     value = evals_per_step / (ms_per_step / 1e3)
 
     # ---- e2e through the public API with host buffers (pinned), H2D + D2H inside
-    q_pin = torch.from_numpy(queries).pin_memory().numpy()
+    q_pin = torch.from_numpy(queries).pin_memory()
     e2e_ms = []
     for s in range(max(args.warmup, 1) + args.steps):
         flush.zero_()
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        if cfg["b"] == 4:
-            bins_h, ids_h, cnt_h, _, _ = db.qadc_search(dq, q_pin, cfg["init_count"], r)
-            d_host = bins_h
+        if world == 1:
+            # the drop-in batched API on host arrays: H2D/D2H inside the C ABI call
+            if cfg["b"] == 4:
+                out = searcher.db.qadc_search(searcher.dq, q_pin.numpy(), cfg["init_count"], r)
+            else:
+                out = searcher.db.adc_search(searcher.dq, q_pin.numpy(), r)
         else:
-            d_host, ids_h, cnt_h = db.adc_search(dq, q_pin, r)
-        if world > 1:
-            import torch.distributed as dist
-
-            dd = torch.from_numpy(np.ascontiguousarray(d_host, dtype=np.float64)).to(dev)
-            ii = torch.from_numpy(ids_h).to(dev)
-            cc = torch.from_numpy(cnt_h).to(dev)
-            gd = [torch.empty_like(dd) for _ in range(world)]
-            gi = [torch.empty_like(ii) for _ in range(world)]
-            gc = [torch.empty_like(cc) for _ in range(world)]
-            dist.all_gather(gd, dd)
-            dist.all_gather(gi, ii)
-            dist.all_gather(gc, cc)
-            md, mi, mc = P.merge_topr(torch.stack(gd).cpu().numpy(), torch.stack(gi).cpu().numpy(),
-                                      torch.stack(gc).cpu().numpy(), r, ctx=ctx)
+            d_, i_, c_ = searcher.search(q_pin.to(dev, non_blocking=True), r)
+            out = (d_.cpu(), i_.cpu(), c_.cpu())
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) * 1e3
         if s >= max(args.warmup, 1):
@@ -333,7 +315,7 @@ def main():
         e2e_total = float(t.item())
     e2e_value = evals_per_step / (e2e_total / len(e2e_ms) / 1e3)
     h2d = queries.nbytes
-    d2h = nq * r * (1 if cfg["b"] == 4 else 8) + nq * r * 8 + nq * 4
+    d2h = nq * r * (1 if (cfg["b"] == 4 and world == 1) else 8) + nq * r * 8 + nq * 4
 
     if rank != 0:
         if world > 1:

@@ -1,0 +1,112 @@
+"""Database sharding across GPUs: one process per GPU.
+
+Each rank owns a contiguous id range of one global code list and scans the
+whole query batch; the per-rank top-r lists are all-gathered with
+torch.distributed (NCCL over NVLink between GPUs; gloo works for CPU tests)
+and merged on the device by `pqs_merge_topr` -- the reference's
+NeighborSet.push merge (scan.py:109-118), exact because the global top-r is a
+subset of the union of the shard top-r under the same (distance, id) order.
+
+Quick ADC needs *global* quantization parameters: qmax is the r-th fp64 ADC
+of the first init_count codes of the global list (quickadc.py:130-137), so
+those codes are replicated to every rank (`prefix_codes`).
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+import numpy as np
+
+
+def shard_range(n_total: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous, balanced id range [lo, hi) of `rank` among `world` shards."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    base, extra = divmod(n_total, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def all_gather_results(dist, ids, cnt, group=None):
+    """Gather (G, nq, r) dist/ids and (G, nq) counts from every rank."""
+    import torch
+    import torch.distributed as dist_
+
+    world = dist_.get_world_size(group)
+    gd = [torch.empty_like(dist) for _ in range(world)]
+    gi = [torch.empty_like(ids) for _ in range(world)]
+    gc = [torch.empty_like(cnt) for _ in range(world)]
+    dist_.all_gather(gd, dist, group=group)
+    dist_.all_gather(gi, ids, group=group)
+    dist_.all_gather(gc, cnt, group=group)
+    return torch.stack(gd), torch.stack(gi), torch.stack(gc)
+
+
+class ShardedSearch:
+    """One rank's shard of a global list plus the exchange + merge step.
+
+    local_search(queries, r) -> (dist float64 (nq, r), ids int64 (nq, r),
+    count int32 (nq,)) with GLOBAL ids; merge(dist, ids, cnt, r) merges the
+    gathered (G, nq, r) lists.  Both default to the device engine; tests
+    inject oracle-backed callables to check the host logic on CPU (gloo).
+    """
+
+    def __init__(self, local_search: Callable, merge: Callable | None = None, group=None):
+        self.local_search = local_search
+        self.merge = merge
+        self.group = group
+
+    @classmethod
+    def quick_adc(cls, codes_local, rank: int, world: int, n_total: int, prefix_codes, pq, init_count: int,
+                  ctx=None, group=None):
+        """Device-backed Quick ADC shard (ids = global offset + local index)."""
+        import torch
+
+        from .engine import DeviceCodes, DeviceQuantizer, merge_topr
+
+        lo, hi = shard_range(n_total, world, rank)
+        if codes_local.shape[0] != hi - lo:
+            raise ValueError("codes_local does not match this rank's shard")
+        db = DeviceCodes(codes_local, 4, id_base=lo, ctx=ctx)
+        db.set_prefix(prefix_codes)
+        dq = DeviceQuantizer(pq, ctx)
+
+        def local(queries, r):
+            bins, ids, cnt, _, _ = db.qadc_search(dq, queries, init_count, r)
+            return bins.to(torch.float64), ids, cnt
+
+        def merge(d, i, c, r):
+            return merge_topr(d, i, c, r, ctx=ctx)
+
+        out = cls(local, merge, group)
+        out.db, out.dq = db, dq
+        return out
+
+    @classmethod
+    def float_adc(cls, codes_local, rank: int, world: int, n_total: int, pq, ctx=None, group=None):
+        from .engine import DeviceCodes, DeviceQuantizer, merge_topr
+
+        lo, hi = shard_range(n_total, world, rank)
+        db = DeviceCodes(codes_local, 8, id_base=lo, ctx=ctx)
+        dq = DeviceQuantizer(pq, ctx)
+
+        def local(queries, r):
+            return db.adc_search(dq, queries, r)
+
+        out = cls(local, lambda d, i, c, r: merge_topr(d, i, c, r, ctx=ctx), group)
+        out.db, out.dq = db, dq
+        return out
+
+    def search(self, queries, r: int):
+        """Global top-r for every query (identical result on every rank)."""
+        import torch.distributed as dist_
+
+        d, i, c = self.local_search(queries, r)
+        if not dist_.is_available() or not dist_.is_initialized() or dist_.get_world_size(self.group) == 1:
+            return d, i, c
+        gd, gi, gc = all_gather_results(d, i, c, self.group)
+        return self.merge(gd, gi, gc, r)
+
+
+__all__ = ["shard_range", "all_gather_results", "ShardedSearch"]
