@@ -441,7 +441,7 @@ static int qadc_common(pqs_ctx* ctx, const pqs_db* db, const float* dt, int64_t 
   // the fallback path reuses S_QTABLES as a gather buffer: keep qtables in its own slot
   uint8_t* qt_work = dqt;
   if (io == PQS_IO_HOST || out_qt == nullptr) {
-    PQS_TRY(scratch(ctx, S_FLAG, (size_t)nq * db->m * 16, &qt_work));
+    PQS_TRY(scratch(ctx, S_QT_WORK, (size_t)nq * db->m * 16, &qt_work));
   }
   PQS_TRY(run_qadc_topr(ctx, db, dt, nq, init_count, r, db_, di, dc, qt_work, dqmm));
   PQS_TRY(copy_out(ctx, out_bins, db_, (size_t)nq * r, io));

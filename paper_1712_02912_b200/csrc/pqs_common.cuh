@@ -53,6 +53,8 @@ enum ScratchSlot {
   S_IVF_WORK2,
   S_IVF_WORK3,
   S_MISC,
+  S_WORK,     // dynamic work counters
+  S_QT_WORK,  // quantized tables of a Quick ADC search
   S_NSLOTS
 };
 
@@ -213,8 +215,6 @@ __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 
 // tables.cu
 int launch_tables_exact(pqs_ctx* ctx, const pqs_pq* pq, const float* d_queries, int64_t nq,
                         float* d_tables);
-int launch_tables_scan8(pqs_ctx* ctx, const float* d_tables, int64_t nq, int m, int k,
-                        float* d_tables_t, float* d_aerr);
 // scan8.cu
 int launch_scan_distances(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t nq,
                           double* d_out);

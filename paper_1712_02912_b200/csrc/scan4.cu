@@ -234,6 +234,8 @@ struct Scan4Args {
   int64_t nq;
   // virtual tiles: tile(i) = tile_off + i * tile_step, i in [0, nvt)
   int64_t nvt, tile_off, tile_step, per_cta;
+  int64_t nqg;             // query groups of SCAN4_THREADS
+  unsigned long long* work;  // dynamic tile counter (zeroed before launch)
   // dense
   uint8_t* out;
   int64_t ld;
@@ -306,41 +308,61 @@ __global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kerne
   uint64_t* stage = reinterpret_cast<uint64_t*>(s_pred + 2 * WORDS) + threadIdx.x;
   int ncand = 0;
 
-  const int64_t q = blockIdx.y * (int64_t)blockDim.x + threadIdx.x;
-  const bool qvalid = q < a.nq;
-
-  // query tables -> registers (components >= m are zero)
-  uint32_t T[MP][4];
-#pragma unroll
-  for (int j = 0; j < MP; ++j) {
-    if (qvalid && j < a.m) {
-      const uint4 t = __ldg(reinterpret_cast<const uint4*>(a.qt + (q * a.m + j) * 16));
-      T[j][0] = t.x;
-      T[j][1] = t.y;
-      T[j][2] = t.z;
-      T[j][3] = t.w;
-    } else {
-      T[j][0] = T[j][1] = T[j][2] = T[j][3] = 0u;
-    }
+  // persistent CTAs grab tiles of the linearised (query group, tile) list from
+  // a global counter (dynamic balance); tables are reloaded at group switches
+  const long long total = a.nqg * a.nvt;
+  __shared__ long long s_w[2];
+  if (threadIdx.x == 0) {
+    s_w[0] = atomicAdd(a.work, 1ull);
+    s_w[1] = atomicAdd(a.work, 1ull);
   }
-  uint32_t theta = 0;
-  if (MODE == MODE_FILTER) theta = qvalid ? a.theta[q] : 0u;
-  const uint32_t bias = (0x7FFFu - theta) * 0x00010001u;
-  const uint32_t one = a.one, k24 = a.k24;
+  __syncthreads();
+  long long w = s_w[0], wn = s_w[1];
+  if (w >= total) return;
 
-  const int64_t i0 = blockIdx.x * a.per_cta;
-  const int64_t i1 = min(i0 + a.per_cta, a.nvt);
-  if (i0 >= i1) return;
+  int64_t q = -1, cur_qg = -1;
+  bool qvalid = false;
+  uint32_t T[MP][4];
+  uint32_t theta = 0, bias = 0;
+  const uint32_t one = a.one, k24 = a.k24;
+  auto load_group = [&](int64_t qg) {
+    q = qg * SCAN4_THREADS + threadIdx.x;
+    qvalid = q < a.nq;
+#pragma unroll
+    for (int j = 0; j < MP; ++j) {
+      if (qvalid && j < a.m) {
+        const uint4 t = __ldg(reinterpret_cast<const uint4*>(a.qt + (q * a.m + j) * 16));
+        T[j][0] = t.x;
+        T[j][1] = t.y;
+        T[j][2] = t.z;
+        T[j][3] = t.w;
+      } else {
+        T[j][0] = T[j][1] = T[j][2] = T[j][3] = 0u;
+      }
+    }
+    theta = (MODE == MODE_FILTER && qvalid) ? a.theta[q] : 0u;
+    bias = (0x7FFFu - theta) * 0x00010001u;
+  };
 
   uint4 regs[PER];
-  load_tile_raw<MP>(a.words, a.tile_off + i0 * a.tile_step, regs, nthreads);
+  load_tile_raw<MP>(a.words, a.tile_off + (w % a.nvt) * a.tile_step, regs, nthreads);
   store_tile_pred<MP>(regs, s_pred, nthreads);
   __syncthreads();
 
   int cur = 0;
-  for (int64_t i = i0; i < i1; ++i) {
-    const bool has_next = (i + 1 < i1);
-    if (has_next) load_tile_raw<MP>(a.words, a.tile_off + (i + 1) * a.tile_step, regs, nthreads);
+  for (int it = 0;; ++it) {
+    const int64_t qg = w / a.nvt;
+    const int64_t i = w - qg * a.nvt;
+    if (qg != cur_qg) {
+      if (MODE == MODE_FILTER && ncand > 0) {
+        flush_cands(stage, ncand, q, a.cand, a.cand_cnt, a.cap);
+        ncand = 0;
+      }
+      load_group(qg);
+      cur_qg = qg;
+    }
+    const bool has_next = (wn < total);
+    if (has_next) load_tile_raw<MP>(a.words, a.tile_off + (wn % a.nvt) * a.tile_step, regs, nthreads);
     const uint4* buf = s_pred + cur * WORDS;
     const int64_t tile = a.tile_off + i * a.tile_step;
     const int64_t code0 = tile * TILE4;
@@ -397,13 +419,15 @@ __global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kerne
         }
       }
     }
-    if (has_next) {
-      store_tile_pred<MP>(regs, s_pred + (cur ^ 1) * WORDS, nthreads);
-      cur ^= 1;
-    }
+    if (has_next) store_tile_pred<MP>(regs, s_pred + (cur ^ 1) * WORDS, nthreads);
+    if (threadIdx.x == 0 && has_next) s_w[it & 1] = atomicAdd(a.work, 1ull);
     __syncthreads();
+    if (!has_next) break;
+    w = wn;
+    wn = s_w[it & 1];
+    cur ^= 1;
   }
-  if (MODE == MODE_FILTER && ncand > 0) flush_cands(stage, ncand, q, a.cand, a.cand_cnt, a.cap);
+  if (MODE == MODE_FILTER && ncand > 0 && q >= 0) flush_cands(stage, ncand, q, a.cand, a.cand_cnt, a.cap);
 }
 
 template <int MP, int MODE>
@@ -414,17 +438,17 @@ int launch_scan4_t(pqs_ctx* ctx, Scan4Args a, int64_t nq) {
   PQS_CUDA(ctx, cudaFuncSetAttribute(scan4_kernel<MP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
   const int threads = SCAN4_THREADS;  // the tile loader assumes a full CTA
-  const int64_t qgroups = cdiv(nq, threads);
-  // split the tiles so that the grid covers the SMs a few times over
-  const int64_t target = (int64_t)ctx->sm_count * 2 * 4;
-  int64_t splits = std::max<int64_t>(1, cdiv(target, qgroups));
-  splits = std::min<int64_t>(splits, a.nvt);
-  a.per_cta = cdiv(a.nvt, splits);
-  splits = cdiv(a.nvt, a.per_cta);
-  if (splits <= 0) return PQS_OK;
+  a.nqg = cdiv(nq, threads);
+  const int64_t total = a.nqg * a.nvt;
+  if (total <= 0) return PQS_OK;
+  int per_sm = 0;
+  PQS_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan4_kernel<MP, MODE>, threads, smem));
+  const int64_t nctas = std::min<int64_t>(total, (int64_t)ctx->sm_count * std::max(per_sm, 1));
   a.one = 1u;
   a.k24 = 1u << 24;
-  dim3 grid((unsigned)splits, (unsigned)qgroups);
+  PQS_TRY(scratch(ctx, S_WORK, 1, &a.work));
+  PQS_CUDA(ctx, cudaMemsetAsync(a.work, 0, sizeof(unsigned long long), ctx->stream));
+  dim3 grid((unsigned)nctas);
   scan4_kernel<MP, MODE><<<grid, threads, smem, ctx->stream>>>(a);
   PQS_LAUNCHED(ctx);
   return PQS_OK;

@@ -4,18 +4,22 @@
 //
 // K3 design: lane = query.  A CTA owns a group of 32
 // queries and W warps; all warps share the group's tables, staged in shared
-// memory in [component][entry][lane] fp32 order so that 32 lanes reading the
-// same entry of their own table hit 32 distinct banks (conflict-free for any
-// code).  Codes are broadcast: the device layout is tile-transposed
-// ([tile][component][1024 codes]) so a warp reads 16 codes' bytes of one
-// component with one broadcast LDS.128.  Each warp owns 64 codes of the 1024
-// code tile and keeps 64 fp32 partial sums per lane in registers while the
-// tables stream through shared memory in component chunks.  Chunks (tables +
-// the tile's matching code bytes) are double-buffered with TMA bulk copies
-// (cp.async.bulk + mbarrier).  The fp32 sums are a filter only: every code
-// whose fp32 distance is within the certified error bound of the threshold
-// becomes a candidate, and candidates are re-scored exactly in fp64 in the
-// reference's order before the (distance, id) selection.
+// memory in [component][entry][lane] order so that 32 lanes reading the same
+// entry of their own table hit distinct banks (conflict-free for any code).
+// The scan tables are u16 fixed-point LOWER BOUNDS of the exact fp32 tables:
+//   t'[j][c] = min(65535, floor((T[j][c] - o_j) * 2^e))   (o_j = min_c T[j][c])
+// so every code's integer sum L satisfies  L <= 2^e (d - O) <= L + m  (d the
+// exact distance, O = sum_j o_j) -- exact integer bounds, no fp error
+// analysis.  Two u16 tables (32 queries x 8 x 256) fit in 128 KB, so for the
+// cfg0 shape the tables stay resident; larger tables stream in component
+// chunks (TMA bulk copies, cp.async.bulk + mbarrier, double-buffered) while
+// each lane keeps 64 u32 partial sums in registers.  Codes are broadcast:
+// the device layout is tile-transposed ([tile][component][1024 codes]), one
+// LDS.128 returns 16 codes' bytes of a component.  A sample pass (scale e0,
+// no saturation) gives an upper bound D' on the r-th smallest d - O; the
+// filter pass (finer scale e1) keeps every code with L <= floor(2^e1 D'),
+// which provably contains the reference's top-r; survivors are re-scored
+// exactly in fp64 (reference order) and selected by (distance, id).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -28,7 +32,7 @@ namespace {
 constexpr int W8 = 16;              // warps per CTA
 constexpr int C8 = TILE8 / W8;     // codes per warp (64)
 constexpr int SCAN8_THREADS = W8 * 32;
-constexpr int CHUNK_BUDGET = 96 * 1024;
+constexpr int CHUNK_BUDGET = 176 * 1024;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -59,214 +63,365 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// ------------------------------------------------------------- table layout
-// tables (nq, m, k) -> tt [qg][j][c][32]; aerr[q] = certified bound on
-// |fp32 sum - fp64 sum| of any code's distance (recursive summation).
-__global__ void tables_scan8_kernel(const float* __restrict__ tables, int64_t nq, int m, int k,
-                                    float* __restrict__ tt) {
+// --------------------------------------------------------- u16 tables
+// per query: o_j = min_c T[j][c] (fp32), e0 = floor(log2(65535 / max_j max_c (T - o_j)))
+__global__ void tables_u16_stats_kernel(const float* __restrict__ tables, int64_t nq, int m, int k,
+                                        float* __restrict__ off, int* __restrict__ e0, double* __restrict__ slack) {
+  const int64_t q = blockIdx.x;
+  __shared__ double s_max[32], s_abs[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double mx = 0.0, absum = 0.0;
+  for (int j = warp; j < m; j += nw) {
+    const float* row = tables + (q * m + j) * (int64_t)k;
+    float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000), am = 0.f;
+    for (int c = lane; c < k; c += 32) {
+      const float v = row[c];
+      lo = fminf(lo, v);
+      hi = fmaxf(hi, v);
+      am = fmaxf(am, fabsf(v));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+    }
+    if (lane == 0) off[q * m + j] = lo;
+    mx = fmax(mx, (double)hi - (double)lo);
+    absum += (double)am;
+  }
+  if (lane == 0) {
+    s_max[warp] = mx;
+    s_abs[warp] = absum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double M = 0.0, A = 0.0;
+    for (int i = 0; i < nw; ++i) {
+      M = fmax(M, s_max[i]);
+      A += s_abs[i];
+    }
+    int e = 0;
+    if (M > 0.0) e = (int)floor(log2(65535.0 / M));
+    while (M > 0.0 && ldexp(M, e) > 65535.0) --e;
+    e0[q] = e;
+    // covers the reference's fp64 rounding of d and of the offset sum
+    slack[q] = A * 4.0 * (double)(m + 2) * 1.1102230246251565e-16;
+  }
+}
+
+// t'[qg][j][c][lane] = min(65535, floor((T - o_j) * 2^e_q)); exact in fp64
+__global__ void tables_u16_kernel(const float* __restrict__ tables, const float* __restrict__ off,
+                                  const int* __restrict__ ex, int64_t nq, int m, int k, uint16_t* __restrict__ tt) {
   const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t nqg = cdiv(nq, 32);
-  const int64_t total = nqg * m * (int64_t)k * 32;
+  const int64_t total = cdiv(nq, 32) * m * (int64_t)k * 32;
   if (gid >= total) return;
   const int lane = (int)(gid & 31);
   int64_t t = gid >> 5;
   const int c = (int)(t % k);
   t /= k;
   const int j = (int)(t % m);
-  const int64_t qg = t / m;
-  const int64_t q = qg * 32 + lane;
-  tt[gid] = q < nq ? tables[(q * m + j) * (int64_t)k + c] : 0.0f;
-}
-
-__global__ void aerr_kernel(const float* __restrict__ tables, int64_t nq, int m, int k, float* __restrict__ aerr) {
-  const int64_t q = blockIdx.x;
-  __shared__ double part[32];
-  double s = 0.0;
-  // one warp per component round-robin
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int j = warp; j < m; j += nw) {
-    float mx = 0.f;
-    for (int c = lane; c < k; c += 32) mx = fmaxf(mx, fabsf(tables[(q * m + j) * (int64_t)k + c]));
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    s += (double)mx;
+  const int64_t q = (t / m) * 32 + lane;
+  uint16_t v = 0;
+  if (q < nq) {
+    const double d = ((double)tables[(q * m + j) * (int64_t)k + c] - (double)off[q * m + j]);
+    const double f = floor(ldexp(d, ex[q]));
+    v = f >= 65535.0 ? (uint16_t)65535 : (uint16_t)f;
   }
-  if (lane == 0) part[warp] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double tot = 0.0;
-    for (int i = 0; i < nw; ++i) tot += part[i];
-    // gamma_{m} for fp32 (u = 2^-24) plus fp64 (u = 2^-53), with slack
-    const double u32 = 5.9604644775390625e-08, u64 = 1.1102230246251565e-16;
-    const double g = (double)m * u32 / (1.0 - (double)m * u32) + (double)m * u64 * 2.0;
-    aerr[q] = (float)(tot * g * 1.01 + 1e-30);
-  }
+  tt[gid] = v;
 }
 
 // --------------------------------------------------------------- K3 kernel
 enum { MODE8_DENSE = 0, MODE8_FILTER = 1 };
+constexpr int CSTAGE8 = 16;
 
 struct Scan8Args {
-  const float* tt;         // [nqg][m][k][32]
+  const uint16_t* tt;      // [nqg][m][k][32]
   const uint8_t* codes;    // [ntiles][m][TILE8]
   int64_t n;
-  int m, k, mc;
+  int m, k, mc, resident;
   int64_t nq;
   int64_t nvt, tile_off, tile_step, per_cta;
-  float* out;              // dense [q][ld]
+  int64_t nqg;             // query groups of 32
+  uint32_t* out;           // dense [q][ld] u32 lower-bound sums (0xFFFFFFFF = no code)
   int64_t ld;
-  const float* theta;      // filter
+  const uint32_t* theta;   // filter: keep L <= theta[q]
   uint64_t* cand;
   int* cand_cnt;
   int64_t cap;
+  uint32_t one;
+  uint32_t c64;            // runtime 64 (entry row stride), keeps the IMAD on the FMA pipe
 };
 
-template <int MODE>
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
+  return d;
+}
+
+__device__ __forceinline__ uint32_t imad8(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+template <int MODE, bool RES>
 __global__ void __launch_bounds__(SCAN8_THREADS, 1) scan8_kernel(Scan8Args a) {
   extern __shared__ __align__(128) unsigned char sm8[];
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ __align__(8) uint64_t bars[3];  // 0/1: stage buffers, 2: resident tables
   const int m = a.m, k = a.k, mc = a.mc;
-  const uint32_t tab_bytes = (uint32_t)mc * k * 32 * 4;
+  const uint32_t row_bytes = (uint32_t)k * 32 * 2;  // one component of 32 queries' tables
+  const uint32_t tab_bytes = RES ? (uint32_t)m * row_bytes : (uint32_t)mc * row_bytes;
+  const uint32_t tab_region = RES ? tab_bytes : 2 * tab_bytes;
   const uint32_t code_bytes = (uint32_t)mc * TILE8;
-  // buffer b: tables at sm8 + b*tab_bytes, codes at sm8 + 2*tab_bytes + b*code_bytes
+  uint8_t* code_base = sm8 + tab_region;
+  uint32_t* stage = reinterpret_cast<uint32_t*>(code_base + 2 * code_bytes) + threadIdx.x;
+  int ncand = 0;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t qg = blockIdx.y;
-  const int64_t q = qg * 32 + lane;
-  const bool qvalid = q < a.nq;
-  const float theta = (MODE == MODE8_FILTER && qvalid) ? a.theta[q] : 0.f;
+  const uint32_t one = a.one;
+  const uint32_t c64 = a.c64;
 
-  const int64_t i0 = blockIdx.x * a.per_cta;
-  const int64_t i1 = min(i0 + a.per_cta, a.nvt);
-  if (i0 >= i1) return;
-  const int nch = (m + mc - 1) / mc;
-  const int64_t S = (i1 - i0) * nch;  // stages
+  // persistent CTA over a balanced range of the linearised (query group, tile) list
+  const int64_t total = a.nqg * a.nvt;
+  const int64_t w0 = (int64_t)blockIdx.x * total / gridDim.x;
+  const int64_t w1 = (int64_t)(blockIdx.x + 1) * total / gridDim.x;
+  if (w0 >= w1) return;
+  const int nch = RES ? 1 : (m + mc - 1) / mc;
+  const int64_t S = (w1 - w0) * nch;  // stages
 
-  const float* tt_q = a.tt + qg * (int64_t)m * k * 32;
-  auto issue_at = [&](int b, int64_t vi, int ch) {
+  auto issue_at = [&](int b, int64_t w, int ch) {
+    const int64_t qg = w / a.nvt;
+    const int64_t tile = a.tile_off + (w - qg * a.nvt) * a.tile_step;
     const int j0 = ch * mc;
     const int mcur = min(mc, m - j0);
-    const int64_t tile = a.tile_off + vi * a.tile_step;
-    const uint32_t tb = (uint32_t)mcur * k * 32 * 4, cb = (uint32_t)mcur * TILE8;
+    const uint32_t cb = (uint32_t)mcur * TILE8;
+    const uint32_t tb = RES ? 0u : (uint32_t)mcur * row_bytes;
     mbar_expect_tx(&bars[b], tb + cb);
-    bulk_g2s(sm8 + b * tab_bytes, tt_q + (int64_t)j0 * k * 32, tb, &bars[b]);
-    bulk_g2s(sm8 + 2 * tab_bytes + b * code_bytes, a.codes + (tile * m + j0) * (int64_t)TILE8, cb, &bars[b]);
+    if (!RES) bulk_g2s(sm8 + b * tab_bytes, a.tt + (qg * m + j0) * (int64_t)k * 32, tb, &bars[b]);
+    bulk_g2s(code_base + b * code_bytes, a.codes + (tile * m + j0) * (int64_t)TILE8, cb, &bars[b]);
+  };
+  auto next_of = [&](int64_t w, int ch, int steps, int64_t& w2, int& ch2) {
+    ch2 = ch + steps;
+    w2 = w;
+    while (ch2 >= nch) {
+      ch2 -= nch;
+      ++w2;
+    }
   };
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    issue_at(0, i0, 0);
+    issue_at(0, w0, 0);
     if (S > 1) {
-      if (nch > 1) issue_at(1, i0, 1);
-      else issue_at(1, i0 + 1, 0);
+      int64_t w2;
+      int ch2;
+      next_of(w0, 0, 1, w2, ch2);
+      issue_at(1, w2, ch2);
     }
   }
 
-  float part[C8];
-#pragma unroll
-  for (int c = 0; c < C8; ++c) part[c] = 0.f;
+  int64_t q = -1, cur_qg = -1;
+  bool qvalid = false;
+  uint32_t theta = 0;
+  uint32_t tphase = 0;
 
-  int64_t s = 0;
-  for (int64_t vi = i0; vi < i1; ++vi) {
-    const int64_t tile = a.tile_off + vi * a.tile_step;
-    for (int ch = 0; ch < nch; ++ch, ++s) {
+  auto flush = [&]() {
+    if (MODE == MODE8_FILTER && ncand > 0) {
+      const int pos = atomicAdd(a.cand_cnt + q, ncand);
+      for (int i = 0; i < ncand; ++i)
+        if (pos + i < a.cap) a.cand[q * a.cap + pos + i] = (uint64_t)stage[i * SCAN8_THREADS];
+      ncand = 0;
+    }
+  };
+  // epilogue for the NV consecutive codes of this warp starting at code c0 / column col
+  auto emit = [&](const auto& vals, int64_t c0, int64_t col) {
+    constexpr int nv = (int)(sizeof(vals) / sizeof(vals[0]));
+    if (!qvalid) return;
+    if (MODE == MODE8_FILTER) {
+      unsigned long long hit = 0;
+#pragma unroll
+      for (int c = 0; c < nv; ++c) hit |= (unsigned long long)(vals[c] <= theta) << c;
+      if (hit) {  // rare: one divergent branch per nv codes
+        const int64_t valid = a.n - c0;
+        if (valid < nv) hit &= valid <= 0 ? 0ull : ((1ull << valid) - 1ull);
+        while (hit) {
+          const int c = __ffsll((long long)hit) - 1;
+          hit &= hit - 1;
+          stage[ncand * SCAN8_THREADS] = (uint32_t)(c0 + c);
+          if (++ncand == CSTAGE8) flush();
+        }
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < nv; c += 4) {
+        uint4 o;
+        o.x = (c0 + c + 0 < a.n) ? vals[c + 0] : 0xFFFFFFFFu;
+        o.y = (c0 + c + 1 < a.n) ? vals[c + 1] : 0xFFFFFFFFu;
+        o.z = (c0 + c + 2 < a.n) ? vals[c + 2] : 0xFFFFFFFFu;
+        o.w = (c0 + c + 3 < a.n) ? vals[c + 3] : 0xFFFFFFFFu;
+        *reinterpret_cast<uint4*>(a.out + q * a.ld + col + c) = o;
+      }
+    }
+  };
+  // 2 x 16 lookups (components jj, jj+1 of 16 codes), one IADD3 per code
+  auto lookup16x2 = [&](uint32_t tj0, const uint4& w0v, uint32_t tj1, const uint4& w1v, uint32_t* acc) {
+    const uint32_t a0[4] = {w0v.x, w0v.y, w0v.z, w0v.w};
+    const uint32_t a1[4] = {w1v.x, w1v.y, w1v.z, w1v.w};
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const uint32_t c0 = prmt(a0[e >> 2], 0u, 0x4440u | (uint32_t)(e & 3));
+      const uint32_t c1 = prmt(a1[e >> 2], 0u, 0x4440u | (uint32_t)(e & 3));
+      uint32_t t0, t1;
+      asm volatile("ld.shared.u16 %0, [%1];" : "=r"(t0) : "r"(imad8(c0, c64, tj0)));
+      asm volatile("ld.shared.u16 %0, [%1];" : "=r"(t1) : "r"(imad8(c1, c64, tj1)));
+      acc[e] = acc[e] + t0 + t1;
+    }
+  };
+  auto lookup16 = [&](uint32_t tj, const uint4& w, uint32_t* acc) {
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const uint32_t code = prmt(ws[e >> 2], 0u, 0x4440u | (uint32_t)(e & 3));
+      uint32_t t;
+      asm volatile("ld.shared.u16 %0, [%1];" : "=r"(t) : "r"(imad8(code, c64, tj)));
+      acc[e] = imad8(t, one, acc[e]);
+    }
+  };
+  auto switch_group = [&](int64_t qg) {
+    flush();
+    q = qg * 32 + lane;
+    qvalid = q < a.nq;
+    theta = (MODE == MODE8_FILTER && qvalid) ? a.theta[q] : 0u;
+    cur_qg = qg;
+  };
+
+  if constexpr (RES) {
+    int64_t s = 0;
+    for (int64_t w = w0; w < w1; ++w, ++s) {
+      const int64_t qg = w / a.nvt;
+      const int64_t vi = w - qg * a.nvt;
+      const int64_t tile = a.tile_off + vi * a.tile_step;
+      if (qg != cur_qg) {
+        switch_group(qg);
+        __syncthreads();  // every warp is done with the previous group's tables
+        if (threadIdx.x == 0) {
+          mbar_expect_tx(&bars[2], tab_bytes);
+          bulk_g2s(sm8, a.tt + qg * (int64_t)m * k * 32, tab_bytes, &bars[2]);
+        }
+        mbar_wait(&bars[2], tphase);
+        tphase ^= 1;
+      }
       const int b = (int)(s & 1);
       mbar_wait(&bars[b], (uint32_t)((s >> 1) & 1));
-      const int mcur = min(mc, m - ch * mc);
-      const float* T = reinterpret_cast<const float*>(sm8 + b * tab_bytes) + lane;
-      const uint8_t* cb = sm8 + 2 * tab_bytes + b * code_bytes + warp * C8;
-#pragma unroll
+      const uint32_t tbase = smem_u32(sm8) + 2u * lane;
+      const uint8_t* cb = code_base + b * code_bytes + warp * C8;
       for (int v = 0; v < C8 / 16; ++v) {
+        uint32_t acc[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) acc[e] = 0u;
         const uint8_t* cv = cb + v * 16;
-        for (int jj = 0; jj < mcur; ++jj) {
-          const float* Tj = T + jj * k * 32;
-          const uint4 w = *reinterpret_cast<const uint4*>(cv + jj * TILE8);
-          const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const uint32_t code = (ws[e >> 2] >> (8 * (e & 3))) & 0xFFu;
-            part[v * 16 + e] += Tj[code * 32];
-          }
-        }
-      }
-      if (ch == nch - 1) {
-        const int64_t c0 = tile * TILE8 + warp * C8;
-        if (MODE == MODE8_FILTER) {
-          if (qvalid) {
-#pragma unroll
-            for (int c = 0; c < C8; ++c) {
-              if (part[c] <= theta && c0 + c < a.n) {
-                const int pos = atomicAdd(a.cand_cnt + q, 1);
-                if (pos < a.cap) a.cand[q * a.cap + pos] = (uint64_t)(uint32_t)(c0 + c);
-              }
-            }
-          }
-        } else {
-          if (qvalid) {
-            const int64_t col = vi * TILE8 + warp * C8;
-            const float inf = __int_as_float(0x7f800000);
-#pragma unroll
-            for (int c = 0; c < C8; c += 4) {
-              float4 o;
-              o.x = (c0 + c + 0 < a.n) ? part[c + 0] : inf;
-              o.y = (c0 + c + 1 < a.n) ? part[c + 1] : inf;
-              o.z = (c0 + c + 2 < a.n) ? part[c + 2] : inf;
-              o.w = (c0 + c + 3 < a.n) ? part[c + 3] : inf;
-              if (col + c + 3 < a.ld) *reinterpret_cast<float4*>(a.out + q * a.ld + col + c) = o;
-            }
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < C8; ++c) part[c] = 0.f;
+        int jj = 0;
+        for (; jj + 1 < m; jj += 2)
+          lookup16x2(tbase + (uint32_t)jj * row_bytes, *reinterpret_cast<const uint4*>(cv + jj * TILE8),
+                     tbase + (uint32_t)(jj + 1) * row_bytes, *reinterpret_cast<const uint4*>(cv + (jj + 1) * TILE8),
+                     acc);
+        if (jj < m) lookup16(tbase + (uint32_t)jj * row_bytes, *reinterpret_cast<const uint4*>(cv + jj * TILE8), acc);
+        emit(acc, tile * TILE8 + warp * C8 + v * 16, vi * TILE8 + warp * C8 + v * 16);
       }
       __syncthreads();
-      if (threadIdx.x == 0 && s + 2 < S) {
-        // stage s+2 lives in buffer b: its tile/chunk follow (vi, ch) by two steps
-        int ch2 = ch + 2;
-        int64_t vi2 = vi;
-        while (ch2 >= nch) {
-          ch2 -= nch;
-          ++vi2;
+      if (threadIdx.x == 0 && s + 2 < S) issue_at(b, w + 2, 0);
+    }
+  } else {
+    uint32_t part[C8];
+#pragma unroll
+    for (int c = 0; c < C8; ++c) part[c] = 0u;
+    int64_t s = 0;
+    for (int64_t w = w0; w < w1; ++w) {
+      const int64_t qg = w / a.nvt;
+      const int64_t vi = w - qg * a.nvt;
+      const int64_t tile = a.tile_off + vi * a.tile_step;
+      if (qg != cur_qg) switch_group(qg);
+      for (int ch = 0; ch < nch; ++ch, ++s) {
+        const int b = (int)(s & 1);
+        mbar_wait(&bars[b], (uint32_t)((s >> 1) & 1));
+        const int mcur = min(mc, m - ch * mc);
+        const uint32_t tbase = smem_u32(sm8 + b * tab_bytes) + 2u * lane;
+        const uint8_t* cb = code_base + b * code_bytes + warp * C8;
+#pragma unroll
+        for (int v = 0; v < C8 / 16; ++v) {
+          const uint8_t* cv = cb + v * 16;
+          int jj = 0;
+          for (; jj + 1 < mcur; jj += 2)
+            lookup16x2(tbase + (uint32_t)jj * row_bytes, *reinterpret_cast<const uint4*>(cv + jj * TILE8),
+                       tbase + (uint32_t)(jj + 1) * row_bytes,
+                       *reinterpret_cast<const uint4*>(cv + (jj + 1) * TILE8), part + v * 16);
+          if (jj < mcur)
+            lookup16(tbase + (uint32_t)jj * row_bytes, *reinterpret_cast<const uint4*>(cv + jj * TILE8),
+                     part + v * 16);
         }
-        issue_at(b, vi2, ch2);
+        if (ch == nch - 1) {
+          emit(part, tile * TILE8 + warp * C8, vi * TILE8 + warp * C8);
+#pragma unroll
+          for (int c = 0; c < C8; ++c) part[c] = 0u;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && s + 2 < S) {
+          int64_t w2;
+          int ch2;
+          next_of(w, ch, 2, w2, ch2);
+          issue_at(b, w2, ch2);
+        }
       }
     }
   }
+  flush();
 }
 
-int pick_mc(int m, int k) {
-  int mc = CHUNK_BUDGET / (k * 128 + TILE8);
-  mc = std::max(1, std::min(mc, m));
-  return mc;
-}
+constexpr int RESIDENT_BUDGET = 160 * 1024;
 
 template <int MODE>
 int launch_scan8(pqs_ctx* ctx, Scan8Args a) {
-  a.mc = pick_mc(a.m, a.k);
-  const size_t smem = 2 * ((size_t)a.mc * a.k * 128 + (size_t)a.mc * TILE8);
-  PQS_CUDA(ctx, cudaFuncSetAttribute(scan8_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t qgroups = cdiv(a.nq, 32);
-  const int64_t target = (int64_t)ctx->sm_count * 4;
-  int64_t splits = std::max<int64_t>(1, cdiv(target, qgroups));
-  splits = std::min<int64_t>(splits, a.nvt);
-  a.per_cta = cdiv(a.nvt, splits);
-  splits = cdiv(a.nvt, a.per_cta);
-  dim3 grid((unsigned)splits, (unsigned)qgroups);
-  scan8_kernel<MODE><<<grid, SCAN8_THREADS, smem, ctx->stream>>>(a);
+  const size_t row_bytes = (size_t)a.k * 64;
+  a.resident = (size_t)a.m * row_bytes <= RESIDENT_BUDGET ? 1 : 0;
+  if (a.resident) {
+    a.mc = a.m;
+  } else {
+    int mc = (int)(CHUNK_BUDGET / (2 * row_bytes + 2 * TILE8));
+    a.mc = std::max(1, std::min(mc, a.m));
+  }
+  const size_t tab = a.resident ? (size_t)a.m * row_bytes : 2 * (size_t)a.mc * row_bytes;
+  size_t smem = tab + 2 * (size_t)a.mc * TILE8;
+  if (MODE == MODE8_FILTER) smem += (size_t)CSTAGE8 * SCAN8_THREADS * 4;
+  if (smem > 227 * 1024) return set_err(ctx, PQS_ERR_UNSUPPORTED, "scan8: table chunk does not fit shared memory");
+  auto kern = a.resident ? scan8_kernel<MODE, true> : scan8_kernel<MODE, false>;
+  PQS_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  a.nqg = cdiv(a.nq, 32);
+  const int64_t total = a.nqg * a.nvt;
+  if (total <= 0) return PQS_OK;
+  const int64_t nctas = std::min<int64_t>(total, (int64_t)ctx->sm_count);  // 1 CTA / SM (smem)
+  a.one = 1u;
+  a.c64 = 64u;
+  dim3 grid((unsigned)nctas);
+  kern<<<grid, SCAN8_THREADS, smem, ctx->stream>>>(a);
   PQS_LAUNCHED(ctx);
   return PQS_OK;
 }
 
-// float threshold: theta = r-th smallest valid sample value + 2*aerr, rounded up
-__global__ void theta8_kernel(const float* __restrict__ sample, int64_t ns, int r, const float* __restrict__ aerr,
-                              float* __restrict__ theta) {
+// threshold from the u32 lower-bound sample (scale e0): t = r-th smallest;
+// D' = (t + m) * 2^-e0 + slack bounds the r-th smallest d - O; the filter
+// scale e1 puts D' near 2^16 * max(1, m/8); theta = floor(D' * 2^e1).
+__global__ void theta8_kernel(const uint32_t* __restrict__ sample, int64_t ns, int r, int m,
+                              const int* __restrict__ e0, const double* __restrict__ slack, int* __restrict__ e1,
+                              uint32_t* __restrict__ theta) {
   __shared__ unsigned int hist[256];
   __shared__ unsigned int s_prefix, s_k, s_valid;
   const int64_t q = blockIdx.x;
-  const float* row = sample + q * ns;
+  const uint32_t* row = sample + q * ns;
   if (threadIdx.x == 0) {
     s_prefix = 0;
     s_k = (unsigned)(r - 1);
@@ -274,11 +429,14 @@ __global__ void theta8_kernel(const float* __restrict__ sample, int64_t ns, int 
   }
   __syncthreads();
   unsigned int valid = 0;
-  for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) valid += isfinite(row[i]) ? 1u : 0u;
+  for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) valid += row[i] != 0xFFFFFFFFu ? 1u : 0u;
   atomicAdd(&s_valid, valid);
   __syncthreads();
   if (s_valid < (unsigned)r) {
-    if (threadIdx.x == 0) theta[q] = __int_as_float(0x7f800000);
+    if (threadIdx.x == 0) {
+      e1[q] = e0[q];
+      theta[q] = 0xFFFFFFFEu;
+    }
     return;
   }
   for (int shift = 24; shift >= 0; shift -= 8) {
@@ -286,11 +444,10 @@ __global__ void theta8_kernel(const float* __restrict__ sample, int64_t ns, int 
     __syncthreads();
     const unsigned prefix = s_prefix;
     for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
-      const float v = row[i];
-      if (!isfinite(v)) continue;
-      const unsigned key = fkey(v);
-      const bool match = (shift == 24) ? true : ((key ^ prefix) >> (shift + 8)) == 0;
-      if (match) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+      const uint32_t v = row[i];
+      if (v == 0xFFFFFFFFu) continue;
+      const bool match = (shift == 24) ? true : ((v ^ prefix) >> (shift + 8)) == 0;
+      if (match) atomicAdd(&hist[(v >> shift) & 255u], 1u);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -306,14 +463,20 @@ __global__ void theta8_kernel(const float* __restrict__ sample, int64_t ns, int 
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    const double t = (double)fkey_inv(s_prefix) + 2.0 * (double)aerr[q];
-    float f = (float)t;
-    if ((double)f < t) f = nextafterf(f, __int_as_float(0x7f800000));
-    theta[q] = nextafterf(f, __int_as_float(0x7f800000));
+    const double Dp = ldexp((double)s_prefix + (double)m, -e0[q]) + slack[q];
+    const double target = 65536.0 * (m > 8 ? m / 8.0 : 1.0);
+    int e = e0[q];
+    if (Dp > 0.0) {
+      e = (int)floor(log2(target / Dp));
+      e = max(-1000, min(1000, e));
+    }
+    const double th = floor(ldexp(Dp, e) * (1.0 + 1e-12));
+    e1[q] = e;
+    theta[q] = th >= 4294967294.0 ? 0xFFFFFFFEu : (uint32_t)th;
   }
 }
 
-__global__ void fill_f32_kernel(float* p, int64_t n, float v) {
+__global__ void fill_u32_kernel(uint32_t* p, int64_t n, uint32_t v) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
 }
@@ -359,52 +522,52 @@ int launch_scan_distances(pqs_ctx* ctx, const pqs_db* db, const float* d_tables,
   return PQS_OK;
 }
 
-int launch_tables_scan8(pqs_ctx* ctx, const float* d_tables, int64_t nq, int m, int k, float* d_tt, float* d_aerr) {
-  const int64_t total = cdiv(nq, 32) * m * (int64_t)k * 32;
-  tables_scan8_kernel<<<(unsigned)cdiv(total, 256), 256, 0, ctx->stream>>>(d_tables, nq, m, k, d_tt);
-  PQS_LAUNCHED(ctx);
-  aerr_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(d_tables, nq, m, k, d_aerr);
-  PQS_LAUNCHED(ctx);
-  return PQS_OK;
-}
-
 int run_adc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t nq, int r, double* d_dist,
                  int64_t* d_ids, int32_t* d_count) {
   const int64_t n = db->n;
   const int m = db->m, k = db->k;
   if (n == 0) {
-    // nothing to scan: every row is empty
     SelArgs s{};
     s.src = SEL_DENSE_F64;
     s.nq = nq;
     s.r = r;
     s.n = 0;
-    s.dense = nullptr;
     s.out_d = d_dist;
     s.out_i = d_ids;
     s.out_c = d_count;
     return launch_select(ctx, s);
   }
-  float* tt = nullptr;
-  float* aerr = nullptr;
+  // ---- u16 lower-bound tables, scale e0 (no saturation)
+  float* off = nullptr;
+  int* e0 = nullptr;
+  int* e1 = nullptr;
+  double* slack = nullptr;
+  uint16_t* tt = nullptr;
+  uint32_t* theta = nullptr;
+  PQS_TRY(scratch(ctx, S_AERR, (size_t)(nq * m), &off));
+  PQS_TRY(scratch(ctx, S_QMINMAX, (size_t)nq * 2, &e0));
+  e1 = e0 + nq;
+  PQS_TRY(scratch(ctx, S_PREFIX, (size_t)nq, &slack));
   PQS_TRY(scratch(ctx, S_TABLES_T, (size_t)(cdiv(nq, 32) * 32 * m * k), &tt));
-  PQS_TRY(scratch(ctx, S_AERR, (size_t)nq, &aerr));
-  PQS_TRY(launch_tables_scan8(ctx, d_tables, nq, m, k, tt, aerr));
+  PQS_TRY(scratch(ctx, S_THETA, (size_t)nq, &theta));
+  tables_u16_stats_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(d_tables, nq, m, k, off, e0, slack);
+  PQS_LAUNCHED(ctx);
+  const int64_t tt_total = cdiv(nq, 32) * m * (int64_t)k * 32;
+  tables_u16_kernel<<<(unsigned)cdiv(tt_total, 256), 256, 0, ctx->stream>>>(d_tables, off, e0, nq, m, k, tt);
+  PQS_LAUNCHED(ctx);
 
-  float* theta = nullptr;
-  PQS_TRY(scratch(ctx, S_THETA, (size_t)nq * 4, (uint8_t**)&theta));
   const int64_t cap = std::min<int64_t>(ctx->cand_cap, n);
   const int64_t r_eff = std::min<int64_t>(r, n);
   if (n <= cap) {
-    fill_f32_kernel<<<(unsigned)cdiv(nq, 256), 256, 0, ctx->stream>>>(theta, nq, __builtin_huge_valf());
+    fill_u32_kernel<<<(unsigned)cdiv(nq, 256), 256, 0, ctx->stream>>>(theta, nq, 0xFFFFFFFEu);
     PQS_LAUNCHED(ctx);
   } else {
     int64_t st = std::max<int64_t>(cdiv(db->ntiles, ctx->sample_div), cdiv(16 * r_eff, TILE8));
     st = std::min<int64_t>(st, db->ntiles);
     const int64_t step = std::max<int64_t>(1, db->ntiles / st);
     const int64_t ns = st * TILE8;
-    float* sample = nullptr;
-    PQS_TRY(scratch(ctx, S_SAMPLE, (size_t)(nq * ns) * 4, (uint8_t**)&sample));
+    uint32_t* sample = nullptr;
+    PQS_TRY(scratch(ctx, S_SAMPLE, (size_t)(nq * ns), &sample));
     Scan8Args a{};
     a.tt = tt;
     a.codes = db->codes8;
@@ -418,7 +581,10 @@ int run_adc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t 
     a.out = sample;
     a.ld = ns;
     PQS_TRY(launch_scan8<MODE8_DENSE>(ctx, a));
-    theta8_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(sample, ns, (int)r_eff, aerr, theta);
+    theta8_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(sample, ns, (int)r_eff, m, e0, slack, e1, theta);
+    PQS_LAUNCHED(ctx);
+    // rebuild the tables at the filter scale e1
+    tables_u16_kernel<<<(unsigned)cdiv(tt_total, 256), 256, 0, ctx->stream>>>(d_tables, off, e1, nq, m, k, tt);
     PQS_LAUNCHED(ctx);
   }
 
