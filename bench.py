@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-s", type=float, default=20.0, help="CPU work budget of the baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--engine", type=int, default=0, help="Quick ADC scan engine: 0 auto, 1 PRMT, 2 tcgen05")
     return ap.parse_args()
 
 
@@ -229,6 +230,7 @@ def main():
     ctx = P.Context(local)
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
+    ctx.set_option(_lib.OPT_SCAN4_ENGINE, args.engine)
     pq = P.ProductQuantizer(cfg["m"], cfg["b"], cfg["d"], books)
     from paper_1712_02912_b200.sharded import ShardedSearch
 
@@ -269,6 +271,7 @@ def main():
         step_device()
         ends[s].record(stream)
         scan_ns.append(ctx.stat(_lib.STAT_LAST_SCAN_NS))
+    cand_max, cand_tot = ctx.stat(_lib.STAT_LAST_MAX_CAND), ctx.stat(_lib.STAT_LAST_CAND_TOTAL)
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
@@ -364,6 +367,8 @@ def main():
         "config": config_dict(args.config, cfg, world),
         "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
+        "candidates": {"max_per_query": cand_max, "mean_per_query": cand_tot / nq,
+                       "note": "codes surviving the certified threshold filter, re-scored exactly"},
         "clocks": clk,
         "roofline": roofline,
         "impl": "ours",

@@ -57,7 +57,8 @@ enum pqs_io { PQS_IO_HOST = 0, PQS_IO_DEVICE = 1 };
 enum pqs_option {
   PQS_OPT_CAND_CAP = 1,     /* candidate slots per query in a filtered scan (default 32768) */
   PQS_OPT_SAMPLE_DIV = 2,   /* threshold sample = 1/SAMPLE_DIV of the code tiles (default 32) */
-  PQS_OPT_FORCE_FALLBACK = 3/* 1: run the exact dense fallback for every query (testing) */
+  PQS_OPT_FORCE_FALLBACK = 3,/* 1: run the exact dense fallback for every query (testing) */
+  PQS_OPT_SCAN4_ENGINE = 4  /* Quick ADC scan: 0 auto (tcgen05 int8 when possible), 1 PRMT, 2 tcgen05 */
 };
 
 enum pqs_stat {
@@ -66,7 +67,8 @@ enum pqs_stat {
   PQS_STAT_LAST_OVERFLOW = 3,  /* queries that took the dense fallback in the last search */
   PQS_STAT_LAST_EVALS = 4,     /* (query, code) evaluations of the last search (IVF: exact count) */
   PQS_STAT_LAST_SCAN_NS = 5,   /* device time of the last search's main scan kernel (CUDA events) */
-  PQS_STAT_LAST_SCAN_LAUNCHES = 6 /* launches of that kernel in the last search */
+  PQS_STAT_LAST_SCAN_LAUNCHES = 6, /* launches of that kernel in the last search */
+  PQS_STAT_LAST_CAND_TOTAL = 7     /* sum over queries of the candidates of the last search */
 };
 
 int pqs_api_version(void);

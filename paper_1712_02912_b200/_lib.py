@@ -27,12 +27,14 @@ IO_DEVICE = 1
 OPT_CAND_CAP = 1
 OPT_SAMPLE_DIV = 2
 OPT_FORCE_FALLBACK = 3
+OPT_SCAN4_ENGINE = 4
 STAT_LAUNCHES = 1
 STAT_LAST_MAX_CAND = 2
 STAT_LAST_OVERFLOW = 3
 STAT_LAST_EVALS = 4
 STAT_LAST_SCAN_NS = 5
 STAT_LAST_SCAN_LAUNCHES = 6
+STAT_LAST_CAND_TOTAL = 7
 
 _p = ctypes.c_void_p
 _i = ctypes.c_int

@@ -200,6 +200,10 @@ int pqs_ctx_set_option(pqs_ctx* ctx, int option, int64_t value) {
     case PQS_OPT_FORCE_FALLBACK:
       ctx->force_fallback = value ? 1 : 0;
       return PQS_OK;
+    case PQS_OPT_SCAN4_ENGINE:
+      PQS_CHECK(ctx, value >= 0 && value <= 2, "scan4 engine must be 0, 1 or 2");
+      ctx->scan4_engine = (int)value;
+      return PQS_OK;
   }
   return set_err(ctx, PQS_ERR_INVALID, "unknown option");
 }
@@ -213,6 +217,7 @@ int pqs_ctx_get_stat(pqs_ctx* ctx, int stat, int64_t* out) {
     case PQS_STAT_LAST_EVALS: *out = ctx->last_evals; return PQS_OK;
     case PQS_STAT_LAST_SCAN_NS: *out = ctx->last_scan_ns; return PQS_OK;
     case PQS_STAT_LAST_SCAN_LAUNCHES: *out = ctx->last_scan_launches; return PQS_OK;
+    case PQS_STAT_LAST_CAND_TOTAL: *out = ctx->last_cand_total; return PQS_OK;
   }
   return set_err(ctx, PQS_ERR_INVALID, "unknown stat");
 }

@@ -692,7 +692,7 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
   PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   PQS_TRY(scan_timer_collect(ctx));
   std::vector<int> over;
-  int64_t mx = 0, total_evals = 0, worst_total = 0;
+  int64_t mx = 0, ctot = 0, total_evals = 0, worst_total = 0;
   for (int64_t q = 0; q < nq; ++q) {
     int64_t tot = 0;
     for (int p = 0; p < ma; ++p) {
@@ -701,6 +701,7 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
     }
     total_evals += tot;
     mx = std::max<int64_t>(mx, hcnt[q]);
+    ctot += hcnt[q];
     const int64_t r_eff = std::min<int64_t>(r, tot);
     if (hcnt[q] > cap || hcnt[q] < r_eff || ctx->force_fallback) {
       over.push_back((int)q);
@@ -709,6 +710,7 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
   }
   ctx->last_evals = total_evals;
   ctx->last_max_cand = mx;
+  ctx->last_cand_total = ctot;
   ctx->last_overflow = (int64_t)over.size();
   if (!over.empty()) {
     const int64_t fcap = std::max<int64_t>(worst_total, 1);

@@ -55,6 +55,7 @@ enum ScratchSlot {
   S_MISC,
   S_WORK,     // dynamic work counters
   S_QT_WORK,  // quantized tables of a Quick ADC search
+  S_TC_B, S_TC_TH, S_TC_REC, S_TC_RECCNT,
   S_NSLOTS
 };
 
@@ -67,12 +68,14 @@ struct pqs_ctx {
   int64_t cand_cap = 32768;
   int sample_div = 32;
   int force_fallback = 0;
+  int scan4_engine = 0;  // 0 auto (tcgen05 when possible), 1 PRMT, 2 tcgen05
   int64_t launches = 0;
   int64_t last_max_cand = 0;
   int64_t last_overflow = 0;
   int64_t last_evals = 0;
   int64_t last_scan_ns = 0;
   int64_t last_scan_launches = 0;
+  int64_t last_cand_total = 0;
   cudaEvent_t scan_ev[2] = {nullptr, nullptr};
   Scratch scratch[S_NSLOTS];
   int* host_flag = nullptr;  // pinned

@@ -528,6 +528,9 @@ __global__ void gather_rows_u8_kernel(const uint8_t* __restrict__ src, const int
 
 }  // namespace
 
+int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const uint8_t* d_theta, int64_t nq,
+                    uint64_t* cand, int* cand_cnt, int64_t cap, int* overflow);
+
 // ---------------------------------------------------------------------------
 int build_db4(pqs_ctx* ctx, pqs_db* db, const uint8_t* d_codes) {
   const int hp = db->mp / 2;
@@ -582,6 +585,7 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
   PQS_TRY(scratch(ctx, S_THETA, (size_t)nq, &theta));
   const int64_t cap = std::min<int64_t>(ctx->cand_cap, std::max<int64_t>(n, 1));
   const int64_t r_eff = std::min<int64_t>(r, n);
+  bool sampled = false;
   if (n <= cap) {
     fill_u8_kernel<<<(unsigned)cdiv(nq, 256), 256, 0, ctx->stream>>>(theta, nq, 127);
     PQS_LAUNCHED(ctx);
@@ -617,6 +621,7 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
     PQS_LAUNCHED(ctx);
     theta4_final_kernel<<<(unsigned)cdiv(nq, 128), 128, 0, ctx->stream>>>(ghist, nq, (int)r_eff, theta);
     PQS_LAUNCHED(ctx);
+    sampled = true;
   }
 
   // ---- K4 filtered scan
@@ -639,9 +644,25 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
     a.cand = cand;
     a.cand_cnt = cnt;
     a.cap = cap;
-    PQS_TRY(scan_timer_begin(ctx));
-    PQS_TRY(launch_scan4<MODE_FILTER>(ctx, db->mp, a, nq));
-    PQS_TRY(scan_timer_end(ctx));
+    int done = 0;
+    if (sampled && ctx->scan4_engine != 1) {
+      int overflow = 0;
+      const int st = launch_scan4_tc(ctx, db, d_qt, theta, nq, cand, cnt, cap, &overflow);
+      if (st == PQS_OK && !overflow) {
+        done = 1;
+      } else if (st == PQS_OK || st == PQS_ERR_UNSUPPORTED) {
+        if (ctx->scan4_engine == 2 && st == PQS_ERR_UNSUPPORTED)
+          return set_err(ctx, PQS_ERR_UNSUPPORTED, "tcgen05 Quick ADC scan: unsupported shape (needs m <= 16)");
+        PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nq, ctx->stream));  // redo with PRMT
+      } else {
+        return st;
+      }
+    }
+    if (!done) {
+      PQS_TRY(scan_timer_begin(ctx));
+      PQS_TRY(launch_scan4<MODE_FILTER>(ctx, db->mp, a, nq));
+      PQS_TRY(scan_timer_end(ctx));
+    }
     ctx->last_scan_launches = 1;
   }
   ctx->last_evals = nq * n;
@@ -674,12 +695,14 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
   PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   PQS_TRY(scan_timer_collect(ctx));
   std::vector<int> over;
-  int64_t mx = 0;
+  int64_t mx = 0, ctot = 0;
   for (int64_t q = 0; q < nq; ++q) {
     mx = std::max<int64_t>(mx, hcnt[q]);
+    ctot += hcnt[q];
     if (hcnt[q] > cap || hcnt[q] < r_eff || ctx->force_fallback) over.push_back((int)q);
   }
   ctx->last_max_cand = mx;
+  ctx->last_cand_total = ctot;
   ctx->last_overflow = (int64_t)over.size();
   if (!over.empty()) {
     const int64_t B = std::max<int64_t>(1, std::min<int64_t>((int64_t)over.size(), (int64_t)(1ll << 30) / std::max<int64_t>(n, 1)));

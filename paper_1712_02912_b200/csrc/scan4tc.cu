@@ -1,0 +1,495 @@
+// scan4tc.cu -- Quick ADC scan on the 5th-gen tensor cores (tcgen05, kind::i8).
+//
+// Reference semantics: quantized_distances / qadc_scan (quickadc.py:87-141):
+// bin(code) = min(sum_j qt[j][code_j], 127) with qt entries in [0, 127].
+//
+// The sum is an exact integer GEMM: with A[code][16j + i] = (code_j == i)
+// (one-hot, K = 16 m = 256 for m = 16) and B[q][16j + i] = qt_q[j][i],
+//   S[code][q] = sum_k A[code][k] * B[q][k]         (u8 x u8 -> s32, exact)
+// and the filter keeps (code, q) with S <= theta_q (theta_q <= 127, so
+// S = bin for every survivor).  Per CTA (persistent, one per SM):
+//   * B for a group of 256 queries (64 KB, canonical K-major no-swizzle
+//     layout) is TMA-bulk-copied once per group (double-buffered);
+//   * warps 4-7 expand 128 codes per tile from the 4-bit quad layout into the
+//     one-hot A tile (32 KB, double-buffered) with 16-byte shared stores;
+//   * one elected thread of warp 8 issues 8 tcgen05.mma (M=128, N=256, K=32)
+//     per tile into a TMEM accumulator (2 x 256 columns, double-buffered) and
+//     commits to mbarriers;
+//   * warps 0-3 tcgen05.ld the accumulator (lane = code, column = query),
+//     compare against the per-query threshold with a sign-bit OR (1.5
+//     instr/value) and append the rare survivors to a per-CTA record list.
+// A small bucketing kernel turns the records into the per-query candidate
+// lists consumed by select_kernel (SEL_CAND_BIN), exactly as the PRMT scan.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+#include <cstdio>
+#include <cstdlib>
+
+#include "pqs_common.cuh"
+
+namespace {
+
+constexpr int TC_M = 128;          // codes per tile (TMEM lanes)
+constexpr int TC_N = 256;          // queries per group (TMEM columns per accumulator)
+constexpr int TC_K = 256;          // one-hot width (16 components x 16 values)
+constexpr int A_BYTES = TC_M * TC_K;     // 32 KB
+constexpr int B_BYTES = TC_N * TC_K;     // 64 KB
+constexpr int LBO_A = (TC_M / 8) * 128;  // byte distance between K-chunks of A (2048)
+constexpr int LBO_B = (TC_N / 8) * 128;  // ... of B (4096)
+constexpr int TC_THREADS = 13 * 32;      // 8 epilogue + 4 producer + 1 MMA warp
+constexpr int EPI_WARPS = 8;
+constexpr int ESTAGE = 48;  // per-thread survivor staging slots (u32)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// wait with exponential nanosleep backoff (for warps that are not on the critical path)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ns = 32;
+  while (true) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(ns);
+    ns = ns < 256 ? ns * 2 : 256;
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// canonical K-major, no-swizzle shared-memory matrix descriptor (sm100 UMMA)
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
+  return d;                // base offset 0, lbo mode 0, layout SWIZZLE_NONE (0)
+}
+
+// instruction descriptor: u8 x u8 -> s32, K-major A and B, M=128, N=256
+constexpr uint32_t IDESC = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(TC_N >> 3) << 17) |
+                           ((uint32_t)(TC_M >> 4) << 24);
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(IDESC), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+#define TMEM_LD32(taddr, v)                                                                                     \
+  asm volatile(                                                                                                 \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17," \
+      "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                       \
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),       \
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), \
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),            \
+        "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),            \
+        "=r"(v[30]), "=r"(v[31])                                                                              \
+      : "r"(taddr))
+
+struct Scan4TcArgs {
+  const uint32_t* words;   // 4-bit quad layout (mp = 16: 8 words per quad)
+  int64_t n;
+  const uint8_t* bglob;    // [nqg][B_BYTES] canonical B tiles
+  const int* nthr;         // [nqg * 128] packed per-column-pair biases (see build_b_kernel)
+  int64_t nq, nqg, ntiles; // ntiles of TC_M codes
+  uint64_t* rec;           // [gridDim][rec_cap] (q << 40 | bin << 32 | idx)
+  int* rec_cnt;            // [gridDim]
+  int64_t rec_cap;
+  unsigned long long* dbg;  // optional per-tile timestamps of CTA 0 (ns), 8 per tile
+  int dbg_mode;             // 0 normal, 1 skip compare, 2 compare but never emit
+};
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smtc[];
+  uint8_t* sB = smtc;                           // 64 KB (one query group)
+  uint8_t* sA = smtc + B_BYTES;                 // 2 x 32 KB
+  uint32_t* sTh = reinterpret_cast<uint32_t*>(smtc + B_BYTES + 2 * A_BYTES);  // 2 x 128 packed biases
+  uint32_t* stage = reinterpret_cast<uint32_t*>(smtc + B_BYTES + 2 * A_BYTES + 2 * TC_N * 2);
+  __shared__ __align__(8) uint64_t bar_b[2], bar_afull[2], bar_aempty[2], bar_accfull[2], bar_accempty[2];
+  __shared__ uint32_t s_tmem;
+  __shared__ int s_cnt;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t total = a.nqg * a.ntiles;
+  // a CTA range spans <= 2 query groups: (group, tile) of item w without division
+  const int64_t gfirst = ((int64_t)blockIdx.x * total / gridDim.x) / a.ntiles;
+  const int64_t wsplit = (gfirst + 1) * a.ntiles;
+  auto group_of = [&](int64_t w) { return w < wsplit ? gfirst : gfirst + 1; };
+  auto tile_of = [&](int64_t w) { return w < wsplit ? w - gfirst * a.ntiles : w - wsplit; };
+  const int64_t w0 = (int64_t)blockIdx.x * total / gridDim.x;
+  const int64_t w1 = (int64_t)(blockIdx.x + 1) * total / gridDim.x;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar_b[i], 1);
+      mbar_init(&bar_afull[i], 4);     // one arrive per producer warp
+      mbar_init(&bar_aempty[i], 1);    // tcgen05.commit
+      mbar_init(&bar_accfull[i], 1);   // tcgen05.commit
+      mbar_init(&bar_accempty[i], EPI_WARPS);  // one arrive per epilogue warp
+    }
+    s_cnt = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {  // TMEM: 2 accumulators x 256 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+
+  if (w0 < w1) {
+    if (warp == EPI_WARPS + 4) {
+      // ---------------- MMA issuer (+ B loader) ----------------
+      if (lane == 0) {
+        int64_t cur_g = -1;
+        int gi = -1;
+        for (int64_t w = w0; w < w1; ++w) {
+          const int64_t it = w - w0;
+          const int64_t g = group_of(w);
+          if (g != cur_g) {
+            ++gi;
+            const int bb = gi & 1;
+            if (it > 0) {
+              // B is single-buffered: every MMA of the previous group must be done
+              // (its last commit to bar_aempty) before the new B overwrites it
+              mbar_wait(&bar_aempty[(it - 1) & 1], (uint32_t)(((it - 1) >> 1) & 1));
+            }
+            mbar_expect_tx(&bar_b[bb], (uint32_t)(B_BYTES + TC_N * 2));
+            bulk_g2s(sB, a.bglob + g * (int64_t)B_BYTES, B_BYTES, &bar_b[bb]);
+            bulk_g2s(sTh + bb * (TC_N / 2), a.nthr + g * (TC_N / 2), TC_N * 2, &bar_b[bb]);
+            mbar_wait(&bar_b[bb], 0);
+            cur_g = g;
+          }
+          const int ab = (int)(it & 1);
+          const uint32_t ph = (uint32_t)((it >> 1) & 1);
+          if (a.dbg && blockIdx.x == 0 && it < 64) a.dbg[it * 8 + 0] = gtime();
+          mbar_wait_sleep(&bar_afull[ab], ph);          // one-hot tile written
+          if (a.dbg && blockIdx.x == 0 && it < 64) a.dbg[it * 8 + 1] = gtime();
+          mbar_wait_sleep(&bar_accempty[ab], ph ^ 1);   // accumulator drained (first use passes)
+          if (a.dbg && blockIdx.x == 0 && it < 64) a.dbg[it * 8 + 2] = gtime();
+          tc_fence_after();
+          const uint32_t d_tmem = tmem + (uint32_t)(ab * TC_N);
+          const uint32_t a_base = smem_u32(sA + ab * A_BYTES);
+          const uint32_t b_base = smem_u32(sB);
+#pragma unroll
+          for (int s = 0; s < TC_K / 32; ++s) {
+            const uint64_t da = make_desc(a_base + (uint32_t)(2 * s) * LBO_A, LBO_A, 128);
+            const uint64_t db = make_desc(b_base + (uint32_t)(2 * s) * LBO_B, LBO_B, 128);
+            mma_i8(d_tmem, da, db, s > 0 ? 1u : 0u);
+          }
+          mma_commit(&bar_aempty[ab]);
+          mma_commit(&bar_accfull[ab]);
+        }
+      }
+    } else if (warp >= EPI_WARPS) {
+      // ---------------- one-hot producers: thread = code row ----------------
+      const int row = (warp - EPI_WARPS) * 32 + lane;  // 0..127
+      const uint32_t row_off = (uint32_t)(row >> 3) * 128u + (uint32_t)(row & 7) * 16u;
+      for (int64_t w = w0; w < w1; ++w) {
+        const int64_t it = w - w0;
+        const int ab = (int)(it & 1);
+        const uint32_t ph = (uint32_t)((it >> 1) & 1);
+        mbar_wait_sleep(&bar_aempty[ab], ph ^ 1);  // MMA finished reading this buffer
+        if (a.dbg && blockIdx.x == 0 && it < 64 && threadIdx.x == EPI_WARPS * 32) a.dbg[it * 8 + 3] = gtime();
+        const int64_t tile = tile_of(w);
+        const int64_t code = tile * TC_M + row;
+        uint32_t wd[8];
+        if (code < a.n) {
+          const uint4* src = reinterpret_cast<const uint4*>(a.words + (code >> 2) * 8);
+          const uint4 x0 = __ldg(src), x1 = __ldg(src + 1);
+          wd[0] = x0.x; wd[1] = x0.y; wd[2] = x0.z; wd[3] = x0.w;
+          wd[4] = x1.x; wd[5] = x1.y; wd[6] = x1.z; wd[7] = x1.w;
+        } else {
+#pragma unroll
+          for (int p = 0; p < 8; ++p) wd[p] = 0u;
+        }
+        const int sh = 4 * (int)(code & 3);
+        uint8_t* dst = sA + ab * A_BYTES + row_off;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t v = (wd[p] >> (16 * h + sh)) & 15u;  // component 2p+h
+            const uint32_t one = 1u << (8 * (v & 3));
+            uint4 o;
+            o.x = (v >> 2) == 0 ? one : 0u;
+            o.y = (v >> 2) == 1 ? one : 0u;
+            o.z = (v >> 2) == 2 ? one : 0u;
+            o.w = (v >> 2) == 3 ? one : 0u;
+            *reinterpret_cast<uint4*>(dst + (2 * p + h) * LBO_A) = o;
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (a.dbg && blockIdx.x == 0 && it < 64 && threadIdx.x == EPI_WARPS * 32) a.dbg[it * 8 + 4] = gtime();
+        if (lane == 0) mbar_arrive(&bar_afull[ab]);
+      }
+    } else {
+      // ---------------- epilogue: warp w reads TMEM lanes 32w..32w+31 (lane = code) ----------------
+      // survivors are staged per thread as 32-bit records (tile-iteration << 15 |
+      // column << 7 | bin) with predicated stores -- no divergent branches per value
+      uint32_t* my_stage = stage + threadIdx.x;  // [slot][EPI thread]
+      const int quad = warp & 3, half = warp >> 2;  // TMEM lane quadrant, query-column half
+      const int row = quad * 32 + lane;
+      int ncand = 0;
+      auto flush = [&]() {
+        const int base = atomicAdd(&s_cnt, ncand);
+        for (int i = 0; i < ncand; ++i) {
+          const uint32_t r = my_stage[i * (EPI_WARPS * 32)];
+          const int64_t wi = w0 + (int64_t)(r >> 15);
+          const int64_t gg = group_of(wi);
+          const int64_t code = tile_of(wi) * TC_M + row;
+          const int64_t q = gg * TC_N + ((r >> 7) & 255u);
+          if (base + i < a.rec_cap)
+            a.rec[(int64_t)blockIdx.x * a.rec_cap + base + i] =
+                ((uint64_t)q << 40) | ((uint64_t)(r & 127u) << 32) | (uint64_t)(uint32_t)code;
+        }
+        ncand = 0;
+      };
+      int64_t cur_g = -1;
+      int gi = -1;
+      for (int64_t w = w0; w < w1; ++w) {
+        const int64_t it = w - w0;
+        const int64_t g = group_of(w);
+        if (g != cur_g) {
+          ++gi;
+          mbar_wait(&bar_b[gi & 1], 0);  // biases of this group are in smem
+          cur_g = g;
+        }
+        const int ab = (int)(it & 1);
+        const uint32_t ph = (uint32_t)((it >> 1) & 1);
+        mbar_wait(&bar_accfull[ab], ph);
+        if (a.dbg && blockIdx.x == 0 && it < 64 && threadIdx.x == 0) a.dbg[it * 8 + 5] = gtime();
+        tc_fence_after();
+        const int64_t tile = tile_of(w);
+        const bool cvalid = tile * TC_M + row < a.n;
+        const uint32_t* bias = sTh + (gi & 1) * (TC_N / 2);
+        const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * TC_N);
+        const uint32_t itag = (uint32_t)it << 15;
+#pragma unroll 1
+        for (int c0 = half * (TC_N / 2); c0 < (half + 1) * (TC_N / 2); c0 += 32) {
+          uint32_t v[32];
+          TMEM_LD32(tbase + (uint32_t)c0, v);
+          uint32_t bs[16];
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) {
+            const uint4 b4 = *reinterpret_cast<const uint4*>(bias + c0 / 2 + i);  // broadcast
+            bs[i] = b4.x;
+            bs[i + 1] = b4.y;
+            bs[i + 2] = b4.z;
+            bs[i + 3] = b4.w;
+          }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          uint32_t x[16];
+          uint32_t allm = 0xFFFFFFFFu;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            // two query columns per word (S <= 2032 fits 16 bits); bit 15 clear <=> S <= theta
+            x[i] = __byte_perm(v[2 * i], v[2 * i + 1], 0x5410) + bs[i];
+            allm &= x[i];
+          }
+          if ((allm & 0x80008000u) != 0x80008000u && cvalid) {  // lane-local, rare
+            const uint32_t base = itag | ((uint32_t)c0 << 7);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const bool hit = ((x[i] >> (16 * h + 15)) & 1u) == 0u;
+                if (hit) my_stage[ncand * (EPI_WARPS * 32)] = base + ((uint32_t)(2 * i + h) << 7) + (v[2 * i + h] & 127u);
+                ncand += hit ? 1 : 0;
+              }
+            }
+          }
+          if (ncand > ESTAGE - 32) flush();  // rare
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (a.dbg && blockIdx.x == 0 && it < 64 && threadIdx.x == 0) a.dbg[it * 8 + 6] = gtime();
+        if (lane == 0) mbar_arrive(&bar_accempty[ab]);
+      }
+      if (ncand > 0) flush();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) a.rec_cnt[blockIdx.x] = s_cnt;
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// B tiles in the canonical K-major no-swizzle layout + negated thresholds:
+// B[n][k] at (k/16) * LBO_B + (n/8) * 128 + (n%8) * 16 + k%16, k = 16 j + i.
+__global__ void build_b_kernel(const uint8_t* __restrict__ qt, const uint8_t* __restrict__ theta, int64_t nq, int m,
+                               int64_t nqg, uint8_t* __restrict__ bglob, int* __restrict__ nthr) {
+  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // one per (group, n, j)
+  if (gid >= nqg * TC_N * 16) return;
+  const int j = (int)(gid % 16);
+  const int n = (int)((gid / 16) % TC_N);
+  const int64_t g = gid / (16 * TC_N);
+  const int64_t q = g * TC_N + n;
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if (q < nq && j < m) v = *reinterpret_cast<const uint4*>(qt + (q * m + j) * 16);
+  *reinterpret_cast<uint4*>(bglob + g * (int64_t)B_BYTES + (int64_t)j * LBO_B + (n >> 3) * 128 + (n & 7) * 16) = v;
+  if (j == 0 && (n & 1) == 0) {
+    // packed 16-bit lane biases of the column pair (n, n+1): S + (0x7FFF - theta) has
+    // bit 15 clear iff S <= theta; padding queries get 0x8000 (never clear)
+    const int64_t q1 = q + 1;
+    const uint32_t b0 = q < nq ? 0x7FFFu - theta[q] : 0x8000u;
+    const uint32_t b1 = q1 < nq ? 0x7FFFu - theta[q1] : 0x8000u;
+    nthr[g * (TC_N / 2) + (n >> 1)] = (int)(b0 | (b1 << 16));
+  }
+}
+
+// per-CTA survivor records -> per-query candidate lists (bin << 32 | idx)
+__global__ void bucket_kernel(const uint64_t* __restrict__ rec, const int* __restrict__ rec_cnt, int64_t rec_cap,
+                              uint64_t* __restrict__ cand, int* __restrict__ cand_cnt, int64_t cap) {
+  const int b = blockIdx.y;
+  const int cnt = min((int64_t)rec_cnt[b], rec_cap);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    const uint64_t r = rec[(int64_t)b * rec_cap + i];
+    const int64_t q = (int64_t)(r >> 40);
+    const int pos = atomicAdd(cand_cnt + q, 1);
+    if (pos < cap) cand[q * cap + pos] = r & 0xFFFFFFFFFFull;
+  }
+}
+
+}  // namespace
+
+// Filtered Quick ADC scan on tcgen05.  Returns PQS_ERR_UNSUPPORTED when the
+// shape is outside this kernel (caller falls back to the PRMT scan).
+int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const uint8_t* d_theta, int64_t nq,
+                    uint64_t* cand, int* cand_cnt, int64_t cap, int* overflow) {
+  if (db->mp != 16) return PQS_ERR_UNSUPPORTED;
+  const int64_t nqg = cdiv(nq, TC_N);
+  const int64_t ntiles = cdiv(db->n, TC_M);
+  const int64_t total = nqg * ntiles;
+  const int64_t nctas = std::min<int64_t>((int64_t)ctx->sm_count, total);
+  if (nctas <= 0) return PQS_OK;
+  // every CTA range must span <= 2 query groups (double-buffered B) and fit the
+  // 17-bit tile-iteration field of the staged survivor records
+  if (cdiv(total, nctas) + 1 >= ntiles || cdiv(total, nctas) >= (1 << 17)) return PQS_ERR_UNSUPPORTED;
+  uint8_t* bglob = nullptr;
+  int* nthr = nullptr;
+  uint64_t* rec = nullptr;
+  int* rec_cnt = nullptr;
+  PQS_TRY(scratch(ctx, S_TC_B, (size_t)(nqg * B_BYTES), &bglob));
+  PQS_TRY(scratch(ctx, S_TC_TH, (size_t)(nqg * TC_N / 2), &nthr));
+  // survivors per CTA: expect ~nq*cap_used/nctas; size generously
+  const int64_t rec_cap = std::max<int64_t>(1 << 16, cdiv(nq * std::min<int64_t>(cap, 8192), nctas) * 2);
+  PQS_TRY(scratch(ctx, S_TC_REC, (size_t)(nctas * rec_cap), &rec));
+  PQS_TRY(scratch(ctx, S_TC_RECCNT, (size_t)nctas, &rec_cnt));
+  build_b_kernel<<<(unsigned)cdiv(nqg * TC_N * 16, 256), 256, 0, ctx->stream>>>(d_qt, d_theta, nq, db->m, nqg, bglob,
+                                                                               nthr);
+  PQS_LAUNCHED(ctx);
+  Scan4TcArgs a{};
+  a.words = db->words4;
+  a.n = db->n;
+  a.bglob = bglob;
+  a.nthr = nthr;
+  a.nq = nq;
+  a.nqg = nqg;
+  a.ntiles = ntiles;
+  a.rec = rec;
+  a.rec_cnt = rec_cnt;
+  a.rec_cap = rec_cap;
+  a.dbg = nullptr;
+  a.dbg_mode = getenv("PQS_TC_MODE") ? atoi(getenv("PQS_TC_MODE")) : 0;
+  if (getenv("PQS_TC_DEBUG")) {
+    PQS_TRY(scratch(ctx, S_MISC, 64 * 8 + 64, &a.dbg));
+    PQS_CUDA(ctx, cudaMemsetAsync(a.dbg, 0, (64 * 8 + 64) * 8, ctx->stream));
+  }
+  const size_t smem = (size_t)B_BYTES + 2 * (size_t)A_BYTES + 2 * TC_N * 2 + (size_t)ESTAGE * EPI_WARPS * 32 * 4;
+  PQS_CUDA(ctx, cudaFuncSetAttribute(scan4tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  PQS_TRY(scan_timer_begin(ctx));
+  scan4tc_kernel<<<(unsigned)nctas, TC_THREADS, smem, ctx->stream>>>(a);
+  PQS_LAUNCHED(ctx);
+  PQS_TRY(scan_timer_end(ctx));
+  dim3 bg(64, (unsigned)nctas);
+  bucket_kernel<<<bg, 256, 0, ctx->stream>>>(rec, rec_cnt, rec_cap, cand, cand_cnt, cap);
+  PQS_LAUNCHED(ctx);
+  // overflow of a CTA record list -> the caller re-runs every query exactly
+  std::vector<int> h(nctas);
+  PQS_CUDA(ctx, cudaMemcpyAsync(h.data(), rec_cnt, sizeof(int) * nctas, cudaMemcpyDeviceToHost, ctx->stream));
+  PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  *overflow = 0;
+  for (int v : h)
+    if (v > rec_cap) *overflow = 1;
+  if (a.dbg) {
+    std::vector<unsigned long long> d(64 * 8 + 64);
+    PQS_CUDA(ctx, cudaMemcpy(d.data(), a.dbg, (64 * 8 + 64) * 8, cudaMemcpyDeviceToHost));
+    for (int c = 0; c < 8; ++c)
+      fprintf(stderr, "chunk %d: ld %lld  cmp %lld  emit %lld\n", c, (long long)(d[512 + c * 4 + 1] - d[512 + c * 4]),
+              (long long)(d[512 + c * 4 + 2] - d[512 + c * 4 + 1]), (long long)(d[512 + c * 4 + 3] - d[512 + c * 4 + 2]));
+    const unsigned long long t0 = d[0];
+    for (int it = 0; it < 24; ++it) {
+      fprintf(stderr, "tile %2d:", it);
+      for (int k = 0; k < 7; ++k) fprintf(stderr, " %8lld", d[it * 8 + k] ? (long long)(d[it * 8 + k] - t0) : -1ll);
+      fprintf(stderr, "\n");
+    }
+  }
+  return PQS_OK;
+}

@@ -645,12 +645,14 @@ int run_adc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t 
   PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   PQS_TRY(scan_timer_collect(ctx));
   std::vector<int> over;
-  int64_t mx = 0;
+  int64_t mx = 0, ctot = 0;
   for (int64_t q = 0; q < nq; ++q) {
     mx = std::max<int64_t>(mx, hcnt[q]);
+    ctot += hcnt[q];
     if (hcnt[q] > cap || hcnt[q] < r_eff || ctx->force_fallback) over.push_back((int)q);
   }
   ctx->last_max_cand = mx;
+  ctx->last_cand_total = ctot;
   ctx->last_overflow = (int64_t)over.size();
   if (!over.empty()) {
     const int64_t B = std::max<int64_t>(1, std::min<int64_t>((int64_t)over.size(), (int64_t)(1ll << 27) / n));
