@@ -404,11 +404,42 @@ __global__ void build_b_kernel(const uint8_t* __restrict__ qt, const uint8_t* __
   }
 }
 
-// per-CTA survivor records -> per-query candidate lists (bin << 32 | idx)
+// per-CTA survivor records -> per-query candidate lists (bin << 32 | idx).
+// One CTA per record region: shared histogram over queries, one global
+// reservation per (region, query), then a scatter -- ~nq global atomics per
+// region instead of one per record.
 __global__ void bucket_kernel(const uint64_t* __restrict__ rec, const int* __restrict__ rec_cnt, int64_t rec_cap,
-                              uint64_t* __restrict__ cand, int* __restrict__ cand_cnt, int64_t cap) {
+                              int64_t nq, uint64_t* __restrict__ cand, int* __restrict__ cand_cnt, int64_t cap) {
+  extern __shared__ int bsm[];
+  int* hist = bsm;        // [nq]
+  int* basev = bsm + nq;  // [nq]
+  const int b = blockIdx.x;
+  const int cnt = (int)min((int64_t)rec_cnt[b], rec_cap);
+  const uint64_t* r = rec + (int64_t)b * rec_cap;
+  for (int64_t i = threadIdx.x; i < nq; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) atomicAdd(&hist[r[i] >> 40], 1);
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < nq; i += blockDim.x) {
+    const int h = hist[i];
+    basev[i] = h ? atomicAdd(cand_cnt + i, h) : 0;
+    hist[i] = 0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const uint64_t x = r[i];
+    const int64_t q = (int64_t)(x >> 40);
+    const int pos = basev[q] + atomicAdd(&hist[q], 1);
+    if (pos < cap) cand[q * cap + pos] = x & 0xFFFFFFFFFFull;
+  }
+}
+
+// fallback for very large query batches (histograms beyond shared memory)
+__global__ void bucket_atomic_kernel(const uint64_t* __restrict__ rec, const int* __restrict__ rec_cnt,
+                                     int64_t rec_cap, uint64_t* __restrict__ cand, int* __restrict__ cand_cnt,
+                                     int64_t cap) {
   const int b = blockIdx.y;
-  const int cnt = min((int64_t)rec_cnt[b], rec_cap);
+  const int cnt = (int)min((int64_t)rec_cnt[b], rec_cap);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
     const uint64_t r = rec[(int64_t)b * rec_cap + i];
     const int64_t q = (int64_t)(r >> 40);
@@ -468,8 +499,14 @@ int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const u
   scan4tc_kernel<<<(unsigned)nctas, TC_THREADS, smem, ctx->stream>>>(a);
   PQS_LAUNCHED(ctx);
   PQS_TRY(scan_timer_end(ctx));
-  dim3 bg(64, (unsigned)nctas);
-  bucket_kernel<<<bg, 256, 0, ctx->stream>>>(rec, rec_cnt, rec_cap, cand, cand_cnt, cap);
+  const size_t bsmem = (size_t)nq * 2 * sizeof(int);
+  if (bsmem <= 200 * 1024) {
+    PQS_CUDA(ctx, cudaFuncSetAttribute(bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
+    bucket_kernel<<<(unsigned)nctas, 1024, bsmem, ctx->stream>>>(rec, rec_cnt, rec_cap, nq, cand, cand_cnt, cap);
+  } else {
+    dim3 bg(64, (unsigned)nctas);
+    bucket_atomic_kernel<<<bg, 256, 0, ctx->stream>>>(rec, rec_cnt, rec_cap, cand, cand_cnt, cap);
+  }
   PQS_LAUNCHED(ctx);
   // overflow of a CTA record list -> the caller re-runs every query exactly
   std::vector<int> h(nctas);
