@@ -235,6 +235,7 @@ struct Scan4Args {
   // virtual tiles: tile(i) = tile_off + i * tile_step, i in [0, nvt)
   int64_t nvt, tile_off, tile_step, per_cta;
   int64_t nqg;             // query groups of SCAN4_THREADS
+  int parts;               // work items per tile (quarter tiles give the small sample pass more CTAs)
   unsigned long long* work;  // dynamic tile counter (zeroed before launch)
   // dense
   uint8_t* out;
@@ -310,7 +311,9 @@ __global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kerne
 
   // persistent CTAs grab tiles of the linearised (query group, tile) list from
   // a global counter (dynamic balance); tables are reloaded at group switches
-  const long long total = a.nqg * a.nvt;
+  const long long per_group = a.nvt * a.parts;
+  const long long total = a.nqg * per_group;
+  const int gq = QUADS4 / a.parts;  // quads per work item
   __shared__ long long s_w[2];
   if (threadIdx.x == 0) {
     s_w[0] = atomicAdd(a.work, 1ull);
@@ -345,14 +348,16 @@ __global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kerne
   };
 
   uint4 regs[PER];
-  load_tile_raw<MP>(a.words, a.tile_off + (w % a.nvt) * a.tile_step, regs, nthreads);
+  load_tile_raw<MP>(a.words, a.tile_off + ((w % per_group) / a.parts) * a.tile_step, regs, nthreads);
   store_tile_pred<MP>(regs, s_pred, nthreads);
   __syncthreads();
 
   int cur = 0;
   for (int it = 0;; ++it) {
-    const int64_t qg = w / a.nvt;
-    const int64_t i = w - qg * a.nvt;
+    const int64_t qg = w / per_group;
+    const int64_t rem = w - qg * per_group;
+    const int64_t i = rem / a.parts;
+    const int part = (int)(rem - i * a.parts);
     if (qg != cur_qg) {
       if (MODE == MODE_FILTER && ncand > 0) {
         flush_cands(stage, ncand, q, a.cand, a.cand_cnt, a.cap);
@@ -362,12 +367,12 @@ __global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kerne
       cur_qg = qg;
     }
     const bool has_next = (wn < total);
-    if (has_next) load_tile_raw<MP>(a.words, a.tile_off + (wn % a.nvt) * a.tile_step, regs, nthreads);
+    if (has_next) load_tile_raw<MP>(a.words, a.tile_off + ((wn % per_group) / a.parts) * a.tile_step, regs, nthreads);
     const uint4* buf = s_pred + cur * WORDS;
     const int64_t tile = a.tile_off + i * a.tile_step;
     const int64_t code0 = tile * TILE4;
 #pragma unroll 2
-    for (int g = 0; g < QUADS4; ++g) {
+    for (int g = part * gq; g < (part + 1) * gq; ++g) {
       uint32_t ae = 0, ao = 0;
 #pragma unroll
       for (int p = 0; p < HP; ++p) {
@@ -439,7 +444,8 @@ int launch_scan4_t(pqs_ctx* ctx, Scan4Args a, int64_t nq) {
                                      (int)smem));
   const int threads = SCAN4_THREADS;  // the tile loader assumes a full CTA
   a.nqg = cdiv(nq, threads);
-  const int64_t total = a.nqg * a.nvt;
+  if (a.parts <= 0) a.parts = 1;
+  const int64_t total = a.nqg * a.nvt * a.parts;
   if (total <= 0) return PQS_OK;
   int per_sm = 0;
   PQS_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan4_kernel<MP, MODE>, threads, smem));
@@ -599,6 +605,7 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
     PQS_TRY(scratch(ctx, S_SAMPLE, (size_t)(nq * ns), &sample));
     Scan4Args a{};
     a.tout = 1;
+    a.parts = 4;
     a.words = db->words4;
     a.n = n;
     a.m = m;

@@ -22,7 +22,7 @@ namespace {
 using namespace seldev;
 
 constexpr int SEL_THREADS = 512;
-constexpr int SMEM_CAP = 2048;  // materialised elements kept in shared memory
+constexpr int SMEM_CAP = 4096;  // materialised elements kept in shared memory
 
 // Element access -----------------------------------------------------------
 struct ElemSrc {
