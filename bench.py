@@ -330,35 +330,51 @@ def main():
     # ---- roofline of the dominant kernel (the filtered scan), live CUDA events
     scan_ms = statistics.mean(scan_ns) / 1e6
     m = cfg["m"]
+    engine = ctx.stat(_lib.STAT_LAST_SCAN_ENGINE)
+    work = ctx.stat(_lib.STAT_LAST_SCAN_WORK)
     lookups = float(nq) * n * m
-    achieved = lookups / (scan_ms / 1e3) / 1e9          # Glookup/s
-    import json as _json
-
     peaks = {}
     try:
-        peaks = _json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
     f_mhz = clk.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
-    lut_peak = sm_count * 32 * f_mhz * 1e6 / 1e9       # Glookup/s, shared-memory LUT rate
+    lut_peak = sm_count * 32 * f_mhz * 1e6 / 1e9       # Glookup/s, shared-memory LUT rate (north star)
+    lut_rate = lookups / (scan_ms / 1e3) / 1e9
     code_bytes = n * (m // 2 if cfg["b"] == 4 else m)
-    hbm_alg = code_bytes + nq * m * (16 if cfg["b"] == 4 else cfg.get("k", 1 << cfg["b"]) * 4)
+    hbm_alg = code_bytes + nq * m * (16 if cfg["b"] == 4 else (1 << cfg["b"]) * 4)
     hbm_peak = peaks.get("hbm_gbs", 6553.6)
-    roofline = {
-        "bound": "lut",
-        "achieved": achieved, "peak": lut_peak, "unit": "Glookup/s", "frac": achieved / lut_peak,
-        "traffic": None,
-        "kernel": "scan4_kernel<16,FILTER>" if cfg["b"] == 4 else "scan8_kernel<FILTER>",
-        "per_unit": f"{m} table lookups per (query, code) evaluation; {nq} x {n} evaluations per launch",
-        "peak_source": f"shared-memory LUT rate {sm_count} SM x 32 lookups/clk x median SM clock under load "
-                       f"({f_mhz:.0f} MHz, nvidia-smi during the timed region); north-star roofline",
-        "kernel_ms": scan_ms,
-        "hbm": {"algorithmic_bytes": hbm_alg, "achieved_GBs": hbm_alg / (scan_ms / 1e3) / 1e9,
-                "peak_GBs": hbm_peak, "frac": hbm_alg / (scan_ms / 1e3) / 1e9 / hbm_peak,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
-        "share_of_step": scan_ms / ms_per_step,
-    }
+    hbm = {"algorithmic_bytes": hbm_alg, "achieved_GBs": hbm_alg / (scan_ms / 1e3) / 1e9, "peak_GBs": hbm_peak,
+           "frac": hbm_alg / (scan_ms / 1e3) / 1e9 / hbm_peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"}
+    lut = {"achieved": lut_rate, "peak": lut_peak, "unit": "Glookup/s", "frac": lut_rate / lut_peak,
+           "per_unit": f"{m} table lookups per (query, code) evaluation; {nq} x {n} evaluations per launch",
+           "peak_source": f"shared-memory LUT rate {sm_count} SM x 32 lookups/clk x median SM clock under load "
+                          f"({f_mhz:.0f} MHz, nvidia-smi during the timed region)"}
+    traffic_db = {}
+    try:
+        traffic_db = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+    except Exception:
+        pass
+    if engine == 2:
+        # tcgen05 kind::i8 one-hot GEMM: int8 MMA ops actually issued per launch
+        i8_peak = 2.0 * peaks.get("bf16_tflops", 1682.0)  # dense int8 = 2x dense bf16 (nominal 4.5 vs 2.25 P)
+        achieved = work / (scan_ms / 1e3) / 1e12
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": i8_peak, "unit": "TOP/s (int8)",
+                    "frac": achieved / i8_peak,
+                    "traffic": traffic_db.get("scan4tc_kernel", {}).get("bytes"),
+                    "traffic_note": "DRAM bytes per launch from the committed ncu capture (profiles/)",
+                    "kernel": "scan4tc_kernel (tcgen05.mma kind::i8, M=128 N=256 K=256 per tile)",
+                    "per_unit": "2 x 256 int8 MACs per (query, code) over 256-query groups and 128-code tiles "
+                                f"({work:.3e} ops per launch)",
+                    "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (measured cuBLAS bf16; int8 dense "
+                                   "rate is 2x bf16 on B200) -- derived, not separately measured",
+                    "lut_equivalent": lut, "hbm": hbm, "kernel_ms": scan_ms, "share_of_step": scan_ms / ms_per_step}
+    else:
+        roofline = {"bound": "lut", **lut, "traffic": None,
+                    "kernel": {1: "scan4_kernel<16,FILTER> (PRMT register LUT)", 3: "scan8_kernel (smem LUT)"}.get(
+                        engine, str(engine)),
+                    "hbm": hbm, "kernel_ms": scan_ms, "share_of_step": scan_ms / ms_per_step}
     line = {
         "metric": metric_name(args.config), "value": value, "unit": "evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,

@@ -35,6 +35,8 @@ STAT_LAST_EVALS = 4
 STAT_LAST_SCAN_NS = 5
 STAT_LAST_SCAN_LAUNCHES = 6
 STAT_LAST_CAND_TOTAL = 7
+STAT_LAST_SCAN_ENGINE = 8
+STAT_LAST_SCAN_WORK = 9
 
 _p = ctypes.c_void_p
 _i = ctypes.c_int

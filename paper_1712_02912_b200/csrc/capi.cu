@@ -218,6 +218,8 @@ int pqs_ctx_get_stat(pqs_ctx* ctx, int stat, int64_t* out) {
     case PQS_STAT_LAST_SCAN_NS: *out = ctx->last_scan_ns; return PQS_OK;
     case PQS_STAT_LAST_SCAN_LAUNCHES: *out = ctx->last_scan_launches; return PQS_OK;
     case PQS_STAT_LAST_CAND_TOTAL: *out = ctx->last_cand_total; return PQS_OK;
+    case PQS_STAT_LAST_SCAN_ENGINE: *out = ctx->last_scan_engine; return PQS_OK;
+    case PQS_STAT_LAST_SCAN_WORK: *out = (int64_t)ctx->last_scan_work; return PQS_OK;
   }
   return set_err(ctx, PQS_ERR_INVALID, "unknown stat");
 }

@@ -656,6 +656,7 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
   PQS_LAUNCHED(ctx);
   PQS_TRY(scan_timer_end(ctx));
   ctx->last_scan_launches = 1;
+  ctx->last_scan_engine = 4;
   // exact rerank + select
   uint64_t* gk = nullptr;
   int64_t* gi = nullptr;
@@ -709,6 +710,7 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
     }
   }
   ctx->last_evals = total_evals;
+  ctx->last_scan_work = (double)total_evals * (double)m;
   ctx->last_max_cand = mx;
   ctx->last_cand_total = ctot;
   ctx->last_overflow = (int64_t)over.size();

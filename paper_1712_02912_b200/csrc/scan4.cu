@@ -657,6 +657,8 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
       const int st = launch_scan4_tc(ctx, db, d_qt, theta, nq, cand, cnt, cap, &overflow);
       if (st == PQS_OK && !overflow) {
         done = 1;
+        ctx->last_scan_engine = 2;
+        ctx->last_scan_work = 2.0 * (double)cdiv(nq, 256) * 256.0 * (double)cdiv(n, 128) * 128.0 * 256.0;
       } else if (st == PQS_OK || st == PQS_ERR_UNSUPPORTED) {
         if (ctx->scan4_engine == 2 && st == PQS_ERR_UNSUPPORTED)
           return set_err(ctx, PQS_ERR_UNSUPPORTED, "tcgen05 Quick ADC scan: unsupported shape (needs m <= 16)");
@@ -669,6 +671,8 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
       PQS_TRY(scan_timer_begin(ctx));
       PQS_TRY(launch_scan4<MODE_FILTER>(ctx, db->mp, a, nq));
       PQS_TRY(scan_timer_end(ctx));
+      ctx->last_scan_engine = 1;
+      ctx->last_scan_work = (double)nq * (double)n * (double)m;
     }
     ctx->last_scan_launches = 1;
   }

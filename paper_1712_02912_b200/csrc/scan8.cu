@@ -612,6 +612,8 @@ int run_adc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t 
     PQS_TRY(launch_scan8<MODE8_FILTER>(ctx, a));
     PQS_TRY(scan_timer_end(ctx));
     ctx->last_scan_launches = 1;
+    ctx->last_scan_engine = 3;
+    ctx->last_scan_work = (double)nq * (double)n * (double)m;
   }
   ctx->last_evals = nq * n;
 
