@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg1", choices=["cfg0", "cfg1", "cfg2"])
+    ap.add_argument("--config", default="cfg1", choices=["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--n-per-gpu", type=int, default=None, help="override the per-GPU code count (cfg4)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-s", type=float, default=20.0, help="CPU work budget of the baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -53,6 +54,23 @@ def parse():
 
 
 # --------------------------------------------------------------------- data
+CFG4_PER_GPU = 125_000_000   # BASELINE cfg4: 1e9 codes sharded over 8 GPUs
+
+
+def make_data_device(cfg_name: str, rank: int, world: int, ctx, n_per_gpu=None):
+    """cfg4: each rank generates and encodes its own 125M-code shard on the GPU
+    (Philox rows -> exact encode kernel); prefix = global rows [0, init_count)."""
+    import paper_1712_02912_b200 as P
+    from paper_1712_02912_b200 import datagen as G
+
+    cfg = G.CONFIGS[cfg_name]
+    n = n_per_gpu or CFG4_PER_GPU
+    books, codes, prefix, queries = G.make_quick_adc_shard(
+        cfg_name, rank, world, lambda b: P.DeviceQuantizer(P.ProductQuantizer(cfg["m"], cfg["b"], cfg["d"], b), ctx),
+        n=n, device=f"cuda:{ctx.device}")
+    return cfg, books, codes, queries, prefix
+
+
 def make_data(cfg_name: str, rank: int):
     from paper_1712_02912_b200 import datagen as G
 
@@ -132,7 +150,10 @@ def _cpu_query(qi):
     return qi
 
 
-def cpu_baseline(cfg, books, codes, queries, budget_s: float):
+CPU_CODE_SAMPLE = 4_000_000
+
+
+def cpu_baseline(cfg, books, codes, queries, budget_s: float, n_full: int | None = None):
     """Oracle port of the reference CPU path, fork process pool over all host
     cores (threads do not scale: GIL, SURVEY finding 8)."""
     import multiprocessing as mp
@@ -154,8 +175,10 @@ def cpu_baseline(cfg, books, codes, queries, budget_s: float):
         wall = time.perf_counter() - t0
     evals = nq * codes.shape[0]
     return {"value": evals / wall, "unit": "evals/s", "cores": cores, "kind": "port",
-            "sample": f"{nq} of {queries.shape[0]} queries over all {codes.shape[0]} codes "
-                      f"(oracle/pqscan_oracle.py, fork pool x{cores}); single-core {per_q * 1e3:.1f} ms/query"}
+            "sample": f"{nq} of {queries.shape[0]} queries over "
+                      + (f"all {codes.shape[0]} codes" if n_full is None else
+                         f"the first {codes.shape[0]} of {n_full} codes (evals/s is per (query, code))")
+                      + f" (oracle/pqscan_oracle.py, fork pool x{cores}); single-core {per_q * 1e3:.1f} ms/query"}
 
 
 # ------------------------------------------------------------------ driver
@@ -174,21 +197,60 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    cfg, books, codes, queries, _ = make_data(args.config, 0)
+    n_full = None
+    if args.config == "cfg3":
+        # the index is built on the GPU (data preparation, untimed); the timed
+        # path is the oracle's query_ivf on the host cores
+        import torch
+
+        import paper_1712_02912_b200 as P
+
+        ctx = P.Context(0)
+        cfg, books, coarse, sizes, codes, ids, queries = make_ivf(args, ctx, torch.device("cuda", 0))
+        vals = []
+        for s in range(args.warmup + args.steps):
+            base = cpu_baseline_ivf(books, coarse.cpu().numpy(), sizes, codes.cpu().numpy(), ids.cpu().numpy(),
+                                    queries, cfg["nprobe"], cfg["r"],
+                                    max(2.0, args.cpu_sample_s / max(args.steps, 1)))
+            if s >= args.warmup:
+                vals.append(base["value"])
+        value = statistics.median(vals)
+        print(json.dumps({
+            "impl": "reference", "metric": metric_name("cfg3"), "value": value, "unit": "evals/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded stand-in; index built on the GPU, untimed)",
+            "config": {"workload": "IVFADC K=65536, residual PQ 8x8, nprobe 64", "baseline_config_index": 3},
+            "cpu_baseline": {"value": value, "unit": "evals/s", "cores": base["cores"], "kind": "port",
+                             "sample": base["sample"]},
+            "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+            flush=True)
+        return
+    if args.config == "cfg4":
+        # host-generated sample of a shard (same distribution; the full shard
+        # is GPU-generated in the "ours" arm); evals/s is per (query, code)
+        from paper_1712_02912_b200 import datagen as G
+
+        n_full = args.n_per_gpu or CFG4_PER_GPU
+        cfg = G.CONFIGS["cfg4"]
+        books, codes, queries = G.make_exhaustive("cfg4", n=CPU_CODE_SAMPLE)
+    else:
+        cfg, books, codes, queries, _ = make_data(args.config, 0)
     base = None
     vals = []
     for s in range(args.warmup + args.steps):
-        base = cpu_baseline(cfg, books, codes, queries, budget_s=max(2.0, args.cpu_sample_s / max(args.steps, 1)))
+        base = cpu_baseline(cfg, books, codes, queries, budget_s=max(2.0, args.cpu_sample_s / max(args.steps, 1)),
+                            n_full=n_full)
         if s >= args.warmup:
             vals.append(base["value"])
     value = statistics.median(vals)
     line = {
         "impl": "reference", "metric": metric_name(args.config), "value": value, "unit": "evals/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": codes.shape[0] * queries.shape[0] / value * 1e3, "higher_is_better": True,
+        "ms_per_step": (n_full or codes.shape[0]) * queries.shape[0] / value * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8" if cfg["b"] == 4 else "f64",
         "data": "synthetic (seeded stand-in for the BASELINE config; see DESIGN.md)",
-        "config": config_dict(args.config, cfg, world),
+        "config": config_dict(args.config, cfg, world, args.n_per_gpu),
         "cpu_baseline": {"value": value, "unit": "evals/s", "cores": base["cores"], "kind": "port",
                          "sample": base["sample"]},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -196,10 +258,12 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def config_dict(name, cfg, world):
+def config_dict(name, cfg, world, n_per_gpu=None):
+    n_per = cfg["N"] if name != "cfg4" else (n_per_gpu or CFG4_PER_GPU)
     d = {"workload": {"cfg0": "exhaustive PQ 8x8 float ADC", "cfg1": "Quick ADC PQ 16x4 exhaustive",
-                      "cfg2": "high-dim PQ 64x8 float ADC"}[name],
-         "baseline_config_index": int(name[-1]), "N_per_gpu": cfg["N"], "N_total": cfg["N"] * world,
+                      "cfg2": "high-dim PQ 64x8 float ADC",
+                      "cfg4": "billion-scale sharded Quick ADC PQ 16x4 (d=96), one 125M-code shard per GPU"}[name],
+         "baseline_config_index": int(name[-1]), "N_per_gpu": n_per, "N_total": n_per * world,
          "queries": cfg["Q"], "d": cfg["d"], "m": cfg["m"], "b": cfg["b"], "r": cfg["r"],
          "parallelism": f"shard{world}" if world > 1 else "single", "l2": "flushed between timed steps (256 MB write)"}
     if cfg["b"] == 4:
@@ -207,10 +271,215 @@ def config_dict(name, cfg, world):
     return d
 
 
+# --------------------------------------------------------------- IVF (cfg3)
+_IVF = {}
+
+
+def _cpu_ivf_query(qi):
+    from oracle import pqscan_oracle as O
+
+    d = _IVF
+    O.query_ivf(d["coarse"], d["books"], d["lists_codes"], d["lists_ids"], d["queries"][qi], d["ma"], d["r"])
+    return qi
+
+
+def cpu_baseline_ivf(books, coarse, sizes, codes, ids, queries, ma, r, budget_s):
+    """Oracle query_ivf (ivf.py:148-196) in a fork pool over all host cores."""
+    import multiprocessing as mp
+
+    cores = len(os.sched_getaffinity(0))
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    _IVF.update(books=books, coarse=coarse, queries=queries, ma=ma, r=r,
+                lists_codes=[codes[offs[c]:offs[c + 1]] for c in range(len(sizes))],
+                lists_ids=[ids[offs[c]:offs[c + 1]] for c in range(len(sizes))])
+    t0 = time.perf_counter()
+    _cpu_ivf_query(0)
+    per_q = time.perf_counter() - t0
+    nq = min(queries.shape[0], max(cores, (int(budget_s / max(per_q, 1e-3)) // cores) * cores))
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        t0 = time.perf_counter()
+        pool.map(_cpu_ivf_query, range(nq), chunksize=1)
+        wall = time.perf_counter() - t0
+    # exact evaluation count of the sampled queries (untimed): sizes of their probed lists
+    from oracle import pqscan_oracle as O
+
+    cells, _ = O.nearest_k(queries[:nq].astype(np.float64), np.asarray(coarse, np.float32).astype(np.float64), ma)
+    evals = float(np.asarray(sizes)[cells].sum())
+    return {"value": evals / wall, "unit": "evals/s", "cores": cores, "kind": "port",
+            "sample": f"{nq} of {queries.shape[0]} queries, nprobe {ma}, full index (oracle query_ivf, fork pool "
+                      f"x{cores}); {evals:.3e} probed codes; single-core {per_q * 1e3:.1f} ms/query"}
+
+
+def make_ivf(args, ctx, dev):
+    import paper_1712_02912_b200 as P
+    from paper_1712_02912_b200 import datagen as G
+
+    cfg = G.CONFIGS["cfg3"]
+    books, coarse, sizes, codes, ids, queries = G.make_ivf_device(
+        "cfg3", lambda b: P.DeviceQuantizer(P.ProductQuantizer(cfg["m"], cfg["b"], cfg["d"], b), ctx),
+        n=args.n_per_gpu, device=dev)
+    return cfg, books, coarse, sizes, codes, ids, queries
+
+
+def run_ivf(args):
+    """cfg3 (IVFADC): one index per GPU, queries sharded across ranks (each
+    rank searches its own 10k-query batch against a replica of the index:
+    weak scaling, no exchange -- "replicas")."""
+    import torch
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_1712_02912_b200 as P
+    from paper_1712_02912_b200 import _lib
+
+    ctx = P.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+    t_build = time.perf_counter()
+    cfg, books, coarse, sizes, codes, ids, queries = make_ivf(args, ctx, dev)
+    pq = P.ProductQuantizer(cfg["m"], cfg["b"], cfg["d"], books)
+    ivf = P.DeviceIvf.from_arrays(pq, coarse, sizes, codes, ids, ctx=ctx)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t_build
+    ma, r = cfg["nprobe"], cfg["r"]
+    q_dev = torch.from_numpy(queries).to(dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        ivf.search(q_dev, ma, r)
+    torch.cuda.synchronize()
+    launches0 = ctx.stat(_lib.STAT_LAUNCHES)
+    clocks = ClockSampler(local)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    scan_ns, evals = [], []
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    for s in range(args.steps):
+        flush.zero_()
+        starts[s].record(stream)
+        ivf.search(q_dev, ma, r)
+        ends[s].record(stream)
+        scan_ns.append(ctx.stat(_lib.STAT_LAST_SCAN_NS))
+        evals.append(ctx.stat(_lib.STAT_LAST_EVALS))
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = ctx.stat(_lib.STAT_LAUNCHES) - launches0
+    cand_max, cand_tot = ctx.stat(_lib.STAT_LAST_MAX_CAND), ctx.stat(_lib.STAT_LAST_CAND_TOTAL)
+    total_ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
+    evals_step = float(evals[-1])
+    t = torch.tensor([total_ms, evals_step], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+
+        tm = t[:1].clone()
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        ev = t[1:].clone()
+        dist.all_reduce(ev, op=dist.ReduceOp.SUM)
+        total_ms, evals_all = float(tm.item()), float(ev.item())
+    else:
+        evals_all = evals_step
+    ms_per_step = total_ms / args.steps
+    value = evals_all / (ms_per_step / 1e3)
+    # e2e: host queries in, host results out, through the drop-in API call
+    e2e = []
+    for s in range(max(args.warmup, 1) + args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        ivf.search(queries, ma, r)
+        dt = (time.perf_counter() - t0) * 1e3
+        if s >= max(args.warmup, 1):
+            e2e.append(dt)
+    e2e_total = sum(e2e)
+    if world > 1:
+        import torch.distributed as dist
+
+        tt = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_total = float(tt.item())
+    e2e_value = evals_all / (e2e_total / len(e2e) / 1e3)
+    nq = queries.shape[0]
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+        return
+    scan_ms = statistics.mean(scan_ns) / 1e6
+    m = cfg["m"]
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    f_mhz = clk.get("sm_mhz") or 1965.0
+    lut_peak = sm_count * 32 * f_mhz * 1e6 / 1e9
+    lut_rate = evals_step * m / (scan_ms / 1e3) / 1e9
+    hbm_alg = int(codes.shape[0]) * (m + 4)  # list-major: every list's codes + V once per launch
+    hbm_peak = peaks.get("hbm_gbs", 6553.6)
+    line = {
+        "metric": metric_name("cfg3"), "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32+f64",
+        "data": "synthetic (seeded stand-in for the BASELINE config, index built on the GPU; see DESIGN.md)",
+        "config": {"workload": "IVFADC K=65536, residual PQ 8x8, nprobe 64", "baseline_config_index": 3,
+                   "N_per_gpu": int(codes.shape[0]), "queries_per_gpu": nq, "K": int(coarse.shape[0]),
+                   "nprobe": ma, "m": m, "b": cfg["b"], "r": r, "d": cfg["d"],
+                   "evals_per_step_per_gpu": evals_step,
+                   "parallelism": f"query-shard replicas x{world}" if world > 1 else "single",
+                   "l2": "flushed between timed steps (256 MB write); index 1.6 GB > L2",
+                   "index_build_s": t_build},
+        "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": queries.nbytes,
+                "d2h_bytes_per_step": nq * r * 16 + nq * 4},
+        "gpu_launches": launches,
+        "candidates": {"max_per_query": cand_max, "mean_per_query": cand_tot / nq},
+        "clocks": clk,
+        "roofline": {"bound": "lut", "achieved": lut_rate, "peak": lut_peak, "unit": "Glookup/s",
+                     "frac": lut_rate / lut_peak, "traffic": None,
+                     "kernel": "ivf_list_kernel (list-major, smem LUT)",
+                     "per_unit": f"{m} table lookups per probed (query, code); {evals_step:.3e} per launch",
+                     "peak_source": f"shared-memory LUT rate {sm_count} SM x 32 lookups/clk x {f_mhz:.0f} MHz",
+                     "hbm": {"algorithmic_bytes": hbm_alg, "achieved_GBs": hbm_alg / (scan_ms / 1e3) / 1e9,
+                             "peak_GBs": hbm_peak, "frac": hbm_alg / (scan_ms / 1e3) / 1e9 / hbm_peak},
+                     "kernel_ms": scan_ms, "share_of_step": scan_ms / ms_per_step},
+        "impl": "ours",
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline_ivf(books, coarse.cpu().numpy(), sizes, codes.cpu().numpy(),
+                                                ids.cpu().numpy(), queries, ma, r, args.cpu_sample_s)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.config == "cfg3":
+        run_ivf(args)
         return
     import torch
 
@@ -225,9 +494,12 @@ def main():
     import paper_1712_02912_b200 as P
     from paper_1712_02912_b200 import _lib
 
-    cfg, books, codes, queries, prefix = make_data(args.config, rank)
-    nq, n, r = queries.shape[0], codes.shape[0], cfg["r"]
     ctx = P.Context(local)
+    if args.config == "cfg4":
+        cfg, books, codes, queries, prefix = make_data_device(args.config, rank, world, ctx, args.n_per_gpu)
+    else:
+        cfg, books, codes, queries, prefix = make_data(args.config, rank)
+    nq, n, r = queries.shape[0], codes.shape[0], cfg["r"]
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
     ctx.set_option(_lib.OPT_SCAN4_ENGINE, args.engine)
@@ -380,7 +652,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8" if cfg["b"] == 4 else "f32+f64",
         "data": "synthetic (seeded stand-in for the BASELINE config; see DESIGN.md)",
-        "config": config_dict(args.config, cfg, world),
+        "config": config_dict(args.config, cfg, world, args.n_per_gpu),
         "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "candidates": {"max_per_query": cand_max, "mean_per_query": cand_tot / nq,
@@ -390,7 +662,11 @@ def main():
         "impl": "ours",
     }
     if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline(cfg, books, codes, queries, args.cpu_sample_s)
+        if isinstance(codes, np.ndarray):
+            line["cpu_baseline"] = cpu_baseline(cfg, books, codes, queries, args.cpu_sample_s)
+        else:  # device-generated shard: the oracle runs on a host copy of its first codes
+            sample = codes[:CPU_CODE_SAMPLE].cpu().numpy()
+            line["cpu_baseline"] = cpu_baseline(cfg, books, sample, queries, args.cpu_sample_s, n_full=n)
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -18,8 +18,8 @@
  *   - `io` says where the per-call arrays (queries/tables in, results out)
  *     live: PQS_IO_HOST (host memory; copies happen inside the call) or
  *     PQS_IO_DEVICE (device pointers, e.g. torch.Tensor.data_ptr()).
- *     Quantizer / code-list / index handles always own device copies made
- *     from host arrays at creation time.
+ *     Quantizer / code-list / index handles always own device copies; their
+ *     create calls take host or device source arrays by the same flag.
  *   - All work of a context is issued on one CUDA stream (its own, or the
  *     one set with pqs_ctx_set_stream).  A context is single-writer, like
  *     the reference NeighborSet; separate contexts may run
@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define PQS_API_VERSION 1
+#define PQS_API_VERSION 2
 
 typedef struct pqs_ctx pqs_ctx;
 typedef struct pqs_pq pqs_pq;
@@ -58,7 +58,8 @@ enum pqs_option {
   PQS_OPT_CAND_CAP = 1,     /* candidate slots per query in a filtered scan (default 32768) */
   PQS_OPT_SAMPLE_DIV = 2,   /* threshold sample = 1/SAMPLE_DIV of the code tiles (default 32) */
   PQS_OPT_FORCE_FALLBACK = 3,/* 1: run the exact dense fallback for every query (testing) */
-  PQS_OPT_SCAN4_ENGINE = 4  /* Quick ADC scan: 0 auto (tcgen05 int8 when possible), 1 PRMT, 2 tcgen05 */
+  PQS_OPT_SCAN4_ENGINE = 4, /* Quick ADC scan: 0 auto (tcgen05 int8 when possible), 1 PRMT, 2 tcgen05 */
+  PQS_OPT_TC_CHUNK_TILES = 5 /* tcgen05 scan: cap on 128-code tiles per launch (0 = automatic; testing) */
 };
 
 enum pqs_stat {
@@ -90,16 +91,17 @@ int pqs_pq_create(pqs_ctx* ctx, int m, int b, int d, const float* codebooks, pqs
 void pqs_pq_destroy(pqs_pq* pq);
 
 /* ---- code lists: CodeList (scan.py:157-194) / TransposedCodeList (scan.py:209-245)
- * codes: host uint8 (n, m) row-major component values (< 2^b).
+ * codes: uint8 (n, m) row-major component values (< 2^b), host or device (io).
  * b == 8: float-ADC layout (scan8), any m >= 1, 2 <= k <= 256.
  * b == 4: Quick ADC layout (scan4, 4-code PRMT-selector quads), even m <= 32.
- * ids:  host int64 (n,) or NULL for implicit ids id_base + i (CodeList default
- *       ids = arange(n), scan.py:170-171).                                 */
+ * ids:  int64 (n,) (same io) or NULL for implicit ids id_base + i (CodeList
+ *       default ids = arange(n), scan.py:170-171).                         */
 int pqs_db_create(pqs_ctx* ctx, const uint8_t* codes, int64_t n, int m, int b,
-                  const int64_t* ids, int64_t id_base, pqs_db** out);
+                  const int64_t* ids, int64_t id_base, int io, pqs_db** out);
 /* Quick ADC under sharding: qmax must come from the first init_count codes of
- * the GLOBAL list (quickadc.py:130-137).  Supplies them (host uint8 (n_prefix, m)). */
-int pqs_db_set_prefix(pqs_ctx* ctx, pqs_db* db, const uint8_t* prefix_codes, int64_t n_prefix);
+ * the GLOBAL list (quickadc.py:130-137).  Supplies them (uint8 (n_prefix, m)). */
+int pqs_db_set_prefix(pqs_ctx* ctx, pqs_db* db, const uint8_t* prefix_codes, int64_t n_prefix,
+                      int io);
 void pqs_db_destroy(pqs_db* db);
 
 /* ---- tables: compute_tables (scan.py:45-56; sqdist_matrix _dist.py:13-21)
@@ -145,10 +147,11 @@ int pqs_quantized_distances(pqs_ctx* ctx, const pqs_db* db, const uint8_t* qtabl
 
 /* ---- IVFADC: IvfIndex (ivf.py:58-86) + query_ivf kernel='adc' (ivf.py:148-196)
  * coarse (K, d) float32; lists concatenated in cell order: list_sizes (K,),
- * codes (sum, m) uint8 (b == 8), ids (sum,) int64.  All host arrays.       */
+ * codes (sum, m) uint8 (b == 8), ids (sum,) int64.  coarse/codes/ids host
+ * or device (io); list_sizes always host.                                  */
 int pqs_ivf_create(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t K,
                    const int64_t* list_sizes, const uint8_t* codes, const int64_t* ids,
-                   pqs_ivf** out);
+                   int io, pqs_ivf** out);
 void pqs_ivf_destroy(pqs_ivf* ivf);
 /* probes only: nearest_k (_dist.py:42-67) -> out_cells (nq, ma) int64,
  * out_dist (nq, ma) float64 (may be NULL), ascending by (distance, cell).  */
@@ -156,6 +159,15 @@ int pqs_ivf_probe(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_
                   int64_t* out_cells, double* out_dist, int io);
 int pqs_ivf_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_t nq, int ma,
                    int r, double* out_dist, int64_t* out_ids, int32_t* out_count, int io);
+
+/* ---- encode (quantizer.py:308-325, nearest _dist.py:24-39): per sub-space
+ * the nearest centroid by the fp64 cdist sum, ties to the lowest index.
+ * x (n, d) float32 -> out_codes (n, m) uint8 (b <= 8), bit-identical.  With
+ * coarse (K, d) float32 and cells (n,) int64 the residual
+ * fp64(x) - fp64(coarse[cell]) is encoded (build_ivf, ivf.py:137-140);
+ * both NULL for plain PQ.                                                  */
+int pqs_encode(pqs_ctx* ctx, const pqs_pq* pq, const float* x, int64_t n, const float* coarse,
+               int64_t K, const int64_t* cells, uint8_t* out_codes, int io);
 
 /* ---- sharded merge: top-r of the union of G per-shard top-r lists by
  * (distance, id) -- NeighborSet.push semantics (scan.py:109-118).

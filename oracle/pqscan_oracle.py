@@ -301,6 +301,24 @@ def nearest_k(points: np.ndarray, centroids: np.ndarray, k: int):
     return idx, dist
 
 
+def encode(codebooks: np.ndarray, x: np.ndarray, coarse: np.ndarray | None = None,
+           cells: np.ndarray | None = None) -> np.ndarray:
+    """quantizer.py:308-325 (identity rotation -> fp64 rows) with nearest
+    (_dist.py:24-39): per sub-space the argmin of the fp64 sequential-sum
+    distances, ties to the lowest index.  With coarse/cells: the IVF residual
+    fp64(x) - fp64(coarse[cells]) as build_ivf encodes it (ivf.py:137-140)."""
+    books = np.asarray(codebooks, dtype=np.float32)
+    m, k, dsub = books.shape
+    z = np.asarray(x, dtype=np.float64)
+    if coarse is not None:
+        z = z - np.asarray(coarse, np.float32).astype(np.float64)[np.asarray(cells, np.int64)]
+    out = np.empty((z.shape[0], m), dtype=np.uint8 if k <= 256 else np.uint16)
+    for j in range(m):
+        dm = sqdist_matrix(z[:, j * dsub:(j + 1) * dsub], books[j].astype(np.float64))
+        out[:, j] = np.argmin(dm, axis=1)
+    return out
+
+
 def query_ivf(coarse: np.ndarray, codebooks: np.ndarray, lists_codes, lists_ids,
               query: np.ndarray, ma: int, r: int):
     """ivf.py:148-196, kernel='adc': probe the ma nearest cells, scan each

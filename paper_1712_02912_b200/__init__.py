@@ -31,6 +31,7 @@ from .scan import (  # noqa: F401
     scan_distances,
     transpose_blocks,
 )
+from .quantizer import encode  # noqa: F401
 from .quickadc import qadc_block, qadc_scan, quantize, quantize_tables_4bit, quantized_distances  # noqa: F401
 from .ivf import KERNELS, default_r2, query_ivf, query_ivf_batch  # noqa: F401
 from .engine import DeviceCodes, DeviceIvf, DeviceQuantizer, merge_topr  # noqa: F401

@@ -28,6 +28,7 @@ OPT_CAND_CAP = 1
 OPT_SAMPLE_DIV = 2
 OPT_FORCE_FALLBACK = 3
 OPT_SCAN4_ENGINE = 4
+OPT_TC_CHUNK_TILES = 5
 STAT_LAUNCHES = 1
 STAT_LAST_MAX_CAND = 2
 STAT_LAST_OVERFLOW = 3
@@ -55,8 +56,8 @@ SIGNATURES = {
     "pqs_last_error": (ctypes.c_char_p, [_p]),
     "pqs_pq_create": (_i, [_p, _i, _i, _i, _p, ctypes.POINTER(_p)]),
     "pqs_pq_destroy": (None, [_p]),
-    "pqs_db_create": (_i, [_p, _p, _i64, _i, _i, _p, _i64, ctypes.POINTER(_p)]),
-    "pqs_db_set_prefix": (_i, [_p, _p, _p, _i64]),
+    "pqs_db_create": (_i, [_p, _p, _i64, _i, _i, _p, _i64, _i, ctypes.POINTER(_p)]),
+    "pqs_db_set_prefix": (_i, [_p, _p, _p, _i64, _i]),
     "pqs_db_destroy": (None, [_p]),
     "pqs_compute_tables": (_i, [_p, _p, _p, _i64, _p, _i]),
     "pqs_scan_distances": (_i, [_p, _p, _p, _i64, _i, _p, _i]),
@@ -66,7 +67,8 @@ SIGNATURES = {
     "pqs_qadc_search": (_i, [_p, _p, _p, _p, _i64, _i, _i, _p, _p, _p, _p, _p, _i]),
     "pqs_quantized_distances": (_i, [_p, _p, _p, _i64, _p, _i]),
     "pqs_quantize": (_i, [_p, _d, _d, _p, _i64, _p, _i]),
-    "pqs_ivf_create": (_i, [_p, _p, _p, _i64, _p, _p, _p, ctypes.POINTER(_p)]),
+    "pqs_ivf_create": (_i, [_p, _p, _p, _i64, _p, _p, _p, _i, ctypes.POINTER(_p)]),
+    "pqs_encode": (_i, [_p, _p, _p, _i64, _p, _i64, _p, _p, _i]),
     "pqs_ivf_destroy": (None, [_p]),
     "pqs_ivf_probe": (_i, [_p, _p, _p, _i64, _i, _p, _p, _i]),
     "pqs_ivf_search": (_i, [_p, _p, _p, _i64, _i, _i, _p, _p, _p, _i]),
@@ -123,6 +125,8 @@ class Context:
             raise PQSError(f"pqs_ctx_create(device={device}) failed with status {st} (no CUDA device?)")
         self.handle = h
         self.device = int(device)
+        self.follow_torch = True   # device-array calls run on torch's current stream
+        self._bound = None
 
     def check(self, status: int, what: str = "") -> None:
         if status == PQS_OK:
@@ -135,7 +139,30 @@ class Context:
         raise PQSError(f"{what}: {msg} (status {status})")
 
     def set_stream(self, stream_ptr: int | None) -> None:
-        self.check(self.lib.pqs_ctx_set_stream(self.handle, stream_ptr), "set_stream")
+        """Issue this context's work on a CUDA stream: a cudaStream_t handle
+        (torch.cuda.Stream.cuda_stream; 0 = the legacy default stream), or
+        None for the context's own stream.  Disables following torch."""
+        self.follow_torch = False
+        self._set(stream_ptr)
+
+    def _set(self, stream_ptr):
+        # 0 is torch's (legacy) default stream: pass cudaStreamLegacy, since a
+        # NULL handle selects the context's own stream in the C ABI
+        handle = None if stream_ptr is None else (1 if int(stream_ptr) == 0 else int(stream_ptr))
+        self.check(self.lib.pqs_ctx_set_stream(self.handle, handle), "set_stream")
+        self._bound = stream_ptr
+
+    def bind_torch_stream(self) -> None:
+        """Before a call on CUDA tensors: run on torch's current stream of this
+        device, so the call is ordered with the kernels that produced its
+        inputs and those that consume its outputs."""
+        if not self.follow_torch:
+            return
+        import torch
+
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        if s != self._bound:
+            self._set(s)
 
     def synchronize(self) -> None:
         self.check(self.lib.pqs_ctx_synchronize(self.handle), "synchronize")

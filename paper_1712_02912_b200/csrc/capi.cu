@@ -14,10 +14,13 @@
 #include "pqs_common.cuh"
 
 int build_db4(pqs_ctx* ctx, pqs_db* db, const uint8_t* d_codes);
-int build_db8(pqs_ctx* ctx, pqs_db* db, const uint8_t* h_codes);
+int build_db8(pqs_ctx* ctx, pqs_db* db, const uint8_t* d_codes);
+int device_max_u8(pqs_ctx* ctx, const uint8_t* d, int64_t count, int* out);
+int launch_encode(pqs_ctx* ctx, const pqs_pq* pq, const float* d_x, int64_t n, const float* d_coarse,
+                  const int64_t* d_cells, uint8_t* d_out);
 int launch_quantize(pqs_ctx* ctx, double qmin, double qmax, const double* d_v, int64_t n, uint8_t* d_out);
 int ivf_create_impl(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t K, const int64_t* list_sizes,
-                    const uint8_t* codes, const int64_t* ids, pqs_ivf** out);
+                    const uint8_t* codes, const int64_t* ids, int io, pqs_ivf** out);
 void ivf_destroy_impl(pqs_ivf* ivf);
 
 int set_err(pqs_ctx* ctx, int code, const std::string& msg) {
@@ -204,6 +207,10 @@ int pqs_ctx_set_option(pqs_ctx* ctx, int option, int64_t value) {
       PQS_CHECK(ctx, value >= 0 && value <= 2, "scan4 engine must be 0, 1 or 2");
       ctx->scan4_engine = (int)value;
       return PQS_OK;
+    case PQS_OPT_TC_CHUNK_TILES:
+      PQS_CHECK(ctx, value >= 0, "chunk must be >= 0");
+      ctx->tc_chunk_tiles = value;
+      return PQS_OK;
   }
   return set_err(ctx, PQS_ERR_INVALID, "unknown option");
 }
@@ -258,29 +265,38 @@ void pqs_pq_destroy(pqs_pq* pq) {
 
 // ---------------------------------------------------------------- code lists
 int pqs_db_create(pqs_ctx* ctx, const uint8_t* codes, int64_t n, int m, int b, const int64_t* ids, int64_t id_base,
-                  pqs_db** out) {
+                  int io, pqs_db** out) {
   if (!ctx || !out) return PQS_ERR_INVALID;
   *out = nullptr;
+  PQS_TRY(check_io(ctx, io));
   PQS_CHECK(ctx, n >= 0, "n must be >= 0");
   PQS_CHECK(ctx, m >= 1, "m must be >= 1");
   PQS_CHECK(ctx, n < (1ll << 32), "a device code list holds at most 2^32 - 1 codes (shard larger lists)");
   PQS_CHECK(ctx, b == 4 || b == 8, "device code lists support b = 4 (Quick ADC) or b = 8 (float ADC)");
-  PQS_CUDA(ctx, cudaSetDevice(ctx->device));
-  int maxc = 0;
-  for (int64_t i = 0; i < n * m; ++i) maxc = std::max<int>(maxc, codes[i]);
   if (b == 4) {
     PQS_CHECK(ctx, m % 2 == 0, "b=4 transposition needs even m");
     PQS_CHECK(ctx, m <= 32, "Quick ADC device layout supports m <= 32");
-    PQS_CHECK(ctx, maxc < 16, "component out of range for b=4");
+  }
+  PQS_CUDA(ctx, cudaSetDevice(ctx->device));
+  // codes on the device (caller's pointer or a temporary copy)
+  uint8_t* tmp = nullptr;
+  const uint8_t* d_codes = codes;
+  if (io == PQS_IO_HOST && n) {
+    if (cudaMalloc(&tmp, (size_t)n * m) != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(ctx, PQS_ERR_NOMEM, "staging allocation failed");
+    }
+    d_codes = tmp;
+    const int s = upload(ctx, tmp, codes, (size_t)n * m);
+    if (s != PQS_OK) {
+      cudaFree(tmp);
+      return s;
+    }
   }
   pqs_db* db = new pqs_db();
-  db->n = n;
-  db->m = m;
-  db->b = b;
-  db->k = b == 4 ? 16 : 256;
-  db->max_code = maxc;
-  db->id_base = id_base;
-  auto fail = [&](int code, const char* msg) {
+  auto fail = [&](int code, const std::string& msg) {
+    cudaStreamSynchronize(ctx->stream);
+    if (tmp) cudaFree(tmp);
     if (db->codes8) cudaFree(db->codes8);
     if (db->words4) cudaFree(db->words4);
     if (db->ids) cudaFree(db->ids);
@@ -288,13 +304,22 @@ int pqs_db_create(pqs_ctx* ctx, const uint8_t* codes, int64_t n, int m, int b, c
     cudaGetLastError();
     return set_err(ctx, code, msg);
   };
+  int maxc = 0;
+  if (n && device_max_u8(ctx, d_codes, n * m, &maxc) != PQS_OK) return fail(PQS_ERR_CUDA, ctx->err);
+  if (b == 4 && maxc >= 16) return fail(PQS_ERR_INVALID, "component out of range for b=4");
+  db->n = n;
+  db->m = m;
+  db->b = b;
+  db->k = b == 4 ? 16 : 256;
+  db->max_code = maxc;
+  db->id_base = id_base;
   if (b == 8) {
     db->ntiles = cdiv(n, TILE8);
     if (db->ntiles) {
       if (cudaMalloc(&db->codes8, (size_t)db->ntiles * m * TILE8) != cudaSuccess)
         return fail(PQS_ERR_NOMEM, "code allocation failed");
-      int s = build_db8(ctx, db, codes);
-      if (s != PQS_OK) return fail(s, ctx->err.c_str());
+      const int s = build_db8(ctx, db, d_codes);
+      if (s != PQS_OK) return fail(s, ctx->err);
     }
   } else {
     int mp = 2;
@@ -304,13 +329,8 @@ int pqs_db_create(pqs_ctx* ctx, const uint8_t* codes, int64_t n, int m, int b, c
     if (db->ntiles) {
       const size_t words = (size_t)db->ntiles * QUADS4 * (mp / 2);
       if (cudaMalloc(&db->words4, words * 4) != cudaSuccess) return fail(PQS_ERR_NOMEM, "code allocation failed");
-      uint8_t* d_codes = nullptr;
-      if (cudaMalloc(&d_codes, (size_t)n * m) != cudaSuccess) return fail(PQS_ERR_NOMEM, "staging allocation failed");
-      int s = upload(ctx, d_codes, codes, (size_t)n * m);
-      if (s == PQS_OK) s = build_db4(ctx, db, d_codes);
-      cudaStreamSynchronize(ctx->stream);
-      cudaFree(d_codes);
-      if (s != PQS_OK) return fail(s, ctx->err.c_str());
+      const int s = build_db4(ctx, db, d_codes);
+      if (s != PQS_OK) return fail(s, ctx->err);
     }
   }
   if (ids && n) {
@@ -318,19 +338,29 @@ int pqs_db_create(pqs_ctx* ctx, const uint8_t* codes, int64_t n, int m, int b, c
     if (upload(ctx, db->ids, ids, (size_t)n * 8) != PQS_OK) return fail(PQS_ERR_CUDA, "id upload failed");
   }
   PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (tmp) cudaFree(tmp);
   *out = db;
   return PQS_OK;
 }
 
-int pqs_db_set_prefix(pqs_ctx* ctx, pqs_db* db, const uint8_t* prefix, int64_t n_prefix) {
+int pqs_db_set_prefix(pqs_ctx* ctx, pqs_db* db, const uint8_t* prefix, int64_t n_prefix, int io) {
   if (!ctx || !db) return PQS_ERR_INVALID;
+  PQS_TRY(check_io(ctx, io));
   PQS_CHECK(ctx, db->b == 4, "a global prefix applies to Quick ADC (b=4) lists");
   PQS_CHECK(ctx, n_prefix >= 1, "prefix must hold at least one code");
-  for (int64_t i = 0; i < n_prefix * db->m; ++i) PQS_CHECK(ctx, prefix[i] < 16, "component out of range for b=4");
+  PQS_CUDA(ctx, cudaSetDevice(ctx->device));
   if (db->prefix) cudaFree(db->prefix);
   db->prefix = nullptr;
+  db->n_prefix = 0;
   PQS_CUDA(ctx, cudaMalloc(&db->prefix, (size_t)n_prefix * db->m));
   PQS_TRY(upload(ctx, db->prefix, prefix, (size_t)n_prefix * db->m));
+  int maxc = 0;
+  PQS_TRY(device_max_u8(ctx, db->prefix, n_prefix * db->m, &maxc));
+  if (maxc >= 16) {
+    cudaFree(db->prefix);
+    db->prefix = nullptr;
+    return set_err(ctx, PQS_ERR_INVALID, "component out of range for b=4");
+  }
   db->n_prefix = n_prefix;
   return PQS_OK;
 }
@@ -531,10 +561,37 @@ int pqs_quantized_distances(pqs_ctx* ctx, const pqs_db* db, const uint8_t* qtabl
 
 // ---------------------------------------------------------------- IVF
 int pqs_ivf_create(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t K, const int64_t* list_sizes,
-                   const uint8_t* codes, const int64_t* ids, pqs_ivf** out) {
+                   const uint8_t* codes, const int64_t* ids, int io, pqs_ivf** out) {
   if (!ctx || !pq || !out) return PQS_ERR_INVALID;
+  PQS_TRY(check_io(ctx, io));
   PQS_CUDA(ctx, cudaSetDevice(ctx->device));
-  return ivf_create_impl(ctx, pq, coarse, K, list_sizes, codes, ids, out);
+  return ivf_create_impl(ctx, pq, coarse, K, list_sizes, codes, ids, io, out);
+}
+
+// ---------------------------------------------------------------- encode
+int pqs_encode(pqs_ctx* ctx, const pqs_pq* pq, const float* x, int64_t n, const float* coarse, int64_t K,
+               const int64_t* cells, uint8_t* out_codes, int io) {
+  if (!ctx || !pq) return PQS_ERR_INVALID;
+  PQS_TRY(check_io(ctx, io));
+  PQS_CHECK(ctx, n >= 0, "n must be >= 0");
+  PQS_CHECK(ctx, pq->k <= 256, "device encode supports b <= 8 (uint8 codes)");
+  PQS_CHECK(ctx, (coarse == nullptr) == (cells == nullptr), "coarse and cells go together");
+  PQS_CHECK(ctx, coarse == nullptr || K >= 1, "K must be >= 1");
+  if (n == 0) return PQS_OK;
+  PQS_CUDA(ctx, cudaSetDevice(ctx->device));
+  const float* dx = nullptr;
+  const float* dg = nullptr;
+  const int64_t* dc = nullptr;
+  uint8_t* dout = nullptr;
+  PQS_TRY(stage_in(ctx, S_QUERIES, x, (size_t)n * pq->d, io, &dx));
+  if (coarse) {
+    PQS_TRY(stage_in(ctx, S_IVF_WORK, coarse, (size_t)K * pq->d, io, &dg));
+    PQS_TRY(stage_in(ctx, S_PROBE, cells, (size_t)n, io, &dc));
+  }
+  PQS_TRY(stage_out(ctx, S_OUT_B, out_codes, (size_t)n * pq->m, io, &dout));
+  PQS_TRY(launch_encode(ctx, pq, dx, n, dg, dc, dout));
+  PQS_TRY(copy_out(ctx, out_codes, dout, (size_t)n * pq->m, io));
+  return finish(ctx, io);
 }
 
 void pqs_ivf_destroy(pqs_ivf* ivf) { ivf_destroy_impl(ivf); }

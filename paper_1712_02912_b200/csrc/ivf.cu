@@ -464,8 +464,11 @@ int get_cublas(pqs_ctx* ctx, cublasHandle_t* out) {
 void ivf_destroy_impl(pqs_ivf* iv);
 
 // ---------------------------------------------------------------------------
+int device_max_u8(pqs_ctx* ctx, const uint8_t* d, int64_t count, int* out);
+
+// coarse, codes and ids: host or device pointers (io); list_sizes: host
 int ivf_create_impl(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t K, const int64_t* list_sizes,
-                    const uint8_t* codes, const int64_t* ids, pqs_ivf** out) {
+                    const uint8_t* codes, const int64_t* ids, int io, pqs_ivf** out) {
   *out = nullptr;
   PQS_CHECK(ctx, K >= 1, "need at least one coarse centroid");
   PQS_CHECK(ctx, pq->k <= 256, "IVF lists need b <= 8");
@@ -479,7 +482,7 @@ int ivf_create_impl(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t
   const int64_t n = offs[K];
   PQS_CHECK(ctx, n < (1ll << 32), "an IVF shard holds at most 2^32 - 1 codes");
   PQS_CHECK(ctx, K < (1ll << 31), "K must be < 2^31");
-  for (int64_t i = 0; i < n * pq->m; ++i) PQS_CHECK(ctx, codes[i] < pq->k, "code component out of range");
+  (void)io;  // copies below use cudaMemcpyDefault (host or device sources)
   pqs_ivf* iv = new pqs_ivf();
   iv->K = K;
   iv->n = n;
@@ -507,6 +510,12 @@ int ivf_create_impl(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t
   if (n) {
     PQS_TRY(upload(ctx, iv->codes, codes, (size_t)n * pq->m));
     PQS_TRY(upload(ctx, iv->ids, ids, (size_t)n * 8));
+    int maxc = 0;
+    PQS_TRY(device_max_u8(ctx, iv->codes, n * pq->m, &maxc));
+    if (maxc >= pq->k) {
+      ivf_destroy_impl(iv);
+      return set_err(ctx, PQS_ERR_INVALID, "code component out of range");
+    }
   }
   PQS_CUDA(ctx, cudaMemsetAsync(iv->vmax, 0, 16, ctx->stream));
   cnorm_kernel<<<(unsigned)cdiv(K, 256), 256, 0, ctx->stream>>>(iv->coarse, K, d, iv->cnorm, iv->gnorm);

@@ -55,7 +55,7 @@ enum ScratchSlot {
   S_MISC,
   S_WORK,     // dynamic work counters
   S_QT_WORK,  // quantized tables of a Quick ADC search
-  S_TC_B, S_TC_TH, S_TC_REC, S_TC_RECCNT,
+  S_TC_B, S_TC_TH, S_TC_REC, S_TC_RECCNT, S_TC_OVF,
   S_NSLOTS
 };
 
@@ -69,6 +69,7 @@ struct pqs_ctx {
   int sample_div = 32;
   int force_fallback = 0;
   int scan4_engine = 0;  // 0 auto (tcgen05 when possible), 1 PRMT, 2 tcgen05
+  int64_t tc_chunk_tiles = 0;  // tcgen05 scan: max 128-code tiles per launch (0 = auto)
   int64_t launches = 0;
   int64_t last_max_cand = 0;
   int64_t last_overflow = 0;

@@ -224,7 +224,10 @@ __global__ void __launch_bounds__(SCAN4_THREADS) qadc_params_kernel(
 }
 
 // ---------------------------------------------------------------- K4 scan
-enum { MODE_DENSE = 0, MODE_FILTER = 1 };
+enum { MODE_DENSE = 0, MODE_FILTER = 1, MODE_HIST = 2 };
+
+// theta value meaning "no survivors" (a strict threshold below bin 0)
+constexpr uint8_t THETA_NONE = 255;
 
 struct Scan4Args {
   const uint32_t* words;
@@ -242,12 +245,13 @@ struct Scan4Args {
   int64_t ld;
   uint32_t one;            // runtime 1 (see imad)
   uint32_t k24;            // runtime 2^24 (v >> 8 as a high multiply)
-  int tout;                // dense output transposed: u32 [col/4][nq] (4 packed bins)
   // filter
   const uint8_t* theta;
   uint64_t* cand;
   int* cand_cnt;
   int64_t cap;
+  // hist
+  unsigned int* ghist;     // (nq, 128) bin histograms of the scanned codes
 };
 
 template <int MP>
@@ -298,6 +302,23 @@ __device__ __forceinline__ void flush_cands(const uint64_t* stage, int cnt, int6
     if (pos + i < cap) cand[q * cap + pos + i] = stage[i * SCAN4_THREADS];
 }
 
+// MODE_HIST: per-thread (= per-query) u16 bin counters in shared memory,
+// [bin][thread] so a warp's 32 increments touch 16 distinct words of 16
+// banks whatever the bins (conflict-free); flushed to the global (nq, 128)
+// histogram before a counter can wrap.
+constexpr int HIST_FLUSH_CODES = 60000;
+
+__device__ __forceinline__ void flush_hist(uint16_t* h, int64_t q, bool valid, unsigned int* ghist) {
+#pragma unroll 4
+  for (int b = 0; b < 128; ++b) {
+    const unsigned int v = h[b * SCAN4_THREADS];
+    if (v) {
+      if (valid) atomicAdd(ghist + q * 128 + b, v);
+      h[b * SCAN4_THREADS] = 0;
+    }
+  }
+}
+
 template <int MP, int MODE>
 __global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kernel(Scan4Args a) {
   constexpr int HP = MP / 2;
@@ -307,7 +328,12 @@ __global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kerne
   extern __shared__ __align__(16) uint4 s_pred[];  // 2 buffers of WORDS uint4 (+ candidate stage)
   const int nthreads = blockDim.x;
   uint64_t* stage = reinterpret_cast<uint64_t*>(s_pred + 2 * WORDS) + threadIdx.x;
+  uint16_t* hist = reinterpret_cast<uint16_t*>(s_pred + 2 * WORDS) + threadIdx.x;
   int ncand = 0;
+  int hcodes = 0;  // codes counted since the last histogram flush
+  if (MODE == MODE_HIST) {
+    for (int b = 0; b < 128; ++b) hist[b * SCAN4_THREADS] = 0;
+  }
 
   // persistent CTAs grab tiles of the linearised (query group, tile) list from
   // a global counter (dynamic balance); tables are reloaded at group switches
@@ -344,7 +370,10 @@ __global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kerne
       }
     }
     theta = (MODE == MODE_FILTER && qvalid) ? a.theta[q] : 0u;
-    bias = (0x7FFFu - theta) * 0x00010001u;
+    // theta 127 admits every code: bin = min(S, 127) <= 127 for any sum S
+    if (theta == 127u) theta = 0x7FFFu;
+    // THETA_NONE: bit 15 of every lane stays set -> no survivors
+    bias = theta == THETA_NONE ? 0x80008000u : (0x7FFFu - theta) * 0x00010001u;
   };
 
   uint4 regs[PER];
@@ -362,6 +391,10 @@ __global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kerne
       if (MODE == MODE_FILTER && ncand > 0) {
         flush_cands(stage, ncand, q, a.cand, a.cand_cnt, a.cap);
         ncand = 0;
+      }
+      if (MODE == MODE_HIST && hcodes > 0) {
+        flush_hist(hist, q, qvalid, a.ghist);
+        hcodes = 0;
       }
       load_group(qg);
       cur_qg = qg;
@@ -402,26 +435,30 @@ __global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kerne
             }
           }
         }
+      } else if (MODE == MODE_HIST) {
+        const uint32_t S[4] = {ae & 0xFFFFu, ao & 0xFFFFu, ae >> 16, ao >> 16};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t b = S[e] < 127u ? S[e] : 127u;
+          if (c + e < a.n) hist[b * SCAN4_THREADS] += 1;
+        }
       } else {
         if (qvalid) {
           const uint32_t S[4] = {ae & 0xFFFFu, ao & 0xFFFFu, ae >> 16, ao >> 16};
           const int64_t col = i * TILE4 + 4 * g;
-          if (a.tout) {
-            uint32_t packed = 0;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const uint32_t b = (c + e < a.n) ? (S[e] < 127u ? S[e] : 127u) : 255u;
-              packed |= b << (8 * e);
-            }
-            reinterpret_cast<uint32_t*>(a.out)[(col >> 2) * a.nq + q] = packed;
-          } else {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const uint32_t b = S[e] < 127u ? S[e] : 127u;
-              if (col + e < a.ld) a.out[q * a.ld + col + e] = (c + e < a.n) ? (uint8_t)b : (uint8_t)255;
-            }
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t b = S[e] < 127u ? S[e] : 127u;
+            if (col + e < a.ld) a.out[q * a.ld + col + e] = (c + e < a.n) ? (uint8_t)b : (uint8_t)255;
           }
         }
+      }
+    }
+    if (MODE == MODE_HIST) {
+      hcodes += 4 * gq;
+      if (hcodes > HIST_FLUSH_CODES - 4 * gq) {
+        flush_hist(hist, q, qvalid, a.ghist);
+        hcodes = 0;
       }
     }
     if (has_next) store_tile_pred<MP>(regs, s_pred + (cur ^ 1) * WORDS, nthreads);
@@ -433,13 +470,15 @@ __global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kerne
     cur ^= 1;
   }
   if (MODE == MODE_FILTER && ncand > 0 && q >= 0) flush_cands(stage, ncand, q, a.cand, a.cand_cnt, a.cap);
+  if (MODE == MODE_HIST && hcodes > 0) flush_hist(hist, q, qvalid, a.ghist);
 }
 
 template <int MP, int MODE>
 int launch_scan4_t(pqs_ctx* ctx, Scan4Args a, int64_t nq) {
   constexpr int HP = MP / 2;
   const size_t smem = 2 * (size_t)QUADS4 * HP * sizeof(uint4) +
-                      (MODE == MODE_FILTER ? (size_t)CSTAGE * SCAN4_THREADS * sizeof(uint64_t) : 0);
+                      (MODE == MODE_FILTER ? (size_t)CSTAGE * SCAN4_THREADS * sizeof(uint64_t) : 0) +
+                      (MODE == MODE_HIST ? (size_t)128 * SCAN4_THREADS * sizeof(uint16_t) : 0);
   PQS_CUDA(ctx, cudaFuncSetAttribute(scan4_kernel<MP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
   const int threads = SCAN4_THREADS;  // the tile loader assumes a full CTA
@@ -472,39 +511,14 @@ int launch_scan4(pqs_ctx* ctx, int mp, const Scan4Args& a, int64_t nq) {
   return set_err(ctx, PQS_ERR_UNSUPPORTED, "scan4: unsupported padded m");
 }
 
-// per-query threshold bin from the transposed dense sample (u32 [rows][nq],
-// 4 packed bins per word): the r-th smallest valid bin.  theta4_hist_kernel:
-// one CTA per (32 queries, row slice); a conflict-free [bin][lane] shared
-// histogram, then one global atomicAdd per non-zero bin.
-__global__ void theta4_hist_kernel(const uint32_t* __restrict__ sample, int64_t rows, int64_t nq, int64_t rows_per,
-                                   unsigned int* __restrict__ ghist) {
-  __shared__ unsigned int hist[128][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int64_t q = blockIdx.x * 32 + lane;
-  for (int i = threadIdx.x; i < 128 * 32; i += blockDim.x) (&hist[0][0])[i] = 0;
-  __syncthreads();
-  const int64_t r0 = blockIdx.y * rows_per, r1 = min(rows, r0 + rows_per);
-  if (q < nq) {
-    for (int64_t row = r0 + warp; row < r1; row += nw) {
-      const uint32_t w = sample[row * nq + q];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint32_t b = (w >> (8 * e)) & 255u;
-        if (b < 128) atomicAdd(&hist[b][lane], 1u);
-      }
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < 128 * 32; i += blockDim.x) {
-    const int b = i >> 5, l = i & 31;
-    const int64_t qq = blockIdx.x * 32 + l;
-    const unsigned int v = hist[b][l];
-    if (v && qq < nq) atomicAdd(ghist + qq * 128 + b, v);
-  }
-}
-
-__global__ void theta4_final_kernel(const unsigned int* __restrict__ ghist, int64_t nq, int r,
-                                    uint8_t* __restrict__ theta) {
+// theta[q] = the r-th smallest bin of the sample (the first st tiles, the
+// "prefix"); theta_main[q] is the threshold for the codes after the prefix:
+// with ids increasing in storage order, a code outside the prefix has a larger
+// id than every prefix code, so it can only enter the top-r with a bin
+// strictly below theta (the prefix alone holds r codes with bin <= theta) --
+// theta - 1, or THETA_NONE when theta == 0.  With explicit ids: theta.
+__global__ void theta4_final_kernel(const unsigned int* __restrict__ ghist, int64_t nq, int r, int strict,
+                                    uint8_t* __restrict__ theta, uint8_t* __restrict__ theta_main) {
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= nq) return;
   unsigned long long c = 0;
@@ -517,6 +531,7 @@ __global__ void theta4_final_kernel(const unsigned int* __restrict__ ghist, int6
     }
   }
   theta[q] = (uint8_t)t;
+  if (theta_main) theta_main[q] = strict ? (t == 0 ? THETA_NONE : (uint8_t)(t - 1)) : (uint8_t)t;
 }
 
 __global__ void fill_u8_kernel(uint8_t* p, int64_t n, uint8_t v) {
@@ -534,8 +549,9 @@ __global__ void gather_rows_u8_kernel(const uint8_t* __restrict__ src, const int
 
 }  // namespace
 
-int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const uint8_t* d_theta, int64_t nq,
-                    uint64_t* cand, int* cand_cnt, int64_t cap, int* overflow);
+int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const uint8_t* d_theta,
+                    const uint8_t* d_theta_main, int64_t prefix_tiles, int64_t nq, uint64_t* cand, int* cand_cnt,
+                    int64_t cap, int* d_ovf);
 
 // ---------------------------------------------------------------------------
 int build_db4(pqs_ctx* ctx, pqs_db* db, const uint8_t* d_codes) {
@@ -586,25 +602,28 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
                                                                      n_init, d_qt, d_qmm);
   PQS_LAUNCHED(ctx);
 
-  // ---- threshold: exact when every code fits the candidate buffer
+  // ---- threshold: exact when every code fits the candidate buffer.
+  // Otherwise a certified threshold from a sample -- the first st tiles (the
+  // "prefix"): theta = the r-th smallest prefix bin, so the prefix alone holds
+  // >= r codes with bin <= theta and every top-r code has bin <= theta.  The
+  // prefix is filtered with theta, the rest with theta_main (theta4_final_kernel).
   uint8_t* theta = nullptr;
-  PQS_TRY(scratch(ctx, S_THETA, (size_t)nq, &theta));
+  uint8_t* theta_main = nullptr;
+  PQS_TRY(scratch(ctx, S_THETA, (size_t)(2 * nq), &theta));
+  theta_main = theta + nq;
   const int64_t cap = std::min<int64_t>(ctx->cand_cap, std::max<int64_t>(n, 1));
   const int64_t r_eff = std::min<int64_t>(r, n);
-  bool sampled = false;
+  int64_t st = 0;  // prefix tiles (TILE4 codes each); 0 = no sample
   if (n <= cap) {
     fill_u8_kernel<<<(unsigned)cdiv(nq, 256), 256, 0, ctx->stream>>>(theta, nq, 127);
     PQS_LAUNCHED(ctx);
   } else {
-    // strided sample of whole tiles
-    int64_t st = std::max<int64_t>(cdiv(db->ntiles, ctx->sample_div), cdiv(16 * r_eff, TILE4));
+    st = std::max<int64_t>(cdiv(db->ntiles, ctx->sample_div), cdiv(16 * r_eff, TILE4));
     st = std::min<int64_t>(st, db->ntiles);
-    const int64_t step = std::max<int64_t>(1, db->ntiles / st);
-    const int64_t ns = st * TILE4;
-    uint8_t* sample = nullptr;
-    PQS_TRY(scratch(ctx, S_SAMPLE, (size_t)(nq * ns), &sample));
+    unsigned int* ghist = nullptr;
+    PQS_TRY(scratch(ctx, S_IVF_WORK3, (size_t)(nq * 128), &ghist));
+    PQS_CUDA(ctx, cudaMemsetAsync(ghist, 0, sizeof(unsigned int) * nq * 128, ctx->stream));
     Scan4Args a{};
-    a.tout = 1;
     a.parts = 4;
     a.words = db->words4;
     a.n = n;
@@ -613,67 +632,71 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
     a.nq = nq;
     a.nvt = st;
     a.tile_off = 0;
-    a.tile_step = step;
-    a.out = sample;
-    a.ld = ns;
-    PQS_TRY(launch_scan4<MODE_DENSE>(ctx, db->mp, a, nq));
-    unsigned int* ghist = nullptr;
-    PQS_TRY(scratch(ctx, S_IVF_WORK3, (size_t)(nq * 128), &ghist));
-    PQS_CUDA(ctx, cudaMemsetAsync(ghist, 0, sizeof(unsigned int) * nq * 128, ctx->stream));
-    const int64_t rows = ns / 4;
-    const int64_t qg = cdiv(nq, 32);
-    const int64_t rs = std::max<int64_t>(1, std::min<int64_t>(cdiv(rows, 256), cdiv(4 * ctx->sm_count, qg)));
-    dim3 tgrid((unsigned)qg, (unsigned)rs);
-    theta4_hist_kernel<<<tgrid, 256, 0, ctx->stream>>>((const uint32_t*)sample, rows, nq, cdiv(rows, rs), ghist);
+    a.tile_step = 1;
+    a.ghist = ghist;
+    PQS_TRY(launch_scan4<MODE_HIST>(ctx, db->mp, a, nq));
+    theta4_final_kernel<<<(unsigned)cdiv(nq, 128), 128, 0, ctx->stream>>>(ghist, nq, (int)r_eff,
+                                                                           db->ids == nullptr ? 1 : 0, theta,
+                                                                           theta_main);
     PQS_LAUNCHED(ctx);
-    theta4_final_kernel<<<(unsigned)cdiv(nq, 128), 128, 0, ctx->stream>>>(ghist, nq, (int)r_eff, theta);
-    PQS_LAUNCHED(ctx);
-    sampled = true;
   }
 
-  // ---- K4 filtered scan
+  // ---- K4 filtered scan: prefix tiles [0, st) with theta, the rest with theta_main
   uint64_t* cand = nullptr;
   int* cnt = nullptr;
   PQS_TRY(scratch(ctx, S_CAND, (size_t)(nq * cap), &cand));
   PQS_TRY(scratch(ctx, S_CAND_CNT, (size_t)nq, &cnt));
   PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nq, ctx->stream));
   {
-    Scan4Args a{};
-    a.words = db->words4;
-    a.n = n;
-    a.m = m;
-    a.qt = d_qt;
-    a.nq = nq;
-    a.nvt = db->ntiles;
-    a.tile_off = 0;
-    a.tile_step = 1;
-    a.theta = theta;
-    a.cand = cand;
-    a.cand_cnt = cnt;
-    a.cap = cap;
-    int done = 0;
-    if (sampled && ctx->scan4_engine != 1) {
-      int overflow = 0;
-      const int st = launch_scan4_tc(ctx, db, d_qt, theta, nq, cand, cnt, cap, &overflow);
-      if (st == PQS_OK && !overflow) {
-        done = 1;
+    const int64_t t1 = st > 0 ? st : db->ntiles;  // end of the first range
+    PQS_TRY(scan_timer_begin(ctx));
+    bool done = false;
+    if (st > 0 && ctx->scan4_engine != 1) {
+      // tcgen05 engine (128-code tiles); a record overflow -> redo with PRMT
+      int* d_ovf = nullptr;
+      PQS_TRY(scratch(ctx, S_TC_OVF, 1, &d_ovf));
+      PQS_CUDA(ctx, cudaMemsetAsync(d_ovf, 0, sizeof(int), ctx->stream));
+      const int64_t nt128 = cdiv(n, 128);
+      int rc = launch_scan4_tc(ctx, db, d_qt, theta, theta_main, t1 * (TILE4 / 128), nq, cand, cnt, cap, d_ovf);
+      int ovf = 0;
+      if (rc == PQS_OK) PQS_TRY(download(ctx, &ovf, d_ovf, sizeof(int)));
+      if (rc == PQS_OK && !ovf) {
+        done = true;
         ctx->last_scan_engine = 2;
-        ctx->last_scan_work = 2.0 * (double)cdiv(nq, 256) * 256.0 * (double)cdiv(n, 128) * 128.0 * 256.0;
-      } else if (st == PQS_OK || st == PQS_ERR_UNSUPPORTED) {
-        if (ctx->scan4_engine == 2 && st == PQS_ERR_UNSUPPORTED)
+        ctx->last_scan_work = 2.0 * (double)cdiv(nq, 256) * 256.0 * (double)nt128 * 128.0 * 256.0;
+      } else if (rc == PQS_OK || rc == PQS_ERR_UNSUPPORTED) {
+        if (ctx->scan4_engine == 2 && rc == PQS_ERR_UNSUPPORTED)
           return set_err(ctx, PQS_ERR_UNSUPPORTED, "tcgen05 Quick ADC scan: unsupported shape (needs m <= 16)");
         PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nq, ctx->stream));  // redo with PRMT
       } else {
-        return st;
+        return rc;
       }
     }
     if (!done) {
-      PQS_TRY(scan_timer_begin(ctx));
+      Scan4Args a{};
+      a.words = db->words4;
+      a.n = n;
+      a.m = m;
+      a.qt = d_qt;
+      a.nq = nq;
+      a.tile_step = 1;
+      a.cand = cand;
+      a.cand_cnt = cnt;
+      a.cap = cap;
+      a.nvt = t1;
+      a.tile_off = 0;
+      a.theta = theta;
       PQS_TRY(launch_scan4<MODE_FILTER>(ctx, db->mp, a, nq));
-      PQS_TRY(scan_timer_end(ctx));
+      if (t1 < db->ntiles) {
+        a.nvt = db->ntiles - t1;
+        a.tile_off = t1;
+        a.theta = theta_main;
+        PQS_TRY(launch_scan4<MODE_FILTER>(ctx, db->mp, a, nq));
+      }
       ctx->last_scan_engine = 1;
       ctx->last_scan_work = (double)nq * (double)n * (double)m;
     }
+    PQS_TRY(scan_timer_end(ctx));
     ctx->last_scan_launches = 1;
   }
   ctx->last_evals = nq * n;

@@ -143,8 +143,11 @@ struct Scan4TcArgs {
   const uint32_t* words;   // 4-bit quad layout (mp = 16: 8 words per quad)
   int64_t n;
   const uint8_t* bglob;    // [nqg][B_BYTES] canonical B tiles
-  const int* nthr;         // [nqg * 128] packed per-column-pair biases (see build_b_kernel)
-  int64_t nq, nqg, ntiles; // ntiles of TC_M codes
+  const int* nthr;         // [nqg][2][128] packed per-column-pair biases (build_bias_kernel):
+                           // set 0 for tiles < prefix_tiles, set 1 after
+  int64_t prefix_tiles;    // global tile index where the second threshold set starts
+  int64_t nq, nqg, ntiles; // ntiles of TC_M codes in this launch's range
+  int64_t tile0;           // first tile of the range
   uint64_t* rec;           // [gridDim][rec_cap] (q << 40 | bin << 32 | idx)
   int* rec_cnt;            // [gridDim]
   int64_t rec_cap;
@@ -162,8 +165,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smtc[];
   uint8_t* sB = smtc;                           // 64 KB (one query group)
   uint8_t* sA = smtc + B_BYTES;                 // 2 x 32 KB
-  uint32_t* sTh = reinterpret_cast<uint32_t*>(smtc + B_BYTES + 2 * A_BYTES);  // 2 x 128 packed biases
-  uint32_t* stage = reinterpret_cast<uint32_t*>(smtc + B_BYTES + 2 * A_BYTES + 2 * TC_N * 2);
+  uint32_t* sTh = reinterpret_cast<uint32_t*>(smtc + B_BYTES + 2 * A_BYTES);  // [2 buffers][2 sets][128] biases
+  uint32_t* stage = reinterpret_cast<uint32_t*>(smtc + B_BYTES + 2 * A_BYTES + 4 * TC_N * 2);
   __shared__ __align__(8) uint64_t bar_b[2], bar_afull[2], bar_aempty[2], bar_accfull[2], bar_accempty[2];
   __shared__ uint32_t s_tmem;
   __shared__ int s_cnt;
@@ -216,9 +219,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
               // (its last commit to bar_aempty) before the new B overwrites it
               mbar_wait(&bar_aempty[(it - 1) & 1], (uint32_t)(((it - 1) >> 1) & 1));
             }
-            mbar_expect_tx(&bar_b[bb], (uint32_t)(B_BYTES + TC_N * 2));
+            mbar_expect_tx(&bar_b[bb], (uint32_t)(B_BYTES + TC_N * 4));
             bulk_g2s(sB, a.bglob + g * (int64_t)B_BYTES, B_BYTES, &bar_b[bb]);
-            bulk_g2s(sTh + bb * (TC_N / 2), a.nthr + g * (TC_N / 2), TC_N * 2, &bar_b[bb]);
+            bulk_g2s(sTh + bb * TC_N, a.nthr + g * TC_N, TC_N * 4, &bar_b[bb]);
             mbar_wait(&bar_b[bb], 0);
             cur_g = g;
           }
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
         const uint32_t ph = (uint32_t)((it >> 1) & 1);
         mbar_wait_sleep(&bar_aempty[ab], ph ^ 1);  // MMA finished reading this buffer
         if (a.dbg && blockIdx.x == 0 && it < 64 && threadIdx.x == EPI_WARPS * 32) a.dbg[it * 8 + 3] = gtime();
-        const int64_t tile = tile_of(w);
+        const int64_t tile = a.tile0 + tile_of(w);
         const int64_t code = tile * TC_M + row;
         uint32_t wd[8];
         if (code < a.n) {
@@ -300,7 +303,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
           const uint32_t r = my_stage[i * (EPI_WARPS * 32)];
           const int64_t wi = w0 + (int64_t)(r >> 15);
           const int64_t gg = group_of(wi);
-          const int64_t code = tile_of(wi) * TC_M + row;
+          const int64_t code = (a.tile0 + tile_of(wi)) * TC_M + row;
           const int64_t q = gg * TC_N + ((r >> 7) & 255u);
           if (base + i < a.rec_cap)
             a.rec[(int64_t)blockIdx.x * a.rec_cap + base + i] =
@@ -323,9 +326,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
         mbar_wait(&bar_accfull[ab], ph);
         if (a.dbg && blockIdx.x == 0 && it < 64 && threadIdx.x == 0) a.dbg[it * 8 + 5] = gtime();
         tc_fence_after();
-        const int64_t tile = tile_of(w);
+        const int64_t tile = a.tile0 + tile_of(w);
         const bool cvalid = tile * TC_M + row < a.n;
-        const uint32_t* bias = sTh + (gi & 1) * (TC_N / 2);
+        const uint32_t* bias = sTh + (gi & 1) * TC_N + (tile >= a.prefix_tiles ? TC_N / 2 : 0);
         const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * TC_N);
         const uint32_t itag = (uint32_t)it << 15;
 #pragma unroll 1
@@ -357,7 +360,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const bool hit = ((x[i] >> (16 * h + 15)) & 1u) == 0u;
-                if (hit) my_stage[ncand * (EPI_WARPS * 32)] = base + ((uint32_t)(2 * i + h) << 7) + (v[2 * i + h] & 127u);
+                if (hit) my_stage[ncand * (EPI_WARPS * 32)] = base + ((uint32_t)(2 * i + h) << 7) + min(v[2 * i + h], 127u);
                 ncand += hit ? 1 : 0;
               }
             }
@@ -383,8 +386,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
 
 // B tiles in the canonical K-major no-swizzle layout + negated thresholds:
 // B[n][k] at (k/16) * LBO_B + (n/8) * 128 + (n%8) * 16 + k%16, k = 16 j + i.
-__global__ void build_b_kernel(const uint8_t* __restrict__ qt, const uint8_t* __restrict__ theta, int64_t nq, int m,
-                               int64_t nqg, uint8_t* __restrict__ bglob, int* __restrict__ nthr) {
+__global__ void build_b_kernel(const uint8_t* __restrict__ qt, int64_t nq, int m, int64_t nqg,
+                               uint8_t* __restrict__ bglob) {
   const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // one per (group, n, j)
   if (gid >= nqg * TC_N * 16) return;
   const int j = (int)(gid % 16);
@@ -394,14 +397,25 @@ __global__ void build_b_kernel(const uint8_t* __restrict__ qt, const uint8_t* __
   uint4 v = make_uint4(0, 0, 0, 0);
   if (q < nq && j < m) v = *reinterpret_cast<const uint4*>(qt + (q * m + j) * 16);
   *reinterpret_cast<uint4*>(bglob + g * (int64_t)B_BYTES + (int64_t)j * LBO_B + (n >> 3) * 128 + (n & 7) * 16) = v;
-  if (j == 0 && (n & 1) == 0) {
-    // packed 16-bit lane biases of the column pair (n, n+1): S + (0x7FFF - theta) has
-    // bit 15 clear iff S <= theta; padding queries get 0x8000 (never clear)
-    const int64_t q1 = q + 1;
-    const uint32_t b0 = q < nq ? 0x7FFFu - theta[q] : 0x8000u;
-    const uint32_t b1 = q1 < nq ? 0x7FFFu - theta[q1] : 0x8000u;
-    nthr[g * (TC_N / 2) + (n >> 1)] = (int)(b0 | (b1 << 16));
-  }
+}
+
+// packed 16-bit lane biases of the column pair (2i, 2i+1): S + (0x7FFF - theta)
+// has bit 15 clear iff S <= theta; padding queries and THETA_NONE (255) get
+// 0x8000 (never clear)
+// nthr layout [group][set][128 pairs]: set 0 from theta, set 1 from theta2
+__global__ void build_bias_kernel(const uint8_t* __restrict__ theta, const uint8_t* __restrict__ theta2, int64_t nq,
+                                  int64_t npairs, int* __restrict__ nthr) {
+  const int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // (pair, set)
+  if (gi >= 2 * npairs) return;
+  const int set = (int)(gi & 1);
+  const int64_t i = gi >> 1;
+  if (set) theta = theta2;
+  const int64_t q0 = 2 * i, q1 = q0 + 1;
+  const uint32_t t0 = q0 < nq ? theta[q0] : 255u, t1 = q1 < nq ? theta[q1] : 255u;
+  // 127 admits every sum (bin = min(S, 127)): bias 0 keeps bit 15 clear
+  const uint32_t b0 = t0 == 255u ? 0x8000u : (t0 == 127u ? 0u : 0x7FFFu - t0);
+  const uint32_t b1 = t1 == 255u ? 0x8000u : (t1 == 127u ? 0u : 0x7FFFu - t1);
+  nthr[(i / (TC_N / 2)) * TC_N + set * (TC_N / 2) + i % (TC_N / 2)] = (int)(b0 | (b1 << 16));
 }
 
 // per-CTA survivor records -> per-query candidate lists (bin << 32 | idx).
@@ -409,11 +423,13 @@ __global__ void build_b_kernel(const uint8_t* __restrict__ qt, const uint8_t* __
 // reservation per (region, query), then a scatter -- ~nq global atomics per
 // region instead of one per record.
 __global__ void bucket_kernel(const uint64_t* __restrict__ rec, const int* __restrict__ rec_cnt, int64_t rec_cap,
-                              int64_t nq, uint64_t* __restrict__ cand, int* __restrict__ cand_cnt, int64_t cap) {
+                              int64_t nq, uint64_t* __restrict__ cand, int* __restrict__ cand_cnt, int64_t cap,
+                              int* __restrict__ ovf) {
   extern __shared__ int bsm[];
   int* hist = bsm;        // [nq]
   int* basev = bsm + nq;  // [nq]
   const int b = blockIdx.x;
+  if (threadIdx.x == 0 && rec_cnt[b] > rec_cap) atomicOr(ovf, 1);
   const int cnt = (int)min((int64_t)rec_cnt[b], rec_cap);
   const uint64_t* r = rec + (int64_t)b * rec_cap;
   for (int64_t i = threadIdx.x; i < nq; i += blockDim.x) hist[i] = 0;
@@ -437,8 +453,9 @@ __global__ void bucket_kernel(const uint64_t* __restrict__ rec, const int* __res
 // fallback for very large query batches (histograms beyond shared memory)
 __global__ void bucket_atomic_kernel(const uint64_t* __restrict__ rec, const int* __restrict__ rec_cnt,
                                      int64_t rec_cap, uint64_t* __restrict__ cand, int* __restrict__ cand_cnt,
-                                     int64_t cap) {
+                                     int64_t cap, int* __restrict__ ovf) {
   const int b = blockIdx.y;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && rec_cnt[b] > rec_cap) atomicOr(ovf, 1);
   const int cnt = (int)min((int64_t)rec_cnt[b], rec_cap);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
     const uint64_t r = rec[(int64_t)b * rec_cap + i];
@@ -450,83 +467,100 @@ __global__ void bucket_atomic_kernel(const uint64_t* __restrict__ rec, const int
 
 }  // namespace
 
-// Filtered Quick ADC scan on tcgen05.  Returns PQS_ERR_UNSUPPORTED when the
-// shape is outside this kernel (caller falls back to the PRMT scan).
-int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const uint8_t* d_theta, int64_t nq,
-                    uint64_t* cand, int* cand_cnt, int64_t cap, int* overflow) {
+// PQS_TC_DEBUG: per-tile role timestamps of CTA 0 (ns since its first tile)
+static int dump_debug(pqs_ctx* ctx, const unsigned long long* dbg) {
+  std::vector<unsigned long long> d(64 * 8 + 64);
+  PQS_CUDA(ctx, cudaMemcpy(d.data(), dbg, (64 * 8 + 64) * 8, cudaMemcpyDeviceToHost));
+  const unsigned long long t0 = d[0];
+  for (int it = 0; it < 24; ++it) {
+    fprintf(stderr, "tile %2d:", it);
+    for (int k = 0; k < 7; ++k) fprintf(stderr, " %8lld", d[it * 8 + k] ? (long long)(d[it * 8 + k] - t0) : -1ll);
+    fprintf(stderr, "\n");
+  }
+  return PQS_OK;
+}
+
+// Filtered Quick ADC scan on tcgen05 over every tile: tiles (of 128 codes)
+// below prefix_tiles are filtered with theta, the rest with theta_main.
+// Survivors are appended to the per-query candidate lists; a per-CTA record
+// overflow sets *d_ovf (the caller re-runs the scan on the PRMT engine).
+// No host synchronisation.  Returns PQS_ERR_UNSUPPORTED when the shape is
+// outside this kernel.
+int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const uint8_t* d_theta,
+                    const uint8_t* d_theta_main, int64_t prefix_tiles, int64_t nq, uint64_t* cand, int* cand_cnt,
+                    int64_t cap, int* d_ovf) {
   if (db->mp != 16) return PQS_ERR_UNSUPPORTED;
   const int64_t nqg = cdiv(nq, TC_N);
-  const int64_t ntiles = cdiv(db->n, TC_M);
-  const int64_t total = nqg * ntiles;
-  const int64_t nctas = std::min<int64_t>((int64_t)ctx->sm_count, total);
-  if (nctas <= 0) return PQS_OK;
-  // every CTA range must span <= 2 query groups (double-buffered B) and fit the
-  // 17-bit tile-iteration field of the staged survivor records
-  if (cdiv(total, nctas) + 1 >= ntiles || cdiv(total, nctas) >= (1 << 17)) return PQS_ERR_UNSUPPORTED;
+  const int64_t nctas_max = (int64_t)ctx->sm_count;
+  const int64_t nt128 = cdiv(db->n, TC_M);
+  if (nt128 == 0) return PQS_OK;
+  // every CTA range must span <= 2 query groups (single-buffered B, decode of
+  // the staged records) and fit the 17-bit tile-iteration field of a record:
+  // long ranges are scanned in chunks of tiles, one launch each
+  if (nqg >= nctas_max) return PQS_ERR_UNSUPPORTED;
+  int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(nt128, ((1 << 17) - 2) * nctas_max / nqg));
+  if (ctx->tc_chunk_tiles > 0) chunk = std::min<int64_t>(chunk, ctx->tc_chunk_tiles);
+  for (int64_t c0 = 0; c0 < nt128; c0 += chunk) {
+    const int64_t ntiles = std::min<int64_t>(chunk, nt128 - c0);
+    const int64_t total = nqg * ntiles;
+    // a CTA range no longer than a group's tile count spans <= 2 groups
+    if (nqg > 1 && cdiv(total, std::min<int64_t>(nctas_max, total)) >= ntiles) return PQS_ERR_UNSUPPORTED;
+  }
   uint8_t* bglob = nullptr;
   int* nthr = nullptr;
   uint64_t* rec = nullptr;
   int* rec_cnt = nullptr;
   PQS_TRY(scratch(ctx, S_TC_B, (size_t)(nqg * B_BYTES), &bglob));
-  PQS_TRY(scratch(ctx, S_TC_TH, (size_t)(nqg * TC_N / 2), &nthr));
+  PQS_TRY(scratch(ctx, S_TC_TH, (size_t)(nqg * TC_N), &nthr));
   // survivors per CTA: expect ~nq*cap_used/nctas; size generously
-  const int64_t rec_cap = std::max<int64_t>(1 << 16, cdiv(nq * std::min<int64_t>(cap, 8192), nctas) * 2);
-  PQS_TRY(scratch(ctx, S_TC_REC, (size_t)(nctas * rec_cap), &rec));
-  PQS_TRY(scratch(ctx, S_TC_RECCNT, (size_t)nctas, &rec_cnt));
-  build_b_kernel<<<(unsigned)cdiv(nqg * TC_N * 16, 256), 256, 0, ctx->stream>>>(d_qt, d_theta, nq, db->m, nqg, bglob,
-                                                                               nthr);
+  const int64_t rec_cap = std::max<int64_t>(1 << 16, cdiv(nq * std::min<int64_t>(cap, 8192), nctas_max) * 2);
+  PQS_TRY(scratch(ctx, S_TC_REC, (size_t)(nctas_max * rec_cap), &rec));
+  PQS_TRY(scratch(ctx, S_TC_RECCNT, (size_t)nctas_max, &rec_cnt));
+  build_b_kernel<<<(unsigned)cdiv(nqg * TC_N * 16, 256), 256, 0, ctx->stream>>>(d_qt, nq, db->m, nqg, bglob);
   PQS_LAUNCHED(ctx);
-  Scan4TcArgs a{};
-  a.words = db->words4;
-  a.n = db->n;
-  a.bglob = bglob;
-  a.nthr = nthr;
-  a.nq = nq;
-  a.nqg = nqg;
-  a.ntiles = ntiles;
-  a.rec = rec;
-  a.rec_cnt = rec_cnt;
-  a.rec_cap = rec_cap;
-  a.dbg = nullptr;
-  a.dbg_mode = getenv("PQS_TC_MODE") ? atoi(getenv("PQS_TC_MODE")) : 0;
-  if (getenv("PQS_TC_DEBUG")) {
-    PQS_TRY(scratch(ctx, S_MISC, 64 * 8 + 64, &a.dbg));
-    PQS_CUDA(ctx, cudaMemsetAsync(a.dbg, 0, (64 * 8 + 64) * 8, ctx->stream));
-  }
-  const size_t smem = (size_t)B_BYTES + 2 * (size_t)A_BYTES + 2 * TC_N * 2 + (size_t)ESTAGE * EPI_WARPS * 32 * 4;
+  build_bias_kernel<<<(unsigned)cdiv(nqg * TC_N, 256), 256, 0, ctx->stream>>>(
+      d_theta, d_theta_main ? d_theta_main : d_theta, nq, nqg * TC_N / 2, nthr);
+  PQS_LAUNCHED(ctx);
+  const size_t smem = (size_t)B_BYTES + 2 * (size_t)A_BYTES + 4 * TC_N * 2 + (size_t)ESTAGE * EPI_WARPS * 32 * 4;
   PQS_CUDA(ctx, cudaFuncSetAttribute(scan4tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  PQS_TRY(scan_timer_begin(ctx));
-  scan4tc_kernel<<<(unsigned)nctas, TC_THREADS, smem, ctx->stream>>>(a);
-  PQS_LAUNCHED(ctx);
-  PQS_TRY(scan_timer_end(ctx));
   const size_t bsmem = (size_t)nq * 2 * sizeof(int);
-  if (bsmem <= 200 * 1024) {
+  if (bsmem <= 200 * 1024)
     PQS_CUDA(ctx, cudaFuncSetAttribute(bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
-    bucket_kernel<<<(unsigned)nctas, 1024, bsmem, ctx->stream>>>(rec, rec_cnt, rec_cap, nq, cand, cand_cnt, cap);
-  } else {
-    dim3 bg(64, (unsigned)nctas);
-    bucket_atomic_kernel<<<bg, 256, 0, ctx->stream>>>(rec, rec_cnt, rec_cap, cand, cand_cnt, cap);
-  }
-  PQS_LAUNCHED(ctx);
-  // overflow of a CTA record list -> the caller re-runs every query exactly
-  std::vector<int> h(nctas);
-  PQS_CUDA(ctx, cudaMemcpyAsync(h.data(), rec_cnt, sizeof(int) * nctas, cudaMemcpyDeviceToHost, ctx->stream));
-  PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  *overflow = 0;
-  for (int v : h)
-    if (v > rec_cap) *overflow = 1;
-  if (a.dbg) {
-    std::vector<unsigned long long> d(64 * 8 + 64);
-    PQS_CUDA(ctx, cudaMemcpy(d.data(), a.dbg, (64 * 8 + 64) * 8, cudaMemcpyDeviceToHost));
-    for (int c = 0; c < 8; ++c)
-      fprintf(stderr, "chunk %d: ld %lld  cmp %lld  emit %lld\n", c, (long long)(d[512 + c * 4 + 1] - d[512 + c * 4]),
-              (long long)(d[512 + c * 4 + 2] - d[512 + c * 4 + 1]), (long long)(d[512 + c * 4 + 3] - d[512 + c * 4 + 2]));
-    const unsigned long long t0 = d[0];
-    for (int it = 0; it < 24; ++it) {
-      fprintf(stderr, "tile %2d:", it);
-      for (int k = 0; k < 7; ++k) fprintf(stderr, " %8lld", d[it * 8 + k] ? (long long)(d[it * 8 + k] - t0) : -1ll);
-      fprintf(stderr, "\n");
+  const int dbg_mode = getenv("PQS_TC_MODE") ? atoi(getenv("PQS_TC_MODE")) : 0;
+  for (int64_t c0 = 0; c0 < nt128; c0 += chunk) {
+    const int64_t ntiles = std::min<int64_t>(chunk, nt128 - c0);
+    const int64_t total = nqg * ntiles;
+    const int64_t nctas = std::min<int64_t>(nctas_max, total);
+    Scan4TcArgs a{};
+    a.words = db->words4;
+    a.n = db->n;
+    a.bglob = bglob;
+    a.nthr = nthr;
+    a.prefix_tiles = prefix_tiles;
+    a.nq = nq;
+    a.nqg = nqg;
+    a.ntiles = ntiles;
+    a.tile0 = c0;
+    a.rec = rec;
+    a.rec_cnt = rec_cnt;
+    a.rec_cap = rec_cap;
+    a.dbg = nullptr;
+    a.dbg_mode = dbg_mode;
+    if (getenv("PQS_TC_DEBUG")) {
+      PQS_TRY(scratch(ctx, S_MISC, 64 * 8 + 64, &a.dbg));
+      PQS_CUDA(ctx, cudaMemsetAsync(a.dbg, 0, (64 * 8 + 64) * 8, ctx->stream));
     }
+    scan4tc_kernel<<<(unsigned)nctas, TC_THREADS, smem, ctx->stream>>>(a);
+    PQS_LAUNCHED(ctx);
+    if (bsmem <= 200 * 1024) {
+      bucket_kernel<<<(unsigned)nctas, 1024, bsmem, ctx->stream>>>(rec, rec_cnt, rec_cap, nq, cand, cand_cnt, cap,
+                                                                    d_ovf);
+    } else {
+      dim3 bg(64, (unsigned)nctas);
+      bucket_atomic_kernel<<<bg, 256, 0, ctx->stream>>>(rec, rec_cnt, rec_cap, cand, cand_cnt, cap, d_ovf);
+    }
+    PQS_LAUNCHED(ctx);
+    if (a.dbg) PQS_TRY(dump_debug(ctx, a.dbg));
   }
   return PQS_OK;
 }

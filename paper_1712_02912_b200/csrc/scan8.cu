@@ -498,22 +498,6 @@ __global__ void dense_adc_kernel(const float* __restrict__ tables, const uint8_t
 }  // namespace
 
 // ---------------------------------------------------------------------------
-int build_db8(pqs_ctx* ctx, pqs_db* db, const uint8_t* h_codes) {
-  // host-side tile transpose into pinned staging, then one copy
-  const int64_t n = db->n, m = db->m;
-  const size_t bytes = (size_t)db->ntiles * m * TILE8;
-  std::vector<uint8_t> h(bytes, 0);
-  for (int64_t i = 0; i < n; ++i) {
-    const int64_t t = i / TILE8, c = i % TILE8;
-    uint8_t* dst = h.data() + t * m * TILE8 + c;
-    const uint8_t* src = h_codes + i * m;
-    for (int64_t j = 0; j < m; ++j) dst[j * TILE8] = src[j];
-  }
-  PQS_CUDA(ctx, cudaMemcpyAsync(db->codes8, h.data(), bytes, cudaMemcpyHostToDevice, ctx->stream));
-  PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  return PQS_OK;
-}
-
 int launch_scan_distances(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t nq, double* d_out) {
   if (db->n == 0 || nq == 0) return PQS_OK;
   dim3 grid((unsigned)cdiv(db->n, 256), (unsigned)nq);

@@ -107,7 +107,7 @@ __device__ void materialise(const SelArgs& a, int64_t q, int64_t M, uint64_t* K,
       const uint64_t e = cand[i];
       const int64_t idx = (int64_t)(uint32_t)e;
       uint64_t key;
-      if (a.src == SEL_CAND_BIN) key = e >> 32;
+      if (a.src == SEL_CAND_BIN) key = min(e >> 32, (uint64_t)127);  // bin = min(sum, 127)
       else key = dkey(adc_exact(T, a.codes8, a.m, a.k, idx));
       K[i] = key;
       I[i] = map_id(a, idx);

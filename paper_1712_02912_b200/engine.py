@@ -30,6 +30,14 @@ def _io_of(*arrays) -> int:
     return IO_HOST
 
 
+def _io(ctx, *arrays) -> int:
+    """io flag of a call; device calls are bound to torch's current stream."""
+    io = _io_of(*arrays)
+    if io == IO_DEVICE:
+        ctx.bind_torch_stream()
+    return io
+
+
 def _empty(shape, dtype, like):
     if _is_device(like):
         import torch
@@ -76,7 +84,27 @@ class DeviceQuantizer:
             raise ValueError(f"queries must have shape (nq, {self.d})")
         out = _empty((q.shape[0], self.m, self.k), np.float32, q)
         self.ctx.check(self.ctx.lib.pqs_compute_tables(self.ctx.handle, self.handle, ptr(q), q.shape[0], ptr(out),
-                                                       _io_of(q, out)), "compute_tables")
+                                                       _io(self.ctx, q, out)), "compute_tables")
+        return out
+
+    def encode(self, x, coarse=None, cells=None):
+        """encode (quantizer.py:308-325) of (n, d) fp32 vectors -> (n, m) uint8,
+        bit-identical; with coarse (K, d) and cells (n,) the IVF residuals
+        x - coarse[cells] are encoded (build_ivf, ivf.py:137-140)."""
+        x = _host_f32(x, 2, "vectors")
+        if x.shape[1] != self.d:
+            raise ValueError(f"vector dimensionality {x.shape[1]}, expected {self.d}")
+        K = 0
+        if coarse is not None:
+            coarse = _host_f32(coarse, 2, "coarse")
+            K = coarse.shape[0]
+            if _is_device(cells):
+                cells = cells.contiguous()
+            else:
+                cells = np.ascontiguousarray(cells, dtype=np.int64)
+        out = _empty((x.shape[0], self.m), np.uint8, x)
+        self.ctx.check(self.ctx.lib.pqs_encode(self.ctx.handle, self.handle, ptr(x), x.shape[0], ptr(coarse), K,
+                                               ptr(cells), ptr(out), _io(self.ctx, x, coarse, cells, out)), "encode")
         return out
 
     def __del__(self):
@@ -91,31 +119,48 @@ class DeviceCodes:
     """pqs_db: a device-resident code list (b=8 float ADC or b=4 Quick ADC)."""
 
     def __init__(self, codes, b: int, ids=None, id_base: int = 0, ctx=None):
+        """codes: (n, m) numpy array or contiguous CUDA uint8 tensor (built on the
+        device, e.g. by DeviceQuantizer.encode); ids likewise (int64) or None."""
         self.ctx = ctx or default_context()
-        codes = np.asarray(codes)
-        if codes.ndim != 2:
-            raise ValueError("codes must be 2-D (n, m)")
-        if codes.size and int(codes.max()) > 255:
-            raise NotImplementedError("device code lists hold components < 256")
-        codes = np.ascontiguousarray(codes, dtype=np.uint8)
-        self.n, self.m, self.b = codes.shape[0], codes.shape[1], b
-        ids_arr = None if ids is None else np.ascontiguousarray(ids, dtype=np.int64)
+        if _is_device(codes):
+            if str(codes.dtype) != "torch.uint8" or codes.dim() != 2 or not codes.is_contiguous():
+                raise ValueError("device codes must be a contiguous 2-D uint8 tensor")
+            if ids is not None and (not _is_device(ids) or str(ids.dtype) != "torch.int64" or not ids.is_contiguous()):
+                raise ValueError("ids of device codes must be a contiguous int64 CUDA tensor")
+            io = IO_DEVICE
+            ids_arr = ids
+            self.ctx.bind_torch_stream()
+        else:
+            codes = np.asarray(codes)
+            if codes.ndim != 2:
+                raise ValueError("codes must be 2-D (n, m)")
+            if codes.size and int(codes.max()) > 255:
+                raise NotImplementedError("device code lists hold components < 256")
+            codes = np.ascontiguousarray(codes, dtype=np.uint8)
+            ids_arr = None if ids is None else np.ascontiguousarray(ids, dtype=np.int64)
+            io = IO_HOST
+        self.n, self.m, self.b = int(codes.shape[0]), int(codes.shape[1]), b
         h = ctypes.c_void_p()
         self.ctx.check(self.ctx.lib.pqs_db_create(self.ctx.handle, ptr(codes), self.n, self.m, b, ptr(ids_arr),
-                                                  int(id_base), ctypes.byref(h)), "db_create")
+                                                  int(id_base), io, ctypes.byref(h)), "db_create")
         self.handle = h
 
     def set_prefix(self, prefix_codes):
         """Global Quick ADC prefix for a shard (quickadc.py:130-137)."""
-        p = np.ascontiguousarray(prefix_codes, dtype=np.uint8)
-        self.ctx.check(self.ctx.lib.pqs_db_set_prefix(self.ctx.handle, self.handle, ptr(p), p.shape[0]), "set_prefix")
+        if _is_device(prefix_codes):
+            p, io = prefix_codes.contiguous(), IO_DEVICE
+            self.ctx.bind_torch_stream()
+        else:
+            p, io = np.ascontiguousarray(prefix_codes, dtype=np.uint8), IO_HOST
+        self.ctx.check(self.ctx.lib.pqs_db_set_prefix(self.ctx.handle, self.handle, ptr(p), int(p.shape[0]), io),
+                       "set_prefix")
 
     # -- float ADC (b=8) --------------------------------------------------
     def scan_distances(self, tables):
         t = _host_f32(tables, 3, "tables")
         out = _empty((t.shape[0], self.n), np.float64, t)
         self.ctx.check(self.ctx.lib.pqs_scan_distances(self.ctx.handle, self.handle, ptr(t), t.shape[0], t.shape[2],
-                                                       ptr(out), _io_of(t, out)), "scan_distances")
+                                                       ptr(out), _io(self.ctx, t, out)), "scan_distances")
         return out
 
     def adc_scan(self, tables, r: int):
@@ -128,7 +173,7 @@ class DeviceCodes:
         i = _empty((nq, r), np.int64, t)
         c = _empty((nq,), np.int32, t)
         self.ctx.check(self.ctx.lib.pqs_adc_scan(self.ctx.handle, self.handle, ptr(t), nq, t.shape[2], int(r), ptr(d),
-                                                 ptr(i), ptr(c), _io_of(t, d)), "adc_scan")
+                                                 ptr(i), ptr(c), _io(self.ctx, t, d)), "adc_scan")
         return d, i, c
 
     def adc_search(self, dq: DeviceQuantizer, queries, r: int):
@@ -139,7 +184,7 @@ class DeviceCodes:
         i = _empty((nq, r), np.int64, q)
         c = _empty((nq,), np.int32, q)
         self.ctx.check(self.ctx.lib.pqs_adc_search(self.ctx.handle, self.handle, dq.handle, ptr(q), nq, int(r), ptr(d),
-                                                   ptr(i), ptr(c), _io_of(q, d)), "adc_search")
+                                                   ptr(i), ptr(c), _io(self.ctx, q, d)), "adc_search")
         return d, i, c
 
     # -- Quick ADC (b=4) ---------------------------------------------------
@@ -156,7 +201,7 @@ class DeviceCodes:
         qt = _empty((nq, self.m, 16), np.uint8, t)
         qmm = _empty((nq, 2), np.float64, t)
         self.ctx.check(self.ctx.lib.pqs_qadc_scan(self.ctx.handle, self.handle, ptr(t), nq, int(init_count), int(r),
-                                                  ptr(bins), ptr(i), ptr(c), ptr(qt), ptr(qmm), _io_of(t, bins)),
+                                                  ptr(bins), ptr(i), ptr(c), ptr(qt), ptr(qmm), _io(self.ctx, t, bins)),
                        "qadc_scan")
         return bins, i, c, qt, qmm
 
@@ -170,7 +215,7 @@ class DeviceCodes:
         qmm = _empty((nq, 2), np.float64, q) if want_tables else None
         self.ctx.check(self.ctx.lib.pqs_qadc_search(self.ctx.handle, self.handle, dq.handle, ptr(q), nq,
                                                     int(init_count), int(r), ptr(bins), ptr(i), ptr(c), ptr(qt),
-                                                    ptr(qmm), _io_of(q, bins)), "qadc_search")
+                                                    ptr(qmm), _io(self.ctx, q, bins)), "qadc_search")
         return bins, i, c, qt, qmm
 
     def quantized_distances(self, qtables):
@@ -179,7 +224,7 @@ class DeviceCodes:
             raise ValueError(f"codes must have shape (n, {qt.shape[1]})")
         out = _empty((qt.shape[0], self.n), np.uint8, qt)
         self.ctx.check(self.ctx.lib.pqs_quantized_distances(self.ctx.handle, self.handle, ptr(qt), qt.shape[0],
-                                                            ptr(out), _io_of(qt, out)), "quantized_distances")
+                                                            ptr(out), _io(self.ctx, qt, out)), "quantized_distances")
         return out
 
     def __del__(self):
@@ -194,8 +239,6 @@ class DeviceIvf:
     """pqs_ivf: device-resident IVFADC index (coarse + residual PQ + lists)."""
 
     def __init__(self, index, ctx=None):
-        self.ctx = ctx or default_context()
-        self.dq = DeviceQuantizer(index.pq, self.ctx)
         sizes = np.array([lst.n for lst in index.lists], dtype=np.int64)
         m = index.pq.m
         if sizes.sum():
@@ -205,11 +248,29 @@ class DeviceIvf:
         else:
             codes = np.zeros((0, m), np.uint8)
             ids = np.zeros(0, np.int64)
-        coarse = np.ascontiguousarray(index.coarse, dtype=np.float32)
-        self.K, self.d = coarse.shape
+        self._create(index.pq, np.ascontiguousarray(index.coarse, dtype=np.float32), sizes, codes, ids, ctx)
+
+    @classmethod
+    def from_arrays(cls, pq, coarse, list_sizes, codes, ids, ctx=None):
+        """Index from lists already concatenated in cell order: coarse (K, d)
+        fp32, list_sizes (K,) int64 (host), codes (n, m) uint8, ids (n,) int64
+        -- numpy arrays or CUDA tensors (e.g. an index built on the device)."""
+        self = cls.__new__(cls)
+        if not _is_device(coarse):
+            coarse = np.ascontiguousarray(coarse, dtype=np.float32)
+        self._create(pq, coarse, np.ascontiguousarray(list_sizes, dtype=np.int64), codes, ids, ctx)
+        return self
+
+    def _create(self, pq, coarse, sizes, codes, ids, ctx):
+        self.ctx = ctx or default_context()
+        self.dq = DeviceQuantizer(pq, self.ctx)
+        self.K, self.d = int(coarse.shape[0]), int(coarse.shape[1])
+        if sizes.shape != (self.K,):
+            raise ValueError("list_sizes must have one entry per coarse centroid")
         h = ctypes.c_void_p()
         self.ctx.check(self.ctx.lib.pqs_ivf_create(self.ctx.handle, self.dq.handle, ptr(coarse), self.K, ptr(sizes),
-                                                   ptr(codes), ptr(ids), ctypes.byref(h)), "ivf_create")
+                                                   ptr(codes), ptr(ids), _io(self.ctx, coarse, codes, ids),
+                                                   ctypes.byref(h)), "ivf_create")
         self.handle = h
 
     def probe(self, queries, ma: int):
@@ -218,7 +279,7 @@ class DeviceIvf:
         cells = _empty((nq, ma), np.int64, q)
         dist = _empty((nq, ma), np.float64, q)
         self.ctx.check(self.ctx.lib.pqs_ivf_probe(self.ctx.handle, self.handle, ptr(q), nq, int(ma), ptr(cells),
-                                                  ptr(dist), _io_of(q, cells)), "ivf_probe")
+                                                  ptr(dist), _io(self.ctx, q, cells)), "ivf_probe")
         return cells, dist
 
     def search(self, queries, ma: int, r: int):
@@ -230,7 +291,7 @@ class DeviceIvf:
         i = _empty((nq, r), np.int64, q)
         c = _empty((nq,), np.int32, q)
         self.ctx.check(self.ctx.lib.pqs_ivf_search(self.ctx.handle, self.handle, ptr(q), nq, int(ma), int(r), ptr(d),
-                                                   ptr(i), ptr(c), _io_of(q, d)), "ivf_search")
+                                                   ptr(i), ptr(c), _io(self.ctx, q, d)), "ivf_search")
         return d, i, c
 
     def __del__(self):
@@ -256,7 +317,7 @@ def merge_topr(dists, ids, counts, r: int, ctx=None):
     oi = _empty((nq, r), np.int64, dists)
     oc = _empty((nq,), np.int32, dists)
     ctx.check(ctx.lib.pqs_merge_topr(ctx.handle, G, ptr(dists), ptr(ids), ptr(counts), nq, r_in, int(r), ptr(od),
-                                     ptr(oi), ptr(oc), _io_of(dists, od)), "merge_topr")
+                                     ptr(oi), ptr(oc), _io(ctx, dists, od)), "merge_topr")
     return od, oi, oc
 
 

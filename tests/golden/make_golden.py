@@ -205,6 +205,34 @@ def g_ivf():
     save("ivf.npz", **out)
 
 
+def g_encode():
+    """encode (plain and IVF-residual) incl. exact centroid ties."""
+    rng = np.random.default_rng(606)
+    out = {}
+    for tag, (d, m, b, hi, sigma, nx) in {
+        "c1": (96, 16, 4, 1.0, 0.3, 600),
+        "c3": (128, 8, 8, 128.0, 16.0, 600),
+        "c2": (960, 64, 8, 1.0, 0.05, 150),
+    }.items():
+        x = mixture(rng, 1500 + nx, d, 12, hi, sigma, 0.0, 255.0)
+        pq = train_pq(x[:1500], m, b, TrainConfig(kmeans_iters=3, seed=3))
+        books = pq.codebooks.copy()
+        books[:, -1] = books[:, 0]           # duplicate centroid -> exact ties
+        pq = type(pq)(m=m, b=b, d=d, codebooks=books)
+        xs = x[1500:].copy()
+        xs[:50] = books[:, 0].reshape(-1)    # rows exactly on the tied centroid
+        out[f"{tag}_codebooks"] = books
+        out[f"{tag}_x"] = xs
+        out[f"{tag}_codes"] = encode(pq, xs)
+        coarse = x[rng.choice(1500, 40, replace=False)].astype(np.float32)
+        cells = rng.integers(0, 40, xs.shape[0]).astype(np.int64)
+        res = xs.astype(np.float64) - coarse[cells].astype(np.float64)
+        out[f"{tag}_coarse"] = coarse
+        out[f"{tag}_cells"] = cells
+        out[f"{tag}_rescodes"] = encode(pq, res)
+    save("encode.npz", **out)
+
+
 if __name__ == "__main__":
     print("pqscan from", pqscan.__file__)
     g_tables()
@@ -212,3 +240,4 @@ if __name__ == "__main__":
     g_quick_adc()
     g_quantize()
     g_ivf()
+    g_encode()

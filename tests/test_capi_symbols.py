@@ -40,7 +40,7 @@ def test_python_binding_covers_header():
 def test_api_version():
     from paper_1712_02912_b200 import _lib
 
-    assert _lib.load_library().pqs_api_version() == 1
+    assert _lib.load_library().pqs_api_version() == 2
 
 
 def test_no_device_fails_loudly():

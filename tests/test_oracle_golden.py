@@ -106,3 +106,13 @@ def test_ivf_query(golden, ma, r):
         np.testing.assert_array_equal(d, g[f"ma{ma}_r{r}_dist"][qi][:n])
         np.testing.assert_array_equal(i, g[f"ma{ma}_r{r}_ids"][qi][:n])
         assert np.all(g[f"ma{ma}_r{r}_ids"][qi][n:] == -1)
+
+
+@pytest.mark.parametrize("tag", ["c1", "c3", "c2"])
+def test_encode_golden(golden, tag):
+    g = golden("encode.npz")
+    books, x = g[f"{tag}_codebooks"], g[f"{tag}_x"]
+    np.testing.assert_array_equal(O.encode(books, x), g[f"{tag}_codes"])
+    np.testing.assert_array_equal(O.encode(books, x, g[f"{tag}_coarse"], g[f"{tag}_cells"]),
+                                  g[f"{tag}_rescodes"])
+    assert (g[f"{tag}_codes"][:50] == 0).all()  # tied duplicate centroid -> lowest index
