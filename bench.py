@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--cpu-sample-s", type=float, default=20.0, help="CPU work budget of the baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--engine", type=int, default=0, help="Quick ADC scan engine: 0 auto, 1 PRMT, 2 tcgen05")
+    ap.add_argument("--sample-div", type=int, default=0, help="threshold sample = 1/N of the tiles (0: library default)")
     return ap.parse_args()
 
 
@@ -503,6 +504,8 @@ def main():
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
     ctx.set_option(_lib.OPT_SCAN4_ENGINE, args.engine)
+    if args.sample_div:
+        ctx.set_option(_lib.OPT_SAMPLE_DIV, args.sample_div)
     pq = P.ProductQuantizer(cfg["m"], cfg["b"], cfg["d"], books)
     from paper_1712_02912_b200.sharded import ShardedSearch
 

@@ -156,18 +156,53 @@ __device__ unsigned long long kth_smallest(const unsigned long long* keys, int64
       if (match_above4(v, prefix, shift + 8)) atomicAdd(&sh.hist[(v >> shift) & 255u], 1u);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long c = 0, kk = sh.k;
-      int d = 0;
-      for (; d < 256; ++d) {
-        if (kk < c + sh.hist[d]) break;
-        c += sh.hist[d];
+    if (threadIdx.x < 32) {  // lane-parallel digit search: each lane owns 8 bins
+      const int lane = threadIdx.x;
+      unsigned int s8 = 0;
+#pragma unroll
+      for (int b = 0; b < 8; ++b) s8 += sh.hist[lane * 8 + b];
+      unsigned int incl = s8;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
       }
-      sh.k = kk - c;
-      sh.prefix = prefix | ((unsigned long long)d << shift);
+      const unsigned long long kk = sh.k;
+      const unsigned int excl = incl - s8;
+      if (kk >= excl && kk < incl) {
+        unsigned long long c = excl;
+        int d = lane * 8;
+        for (int b = 0; b < 8; ++b) {
+          const unsigned int h = sh.hist[lane * 8 + b];
+          if (kk < c + h) {
+            d = lane * 8 + b;
+            break;
+          }
+          c += h;
+        }
+        sh.k = kk - c;
+        sh.prefix = prefix | ((unsigned long long)d << shift);
+      }
     }
     __syncthreads();
   }
+  return sh.prefix;
+}
+
+// k-th smallest of M <= blockDim.x keys by rank counting (one key per thread,
+// broadcast reads): the key with #less <= k < #less + #equal
+__device__ unsigned long long kth_smallest_small(const unsigned long long* keys, int M, int k, ParamShared& sh) {
+  if (threadIdx.x < M) {
+    const unsigned long long v = keys[threadIdx.x];
+    int less = 0, eq = 0;
+    for (int i = 0; i < M; ++i) {
+      const unsigned long long w = keys[i];
+      less += w < v ? 1 : 0;
+      eq += w == v ? 1 : 0;
+    }
+    if (less <= k && k < less + eq) sh.prefix = v;  // every writer holds the same value
+  }
+  __syncthreads();
   return sh.prefix;
 }
 
@@ -206,10 +241,11 @@ __global__ void __launch_bounds__(SCAN4_THREADS) qadc_params_kernel(
   }
   __syncthreads();
   double qmax;
-  if (n_init >= r) {
-    qmax = dkey_inv(kth_smallest(keys, n_init, (unsigned long long)(r - 1), sh));
+  const int64_t kq = n_init >= r ? r - 1 : n_init - 1;
+  if (n_init <= SCAN4_THREADS) {
+    qmax = dkey_inv(kth_smallest_small(keys, (int)n_init, (int)kq, sh));
   } else {
-    qmax = dkey_inv(kth_smallest(keys, n_init, (unsigned long long)(n_init - 1), sh));
+    qmax = dkey_inv(kth_smallest(keys, n_init, (unsigned long long)kq, sh));
   }
   const double qmin = sh.qmin;
   qmax = qmax > qmin ? qmax : qmin;
@@ -302,18 +338,21 @@ __device__ __forceinline__ void flush_cands(const uint64_t* stage, int cnt, int6
     if (pos + i < cap) cand[q * cap + pos + i] = stage[i * SCAN4_THREADS];
 }
 
-// MODE_HIST: per-thread (= per-query) u16 bin counters in shared memory,
-// [bin][thread] so a warp's 32 increments touch 16 distinct words of 16
-// banks whatever the bins (conflict-free); flushed to the global (nq, 128)
-// histogram before a counter can wrap.
+// MODE_HIST: per-thread (= per-query) u16 counters in shared memory, one per
+// PAIR of bins (2k, 2k+1) -- 32 KB, two CTAs per SM -- laid out
+// [pair][thread] so a warp's 32 increments touch 16 distinct words of 16
+// banks whatever the bins (conflict-free).  Flushed to the global (nq, 128)
+// histogram at the pair's upper bin 2k+1 (the threshold derived from it is
+// then >= the exact one: certified) before a counter can wrap.
+constexpr int HIST_PAIRS = 64;
 constexpr int HIST_FLUSH_CODES = 60000;
 
 __device__ __forceinline__ void flush_hist(uint16_t* h, int64_t q, bool valid, unsigned int* ghist) {
 #pragma unroll 4
-  for (int b = 0; b < 128; ++b) {
+  for (int b = 0; b < HIST_PAIRS; ++b) {
     const unsigned int v = h[b * SCAN4_THREADS];
     if (v) {
-      if (valid) atomicAdd(ghist + q * 128 + b, v);
+      if (valid) atomicAdd(ghist + q * 128 + 2 * b + 1, v);
       h[b * SCAN4_THREADS] = 0;
     }
   }
@@ -332,7 +371,7 @@ __global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kerne
   int ncand = 0;
   int hcodes = 0;  // codes counted since the last histogram flush
   if (MODE == MODE_HIST) {
-    for (int b = 0; b < 128; ++b) hist[b * SCAN4_THREADS] = 0;
+    for (int b = 0; b < HIST_PAIRS; ++b) hist[b * SCAN4_THREADS] = 0;
   }
 
   // persistent CTAs grab tiles of the linearised (query group, tile) list from
@@ -437,10 +476,11 @@ __global__ void __launch_bounds__(SCAN4_THREADS, (MP <= 16 ? 2 : 1)) scan4_kerne
         }
       } else if (MODE == MODE_HIST) {
         const uint32_t S[4] = {ae & 0xFFFFu, ao & 0xFFFFu, ae >> 16, ao >> 16};
+        const int nv = (int)min((int64_t)4, a.n - c);  // valid codes of this quad
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const uint32_t b = S[e] < 127u ? S[e] : 127u;
-          if (c + e < a.n) hist[b * SCAN4_THREADS] += 1;
+          const uint32_t b = (S[e] < 127u ? S[e] : 127u) >> 1;
+          if (e < nv) hist[b * SCAN4_THREADS] += 1;
         }
       } else {
         if (qvalid) {
@@ -478,7 +518,7 @@ int launch_scan4_t(pqs_ctx* ctx, Scan4Args a, int64_t nq) {
   constexpr int HP = MP / 2;
   const size_t smem = 2 * (size_t)QUADS4 * HP * sizeof(uint4) +
                       (MODE == MODE_FILTER ? (size_t)CSTAGE * SCAN4_THREADS * sizeof(uint64_t) : 0) +
-                      (MODE == MODE_HIST ? (size_t)128 * SCAN4_THREADS * sizeof(uint16_t) : 0);
+                      (MODE == MODE_HIST ? (size_t)HIST_PAIRS * SCAN4_THREADS * sizeof(uint16_t) : 0);
   PQS_CUDA(ctx, cudaFuncSetAttribute(scan4_kernel<MP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
   const int threads = SCAN4_THREADS;  // the tile loader assumes a full CTA
@@ -511,14 +551,9 @@ int launch_scan4(pqs_ctx* ctx, int mp, const Scan4Args& a, int64_t nq) {
   return set_err(ctx, PQS_ERR_UNSUPPORTED, "scan4: unsupported padded m");
 }
 
-// theta[q] = the r-th smallest bin of the sample (the first st tiles, the
-// "prefix"); theta_main[q] is the threshold for the codes after the prefix:
-// with ids increasing in storage order, a code outside the prefix has a larger
-// id than every prefix code, so it can only enter the top-r with a bin
-// strictly below theta (the prefix alone holds r codes with bin <= theta) --
-// theta - 1, or THETA_NONE when theta == 0.  With explicit ids: theta.
-__global__ void theta4_final_kernel(const unsigned int* __restrict__ ghist, int64_t nq, int r, int strict,
-                                    uint8_t* __restrict__ theta, uint8_t* __restrict__ theta_main) {
+// theta[q] = the r-th smallest bin of the histogram pass (127 if fewer than r)
+__global__ void theta4_final_kernel(const unsigned int* __restrict__ ghist, int64_t nq, int r,
+                                    uint8_t* __restrict__ theta) {
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= nq) return;
   unsigned long long c = 0;
@@ -531,7 +566,41 @@ __global__ void theta4_final_kernel(const unsigned int* __restrict__ ghist, int6
     }
   }
   theta[q] = (uint8_t)t;
-  if (theta_main) theta_main[q] = strict ? (t == 0 ? THETA_NONE : (uint8_t)(t - 1)) : (uint8_t)t;
+}
+
+// after the prefix pass: theta_main from the prefix candidates (every prefix
+// code with bin <= t0, and t0 >= the prefix's r-th smallest bin t): the r-th
+// smallest candidate bin is t exactly.  An overflowed list (count > cap, the
+// query takes the exact fallback) gets THETA_NONE.
+__global__ void cand_theta_kernel(const uint64_t* __restrict__ cand, const int* __restrict__ cand_cnt, int64_t cap,
+                                  int r, int strict, uint8_t* __restrict__ theta_main) {
+  __shared__ unsigned int hist[128];
+  const int64_t q = blockIdx.x;
+  const int cnt = cand_cnt[q];
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  if (cnt > cap) {
+    if (threadIdx.x == 0) theta_main[q] = THETA_NONE;
+    return;
+  }
+  const uint64_t* c = cand + q * cap;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const uint64_t b = c[i] >> 32;
+    atomicAdd(&hist[b < 127 ? b : 127], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int acc = 0;
+    int t = 127;
+    for (int b = 0; b < 128; ++b) {
+      acc += hist[b];
+      if (acc >= (unsigned)r) {
+        t = b;
+        break;
+      }
+    }
+    theta_main[q] = strict ? (t == 0 ? THETA_NONE : (uint8_t)(t - 1)) : (uint8_t)t;
+  }
 }
 
 __global__ void fill_u8_kernel(uint8_t* p, int64_t n, uint8_t v) {
@@ -549,9 +618,9 @@ __global__ void gather_rows_u8_kernel(const uint8_t* __restrict__ src, const int
 
 }  // namespace
 
-int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const uint8_t* d_theta,
-                    const uint8_t* d_theta_main, int64_t prefix_tiles, int64_t nq, uint64_t* cand, int* cand_cnt,
-                    int64_t cap, int* d_ovf);
+int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const uint8_t* d_theta, int64_t nq,
+                    int64_t tile_begin, int64_t tile_end, bool build_b, uint64_t* cand, int* cand_cnt, int64_t cap,
+                    int* d_ovf);
 
 // ---------------------------------------------------------------------------
 int build_db4(pqs_ctx* ctx, pqs_db* db, const uint8_t* d_codes) {
@@ -603,10 +672,13 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
   PQS_LAUNCHED(ctx);
 
   // ---- threshold: exact when every code fits the candidate buffer.
-  // Otherwise a certified threshold from a sample -- the first st tiles (the
-  // "prefix"): theta = the r-th smallest prefix bin, so the prefix alone holds
-  // >= r codes with bin <= theta and every top-r code has bin <= theta.  The
-  // prefix is filtered with theta, the rest with theta_main (theta4_final_kernel).
+  // Otherwise certified thresholds from the first st tiles (the "prefix"):
+  //   1. t0 = the r-th smallest bin of the first s0 tiles (histogram pass);
+  //   2. the prefix is filtered with t0 (>= the prefix's r-th smallest bin t);
+  //   3. t = the r-th smallest prefix candidate bin (cand_theta_kernel): every
+  //      top-r code has bin <= t, and -- ids increasing in storage order -- a
+  //      code after the prefix needs bin < t (the prefix holds r codes with
+  //      bin <= t and smaller ids), so the rest is filtered with t - 1.
   uint8_t* theta = nullptr;
   uint8_t* theta_main = nullptr;
   PQS_TRY(scratch(ctx, S_THETA, (size_t)(2 * nq), &theta));
@@ -618,8 +690,13 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
     fill_u8_kernel<<<(unsigned)cdiv(nq, 256), 256, 0, ctx->stream>>>(theta, nq, 127);
     PQS_LAUNCHED(ctx);
   } else {
-    st = std::max<int64_t>(cdiv(db->ntiles, ctx->sample_div), cdiv(16 * r_eff, TILE4));
-    st = std::min<int64_t>(st, db->ntiles);
+    const int64_t tmin = cdiv(16 * r_eff, TILE4);
+    // prefix: 1/sample_div of the list, but at least min(1/4 of it, 256 tiles)
+    // -- small lists get a larger prefix (fewer candidates after it)
+    st = std::max<int64_t>(cdiv(db->ntiles, ctx->sample_div),
+                           std::min<int64_t>(cdiv(db->ntiles, 4), 256));
+    st = std::min<int64_t>(std::max<int64_t>(st, tmin), db->ntiles);
+    const int64_t s0 = std::min<int64_t>(std::max<int64_t>(cdiv(st, 8), tmin), st);
     unsigned int* ghist = nullptr;
     PQS_TRY(scratch(ctx, S_IVF_WORK3, (size_t)(nq * 128), &ghist));
     PQS_CUDA(ctx, cudaMemsetAsync(ghist, 0, sizeof(unsigned int) * nq * 128, ctx->stream));
@@ -630,78 +707,74 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
     a.m = m;
     a.qt = d_qt;
     a.nq = nq;
-    a.nvt = st;
+    a.nvt = s0;
     a.tile_off = 0;
     a.tile_step = 1;
     a.ghist = ghist;
     PQS_TRY(launch_scan4<MODE_HIST>(ctx, db->mp, a, nq));
-    theta4_final_kernel<<<(unsigned)cdiv(nq, 128), 128, 0, ctx->stream>>>(ghist, nq, (int)r_eff,
-                                                                           db->ids == nullptr ? 1 : 0, theta,
-                                                                           theta_main);
+    theta4_final_kernel<<<(unsigned)cdiv(nq, 128), 128, 0, ctx->stream>>>(ghist, nq, (int)r_eff, theta);
     PQS_LAUNCHED(ctx);
   }
 
-  // ---- K4 filtered scan: prefix tiles [0, st) with theta, the rest with theta_main
+  // ---- K4 filtered scan
   uint64_t* cand = nullptr;
   int* cnt = nullptr;
   PQS_TRY(scratch(ctx, S_CAND, (size_t)(nq * cap), &cand));
   PQS_TRY(scratch(ctx, S_CAND_CNT, (size_t)nq, &cnt));
   PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nq, ctx->stream));
-  {
-    const int64_t t1 = st > 0 ? st : db->ntiles;  // end of the first range
-    PQS_TRY(scan_timer_begin(ctx));
-    bool done = false;
-    if (st > 0 && ctx->scan4_engine != 1) {
-      // tcgen05 engine (128-code tiles); a record overflow -> redo with PRMT
-      int* d_ovf = nullptr;
-      PQS_TRY(scratch(ctx, S_TC_OVF, 1, &d_ovf));
-      PQS_CUDA(ctx, cudaMemsetAsync(d_ovf, 0, sizeof(int), ctx->stream));
-      const int64_t nt128 = cdiv(n, 128);
-      int rc = launch_scan4_tc(ctx, db, d_qt, theta, theta_main, t1 * (TILE4 / 128), nq, cand, cnt, cap, d_ovf);
-      int ovf = 0;
-      if (rc == PQS_OK) PQS_TRY(download(ctx, &ovf, d_ovf, sizeof(int)));
-      if (rc == PQS_OK && !ovf) {
-        done = true;
-        ctx->last_scan_engine = 2;
-        ctx->last_scan_work = 2.0 * (double)cdiv(nq, 256) * 256.0 * (double)nt128 * 128.0 * 256.0;
-      } else if (rc == PQS_OK || rc == PQS_ERR_UNSUPPORTED) {
-        if (ctx->scan4_engine == 2 && rc == PQS_ERR_UNSUPPORTED)
-          return set_err(ctx, PQS_ERR_UNSUPPORTED, "tcgen05 Quick ADC scan: unsupported shape (needs m <= 16)");
-        PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nq, ctx->stream));  // redo with PRMT
-      } else {
-        return rc;
-      }
+  const int64_t t1 = st > 0 ? st : db->ntiles;  // end of the first range
+  const bool second = st > 0 && st < db->ntiles;
+  const int strict = db->ids == nullptr ? 1 : 0;
+  auto main_theta = [&]() -> int {
+    cand_theta_kernel<<<(unsigned)nq, 128, 0, ctx->stream>>>(cand, cnt, cap, (int)r_eff, strict, theta_main);
+    PQS_LAUNCHED(ctx);
+    return PQS_OK;
+  };
+  int* d_ovf = nullptr;
+  PQS_TRY(scratch(ctx, S_TC_OVF, 1, &d_ovf));
+  // tcgen05 engine (128-code tiles) when sampled; returns UNSUPPORTED for shapes outside it
+  auto scan_tc = [&]() -> int {
+    PQS_CUDA(ctx, cudaMemsetAsync(d_ovf, 0, sizeof(int), ctx->stream));
+    const int64_t nt128 = cdiv(n, 128);
+    const int64_t p128 = std::min<int64_t>(t1 * (TILE4 / 128), nt128);
+    int rc = launch_scan4_tc(ctx, db, d_qt, theta, nq, 0, p128, true, cand, cnt, cap, d_ovf);
+    if (rc == PQS_OK && second) {
+      PQS_TRY(main_theta());
+      rc = launch_scan4_tc(ctx, db, d_qt, theta_main, nq, p128, nt128, false, cand, cnt, cap, d_ovf);
     }
-    if (!done) {
-      Scan4Args a{};
-      a.words = db->words4;
-      a.n = n;
-      a.m = m;
-      a.qt = d_qt;
-      a.nq = nq;
-      a.tile_step = 1;
-      a.cand = cand;
-      a.cand_cnt = cnt;
-      a.cap = cap;
-      a.nvt = t1;
-      a.tile_off = 0;
-      a.theta = theta;
+    if (rc == PQS_OK) {
+      ctx->last_scan_engine = 2;
+      ctx->last_scan_work = 2.0 * (double)cdiv(nq, 256) * 256.0 * (double)nt128 * 128.0 * 256.0;
+    }
+    return rc;
+  };
+  auto scan_prmt = [&]() -> int {
+    Scan4Args a{};
+    a.words = db->words4;
+    a.n = n;
+    a.m = m;
+    a.qt = d_qt;
+    a.nq = nq;
+    a.tile_step = 1;
+    a.cand = cand;
+    a.cand_cnt = cnt;
+    a.cap = cap;
+    a.nvt = t1;
+    a.tile_off = 0;
+    a.theta = theta;
+    PQS_TRY(launch_scan4<MODE_FILTER>(ctx, db->mp, a, nq));
+    if (second) {
+      PQS_TRY(main_theta());
+      a.nvt = db->ntiles - t1;
+      a.tile_off = t1;
+      a.theta = theta_main;
       PQS_TRY(launch_scan4<MODE_FILTER>(ctx, db->mp, a, nq));
-      if (t1 < db->ntiles) {
-        a.nvt = db->ntiles - t1;
-        a.tile_off = t1;
-        a.theta = theta_main;
-        PQS_TRY(launch_scan4<MODE_FILTER>(ctx, db->mp, a, nq));
-      }
-      ctx->last_scan_engine = 1;
-      ctx->last_scan_work = (double)nq * (double)n * (double)m;
     }
-    PQS_TRY(scan_timer_end(ctx));
-    ctx->last_scan_launches = 1;
-  }
-  ctx->last_evals = nq * n;
-
-  // ---- K5 select
+    ctx->last_scan_engine = 1;
+    ctx->last_scan_work = (double)nq * (double)n * (double)m;
+    return PQS_OK;
+  };
+  // ---- K5 select (bins, ties by id)
   uint64_t* gk = nullptr;
   int64_t* gi = nullptr;
   PQS_TRY(scratch(ctx, S_KEYS, (size_t)(nq * cap), &gk));
@@ -721,12 +794,42 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
   s.gkeys = gk;
   s.gids = gi;
   s.gcap = cap;
+  std::vector<int> hcnt(nq);
+  bool used_tc = false;
+  PQS_TRY(scan_timer_begin(ctx));
+  if (st > 0 && ctx->scan4_engine != 1) {
+    const int rc = scan_tc();
+    if (rc == PQS_OK) {
+      used_tc = true;
+    } else if (rc == PQS_ERR_UNSUPPORTED) {
+      if (ctx->scan4_engine == 2)
+        return set_err(ctx, PQS_ERR_UNSUPPORTED, "tcgen05 Quick ADC scan: unsupported shape (needs m <= 16)");
+      PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nq, ctx->stream));
+    } else {
+      return rc;
+    }
+  }
+  if (!used_tc) PQS_TRY(scan_prmt());
+  PQS_TRY(scan_timer_end(ctx));
+  ctx->last_scan_launches = second ? 2 : 1;
   PQS_TRY(launch_select(ctx, s));
+  // one synchronisation: candidate counts (+ the tcgen05 record-overflow flag)
+  int ovf = 0;
+  PQS_CUDA(ctx, cudaMemcpyAsync(hcnt.data(), cnt, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
+  if (used_tc) PQS_CUDA(ctx, cudaMemcpyAsync(&ovf, d_ovf, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (ovf) {  // a CTA record list overflowed: redo the scan on the PRMT engine
+    PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nq, ctx->stream));
+    PQS_TRY(scan_timer_begin(ctx));
+    PQS_TRY(scan_prmt());
+    PQS_TRY(scan_timer_end(ctx));
+    PQS_TRY(launch_select(ctx, s));
+    PQS_CUDA(ctx, cudaMemcpyAsync(hcnt.data(), cnt, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
+    PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  ctx->last_evals = nq * n;
 
   // ---- overflow check -> exact dense fallback for those queries
-  std::vector<int> hcnt(nq);
-  PQS_CUDA(ctx, cudaMemcpyAsync(hcnt.data(), cnt, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
-  PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   PQS_TRY(scan_timer_collect(ctx));
   std::vector<int> over;
   int64_t mx = 0, ctot = 0;

@@ -82,7 +82,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
         : "memory");
     if (ok) return;
     __nanosleep(ns);
-    ns = ns < 256 ? ns * 2 : 256;
+    ns = ns < 64 ? ns * 2 : 64;
   }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -143,9 +143,7 @@ struct Scan4TcArgs {
   const uint32_t* words;   // 4-bit quad layout (mp = 16: 8 words per quad)
   int64_t n;
   const uint8_t* bglob;    // [nqg][B_BYTES] canonical B tiles
-  const int* nthr;         // [nqg][2][128] packed per-column-pair biases (build_bias_kernel):
-                           // set 0 for tiles < prefix_tiles, set 1 after
-  int64_t prefix_tiles;    // global tile index where the second threshold set starts
+  const int* nthr;         // [nqg][128] packed per-column-pair biases (build_bias_kernel)
   int64_t nq, nqg, ntiles; // ntiles of TC_M codes in this launch's range
   int64_t tile0;           // first tile of the range
   uint64_t* rec;           // [gridDim][rec_cap] (q << 40 | bin << 32 | idx)
@@ -165,8 +163,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smtc[];
   uint8_t* sB = smtc;                           // 64 KB (one query group)
   uint8_t* sA = smtc + B_BYTES;                 // 2 x 32 KB
-  uint32_t* sTh = reinterpret_cast<uint32_t*>(smtc + B_BYTES + 2 * A_BYTES);  // [2 buffers][2 sets][128] biases
-  uint32_t* stage = reinterpret_cast<uint32_t*>(smtc + B_BYTES + 2 * A_BYTES + 4 * TC_N * 2);
+  uint32_t* sTh = reinterpret_cast<uint32_t*>(smtc + B_BYTES + 2 * A_BYTES);  // [2 buffers][128] biases
+  uint32_t* stage = reinterpret_cast<uint32_t*>(smtc + B_BYTES + 2 * A_BYTES + 2 * TC_N * 2);
   __shared__ __align__(8) uint64_t bar_b[2], bar_afull[2], bar_aempty[2], bar_accfull[2], bar_accempty[2];
   __shared__ uint32_t s_tmem;
   __shared__ int s_cnt;
@@ -219,18 +217,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
               // (its last commit to bar_aempty) before the new B overwrites it
               mbar_wait(&bar_aempty[(it - 1) & 1], (uint32_t)(((it - 1) >> 1) & 1));
             }
-            mbar_expect_tx(&bar_b[bb], (uint32_t)(B_BYTES + TC_N * 4));
+            mbar_expect_tx(&bar_b[bb], (uint32_t)(B_BYTES + TC_N * 2));
             bulk_g2s(sB, a.bglob + g * (int64_t)B_BYTES, B_BYTES, &bar_b[bb]);
-            bulk_g2s(sTh + bb * TC_N, a.nthr + g * TC_N, TC_N * 4, &bar_b[bb]);
+            bulk_g2s(sTh + bb * (TC_N / 2), a.nthr + g * (TC_N / 2), TC_N * 2, &bar_b[bb]);
             mbar_wait(&bar_b[bb], 0);
             cur_g = g;
           }
           const int ab = (int)(it & 1);
           const uint32_t ph = (uint32_t)((it >> 1) & 1);
           if (a.dbg && blockIdx.x == 0 && it < 64) a.dbg[it * 8 + 0] = gtime();
-          mbar_wait_sleep(&bar_afull[ab], ph);          // one-hot tile written
+          mbar_wait(&bar_afull[ab], ph);          // one-hot tile written (spin: critical path)
           if (a.dbg && blockIdx.x == 0 && it < 64) a.dbg[it * 8 + 1] = gtime();
-          mbar_wait_sleep(&bar_accempty[ab], ph ^ 1);   // accumulator drained (first use passes)
+          mbar_wait(&bar_accempty[ab], ph ^ 1);   // accumulator drained (first use passes)
           if (a.dbg && blockIdx.x == 0 && it < 64) a.dbg[it * 8 + 2] = gtime();
           tc_fence_after();
           const uint32_t d_tmem = tmem + (uint32_t)(ab * TC_N);
@@ -294,6 +292,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
       // survivors are staged per thread as 32-bit records (tile-iteration << 15 |
       // column << 7 | bin) with predicated stores -- no divergent branches per value
       uint32_t* my_stage = stage + threadIdx.x;  // [slot][EPI thread]
+      uint32_t* my_x = stage + ESTAGE * EPI_WARPS * 32 + threadIdx.x;  // [16][EPI thread] word stash
       const int quad = warp & 3, half = warp >> 2;  // TMEM lane quadrant, query-column half
       const int row = quad * 32 + lane;
       int ncand = 0;
@@ -328,7 +327,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
         tc_fence_after();
         const int64_t tile = a.tile0 + tile_of(w);
         const bool cvalid = tile * TC_M + row < a.n;
-        const uint32_t* bias = sTh + (gi & 1) * TC_N + (tile >= a.prefix_tiles ? TC_N / 2 : 0);
+        const uint32_t* bias = sTh + (gi & 1) * (TC_N / 2);
         const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * TC_N);
         const uint32_t itag = (uint32_t)it << 15;
 #pragma unroll 1
@@ -354,15 +353,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
             allm &= x[i];
           }
           if ((allm & 0x80008000u) != 0x80008000u && cvalid) {  // lane-local, rare
-            const uint32_t base = itag | ((uint32_t)c0 << 7);
+            // hit mask: bit i <- column 2i, bit 16+i <- column 2i+1 (flag = bit 15 clear);
+            // the packed words go to a per-thread stash for the dynamic reads below
+            uint32_t mask = 0;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const bool hit = ((x[i] >> (16 * h + 15)) & 1u) == 0u;
-                if (hit) my_stage[ncand * (EPI_WARPS * 32)] = base + ((uint32_t)(2 * i + h) << 7) + min(v[2 * i + h], 127u);
-                ncand += hit ? 1 : 0;
-              }
+              mask |= (~x[i] >> (15 - i)) & (0x00010001u << i);
+              my_x[i * (EPI_WARPS * 32)] = x[i];
+            }
+            const uint32_t base = itag | ((uint32_t)c0 << 7);
+            while (mask) {
+              const int b = __ffs(mask) - 1;
+              mask &= mask - 1;
+              const int i = b & 15, h = b >> 4;
+              const uint32_t pk = my_x[i * (EPI_WARPS * 32)] - bias[c0 / 2 + i];  // packed sums (no lane carry)
+              const uint32_t S = (pk >> (16 * h)) & 0xFFFFu;
+              my_stage[ncand * (EPI_WARPS * 32)] = base + ((uint32_t)(2 * i + h) << 7) + min(S, 127u);
+              ++ncand;
             }
           }
           if (ncand > ESTAGE - 32) flush();  // rare
@@ -402,20 +409,16 @@ __global__ void build_b_kernel(const uint8_t* __restrict__ qt, int64_t nq, int m
 // packed 16-bit lane biases of the column pair (2i, 2i+1): S + (0x7FFF - theta)
 // has bit 15 clear iff S <= theta; padding queries and THETA_NONE (255) get
 // 0x8000 (never clear)
-// nthr layout [group][set][128 pairs]: set 0 from theta, set 1 from theta2
-__global__ void build_bias_kernel(const uint8_t* __restrict__ theta, const uint8_t* __restrict__ theta2, int64_t nq,
-                                  int64_t npairs, int* __restrict__ nthr) {
-  const int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // (pair, set)
-  if (gi >= 2 * npairs) return;
-  const int set = (int)(gi & 1);
-  const int64_t i = gi >> 1;
-  if (set) theta = theta2;
+__global__ void build_bias_kernel(const uint8_t* __restrict__ theta, int64_t nq, int64_t npairs,
+                                  int* __restrict__ nthr) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= npairs) return;
   const int64_t q0 = 2 * i, q1 = q0 + 1;
   const uint32_t t0 = q0 < nq ? theta[q0] : 255u, t1 = q1 < nq ? theta[q1] : 255u;
   // 127 admits every sum (bin = min(S, 127)): bias 0 keeps bit 15 clear
   const uint32_t b0 = t0 == 255u ? 0x8000u : (t0 == 127u ? 0u : 0x7FFFu - t0);
   const uint32_t b1 = t1 == 255u ? 0x8000u : (t1 == 127u ? 0u : 0x7FFFu - t1);
-  nthr[(i / (TC_N / 2)) * TC_N + set * (TC_N / 2) + i % (TC_N / 2)] = (int)(b0 | (b1 << 16));
+  nthr[i] = (int)(b0 | (b1 << 16));
 }
 
 // per-CTA survivor records -> per-query candidate lists (bin << 32 | idx).
@@ -480,28 +483,27 @@ static int dump_debug(pqs_ctx* ctx, const unsigned long long* dbg) {
   return PQS_OK;
 }
 
-// Filtered Quick ADC scan on tcgen05 over every tile: tiles (of 128 codes)
-// below prefix_tiles are filtered with theta, the rest with theta_main.
-// Survivors are appended to the per-query candidate lists; a per-CTA record
-// overflow sets *d_ovf (the caller re-runs the scan on the PRMT engine).
-// No host synchronisation.  Returns PQS_ERR_UNSUPPORTED when the shape is
-// outside this kernel.
-int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const uint8_t* d_theta,
-                    const uint8_t* d_theta_main, int64_t prefix_tiles, int64_t nq, uint64_t* cand, int* cand_cnt,
-                    int64_t cap, int* d_ovf) {
+// Filtered Quick ADC scan on tcgen05 over the 128-code tiles [tile_begin,
+// tile_end) with per-query thresholds theta (build_b: also (re)build the B
+// tiles of the quantized tables).  Survivors are appended to the per-query
+// candidate lists; a per-CTA record overflow sets *d_ovf (the caller re-runs
+// the scan on the PRMT engine).  No host synchronisation.  Returns
+// PQS_ERR_UNSUPPORTED when the shape is outside this kernel.
+int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const uint8_t* d_theta, int64_t nq,
+                    int64_t tile_begin, int64_t tile_end, bool build_b, uint64_t* cand, int* cand_cnt, int64_t cap,
+                    int* d_ovf) {
   if (db->mp != 16) return PQS_ERR_UNSUPPORTED;
   const int64_t nqg = cdiv(nq, TC_N);
   const int64_t nctas_max = (int64_t)ctx->sm_count;
-  const int64_t nt128 = cdiv(db->n, TC_M);
-  if (nt128 == 0) return PQS_OK;
+  if (tile_end <= tile_begin) return PQS_OK;
   // every CTA range must span <= 2 query groups (single-buffered B, decode of
   // the staged records) and fit the 17-bit tile-iteration field of a record:
   // long ranges are scanned in chunks of tiles, one launch each
   if (nqg >= nctas_max) return PQS_ERR_UNSUPPORTED;
-  int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(nt128, ((1 << 17) - 2) * nctas_max / nqg));
+  int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(tile_end - tile_begin, ((1 << 17) - 2) * nctas_max / nqg));
   if (ctx->tc_chunk_tiles > 0) chunk = std::min<int64_t>(chunk, ctx->tc_chunk_tiles);
-  for (int64_t c0 = 0; c0 < nt128; c0 += chunk) {
-    const int64_t ntiles = std::min<int64_t>(chunk, nt128 - c0);
+  for (int64_t c0 = tile_begin; c0 < tile_end; c0 += chunk) {
+    const int64_t ntiles = std::min<int64_t>(chunk, tile_end - c0);
     const int64_t total = nqg * ntiles;
     // a CTA range no longer than a group's tile count spans <= 2 groups
     if (nqg > 1 && cdiv(total, std::min<int64_t>(nctas_max, total)) >= ntiles) return PQS_ERR_UNSUPPORTED;
@@ -511,24 +513,26 @@ int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const u
   uint64_t* rec = nullptr;
   int* rec_cnt = nullptr;
   PQS_TRY(scratch(ctx, S_TC_B, (size_t)(nqg * B_BYTES), &bglob));
-  PQS_TRY(scratch(ctx, S_TC_TH, (size_t)(nqg * TC_N), &nthr));
+  PQS_TRY(scratch(ctx, S_TC_TH, (size_t)(nqg * TC_N / 2), &nthr));
   // survivors per CTA: expect ~nq*cap_used/nctas; size generously
   const int64_t rec_cap = std::max<int64_t>(1 << 16, cdiv(nq * std::min<int64_t>(cap, 8192), nctas_max) * 2);
   PQS_TRY(scratch(ctx, S_TC_REC, (size_t)(nctas_max * rec_cap), &rec));
   PQS_TRY(scratch(ctx, S_TC_RECCNT, (size_t)nctas_max, &rec_cnt));
-  build_b_kernel<<<(unsigned)cdiv(nqg * TC_N * 16, 256), 256, 0, ctx->stream>>>(d_qt, nq, db->m, nqg, bglob);
+  if (build_b) {
+    build_b_kernel<<<(unsigned)cdiv(nqg * TC_N * 16, 256), 256, 0, ctx->stream>>>(d_qt, nq, db->m, nqg, bglob);
+    PQS_LAUNCHED(ctx);
+  }
+  build_bias_kernel<<<(unsigned)cdiv(nqg * TC_N / 2, 256), 256, 0, ctx->stream>>>(d_theta, nq, nqg * TC_N / 2, nthr);
   PQS_LAUNCHED(ctx);
-  build_bias_kernel<<<(unsigned)cdiv(nqg * TC_N, 256), 256, 0, ctx->stream>>>(
-      d_theta, d_theta_main ? d_theta_main : d_theta, nq, nqg * TC_N / 2, nthr);
-  PQS_LAUNCHED(ctx);
-  const size_t smem = (size_t)B_BYTES + 2 * (size_t)A_BYTES + 4 * TC_N * 2 + (size_t)ESTAGE * EPI_WARPS * 32 * 4;
+  const size_t smem =
+      (size_t)B_BYTES + 2 * (size_t)A_BYTES + 2 * TC_N * 2 + (size_t)(ESTAGE + 16) * EPI_WARPS * 32 * 4;
   PQS_CUDA(ctx, cudaFuncSetAttribute(scan4tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const size_t bsmem = (size_t)nq * 2 * sizeof(int);
   if (bsmem <= 200 * 1024)
     PQS_CUDA(ctx, cudaFuncSetAttribute(bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
   const int dbg_mode = getenv("PQS_TC_MODE") ? atoi(getenv("PQS_TC_MODE")) : 0;
-  for (int64_t c0 = 0; c0 < nt128; c0 += chunk) {
-    const int64_t ntiles = std::min<int64_t>(chunk, nt128 - c0);
+  for (int64_t c0 = tile_begin; c0 < tile_end; c0 += chunk) {
+    const int64_t ntiles = std::min<int64_t>(chunk, tile_end - c0);
     const int64_t total = nqg * ntiles;
     const int64_t nctas = std::min<int64_t>(nctas_max, total);
     Scan4TcArgs a{};
@@ -536,7 +540,6 @@ int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const u
     a.n = db->n;
     a.bglob = bglob;
     a.nthr = nthr;
-    a.prefix_tiles = prefix_tiles;
     a.nq = nq;
     a.nqg = nqg;
     a.ntiles = ntiles;

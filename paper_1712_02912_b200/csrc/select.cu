@@ -174,7 +174,24 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(SelArgs a, int sort
       get_elem(es, i, v, id);
       return true;
     };
-    block_radix_select(M, getk, (unsigned long long)(r_eff - 1), sh);
+    if (a.src == SEL_CAND_BIN) {
+      // bins < 128: one shared histogram pass finds the cut bin
+      for (int i = threadIdx.x; i < 128; i += blockDim.x) sh.hist[i] = 0;
+      __syncthreads();
+      for (int64_t i = threadIdx.x; i < M; i += blockDim.x) atomicAdd(&sh.hist[es.K[i]], 1u);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned long long c = 0;
+        int b = 0;
+        for (; b < 127 && c + sh.hist[b] <= (unsigned long long)(r_eff - 1); ++b) c += sh.hist[b];
+        sh.prefix = (unsigned long long)b;
+        sh.less = c;
+        sh.eq = sh.hist[b];
+      }
+      __syncthreads();
+    } else {
+      block_radix_select(M, getk, (unsigned long long)(r_eff - 1), sh);
+    }
     kstar = sh.prefix;
     const unsigned long long less = sh.less, eq = sh.eq;
     const unsigned long long need = (unsigned long long)r_eff - less;

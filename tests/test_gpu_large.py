@@ -97,11 +97,16 @@ def test_bin_zero_ties(big, engine):
 @pytest.mark.parametrize("engine", [1, 2])
 @pytest.mark.parametrize("n,cap", [(20_000, 32768), (300_000, 60_000)])
 def test_saturated_bins(big, engine, n, cap):
-    """init_count 3 puts qmax low: most sums saturate (bin 127 = min(S, 127)
-    for any S >= 127), so the top-r ends in a 127-bin tie broken by id --
-    codes with S > 127 must compete with S == 127 (theta 127 admits all)."""
+    """init_count 1 with queries next to the first code's reconstruction puts
+    qmax just above qmin: nearly every sum saturates (bin 127 = min(S, 127)
+    for any S >= 127), so the top-r is decided by a 127-bin tie broken by id
+    -- codes with S > 127 must compete with S == 127 (theta 127 admits all)."""
     books, codes, qs = big
-    out, ctx = _run(books, codes[:n], qs[:12], 500, 3,
+    c0 = codes[0]
+    rec = np.concatenate([books[j, c0[j]] for j in range(16)]).astype(np.float32)
+    rng = np.random.default_rng(34)
+    qq = (rec[None] + rng.normal(0, 0.5, (12, 64))).astype(np.float32)
+    out, ctx = _run(books, codes[:n], qq, 500, 1,
                     opts={P._lib.OPT_SCAN4_ENGINE: engine, P._lib.OPT_CAND_CAP: cap})
-    assert (out[0][:, -1] == 127).any()
-    _check_oracle(books, codes[:n], qs, out, 500, 3, range(12))
+    assert (out[0][:, -1] == 127).all()
+    _check_oracle(books, codes[:n], qq, out, 500, 1, range(12))
