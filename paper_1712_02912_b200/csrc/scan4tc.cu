@@ -139,6 +139,11 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
         "=r"(v[30]), "=r"(v[31])                                                                              \
       : "r"(taddr))
 
+#define TMEM_LD64(taddr, v)                                                                \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"                     \
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31]), "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]), "=r"(v[39]), "=r"(v[40]), "=r"(v[41]), "=r"(v[42]), "=r"(v[43]), "=r"(v[44]), "=r"(v[45]), "=r"(v[46]), "=r"(v[47]), "=r"(v[48]), "=r"(v[49]), "=r"(v[50]), "=r"(v[51]), "=r"(v[52]), "=r"(v[53]), "=r"(v[54]), "=r"(v[55]), "=r"(v[56]), "=r"(v[57]), "=r"(v[58]), "=r"(v[59]), "=r"(v[60]), "=r"(v[61]), "=r"(v[62]), "=r"(v[63])                                                                      \
+               : "r"(taddr))
+
 struct Scan4TcArgs {
   const uint32_t* words;   // 4-bit quad layout (mp = 16: 8 words per quad)
   int64_t n;
@@ -150,7 +155,7 @@ struct Scan4TcArgs {
   int* rec_cnt;            // [gridDim]
   int64_t rec_cap;
   unsigned long long* dbg;  // optional per-tile timestamps of CTA 0 (ns), 8 per tile
-  int dbg_mode;             // 0 normal, 1 skip compare, 2 compare but never emit
+  int dbg_mode;             // timing experiments (PQS_TC_MODE): bit 0 skip the epilogue work, bit 1 skip the one-hot writes
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -268,6 +273,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
         }
         const int sh = 4 * (int)(code & 3);
         uint8_t* dst = sA + ab * A_BYTES + row_off;
+        if (a.dbg_mode & 2) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar_afull[ab]);
+          continue;
+        }
 #pragma unroll
         for (int p = 0; p < 8; ++p) {
 #pragma unroll
@@ -331,12 +341,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
         const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * TC_N);
         const uint32_t itag = (uint32_t)it << 15;
 #pragma unroll 1
-        for (int c0 = half * (TC_N / 2); c0 < (half + 1) * (TC_N / 2); c0 += 32) {
-          uint32_t v[32];
-          TMEM_LD32(tbase + (uint32_t)c0, v);
-          uint32_t bs[16];
+        for (int c0 = half * (TC_N / 2); c0 < (half + 1) * (TC_N / 2) && !(a.dbg_mode & 1); c0 += 64) {
+          uint32_t v[64];
+          TMEM_LD64(tbase + (uint32_t)c0, v);
+          uint32_t bs[32];
 #pragma unroll
-          for (int i = 0; i < 16; i += 4) {
+          for (int i = 0; i < 32; i += 4) {
             const uint4 b4 = *reinterpret_cast<const uint4*>(bias + c0 / 2 + i);  // broadcast
             bs[i] = b4.x;
             bs[i + 1] = b4.y;
@@ -344,35 +354,39 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
             bs[i + 3] = b4.w;
           }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          uint32_t x[16];
-          uint32_t allm = 0xFFFFFFFFu;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            // two query columns per word (S <= 2032 fits 16 bits); bit 15 clear <=> S <= theta
-            x[i] = __byte_perm(v[2 * i], v[2 * i + 1], 0x5410) + bs[i];
-            allm &= x[i];
-          }
-          if ((allm & 0x80008000u) != 0x80008000u && cvalid) {  // lane-local, rare
-            // hit mask: bit i <- column 2i, bit 16+i <- column 2i+1 (flag = bit 15 clear);
-            // the packed words go to a per-thread stash for the dynamic reads below
-            uint32_t mask = 0;
+          for (int hh = 0; hh < 2; ++hh) {  // two 32-column halves of the load
+            const int cc = c0 + 32 * hh;
+            uint32_t x[16];
+            uint32_t allm = 0xFFFFFFFFu;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              mask |= (~x[i] >> (15 - i)) & (0x00010001u << i);
-              my_x[i * (EPI_WARPS * 32)] = x[i];
+              // two query columns per word (S <= 2032 fits 16 bits); bit 15 clear <=> S <= theta
+              x[i] = __byte_perm(v[32 * hh + 2 * i], v[32 * hh + 2 * i + 1], 0x5410) + bs[16 * hh + i];
+              allm &= x[i];
             }
-            const uint32_t base = itag | ((uint32_t)c0 << 7);
-            while (mask) {
-              const int b = __ffs(mask) - 1;
-              mask &= mask - 1;
-              const int i = b & 15, h = b >> 4;
-              const uint32_t pk = my_x[i * (EPI_WARPS * 32)] - bias[c0 / 2 + i];  // packed sums (no lane carry)
-              const uint32_t S = (pk >> (16 * h)) & 0xFFFFu;
-              my_stage[ncand * (EPI_WARPS * 32)] = base + ((uint32_t)(2 * i + h) << 7) + min(S, 127u);
-              ++ncand;
+            if ((allm & 0x80008000u) != 0x80008000u && cvalid) {  // lane-local, rare
+              // hit mask: bit i <- column 2i, bit 16+i <- column 2i+1 (flag = bit 15 clear);
+              // the packed words go to a per-thread stash for the dynamic reads below
+              uint32_t mask = 0;
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                mask |= (~x[i] >> (15 - i)) & (0x00010001u << i);
+                my_x[i * (EPI_WARPS * 32)] = x[i];
+              }
+              const uint32_t base = itag | ((uint32_t)cc << 7);
+              while (mask) {
+                const int b = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const int i = b & 15, h = b >> 4;
+                const uint32_t pk = my_x[i * (EPI_WARPS * 32)] - bias[cc / 2 + i];  // packed sums (no lane carry)
+                const uint32_t S = (pk >> (16 * h)) & 0xFFFFu;
+                my_stage[ncand * (EPI_WARPS * 32)] = base + ((uint32_t)(2 * i + h) << 7) + min(S, 127u);
+                ++ncand;
+              }
             }
+            if (ncand > ESTAGE - 32) flush();  // rare
           }
-          if (ncand > ESTAGE - 32) flush();  // rare
         }
         tc_fence_before();
         __syncwarp();

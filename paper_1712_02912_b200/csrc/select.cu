@@ -21,8 +21,8 @@ namespace {
 
 using namespace seldev;
 
-constexpr int SEL_THREADS = 512;
-constexpr int SMEM_CAP = 4096;  // materialised elements kept in shared memory
+constexpr int SEL_THREADS = 256;
+constexpr int SMEM_CAP = 2048;  // materialised elements kept in shared memory (more: global scratch)
 
 // Element access -----------------------------------------------------------
 struct ElemSrc {

@@ -148,23 +148,40 @@ static __device__ __forceinline__ bool pair_less(uint64_t ka, int64_t ia, uint64
   return ka < kb || (ka == kb && ia < ib);
 }
 
+static __device__ __forceinline__ void bitonic_step(uint64_t* K, int64_t* I, int t, int size, int stride) {
+  const int lo = 2 * t - (t & (stride - 1));
+  const int hi = lo + stride;
+  const bool up = ((lo & size) == 0);
+  const uint64_t ka = K[lo], kb = K[hi];
+  const int64_t ia = I[lo], ib = I[hi];
+  const bool sw = up ? pair_less(kb, ib, ka, ia) : pair_less(ka, ia, kb, ib);
+  if (sw) {
+    K[lo] = kb;
+    K[hi] = ka;
+    I[lo] = ib;
+    I[hi] = ia;
+  }
+}
+
+// Sort P (power of two) (key, id) pairs in shared memory ascending.  Small
+// arrays are sorted by warp 0 alone (warp-level syncs instead of ~log^2 P
+// block barriers); every thread of the block must call this.
 static __device__ void bitonic_sort(uint64_t* K, int64_t* I, int P) {
-  for (int size = 2; size <= P; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = threadIdx.x; t < P / 2; t += blockDim.x) {
-        const int lo = 2 * t - (t & (stride - 1));
-        const int hi = lo + stride;
-        const bool up = ((lo & size) == 0);
-        const uint64_t ka = K[lo], kb = K[hi];
-        const int64_t ia = I[lo], ib = I[hi];
-        const bool sw = up ? pair_less(kb, ib, ka, ia) : pair_less(ka, ia, kb, ib);
-        if (sw) {
-          K[lo] = kb;
-          K[hi] = ka;
-          I[lo] = ib;
-          I[hi] = ia;
+  if (P <= 1024) {
+    if (threadIdx.x < 32) {
+      for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+          for (int t = threadIdx.x; t < P / 2; t += 32) bitonic_step(K, I, t, size, stride);
+          __syncwarp();
         }
       }
+    }
+    __syncthreads();
+    return;
+  }
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < P / 2; t += blockDim.x) bitonic_step(K, I, t, size, stride);
       __syncthreads();
     }
   }
