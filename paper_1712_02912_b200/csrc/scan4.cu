@@ -551,15 +551,16 @@ int launch_scan4(pqs_ctx* ctx, int mp, const Scan4Args& a, int64_t nq) {
   return set_err(ctx, PQS_ERR_UNSUPPORTED, "scan4: unsupported padded m");
 }
 
-// theta[q] = the r-th smallest bin of the histogram pass (127 if fewer than r)
-__global__ void theta4_final_kernel(const unsigned int* __restrict__ ghist, int64_t nq, int r,
+// theta[q] = the r-th smallest bin of the histogram pass (127 if fewer than r);
+// pad1 zero-sum padding codes counted in bin 1 are removed
+__global__ void theta4_final_kernel(const unsigned int* __restrict__ ghist, int64_t nq, int r, unsigned int pad1,
                                     uint8_t* __restrict__ theta) {
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= nq) return;
   unsigned long long c = 0;
   int t = 127;
   for (int b = 0; b < 128; ++b) {
-    c += ghist[q * 128 + b];
+    c += ghist[q * 128 + b] - (b == 1 ? pad1 : 0u);
     if (c >= (unsigned long long)r) {
       t = b;
       break;
@@ -621,6 +622,8 @@ __global__ void gather_rows_u8_kernel(const uint8_t* __restrict__ src, const int
 int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const uint8_t* d_theta, int64_t nq,
                     int64_t tile_begin, int64_t tile_end, bool build_b, uint64_t* cand, int* cand_cnt, int64_t cap,
                     int* d_ovf);
+int launch_hist_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, int64_t nq, int64_t nh,
+                   unsigned int* ghist);
 
 // ---------------------------------------------------------------------------
 int build_db4(pqs_ctx* ctx, pqs_db* db, const uint8_t* d_codes) {
@@ -686,6 +689,7 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
   const int64_t cap = std::min<int64_t>(ctx->cand_cap, std::max<int64_t>(n, 1));
   const int64_t r_eff = std::min<int64_t>(r, n);
   int64_t st = 0;  // prefix tiles (TILE4 codes each); 0 = no sample
+  bool b_built = false;  // tcgen05 B tiles (query tables) already built by the histogram pass
   if (n <= cap) {
     fill_u8_kernel<<<(unsigned)cdiv(nq, 256), 256, 0, ctx->stream>>>(theta, nq, 127);
     PQS_LAUNCHED(ctx);
@@ -700,19 +704,33 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
     unsigned int* ghist = nullptr;
     PQS_TRY(scratch(ctx, S_IVF_WORK3, (size_t)(nq * 128), &ghist));
     PQS_CUDA(ctx, cudaMemsetAsync(ghist, 0, sizeof(unsigned int) * nq * 128, ctx->stream));
-    Scan4Args a{};
-    a.parts = 4;
-    a.words = db->words4;
-    a.n = n;
-    a.m = m;
-    a.qt = d_qt;
-    a.nq = nq;
-    a.nvt = s0;
-    a.tile_off = 0;
-    a.tile_step = 1;
-    a.ghist = ghist;
-    PQS_TRY(launch_scan4<MODE_HIST>(ctx, db->mp, a, nq));
-    theta4_final_kernel<<<(unsigned)cdiv(nq, 128), 128, 0, ctx->stream>>>(ghist, nq, (int)r_eff, theta);
+    // the histogram of the first s0 tiles: tcgen05 when the filter will run there
+    const int64_t nh = std::min<int64_t>(s0 * TILE4, n);
+    unsigned int pad1 = 0;
+    int hrc = PQS_ERR_UNSUPPORTED;
+    if (ctx->scan4_engine != 1 && cdiv(nq, 256) < ctx->sm_count) {
+      hrc = launch_hist_tc(ctx, db, d_qt, nq, nh, ghist);
+      if (hrc != PQS_OK && hrc != PQS_ERR_UNSUPPORTED) return hrc;
+      if (hrc == PQS_OK) {
+        pad1 = (unsigned int)(cdiv(nh, 256) * 256 - nh);
+        b_built = true;
+      }
+    }
+    if (hrc != PQS_OK) {
+      Scan4Args a{};
+      a.parts = 4;
+      a.words = db->words4;
+      a.n = n;
+      a.m = m;
+      a.qt = d_qt;
+      a.nq = nq;
+      a.nvt = s0;
+      a.tile_off = 0;
+      a.tile_step = 1;
+      a.ghist = ghist;
+      PQS_TRY(launch_scan4<MODE_HIST>(ctx, db->mp, a, nq));
+    }
+    theta4_final_kernel<<<(unsigned)cdiv(nq, 128), 128, 0, ctx->stream>>>(ghist, nq, (int)r_eff, pad1, theta);
     PQS_LAUNCHED(ctx);
   }
 
@@ -737,7 +755,7 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
     PQS_CUDA(ctx, cudaMemsetAsync(d_ovf, 0, sizeof(int), ctx->stream));
     const int64_t nt128 = cdiv(n, 128);
     const int64_t p128 = std::min<int64_t>(t1 * (TILE4 / 128), nt128);
-    int rc = launch_scan4_tc(ctx, db, d_qt, theta, nq, 0, p128, true, cand, cnt, cap, d_ovf);
+    int rc = launch_scan4_tc(ctx, db, d_qt, theta, nq, 0, p128, !b_built, cand, cnt, cap, d_ovf);
     if (rc == PQS_OK && second) {
       PQS_TRY(main_theta());
       rc = launch_scan4_tc(ctx, db, d_qt, theta_main, nq, p128, nt128, false, cand, cnt, cap, d_ovf);

@@ -405,6 +405,210 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Threshold-sample histogram on tcgen05 (roles transposed w.r.t. the filter):
+// A = the quantized tables of 128 queries (one half of a 256-query group's B
+// tile, read in place: rows n in [128h, 128h+128) sit at byte offset 2048h
+// of every 4096-byte K chunk), B = the one-hot of 256 codes (N = 256,
+// K-major, K chunk stride 4096), D = 128 query lanes x 256 code columns in
+// TMEM.  Each epilogue thread owns one query lane and adds its 256 sums'
+// bins into shared u32 counters [pair of bins][query] (shared atomics,
+// conflict-free: consecutive lanes are consecutive words), flushed to the
+// global (nq, 128) histogram at each pair's upper bin.  Codes >= nh are
+// zero rows (sum 0 -> pair 0); the caller subtracts them.
+constexpr int HN = 256;                       // codes per tile (N)
+constexpr int HO_BYTES = HN * TC_K;           // one-hot tile, 64 KB
+constexpr int LBO_O = (HN / 8) * 128;         // 4096
+constexpr int H_EPI_WARPS = 8;                // 2 per TMEM lane quadrant, 128 code columns each
+constexpr int H_THREADS = (H_EPI_WARPS + 8 + 1) * 32;  // epilogue + 8 producer + 1 MMA warp
+constexpr int H_PAIRS = 64;
+constexpr uint32_t IDESC_H = (2u << 4) | ((uint32_t)(HN >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+
+struct HistTcArgs {
+  const uint32_t* words;
+  int64_t nh;              // codes [0, nh) are counted
+  const uint8_t* bglob;    // [nqg][B_BYTES]
+  int64_t nq, nqg, ntiles; // ntiles of HN codes
+  unsigned int* ghist;     // (nq, 128)
+};
+
+__device__ __forceinline__ void mma_i8_h(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(IDESC_H), "r"(accumulate)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(H_THREADS, 1) scan4tc_hist_kernel(HistTcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smh[];
+  uint8_t* sG = smh;                                    // 64 KB: query tables of one group
+  uint8_t* sO = smh + B_BYTES;                          // 64 KB: one-hot of 256 codes
+  unsigned int* hist = reinterpret_cast<unsigned int*>(smh + B_BYTES + HO_BYTES);  // [64][256]
+  __shared__ __align__(8) uint64_t bar_g, bar_ofull, bar_oempty, bar_accfull[2], bar_accempty[2];
+  __shared__ uint32_t s_tmem;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t total = a.nqg * a.ntiles;
+  const int64_t w0 = (int64_t)blockIdx.x * total / gridDim.x;
+  const int64_t w1 = (int64_t)(blockIdx.x + 1) * total / gridDim.x;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bar_g, 1);
+    mbar_init(&bar_ofull, 8);       // one arrive per producer warp
+    mbar_init(&bar_oempty, 1);      // tcgen05.commit after both halves
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar_accfull[i], 1);
+      mbar_init(&bar_accempty[i], H_EPI_WARPS);  // every epilogue warp reads both query halves
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < H_PAIRS * TC_N; i += blockDim.x) hist[i] = 0;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+
+  if (w0 < w1) {
+    if (warp == H_EPI_WARPS + 8) {
+      // ---------------- MMA issuer (+ group table loader) ----------------
+      if (lane == 0) {
+        int64_t cur_g = -1;
+        int gi = -1;
+        for (int64_t w = w0; w < w1; ++w) {
+          const int64_t it = w - w0;
+          const int64_t g = w / a.ntiles;
+          if (g != cur_g) {
+            ++gi;
+            if (it > 0) mbar_wait(&bar_oempty, (uint32_t)((it - 1) & 1));  // all MMAs on the old tables done
+            mbar_expect_tx(&bar_g, (uint32_t)B_BYTES);
+            bulk_g2s(sG, a.bglob + g * (int64_t)B_BYTES, B_BYTES, &bar_g);
+            mbar_wait(&bar_g, (uint32_t)(gi & 1));
+            cur_g = g;
+          }
+          const uint32_t ph = (uint32_t)(it & 1);
+          mbar_wait(&bar_ofull, ph);  // one-hot of this tile written
+          const uint32_t o_base = smem_u32(sO);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            mbar_wait(&bar_accempty[h], ph ^ 1u);  // previous tile's half h drained
+            tc_fence_after();
+            const uint32_t g_base = smem_u32(sG) + (uint32_t)h * 2048u;
+            const uint32_t d_tmem = tmem + (uint32_t)(h * HN);
+#pragma unroll
+            for (int s2 = 0; s2 < TC_K / 32; ++s2) {
+              const uint64_t da = make_desc(g_base + (uint32_t)(2 * s2) * LBO_B, LBO_B, 128);
+              const uint64_t db = make_desc(o_base + (uint32_t)(2 * s2) * LBO_O, LBO_O, 128);
+              mma_i8_h(d_tmem, da, db, s2 > 0 ? 1u : 0u);
+            }
+            mma_commit(&bar_accfull[h]);
+          }
+          mma_commit(&bar_oempty);
+        }
+      }
+    } else if (warp >= H_EPI_WARPS) {
+      // ---------------- one-hot producers: thread = code row (256 rows) ----------------
+      const int row = (warp - H_EPI_WARPS) * 32 + lane;  // 0..255
+      const uint32_t row_off = (uint32_t)(row >> 3) * 128u + (uint32_t)(row & 7) * 16u;
+      for (int64_t w = w0; w < w1; ++w) {
+        const int64_t it = w - w0;
+        mbar_wait_sleep(&bar_oempty, (uint32_t)((it & 1) ^ 1));  // MMAs of the previous tile done
+        const int64_t tile = w % a.ntiles;
+        const int64_t code = tile * HN + row;
+        uint8_t* dst = sO + row_off;
+        if (code < a.nh) {
+          const uint4* src = reinterpret_cast<const uint4*>(a.words + (code >> 2) * 8);
+          const uint4 x0 = __ldg(src), x1 = __ldg(src + 1);
+          const uint32_t wd[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+          const int sh = 4 * (int)(code & 3);
+#pragma unroll
+          for (int p = 0; p < 8; ++p) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t v = (wd[p] >> (16 * h + sh)) & 15u;  // component 2p+h
+              const uint32_t one = 1u << (8 * (v & 3));
+              uint4 o;
+              o.x = (v >> 2) == 0 ? one : 0u;
+              o.y = (v >> 2) == 1 ? one : 0u;
+              o.z = (v >> 2) == 2 ? one : 0u;
+              o.w = (v >> 2) == 3 ? one : 0u;
+              *reinterpret_cast<uint4*>(dst + (2 * p + h) * LBO_O) = o;
+            }
+          }
+        } else {  // beyond the counted range: an all-zero row (sum 0)
+#pragma unroll
+          for (int k = 0; k < 16; ++k) *reinterpret_cast<uint4*>(dst + k * LBO_O) = make_uint4(0, 0, 0, 0);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar_ofull);
+      }
+    } else {
+      // ---------------- epilogue: thread = query lane, 128 code columns per warp ----------------
+      const int quad = warp & 3, half_c = warp >> 2;
+      const int row = quad * 32 + lane;  // query lane within the 128-query half
+      int64_t cur_g = -1;
+      auto flush = [&](int64_t g) {
+        // the 8 epilogue warps' 256 threads own the 256 queries of the group
+        asm volatile("bar.sync 1, %0;" ::"r"(H_EPI_WARPS * 32));
+        const int t = warp * 32 + lane;
+        const int64_t q = g * TC_N + t;
+        for (int b = 0; b < H_PAIRS; ++b) {
+          const unsigned int v = hist[b * TC_N + t];
+          if (v) {
+            if (q < a.nq) atomicAdd(a.ghist + q * 128 + 2 * b + 1, v);
+            hist[b * TC_N + t] = 0;
+          }
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(H_EPI_WARPS * 32));
+      };
+      for (int64_t w = w0; w < w1; ++w) {
+        const int64_t it = w - w0;
+        const int64_t g = w / a.ntiles;
+        if (g != cur_g) {
+          if (cur_g >= 0) flush(cur_g);
+          cur_g = g;
+        }
+        const uint32_t ph = (uint32_t)(it & 1);
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait(&bar_accfull[h], ph);
+          tc_fence_after();
+          unsigned int* hq = hist + h * 128 + row;  // this lane's query column
+          const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(h * HN + half_c * 128);
+#pragma unroll 1
+          for (int c0 = 0; c0 < 128; c0 += 64) {
+            uint32_t v[64];
+            TMEM_LD64(tbase + (uint32_t)c0, v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int i = 0; i < 64; ++i) atomicAdd(hq + (min(v[i], 127u) >> 1) * TC_N, 1u);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar_accempty[h]);
+        }
+      }
+      if (cur_g >= 0) flush(cur_g);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 // B tiles in the canonical K-major no-swizzle layout + negated thresholds:
 // B[n][k] at (k/16) * LBO_B + (n/8) * 128 + (n%8) * 16 + k%16, k = 16 j + i.
 __global__ void build_b_kernel(const uint8_t* __restrict__ qt, int64_t nq, int m, int64_t nqg,
@@ -579,5 +783,37 @@ int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const u
     PQS_LAUNCHED(ctx);
     if (a.dbg) PQS_TRY(dump_debug(ctx, a.dbg));
   }
+  return PQS_OK;
+}
+
+// Bin histogram of the codes [0, nh) for every query on tcgen05 (see
+// scan4tc_hist_kernel); adds into ghist (nq, 128) at each bin pair's upper
+// bin; the zero rows padding the last 256-code tile land in bin 1 (the
+// caller subtracts cdiv(nh, 256) * 256 - nh there).  Builds the B tiles
+// (query tables) that launch_scan4_tc then reuses (build_b = false).
+int launch_hist_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, int64_t nq, int64_t nh,
+                   unsigned int* ghist) {
+  if (db->mp != 16) return PQS_ERR_UNSUPPORTED;
+  const int64_t nqg = cdiv(nq, TC_N);
+  const int64_t ntiles = cdiv(nh, HN);
+  const int64_t total = nqg * ntiles;
+  if (total == 0) return PQS_OK;
+  uint8_t* bglob = nullptr;
+  PQS_TRY(scratch(ctx, S_TC_B, (size_t)(nqg * B_BYTES), &bglob));
+  build_b_kernel<<<(unsigned)cdiv(nqg * TC_N * 16, 256), 256, 0, ctx->stream>>>(d_qt, nq, db->m, nqg, bglob);
+  PQS_LAUNCHED(ctx);
+  HistTcArgs a{};
+  a.words = db->words4;
+  a.nh = nh;
+  a.bglob = bglob;
+  a.nq = nq;
+  a.nqg = nqg;
+  a.ntiles = ntiles;
+  a.ghist = ghist;
+  const size_t smem = (size_t)B_BYTES + HO_BYTES + (size_t)H_PAIRS * TC_N * 4;
+  PQS_CUDA(ctx, cudaFuncSetAttribute(scan4tc_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t nctas = std::min<int64_t>((int64_t)ctx->sm_count, total);
+  scan4tc_hist_kernel<<<(unsigned)nctas, H_THREADS, smem, ctx->stream>>>(a);
+  PQS_LAUNCHED(ctx);
   return PQS_OK;
 }
