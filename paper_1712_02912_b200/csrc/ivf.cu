@@ -35,7 +35,6 @@ namespace {
 
 using namespace seldev;
 
-constexpr int SAMPLE_PER_LIST = 64;
 
 // ------------------------------------------------------------ index build
 __global__ void cnorm_kernel(const float* __restrict__ coarse, int64_t K, int d, double* __restrict__ cnorm,
@@ -168,47 +167,89 @@ __global__ void __launch_bounds__(PROBE_THREADS) probe_select_kernel(ProbeArgs a
   auto approx = [&](int64_t c) { return a.cnorm[c] - 2.0 * (double)dots[c]; };
   double thr = 1e300;
   if (ma < K) {
-    auto getk = [&](int64_t c, uint64_t& v) {
-      v = dkey(approx(c));
+    // certified cut from a strided sample of S >= ma cells: its ma-th smallest
+    // approximate distance bounds the ma-th smallest of all K from above, so
+    // every true probe has approx <= that + 2 eps (one pass over the dots,
+    // ~ma * K / S cells re-scored exactly)
+    const int64_t S = K < PROBE_SMEM_CAP ? K : PROBE_SMEM_CAP;
+    for (int64_t i = threadIdx.x; i < S; i += blockDim.x) ck[i] = dkey(approx(i * K / S));
+    __syncthreads();
+    auto getk = [&](int64_t i, uint64_t& v) {
+      v = ck[i];
       return true;
     };
-    block_radix_select(K, getk, (unsigned long long)(ma - 1), sh);
+    block_radix_select(S, getk, (unsigned long long)(ma - 1), sh);
     thr = dkey_inv(sh.prefix) + 2.0 * eps;
     __syncthreads();
   }
-  // gather candidates, exact fp64 distance (sequential, as scipy cdist)
-  const bool use_global = false;
-  (void)use_global;
+  // gather the cells with approx <= thr (approximate keys first)
   for (int64_t c = threadIdx.x; c < K; c += blockDim.x) {
-    if (approx(c) <= thr) {
+    const double ap = approx(c);
+    if (ap <= thr) {
       const int p = atomicAdd(&s_cnt, 1);
-      const float* g = a.coarse + c * (int64_t)a.d;
-      double s = 0.0;
-      for (int t = 0; t < a.d; ++t) {
-        const double df = __dsub_rn((double)qv[t], (double)g[t]);
-        s = __dadd_rn(s, __dmul_rn(df, df));
-      }
       if (p < PROBE_SMEM_CAP) {
-        ck[p] = dkey(s);
+        ck[p] = dkey(ap);
         ci[p] = c;
       } else {
-        a.gkeys[ql * K + p] = dkey(s);
+        a.gkeys[ql * K + p] = dkey(ap);
         a.gids[ql * K + p] = c;
       }
     }
   }
   __syncthreads();
   const int64_t M = s_cnt;
-  const uint64_t* KK = M <= PROBE_SMEM_CAP ? ck : a.gkeys + ql * K;
-  const int64_t* II = M <= PROBE_SMEM_CAP ? ci : a.gids + ql * K;
-  if (M > PROBE_SMEM_CAP) {
-    // move the shared part to global so that one array holds all
-    for (int p = threadIdx.x; p < PROBE_SMEM_CAP; p += blockDim.x) {
-      a.gkeys[ql * K + p] = ck[p];
-      a.gids[ql * K + p] = ci[p];
+  {
+    uint64_t* AK = M <= PROBE_SMEM_CAP ? ck : a.gkeys + ql * K;
+    int64_t* AI = M <= PROBE_SMEM_CAP ? ci : a.gids + ql * K;
+    if (M > PROBE_SMEM_CAP) {
+      for (int p = threadIdx.x; p < PROBE_SMEM_CAP; p += blockDim.x) {
+        a.gkeys[ql * K + p] = ck[p];
+        a.gids[ql * K + p] = ci[p];
+      }
+      __syncthreads();
+    }
+    // tighten: the ma-th smallest approx among the gathered cells is the
+    // ma-th smallest overall (all cells up to it were gathered)
+    double thr2 = thr;
+    if (ma < M) {
+      auto getk2 = [&](int64_t i, uint64_t& v) {
+        v = AK[i];
+        return true;
+      };
+      block_radix_select(M, getk2, (unsigned long long)(ma - 1), sh);
+      thr2 = dkey_inv(sh.prefix) + 2.0 * eps;
+      __syncthreads();
+    }
+    // exact fp64 distance (sequential, as scipy cdist) of the cells within
+    // thr2; the others get the largest key (never selected: >= ma are exact)
+    for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+      if (dkey_inv(AK[i]) <= thr2) {
+        const float* g = a.coarse + AI[i] * (int64_t)a.d;
+        double s2 = 0.0;
+        for (int t0 = 0; t0 < a.d; t0 += 8) {
+          float qa[8], ga[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            qa[u] = t0 + u < a.d ? qv[t0 + u] : 0.f;
+            ga[u] = t0 + u < a.d ? g[t0 + u] : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (t0 + u < a.d) {
+              const double df = __dsub_rn((double)qa[u], (double)ga[u]);
+              s2 = __dadd_rn(s2, __dmul_rn(df, df));
+            }
+          }
+        }
+        AK[i] = dkey(s2);
+      } else {
+        AK[i] = ~0ull;
+      }
     }
     __syncthreads();
   }
+  const uint64_t* KK = M <= PROBE_SMEM_CAP ? ck : a.gkeys + ql * K;
+  const int64_t* II = M <= PROBE_SMEM_CAP ? ci : a.gids + ql * K;
   unsigned long long kstar = ~0ull;
   long long istar = 0x7FFFFFFFFFFFFFFFll;
   bool all_ties = true;
@@ -260,31 +301,100 @@ __global__ void __launch_bounds__(PROBE_THREADS) probe_select_kernel(ProbeArgs a
 }
 
 // ------------------------------------------------------------ K8 helpers
-// sample: the first SAMPLE_PER_LIST codes of every probed list, query-major
-__global__ void ivf_sample_kernel(const float* __restrict__ U, const int64_t* __restrict__ cells,
-                                  const double* __restrict__ pdist, const int64_t* __restrict__ offsets,
-                                  const uint8_t* __restrict__ codes, const float* __restrict__ V, int ma, int m, int k,
-                                  float* __restrict__ sample) {
-  extern __shared__ float su[];
+// Filter threshold per query from a sample -- the first spl codes of every
+// probed list -- computed and selected in one CTA: theta = (r-th smallest
+// sampled filter distance) + 2 * aerr, rounded up (a certified upper bound
+// of the r-th smallest exact distance over the probed lists); +inf when the
+// sample holds fewer than r codes.
+constexpr int THETA_THREADS = 512;
+constexpr int THETA_SAMPLE_CAP = 16384;
+
+__global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
+    const float* __restrict__ U, const int64_t* __restrict__ cells, const double* __restrict__ pdist,
+    const int64_t* __restrict__ offsets, const uint8_t* __restrict__ codes, const float* __restrict__ V, int ma,
+    int spl, int m, int k, int r, const float* __restrict__ aerr, float* __restrict__ theta) {
+  extern __shared__ __align__(16) unsigned char tsm[];
+  float* su = (float*)tsm;                                   // [m*k]
+  unsigned int* keys = (unsigned int*)(su + (size_t)m * k);  // [ma*spl]
+  __shared__ unsigned int hist[256];
+  __shared__ unsigned int s_prefix, s_k, s_valid;
   const int64_t q = blockIdx.x;
   for (int i = threadIdx.x; i < m * k; i += blockDim.x) su[i] = U[q * (int64_t)m * k + i];
+  if (threadIdx.x == 0) {
+    s_prefix = 0;
+    s_k = (unsigned)(r - 1);
+    s_valid = 0;
+  }
   __syncthreads();
-  const int64_t ns = (int64_t)ma * SAMPLE_PER_LIST;
-  for (int64_t s = threadIdx.x; s < ns; s += blockDim.x) {
-    const int p = (int)(s / SAMPLE_PER_LIST);
-    const int i = (int)(s % SAMPLE_PER_LIST);
+  const int ns = ma * spl;
+  unsigned int valid = 0;
+  for (int s2 = threadIdx.x; s2 < ns; s2 += blockDim.x) {
+    const int p = s2 / spl, i = s2 - p * spl;
     const int64_t c = cells[q * ma + p];
-    float out = __int_as_float(0x7f800000);
+    unsigned int key = 0xFFFFFFFFu;
     if (c >= 0) {
       const int64_t b = offsets[c], e = offsets[c + 1];
       if (b + i < e) {
         const int64_t pos = b + i;
         float acc = (float)pdist[q * ma + p] + V[pos];
         for (int j = 0; j < m; ++j) acc += su[j * k + codes[pos * m + j]];
-        out = acc;
+        key = fkey(acc);
+        ++valid;
       }
     }
-    sample[q * ns + s] = out;
+    keys[s2] = key;
+  }
+  atomicAdd(&s_valid, valid);
+  __syncthreads();
+  if (s_valid < (unsigned)r) {
+    if (threadIdx.x == 0) theta[q] = __int_as_float(0x7f800000);
+    return;
+  }
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const unsigned prefix = s_prefix;
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+      const unsigned key = keys[i];
+      if (key == 0xFFFFFFFFu) continue;
+      const bool match = (shift == 24) ? true : ((key ^ prefix) >> (shift + 8)) == 0;
+      if (match) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // lane-parallel digit search: each lane owns 8 bins
+      const int lane = threadIdx.x;
+      unsigned int s8 = 0;
+#pragma unroll
+      for (int bb = 0; bb < 8; ++bb) s8 += hist[lane * 8 + bb];
+      unsigned int incl = s8;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const unsigned int kk = s_k, excl = incl - s8;
+      if (kk >= excl && kk < incl) {
+        unsigned int cc = excl;
+        int d = lane * 8;
+        for (int bb = 0; bb < 8; ++bb) {
+          const unsigned int h = hist[lane * 8 + bb];
+          if (kk < cc + h) {
+            d = lane * 8 + bb;
+            break;
+          }
+          cc += h;
+        }
+        s_k = kk - cc;
+        s_prefix = prefix | ((unsigned)d << shift);
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double t = (double)fkey_inv(s_prefix) + 2.0 * (double)aerr[q];
+    float f = (float)t;
+    if ((double)f < t) f = nextafterf(f, __int_as_float(0x7f800000));
+    theta[q] = nextafterf(f, __int_as_float(0x7f800000));
   }
 }
 
@@ -332,45 +442,282 @@ __global__ void pair_fill_kernel(const int64_t* __restrict__ cells, const double
   pa[o] = (float)pdist[i];
 }
 
-// one CTA per inverted list: every probing query scans the list's codes
-__global__ void __launch_bounds__(256) ivf_list_kernel(const float* __restrict__ U, const int64_t* __restrict__ starts,
-                                                       const int* __restrict__ pq, const float* __restrict__ pa,
-                                                       const int64_t* __restrict__ offsets,
-                                                       const uint8_t* __restrict__ codes, const float* __restrict__ V,
-                                                       int m, int k, const float* __restrict__ theta,
-                                                       uint64_t* __restrict__ cand, int* __restrict__ cand_cnt,
-                                                       int64_t cap, int LIST_CHUNK) {
+// One CTA per inverted list; the queries probing it are processed 16 at a
+// time ("slots"): their U tables are staged in shared memory interleaved as
+// [j*k + entry][slot] (row stride 17 words), a half-warp evaluates one code
+// for all 16 slots (lane = slot, the code's bytes are a broadcast read), so
+// the 16 lookups of one table row hit 16 consecutive banks.  Survivors are
+// staged per slot in shared memory and appended to the query's candidate
+// list with one global reservation per (list, slot).
+constexpr int LQ = 16;
+constexpr int LROW = 17;           // padded row stride (words) of the slot-interleaved tables
+constexpr int LIST_THREADS = 512;
+constexpr int LCH = 1024;          // codes per chunk
+constexpr int LSTAGE = 256;        // staged survivors per slot
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int MT, int KT>  // compile-time (m, k), or (0, 0) for runtime values
+__global__ void __launch_bounds__(LIST_THREADS) ivf_list_kernel(
+    const float* __restrict__ U, const int64_t* __restrict__ starts, const int* __restrict__ pq,
+    const float* __restrict__ pa, const int64_t* __restrict__ offsets, const uint8_t* __restrict__ codes,
+    const float* __restrict__ V, int m_rt, int k_rt, const float* __restrict__ theta, uint64_t* __restrict__ cand,
+    float* __restrict__ cand_apx, int* __restrict__ cand_cnt, int64_t cap) {
+  const int m = MT > 0 ? MT : m_rt;
+  const int k = KT > 0 ? KT : k_rt;
   extern __shared__ __align__(16) unsigned char lsm[];
+  float* su = (float*)lsm;                                         // [m*k][LROW]
+  uint32_t* scode = (uint32_t*)(su + (size_t)m * k * LROW);        // [LCH][m/4] (m % 4 == 0) or bytes
+  float* sv = (float*)(scode + (size_t)LCH * ((m + 3) / 4));       // [LCH]
+  uint32_t* sst = (uint32_t*)(sv + LCH);                           // [LQ][LSTAGE] list offsets
+  float* ssa = (float*)(sst + LQ * LSTAGE);                        // [LQ][LSTAGE] filter distances
+  __shared__ int s_cnt[LQ], s_q[LQ];
+  __shared__ float s_a[LQ], s_th[LQ];
   const int64_t c = blockIdx.x;
   const int64_t p0 = starts[c], p1 = starts[c + 1];
   if (p0 == p1) return;
   const int64_t b = offsets[c], e = offsets[c + 1];
   if (b == e) return;
-  float* su = (float*)lsm;                              // m*k
-  uint8_t* sc = lsm + (size_t)m * k * 4;                // chunk codes
-  float* sv = (float*)(sc + ((size_t)LIST_CHUNK * m + 15) / 16 * 16);
-  for (int64_t cb = b; cb < e; cb += LIST_CHUNK) {
-    const int64_t ce = min(cb + (int64_t)LIST_CHUNK, e);
-    const int nc = (int)(ce - cb);
+  const int mk = m * k;
+  const int mw = (m + 3) / 4;   // code words per code
+  const int slot = threadIdx.x & (LQ - 1);
+  const int hw = threadIdx.x >> 4, nhw = blockDim.x >> 4;
+  const float* su_s = su + slot;
+  for (int64_t g0 = p0; g0 < p1; g0 += LQ) {
+    const int ns = (int)min((int64_t)LQ, p1 - g0);
     __syncthreads();
-    for (int i = threadIdx.x; i < nc * m; i += blockDim.x) sc[i] = codes[cb * m + i];
-    for (int i = threadIdx.x; i < nc; i += blockDim.x) sv[i] = V[cb + i];
-    for (int64_t pp = p0; pp < p1; ++pp) {
-      const int q = pq[pp];
-      const float A = pa[pp];
-      const float th = theta[q];
+    if (threadIdx.x < LQ) {
+      const bool ok = threadIdx.x < ns;
+      s_q[threadIdx.x] = ok ? pq[g0 + threadIdx.x] : 0;
+      s_a[threadIdx.x] = ok ? pa[g0 + threadIdx.x] : 0.f;
+      s_th[threadIdx.x] = ok ? theta[pq[g0 + threadIdx.x]] : -__int_as_float(0x7f800000);
+      s_cnt[threadIdx.x] = 0;
+    }
+    __syncthreads();
+    // stage the tables: row-contiguous global reads, stride-17 shared writes
+    // (conflict-free), asynchronous copies (completed with the first code chunk)
+    for (int idx = threadIdx.x; idx < ns * mk; idx += LIST_THREADS) {
+      const int sl = idx / mk, i = idx - sl * mk;
+      cp_async4(su + i * LROW + sl, U + (int64_t)s_q[sl] * mk + i);
+    }
+    const int q = s_q[slot];
+    const float A = s_a[slot], th = s_th[slot];
+    for (int64_t cb = b; cb < e; cb += LCH) {
+      const int nc = (int)min((int64_t)LCH, e - cb);
       __syncthreads();
-      for (int i = threadIdx.x; i < m * k; i += blockDim.x) su[i] = U[(int64_t)q * m * k + i];
+      // codes and V of the chunk: asynchronous copies, all in flight at once
+      if ((m & 3) == 0) {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(codes + cb * m);
+        for (int i = threadIdx.x; i < nc * mw; i += blockDim.x) cp_async4(scode + i, src + i);
+      } else {
+        uint8_t* sc8 = (uint8_t*)scode;
+        for (int i = threadIdx.x; i < nc * m; i += blockDim.x) sc8[i] = codes[cb * m + i];
+      }
+      for (int i = threadIdx.x; i < nc; i += blockDim.x) cp_async4(sv + i, V + cb + i);
+      cp_async_wait_all();
       __syncthreads();
-      for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+      for (int i = hw; i < nc; i += nhw) {
         float acc = A + sv[i];
-        const uint8_t* cd = sc + i * m;
-        for (int j = 0; j < m; ++j) acc += su[j * k + cd[j]];
+        if (MT > 0 && (MT & 3) == 0) {
+#pragma unroll
+          for (int w = 0; w < MT / 4; ++w) {
+            const uint32_t cw = scode[i * (MT / 4) + w];  // broadcast
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              acc += su_s[((4 * w + t) * KT + (int)__byte_perm(cw, 0u, 0x4440 + t)) * LROW];
+          }
+        } else if ((m & 3) == 0) {
+          for (int w = 0; w < mw; ++w) {
+            const uint32_t cw = scode[i * mw + w];  // broadcast
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int j = 4 * w + t;
+              acc += su_s[(j * k + (int)((cw >> (8 * t)) & 255u)) * LROW];
+            }
+          }
+        } else {
+          const uint8_t* cd = (const uint8_t*)scode + i * m;
+          for (int j = 0; j < m; ++j) acc += su_s[(j * k + cd[j]) * LROW];
+        }
         if (acc <= th) {
-          const int pos = atomicAdd(cand_cnt + q, 1);
-          if (pos < cap) cand[(int64_t)q * cap + pos] = ((uint64_t)c << 32) | (uint64_t)(uint32_t)(cb + i);
+          const int pos = atomicAdd(&s_cnt[slot], 1);
+          const uint32_t off = (uint32_t)(cb - b + i);
+          if (pos < LSTAGE) {
+            sst[slot * LSTAGE + pos] = off;
+            ssa[slot * LSTAGE + pos] = acc;
+          } else {  // stage full: direct append
+            const int gp = atomicAdd(cand_cnt + q, 1);
+            if (gp < cap) {
+              cand[(int64_t)q * cap + gp] = ((uint64_t)c << 32) | (uint64_t)(uint32_t)(b + off);
+              cand_apx[(int64_t)q * cap + gp] = acc;
+            }
+          }
         }
       }
+    }
+    __syncthreads();
+    // flush the staged survivors: one reservation per slot (warp w handles slot w)
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (w < ns) {
+      const int n = min(s_cnt[w], LSTAGE);
+      const int qq = s_q[w];
+      int base = 0;
+      if (lane == 0 && n) base = atomicAdd(cand_cnt + qq, n);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      for (int i = lane; i < n; i += 32)
+        if (base + i < cap) {
+          cand[(int64_t)qq * cap + base + i] = ((uint64_t)c << 32) | (uint64_t)(uint32_t)(b + sst[w * LSTAGE + i]);
+          cand_apx[(int64_t)qq * cap + base + i] = ssa[w * LSTAGE + i];
+        }
+    }
+  }
+}
+
+
+
+// After the list scan: every probed code with filter distance <= theta is a
+// candidate, and theta >= the r-th smallest filter distance, so the r-th
+// smallest candidate filter distance is the r-th smallest overall; a code can
+// only be in the exact top-r if its filter distance is within 2 * aerr of it
+// (|filter - exact| <= aerr).  Those candidates are compacted into out (count
+// cnt2) for the exact re-score; lists past cap are left whole (the caller's
+// fallback re-runs those queries).
+constexpr int CT_THREADS = 256;
+constexpr int CT_SMEM = 4096;
+
+__global__ void __launch_bounds__(CT_THREADS) ivf_cand_theta_kernel(const uint64_t* __restrict__ cand,
+                                                                    const float* __restrict__ apx,
+                                                                    const int* __restrict__ cand_cnt, int64_t cap,
+                                                                    int r, const float* __restrict__ aerr,
+                                                                    uint64_t* __restrict__ out, int* __restrict__ cnt2) {
+  __shared__ unsigned int keys[CT_SMEM];
+  __shared__ unsigned int hist[256];
+  __shared__ unsigned int s_prefix, s_k;
+  __shared__ int s_n;
+  const int64_t q = blockIdx.x;
+  const int64_t M = min((int64_t)cand_cnt[q], cap);
+  const uint64_t* cq = cand + q * cap;
+  const float* aq = apx + q * cap;
+  uint64_t* oq = out + q * cap;
+  float th2 = __int_as_float(0x7f800000);
+  if (cand_cnt[q] <= cap && M > r && M <= CT_SMEM) {
+    for (int i = threadIdx.x; i < M; i += blockDim.x) keys[i] = fkey(aq[i]);
+    if (threadIdx.x == 0) {
+      s_prefix = 0;
+      s_k = (unsigned)(r - 1);
+    }
+    __syncthreads();
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      const unsigned prefix = s_prefix;
+      for (int i = threadIdx.x; i < M; i += blockDim.x) {
+        const unsigned key = keys[i];
+        const bool match = (shift == 24) ? true : ((key ^ prefix) >> (shift + 8)) == 0;
+        if (match) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        unsigned int s8 = 0;
+#pragma unroll
+        for (int bb = 0; bb < 8; ++bb) s8 += hist[lane * 8 + bb];
+        unsigned int incl = s8;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const unsigned int kk = s_k, excl = incl - s8;
+        if (kk >= excl && kk < incl) {
+          unsigned int cc = excl;
+          int d = lane * 8;
+          for (int bb = 0; bb < 8; ++bb) {
+            const unsigned int h = hist[lane * 8 + bb];
+            if (kk < cc + h) {
+              d = lane * 8 + bb;
+              break;
+            }
+            cc += h;
+          }
+          s_k = kk - cc;
+          s_prefix = prefix | ((unsigned)d << shift);
+        }
+      }
+      __syncthreads();
+    }
+    const double t = (double)fkey_inv(s_prefix) + 2.0 * (double)aerr[q];
+    float f = (float)t;
+    if ((double)f < t) f = nextafterf(f, __int_as_float(0x7f800000));
+    th2 = nextafterf(f, __int_as_float(0x7f800000));
+  }
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+    if (aq[i] <= th2) {
+      const int p = atomicAdd(&s_n, 1);
+      oq[p] = cq[i];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) cnt2[q] = s_n;
+}
+
+// K6 for IVF: exact fp64 re-score of every candidate (list << 32 | pos), in
+// place: the slot gets dkey(distance), pids the stored id.  Reference
+// arithmetic (query_ivf, ivf.py:179-183 -> compute_tables scan.py:45-56 ->
+// scan_distances scan.py:77-81): r = fp64(q) - fp64(coarse[c]); table entry
+// j = fp32(sum_t (r_t - C_j[code_j][t])^2) summed over t in order; distance =
+// fp64 sum over j in order.  8 lanes per candidate (lane j0 builds entries
+// j0, j0 + 8, ...), the ordered j-sum by shuffles; grid (query, slice).
+constexpr int RERANK_THREADS = 256;
+
+__global__ void __launch_bounds__(RERANK_THREADS, 4) ivf_rerank_kernel(
+    uint64_t* __restrict__ cand, const int* __restrict__ cand_cnt, int64_t cap, const int64_t* __restrict__ ids,
+    const float* __restrict__ queries, const float* __restrict__ coarse, const float* __restrict__ books,
+    const uint8_t* __restrict__ codes, int m, int k, int d, int dsub, int64_t* __restrict__ pids) {
+  const int64_t q = blockIdx.x;
+  const int64_t M = min((int64_t)cand_cnt[q], cap);
+  uint64_t* cq = cand + q * cap;
+  int64_t* iq = pids + q * cap;
+  const float* qv = queries + q * (int64_t)d;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane >> 3, j0 = lane & 7;
+  const int64_t step = (int64_t)gridDim.y * (RERANK_THREADS / 32) * 4;
+  for (int64_t base = ((int64_t)blockIdx.y * (RERANK_THREADS / 32) + warp) * 4; base < M; base += step) {
+    const int64_t i = base + sub;
+    const bool valid = i < M;
+    const uint64_t e = valid ? cq[i] : 0ull;
+    const int64_t pos = (int64_t)(uint32_t)e;
+    const int64_t c = (int64_t)(e >> 32);
+    const float* g = coarse + c * (int64_t)d;
+    const uint8_t* code = codes + pos * (int64_t)m;
+    double acc = 0.0;
+    for (int jb = 0; jb < m; jb += 8) {
+      const int j = jb + j0;
+      float tf = 0.f;
+      if (valid && j < m) {
+        const float* cb = books + ((int64_t)j * k + code[j]) * dsub;
+        double t = 0.0;
+        for (int s2 = 0; s2 < dsub; ++s2) {
+          const int dd = j * dsub + s2;
+          const double rr = __dsub_rn((double)__ldg(qv + dd), (double)__ldg(g + dd));
+          const double df = __dsub_rn(rr, (double)__ldg(cb + s2));
+          t = __dadd_rn(t, __dmul_rn(df, df));
+        }
+        tf = __double2float_rn(t);
+      }
+      const int nj = min(8, m - jb);
+      for (int u = 0; u < nj; ++u) acc = __dadd_rn(acc, (double)__shfl_sync(0xffffffffu, tf, (sub << 3) + u));
+    }
+    if (valid && j0 == 0) {
+      cq[i] = dkey(acc);
+      iq[i] = ids[pos];
     }
   }
 }
@@ -386,58 +733,6 @@ __global__ void ivf_all_kernel(const int64_t* __restrict__ cells_row, int ma, co
       const int s = atomicAdd(cnt, 1);
       if (s < cap) cand[s] = ((uint64_t)c << 32) | (uint64_t)(uint32_t)pos;
     }
-  }
-}
-
-__global__ void theta_ivf_kernel(const float* __restrict__ sample, int64_t ns, int r, const float* __restrict__ aerr,
-                                 float* __restrict__ theta) {
-  __shared__ unsigned int hist[256];
-  __shared__ unsigned int s_prefix, s_k, s_valid;
-  const int64_t q = blockIdx.x;
-  const float* row = sample + q * ns;
-  if (threadIdx.x == 0) {
-    s_prefix = 0;
-    s_k = (unsigned)(r - 1);
-    s_valid = 0;
-  }
-  __syncthreads();
-  unsigned int valid = 0;
-  for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) valid += isfinite(row[i]) ? 1u : 0u;
-  atomicAdd(&s_valid, valid);
-  __syncthreads();
-  if (s_valid < (unsigned)r) {
-    if (threadIdx.x == 0) theta[q] = __int_as_float(0x7f800000);
-    return;
-  }
-  for (int shift = 24; shift >= 0; shift -= 8) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    const unsigned prefix = s_prefix;
-    for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
-      const float v = row[i];
-      if (!isfinite(v)) continue;
-      const unsigned key = fkey(v);
-      const bool match = (shift == 24) ? true : ((key ^ prefix) >> (shift + 8)) == 0;
-      if (match) atomicAdd(&hist[(key >> shift) & 255u], 1u);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned cc = 0, kk = s_k;
-      int d = 0;
-      for (; d < 256; ++d) {
-        if (kk < cc + hist[d]) break;
-        cc += hist[d];
-      }
-      s_k = kk - cc;
-      s_prefix = prefix | ((unsigned)d << shift);
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    const double t = (double)fkey_inv(s_prefix) + 2.0 * (double)aerr[q];
-    float f = (float)t;
-    if ((double)f < t) f = nextafterf(f, __int_as_float(0x7f800000));
-    theta[q] = nextafterf(f, __int_as_float(0x7f800000));
   }
 }
 
@@ -619,18 +914,16 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
   PQS_LAUNCHED(ctx);
   ivf_bound_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(U, pdist, nq, ma, m, k, iv->vmax, aerr);
   PQS_LAUNCHED(ctx);
-  // threshold from the sample
-  const int64_t ns = (int64_t)ma * SAMPLE_PER_LIST;
-  float* sample = nullptr;
+  // threshold from the sample (the first spl codes of every probed list)
+  const int spl = std::min(256, std::max(1, THETA_SAMPLE_CAP / std::max(ma, 1)));
   float* theta = nullptr;
-  PQS_TRY(scratch(ctx, S_SAMPLE, (size_t)(nq * ns) * 4, (uint8_t**)&sample));
   PQS_TRY(scratch(ctx, S_THETA, (size_t)nq * 4, (uint8_t**)&theta));
   const size_t usm = (size_t)m * k * 4;
-  PQS_CUDA(ctx, cudaFuncSetAttribute(ivf_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usm));
-  ivf_sample_kernel<<<(unsigned)nq, 256, usm, ctx->stream>>>(U, cells, pdist, iv->offsets, iv->codes, iv->vtab, ma, m, k,
-                                                            sample);
-  PQS_LAUNCHED(ctx);
-  theta_ivf_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(sample, ns, r, aerr, theta);
+  const size_t tsm = usm + (size_t)ma * spl * 4;
+  PQS_CHECK(ctx, tsm <= 200 * 1024, "IVF threshold sample: m * k too large");
+  PQS_CUDA(ctx, cudaFuncSetAttribute(ivf_theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+  ivf_theta_kernel<<<(unsigned)nq, THETA_THREADS, tsm, ctx->stream>>>(U, cells, pdist, iv->offsets, iv->codes,
+                                                                     iv->vtab, ma, spl, m, k, r, aerr, theta);
   PQS_LAUNCHED(ctx);
   // bucket (query, probe) pairs by list
   int* lcnt = nullptr;
@@ -656,37 +949,49 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
   PQS_TRY(scratch(ctx, S_CAND, (size_t)(nq * cap), &cand));
   PQS_TRY(scratch(ctx, S_CAND_CNT, (size_t)nq, &cnt));
   PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nq, ctx->stream));
-  const int LIST_CHUNK = std::max(64, std::min(4096, 65536 / m));
-  const size_t lsm = usm + ((size_t)LIST_CHUNK * m + 15) / 16 * 16 + (size_t)LIST_CHUNK * 4;
-  PQS_CUDA(ctx, cudaFuncSetAttribute(ivf_list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+  const size_t lsm = (size_t)m * k * LROW * 4 + (size_t)LCH * ((m + 3) / 4) * 4 + (size_t)LCH * 4 +
+                     (size_t)LQ * LSTAGE * 8;
+  float* capx = nullptr;
+  PQS_TRY(scratch(ctx, S_IVF_APX, (size_t)(nq * cap), &capx));
+  PQS_CHECK(ctx, lsm <= 220 * 1024, "IVF list scan: m * k too large for the shared-memory tables");
+  auto list_kernel = (m == 8 && k == 256) ? ivf_list_kernel<8, 256> : ivf_list_kernel<0, 0>;
+  PQS_CUDA(ctx, cudaFuncSetAttribute(list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
   PQS_TRY(scan_timer_begin(ctx));
-  ivf_list_kernel<<<(unsigned)K, 256, lsm, ctx->stream>>>(U, starts, pq_, pa, iv->offsets, iv->codes, iv->vtab, m, k,
-                                                         theta, cand, cnt, cap, LIST_CHUNK);
+  list_kernel<<<(unsigned)K, LIST_THREADS, lsm, ctx->stream>>>(U, starts, pq_, pa, iv->offsets, iv->codes, iv->vtab,
+                                                              m, k, theta, cand, capx, cnt, cap);
   PQS_LAUNCHED(ctx);
   PQS_TRY(scan_timer_end(ctx));
   ctx->last_scan_launches = 1;
   ctx->last_scan_engine = 4;
-  // exact rerank + select
+  // tighten to the candidates within 2 aerr of the r-th filter distance,
+  // exact rerank (keys in place in cand2, ids into cand) + select
+  uint64_t* cand2 = nullptr;
+  int* cnt2 = nullptr;
+  PQS_TRY(scratch(ctx, S_PIDS, (size_t)(nq * cap), &cand2));
+  PQS_TRY(scratch(ctx, S_IVF_CNT2, (size_t)nq, &cnt2));
+  ivf_cand_theta_kernel<<<(unsigned)nq, CT_THREADS, 0, ctx->stream>>>(cand, capx, cnt, cap, r, aerr, cand2, cnt2);
+  PQS_LAUNCHED(ctx);
+  int64_t* pids = reinterpret_cast<int64_t*>(cand);
+  auto rerank = [&](uint64_t* cd, const int* cc, int64_t cp, const float* qs, int64_t nqr, int64_t* pi) -> int {
+    dim3 rg((unsigned)nqr, 8);
+    ivf_rerank_kernel<<<rg, RERANK_THREADS, 0, ctx->stream>>>(cd, cc, cp, iv->ids, qs, iv->coarse, iv->books,
+                                                              iv->codes, m, k, iv->d, iv->dsub, pi);
+    PQS_LAUNCHED(ctx);
+    return PQS_OK;
+  };
+  PQS_TRY(rerank(cand2, cnt2, cap, d_queries, nq, pids));
   uint64_t* gk = nullptr;
   int64_t* gi = nullptr;
   PQS_TRY(scratch(ctx, S_KEYS, (size_t)(nq * cap), &gk));
   PQS_TRY(scratch(ctx, S_IDS, (size_t)(nq * cap), &gi));
   SelArgs s{};
-  s.src = SEL_CAND_IVF;
+  s.src = SEL_KEYS;
   s.nq = nq;
   s.r = r;
-  s.cand = cand;
-  s.cand_cnt = cnt;
+  s.cand = cand2;
+  s.cand_cnt = cnt2;
   s.cap = cap;
-  s.ids = iv->ids;
-  s.ivf_q = d_queries;
-  s.ivf_coarse = iv->coarse;
-  s.ivf_books = iv->books;
-  s.ivf_codes = iv->codes;
-  s.m = m;
-  s.k = k;
-  s.d = iv->d;
-  s.dsub = iv->dsub;
+  s.pids = pids;
   s.out_d = d_dist;
   s.out_i = d_ids;
   s.out_c = d_count;
@@ -738,12 +1043,15 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
       const int qg = over[i];
       ivf_all_kernel<<<1, 256, 0, ctx->stream>>>(cells + (int64_t)qg * ma, ma, iv->offsets, fc, fcnt, fcap);
       PQS_LAUNCHED(ctx);
+      int64_t* fpi = nullptr;
+      PQS_TRY(scratch(ctx, S_PIDS, (size_t)fcap, &fpi));
+      PQS_TRY(rerank(fc, fcnt, fcap, d_queries + (int64_t)qg * iv->d, 1, fpi));
       SelArgs f = s;
       f.nq = 1;
       f.cand = fc;
       f.cand_cnt = fcnt;
       f.cap = fcap;
-      f.ivf_q = d_queries + (int64_t)qg * iv->d;
+      f.pids = fpi;
       f.out_d = d_dist + (int64_t)qg * r;
       f.out_i = d_ids + (int64_t)qg * r;
       f.out_c = d_count + qg;

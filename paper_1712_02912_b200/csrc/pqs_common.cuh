@@ -56,6 +56,9 @@ enum ScratchSlot {
   S_WORK,     // dynamic work counters
   S_QT_WORK,  // quantized tables of a Quick ADC search
   S_TC_B, S_TC_TH, S_TC_REC, S_TC_RECCNT, S_TC_OVF,
+  S_PIDS,     // compacted IVF candidates (then their exact keys)
+  S_IVF_APX,  // IVF candidates' filter distances
+  S_IVF_CNT2, // IVF compacted candidate counts
   S_NSLOTS
 };
 
@@ -239,7 +242,7 @@ enum SelSource {
   SEL_DENSE_F64 = 2,  // dense fp64 [q][n], key = value
   SEL_DENSE_U8 = 3,   // dense u8 [q][n], key = value
   SEL_MERGE = 4,      // G lists of (double, id)
-  SEL_CAND_IVF = 5    // candidates (list<<32 | pos), key = exact fp64 residual ADC
+  SEL_KEYS = 6        // precomputed keys (cand) and ids (pids) per candidate slot (IVF: ivf_rerank_kernel)
 };
 struct SelArgs {
   int src = 0;
@@ -259,12 +262,8 @@ struct SelArgs {
   const float* tables = nullptr;  // (nq, m, k)
   const uint8_t* codes8 = nullptr;
   int m = 0, k = 0;
-  // IVF rerank (SEL_CAND_IVF)
-  const float* ivf_q = nullptr;       // (nq, d)
-  const float* ivf_coarse = nullptr;  // (K, d)
-  const float* ivf_books = nullptr;   // (m, k, dsub)
-  const uint8_t* ivf_codes = nullptr; // (n, m) row-major
-  int d = 0, dsub = 0;
+  // precomputed ids (SEL_KEYS; keys in cand)
+  const int64_t* pids = nullptr;
   // merge
   int G = 0;
   int r_in = 0;

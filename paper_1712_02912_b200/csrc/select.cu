@@ -66,39 +66,14 @@ __device__ __forceinline__ double adc_exact(const float* __restrict__ T, const u
   return acc;
 }
 
-// exact fp64 ADC of an IVF list entry against the query residual:
-// r = fp64(q) - fp64(coarse[c]) (ivf.py:179); table entry j =
-// fp32(sum_t (r_t - C_j[code_j][t])^2) (compute_tables on the residual,
-// scan.py:45-56); distance = fp64 sum over j (scan.py:77-81).
-__device__ __forceinline__ double ivf_exact(const SelArgs& a, int64_t q, int64_t c, int64_t pos) {
-  const float* qv = a.ivf_q + q * (int64_t)a.d;
-  const float* g = a.ivf_coarse + c * (int64_t)a.d;
-  const uint8_t* code = a.ivf_codes + pos * (int64_t)a.m;
-  double acc = 0.0;
-  for (int j = 0; j < a.m; ++j) {
-    const float* cb = a.ivf_books + ((int64_t)j * a.k + code[j]) * a.dsub;
-    double t = 0.0;
-    for (int s = 0; s < a.dsub; ++s) {
-      const int dd = j * a.dsub + s;
-      const double rr = __dsub_rn((double)__ldg(qv + dd), (double)__ldg(g + dd));
-      const double df = __dsub_rn(rr, (double)__ldg(cb + s));
-      t = __dadd_rn(t, __dmul_rn(df, df));
-    }
-    acc = __dadd_rn(acc, (double)__double2float_rn(t));
-  }
-  return acc;
-}
-
 __device__ void materialise(const SelArgs& a, int64_t q, int64_t M, uint64_t* K, int64_t* I,
                             SelShared& sh) {
-  if (a.src == SEL_CAND_IVF) {
-    const uint64_t* cand = a.cand + q * a.cap;
+  if (a.src == SEL_KEYS) {
+    const uint64_t* ck = a.cand + q * a.cap;
+    const int64_t* ci = a.pids + q * a.cap;
     for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
-      const uint64_t e = cand[i];
-      const int64_t pos = (int64_t)(uint32_t)e;
-      const int64_t c = (int64_t)(e >> 32);
-      K[i] = dkey(ivf_exact(a, q, c, pos));
-      I[i] = a.ids[pos];
+      K[i] = ck[i];
+      I[i] = ci[i];
     }
   } else if (a.src == SEL_CAND_BIN || a.src == SEL_CAND_ADC) {
     const uint64_t* cand = a.cand + q * a.cap;
@@ -139,7 +114,7 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(SelArgs a, int sort
 
   if (threadIdx.x == 0) {
     long long M = 0;
-    if (a.src == SEL_CAND_BIN || a.src == SEL_CAND_ADC || a.src == SEL_CAND_IVF) {
+    if (a.src == SEL_CAND_BIN || a.src == SEL_CAND_ADC || a.src == SEL_KEYS) {
       long long c = a.cand_cnt[q];
       M = c < a.cap ? c : a.cap;
     } else if (a.src == SEL_MERGE) {
