@@ -461,6 +461,19 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
                : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// streaming copy (codes / V are read once per list): L2 evict-first, so the
+// query tables stay resident
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void cp_async4_stream(void* smem, const void* gmem, uint64_t pol) {
+  asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem), "l"(pol)
+               : "memory");
+}
 
 template <int MT, int KT>  // compile-time (m, k), or (0, 0) for runtime values
 __global__ void __launch_bounds__(LIST_THREADS) ivf_list_kernel(
@@ -511,26 +524,34 @@ __global__ void __launch_bounds__(LIST_THREADS) ivf_list_kernel(
       const int nc = (int)min((int64_t)LCH, e - cb);
       __syncthreads();
       // codes and V of the chunk: asynchronous copies, all in flight at once
+      const uint64_t pol = evict_first_policy();
       if ((m & 3) == 0) {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(codes + cb * m);
-        for (int i = threadIdx.x; i < nc * mw; i += blockDim.x) cp_async4(scode + i, src + i);
+        for (int i = threadIdx.x; i < nc * mw; i += blockDim.x) cp_async4_stream(scode + i, src + i, pol);
       } else {
         uint8_t* sc8 = (uint8_t*)scode;
         for (int i = threadIdx.x; i < nc * m; i += blockDim.x) sc8[i] = codes[cb * m + i];
       }
-      for (int i = threadIdx.x; i < nc; i += blockDim.x) cp_async4(sv + i, V + cb + i);
+      for (int i = threadIdx.x; i < nc; i += blockDim.x) cp_async4_stream(sv + i, V + cb + i, pol);
       cp_async_wait_all();
       __syncthreads();
       for (int i = hw; i < nc; i += nhw) {
         float acc = A + sv[i];
         if (MT > 0 && (MT & 3) == 0) {
+          // pairwise (tree) sum: the filter bound holds for any summation order
+          float part[MT >= 4 ? MT / 4 : 1];
 #pragma unroll
           for (int w = 0; w < MT / 4; ++w) {
             const uint32_t cw = scode[i * (MT / 4) + w];  // broadcast
+            float t4[4];
 #pragma unroll
             for (int t = 0; t < 4; ++t)
-              acc += su_s[((4 * w + t) * KT + (int)__byte_perm(cw, 0u, 0x4440 + t)) * LROW];
+              t4[t] = su_s[((4 * w + t) * KT + (int)__byte_perm(cw, 0u, 0x4440 + t)) * LROW];
+            part[w] = (t4[0] + t4[1]) + (t4[2] + t4[3]);
           }
+#pragma unroll
+          for (int w = 1; w < MT / 4; ++w) part[0] += part[w];
+          acc += part[0];
         } else if ((m & 3) == 0) {
           for (int w = 0; w < mw; ++w) {
             const uint32_t cw = scode[i * mw + w];  // broadcast
