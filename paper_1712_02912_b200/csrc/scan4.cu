@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "pqs_common.cuh"
@@ -697,10 +698,12 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
     const int64_t tmin = cdiv(16 * r_eff, TILE4);
     // prefix: 1/sample_div of the list, but at least min(1/4 of it, 256 tiles)
     // -- small lists get a larger prefix (fewer candidates after it)
+    static const int pdiv = getenv("PQS_PREFIX_DIV") ? atoi(getenv("PQS_PREFIX_DIV")) : 4;   // tuning experiments
+    static const int s0div = getenv("PQS_S0_DIV") ? atoi(getenv("PQS_S0_DIV")) : 2;
     st = std::max<int64_t>(cdiv(db->ntiles, ctx->sample_div),
-                           std::min<int64_t>(cdiv(db->ntiles, 4), 256));
+                           std::min<int64_t>(cdiv(db->ntiles, pdiv), 1024 / pdiv));
     st = std::min<int64_t>(std::max<int64_t>(st, tmin), db->ntiles);
-    const int64_t s0 = std::min<int64_t>(std::max<int64_t>(cdiv(st, 8), tmin), st);
+    const int64_t s0 = std::min<int64_t>(std::max<int64_t>(cdiv(st, s0div), tmin), st);
     unsigned int* ghist = nullptr;
     PQS_TRY(scratch(ctx, S_IVF_WORK3, (size_t)(nq * 128), &ghist));
     PQS_CUDA(ctx, cudaMemsetAsync(ghist, 0, sizeof(unsigned int) * nq * 128, ctx->stream));
