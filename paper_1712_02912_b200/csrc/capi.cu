@@ -40,6 +40,7 @@ int scratch_get(pqs_ctx* ctx, int slot, size_t bytes, void** out) {
     }
     size_t want = std::max(bytes, (size_t)(s.cap * 5 / 4));
     want = (want + 255) & ~(size_t)255;
+    ctx->scratch_epoch++;
     cudaError_t e = cudaMalloc(&s.p, want);
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -52,18 +53,28 @@ int scratch_get(pqs_ctx* ctx, int slot, size_t bytes, void** out) {
   return PQS_OK;
 }
 
+// inside a stream capture the record must be "external" to become an
+// event-record node of the graph (a plain record only orders the capture)
+static int record_timer(pqs_ctx* ctx, cudaEvent_t ev) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  PQS_CUDA(ctx, cudaStreamIsCapturing(ctx->stream, &cs));
+  if (cs == cudaStreamCaptureStatusActive)
+    PQS_CUDA(ctx, cudaEventRecordWithFlags(ev, ctx->stream, cudaEventRecordExternal));
+  else
+    PQS_CUDA(ctx, cudaEventRecord(ev, ctx->stream));
+  return PQS_OK;
+}
+
 int scan_timer_begin(pqs_ctx* ctx) {
   if (!ctx->scan_ev[0]) {
     PQS_CUDA(ctx, cudaEventCreate(&ctx->scan_ev[0]));
     PQS_CUDA(ctx, cudaEventCreate(&ctx->scan_ev[1]));
   }
-  PQS_CUDA(ctx, cudaEventRecord(ctx->scan_ev[0], ctx->stream));
-  return PQS_OK;
+  return record_timer(ctx, ctx->scan_ev[0]);
 }
 
 int scan_timer_end(pqs_ctx* ctx) {
-  PQS_CUDA(ctx, cudaEventRecord(ctx->scan_ev[1], ctx->stream));
-  return PQS_OK;
+  return record_timer(ctx, ctx->scan_ev[1]);
 }
 
 int scan_timer_collect(pqs_ctx* ctx) {
@@ -127,6 +138,15 @@ int copy_out(pqs_ctx* ctx, T* host, const T* dev, size_t count, int io) {
   return PQS_OK;
 }
 
+// copy a scratch result to the caller's buffer (host or device)
+template <class T>
+int copy_any(pqs_ctx* ctx, T* dst, const T* dev, size_t count, int io) {
+  if (dst == nullptr || count == 0) return PQS_OK;
+  PQS_CUDA(ctx, cudaMemcpyAsync(dst, dev, count * sizeof(T),
+                                io == PQS_IO_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx->stream));
+  return PQS_OK;
+}
+
 int finish(pqs_ctx* ctx, int io) {
   if (io == PQS_IO_HOST) PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return PQS_OK;
@@ -171,6 +191,8 @@ void pqs_ctx_destroy(pqs_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (auto& s : ctx->scratch)
     if (s.p) cudaFree(s.p);
+  if (ctx->qg.exec) cudaGraphExecDestroy(ctx->qg.exec);
+  if (ctx->h_cnt) cudaFreeHost(ctx->h_cnt);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   for (auto& e : ctx->scan_ev)
     if (e) cudaEventDestroy(e);
@@ -465,27 +487,24 @@ int pqs_adc_search(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* pq, const float
 static int qadc_common(pqs_ctx* ctx, const pqs_db* db, const float* dt, int64_t nq, int init_count, int r,
                        uint8_t* out_bins, int64_t* out_ids, int32_t* out_count, uint8_t* out_qt, double* out_qmm,
                        int io) {
+  // results land in the context's scratch (stable addresses: the device phase
+  // is replayed as a CUDA graph, see run_qadc_topr) and are copied out
   uint8_t* db_ = nullptr;
   int64_t* di = nullptr;
   int32_t* dc = nullptr;
-  uint8_t* dqt = nullptr;
+  uint8_t* qt_work = nullptr;
   double* dqmm = nullptr;
-  PQS_TRY(stage_out(ctx, S_OUT_B, out_bins, (size_t)nq * r, io, &db_));
-  PQS_TRY(stage_out(ctx, S_OUT_I, out_ids, (size_t)nq * r, io, &di));
-  PQS_TRY(stage_out(ctx, S_OUT_C, out_count, (size_t)nq, io, &dc));
-  PQS_TRY(stage_out(ctx, S_QTABLES + 0, out_qt, (size_t)nq * db->m * 16, io, &dqt));
-  PQS_TRY(stage_out(ctx, S_QMINMAX, out_qmm, (size_t)nq * 2, io, &dqmm));
-  // the fallback path reuses S_QTABLES as a gather buffer: keep qtables in its own slot
-  uint8_t* qt_work = dqt;
-  if (io == PQS_IO_HOST || out_qt == nullptr) {
-    PQS_TRY(scratch(ctx, S_QT_WORK, (size_t)nq * db->m * 16, &qt_work));
-  }
+  PQS_TRY(scratch(ctx, S_OUT_B, (size_t)nq * r, &db_));
+  PQS_TRY(scratch(ctx, S_OUT_I, (size_t)nq * r, &di));
+  PQS_TRY(scratch(ctx, S_OUT_C, (size_t)nq, &dc));
+  PQS_TRY(scratch(ctx, S_QT_WORK, (size_t)nq * db->m * 16, &qt_work));
+  PQS_TRY(scratch(ctx, S_QMINMAX, (size_t)nq * 2, &dqmm));
   PQS_TRY(run_qadc_topr(ctx, db, dt, nq, init_count, r, db_, di, dc, qt_work, dqmm));
-  PQS_TRY(copy_out(ctx, out_bins, db_, (size_t)nq * r, io));
-  PQS_TRY(copy_out(ctx, out_ids, di, (size_t)nq * r, io));
-  PQS_TRY(copy_out(ctx, out_count, dc, (size_t)nq, io));
-  PQS_TRY(copy_out(ctx, out_qt, (const uint8_t*)qt_work, (size_t)nq * db->m * 16, io));
-  PQS_TRY(copy_out(ctx, out_qmm, dqmm, (size_t)nq * 2, io));
+  PQS_TRY(copy_any(ctx, out_bins, db_, (size_t)nq * r, io));
+  PQS_TRY(copy_any(ctx, out_ids, di, (size_t)nq * r, io));
+  PQS_TRY(copy_any(ctx, out_count, dc, (size_t)nq, io));
+  PQS_TRY(copy_any(ctx, out_qt, (const uint8_t*)qt_work, (size_t)nq * db->m * 16, io));
+  PQS_TRY(copy_any(ctx, out_qmm, dqmm, (size_t)nq * 2, io));
   return finish(ctx, io);
 }
 

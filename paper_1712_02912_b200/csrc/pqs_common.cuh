@@ -84,7 +84,20 @@ struct pqs_ctx {
   double last_scan_work = 0;
   cudaEvent_t scan_ev[2] = {nullptr, nullptr};
   Scratch scratch[S_NSLOTS];
+  int64_t scratch_epoch = 0;  // bumped whenever a scratch slot is (re)allocated
   int* host_flag = nullptr;  // pinned
+  // pinned host landing buffers of the per-query candidate counts (+ flags)
+  int* h_cnt = nullptr;
+  int64_t h_cnt_cap = 0;
+  // captured Quick ADC search pipeline (CUDA graph), see run_qadc_topr
+  struct QGraph {
+    std::vector<int64_t> key, seen;
+    cudaGraphExec_t exec = nullptr;
+    int64_t epoch = -1;
+    int64_t launches = 0;
+    int used_tc = 0, second = 0;
+    double scan_work = 0;
+  } qg;
 };
 
 struct pqs_pq {

@@ -662,114 +662,45 @@ int launch_scan4_dense(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qtables,
   return launch_scan4<MODE_DENSE>(ctx, db->mp, a, nq);
 }
 
-int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t nq, int init_count, int r,
-                  uint8_t* d_bins, int64_t* d_ids, int32_t* d_count, uint8_t* d_qt, double* d_qmm) {
-  const int64_t n = db->n;
-  const int m = db->m;
-  // ---- K9: params + quantized tables
-  const int64_t n_src = db->prefix ? db->n_prefix : n;
-  const int64_t n_init = std::min<int64_t>(init_count, n_src);
-  unsigned long long* pscratch = nullptr;
-  if (n_init > 2048) PQS_TRY(scratch(ctx, S_PREFIX, (size_t)(nq * n_init), &pscratch));
-  qadc_params_kernel<<<(unsigned)nq, SCAN4_THREADS, 0, ctx->stream>>>(*db, d_tables, nq, init_count, r, pscratch,
-                                                                     n_init, d_qt, d_qmm);
-  PQS_LAUNCHED(ctx);
+// ---------------------------------------------------------------------------
+// Quick ADC top-r search.  The device phase (params -> threshold sample ->
+// filtered scan -> select -> candidate counts into pinned host memory) makes
+// no host decision that depends on device data, so it is captured once per
+// (list, batch shape, options, scratch layout) as a CUDA graph and replayed;
+// the host phase (record-overflow redo, exact dense fallback, statistics)
+// runs after the single synchronisation.
+namespace {
 
-  // ---- threshold: exact when every code fits the candidate buffer.
-  // Otherwise certified thresholds from the first st tiles (the "prefix"):
-  //   1. t0 = the r-th smallest bin of the first s0 tiles (histogram pass);
-  //   2. the prefix is filtered with t0 (>= the prefix's r-th smallest bin t);
-  //   3. t = the r-th smallest prefix candidate bin (cand_theta_kernel): every
-  //      top-r code has bin <= t, and -- ids increasing in storage order -- a
-  //      code after the prefix needs bin < t (the prefix holds r codes with
-  //      bin <= t and smaller ids), so the rest is filtered with t - 1.
-  uint8_t* theta = nullptr;
-  uint8_t* theta_main = nullptr;
-  PQS_TRY(scratch(ctx, S_THETA, (size_t)(2 * nq), &theta));
-  theta_main = theta + nq;
-  const int64_t cap = std::min<int64_t>(ctx->cand_cap, std::max<int64_t>(n, 1));
-  const int64_t r_eff = std::min<int64_t>(r, n);
-  int64_t st = 0;  // prefix tiles (TILE4 codes each); 0 = no sample
-  bool b_built = false;  // tcgen05 B tiles (query tables) already built by the histogram pass
-  if (n <= cap) {
-    fill_u8_kernel<<<(unsigned)cdiv(nq, 256), 256, 0, ctx->stream>>>(theta, nq, 127);
-    PQS_LAUNCHED(ctx);
-  } else {
-    const int64_t tmin = cdiv(16 * r_eff, TILE4);
-    // prefix: 1/sample_div of the list, but at least min(1/4 of it, 256 tiles)
-    // -- small lists get a larger prefix (fewer candidates after it)
-    static const int pdiv = getenv("PQS_PREFIX_DIV") ? atoi(getenv("PQS_PREFIX_DIV")) : 4;   // tuning experiments
-    static const int s0div = getenv("PQS_S0_DIV") ? atoi(getenv("PQS_S0_DIV")) : 2;
-    st = std::max<int64_t>(cdiv(db->ntiles, ctx->sample_div),
-                           std::min<int64_t>(cdiv(db->ntiles, pdiv), 1024 / pdiv));
-    st = std::min<int64_t>(std::max<int64_t>(st, tmin), db->ntiles);
-    const int64_t s0 = std::min<int64_t>(std::max<int64_t>(cdiv(st, s0div), tmin), st);
-    unsigned int* ghist = nullptr;
-    PQS_TRY(scratch(ctx, S_IVF_WORK3, (size_t)(nq * 128), &ghist));
-    PQS_CUDA(ctx, cudaMemsetAsync(ghist, 0, sizeof(unsigned int) * nq * 128, ctx->stream));
-    // the histogram of the first s0 tiles: tcgen05 when the filter will run there
-    const int64_t nh = std::min<int64_t>(s0 * TILE4, n);
-    unsigned int pad1 = 0;
-    int hrc = PQS_ERR_UNSUPPORTED;
-    if (ctx->scan4_engine != 1 && cdiv(nq, 256) < ctx->sm_count) {
-      hrc = launch_hist_tc(ctx, db, d_qt, nq, nh, ghist);
-      if (hrc != PQS_OK && hrc != PQS_ERR_UNSUPPORTED) return hrc;
-      if (hrc == PQS_OK) {
-        pad1 = (unsigned int)(cdiv(nh, 256) * 256 - nh);
-        b_built = true;
-      }
-    }
-    if (hrc != PQS_OK) {
-      Scan4Args a{};
-      a.parts = 4;
-      a.words = db->words4;
-      a.n = n;
-      a.m = m;
-      a.qt = d_qt;
-      a.nq = nq;
-      a.nvt = s0;
-      a.tile_off = 0;
-      a.tile_step = 1;
-      a.ghist = ghist;
-      PQS_TRY(launch_scan4<MODE_HIST>(ctx, db->mp, a, nq));
-    }
-    theta4_final_kernel<<<(unsigned)cdiv(nq, 128), 128, 0, ctx->stream>>>(ghist, nq, (int)r_eff, pad1, theta);
-    PQS_LAUNCHED(ctx);
-  }
-
-  // ---- K4 filtered scan
+struct QadcRun {
+  pqs_ctx* ctx;
+  const pqs_db* db;
+  const float* d_tables;
+  int64_t nq;
+  int init_count, r;
+  uint8_t *d_bins, *d_qt;
+  int64_t* d_ids;
+  int32_t* d_count;
+  double* d_qmm;
+  // plan
+  int64_t n = 0, cap = 0, r_eff = 0, st = 0, t1 = 0;
+  int m = 0;
+  bool second = false, used_tc = false;
+  // buffers
+  uint8_t *theta = nullptr, *theta_main = nullptr;
   uint64_t* cand = nullptr;
   int* cnt = nullptr;
-  PQS_TRY(scratch(ctx, S_CAND, (size_t)(nq * cap), &cand));
-  PQS_TRY(scratch(ctx, S_CAND_CNT, (size_t)nq, &cnt));
-  PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nq, ctx->stream));
-  const int64_t t1 = st > 0 ? st : db->ntiles;  // end of the first range
-  const bool second = st > 0 && st < db->ntiles;
-  const int strict = db->ids == nullptr ? 1 : 0;
-  auto main_theta = [&]() -> int {
-    cand_theta_kernel<<<(unsigned)nq, 128, 0, ctx->stream>>>(cand, cnt, cap, (int)r_eff, strict, theta_main);
+  int* d_ovf = nullptr;
+  SelArgs sel{};
+
+  int main_theta() {
+    cand_theta_kernel<<<(unsigned)nq, 128, 0, ctx->stream>>>(cand, cnt, cap, (int)r_eff, db->ids == nullptr ? 1 : 0,
+                                                            theta_main);
     PQS_LAUNCHED(ctx);
     return PQS_OK;
-  };
-  int* d_ovf = nullptr;
-  PQS_TRY(scratch(ctx, S_TC_OVF, 1, &d_ovf));
-  // tcgen05 engine (128-code tiles) when sampled; returns UNSUPPORTED for shapes outside it
-  auto scan_tc = [&]() -> int {
-    PQS_CUDA(ctx, cudaMemsetAsync(d_ovf, 0, sizeof(int), ctx->stream));
-    const int64_t nt128 = cdiv(n, 128);
-    const int64_t p128 = std::min<int64_t>(t1 * (TILE4 / 128), nt128);
-    int rc = launch_scan4_tc(ctx, db, d_qt, theta, nq, 0, p128, !b_built, cand, cnt, cap, d_ovf);
-    if (rc == PQS_OK && second) {
-      PQS_TRY(main_theta());
-      rc = launch_scan4_tc(ctx, db, d_qt, theta_main, nq, p128, nt128, false, cand, cnt, cap, d_ovf);
-    }
-    if (rc == PQS_OK) {
-      ctx->last_scan_engine = 2;
-      ctx->last_scan_work = 2.0 * (double)cdiv(nq, 256) * 256.0 * (double)nt128 * 128.0 * 256.0;
-    }
-    return rc;
-  };
-  auto scan_prmt = [&]() -> int {
+  }
+
+  // PRMT engine over the same two ranges
+  int scan_prmt() {
     Scan4Args a{};
     a.words = db->words4;
     a.n = n;
@@ -794,103 +725,313 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
     ctx->last_scan_engine = 1;
     ctx->last_scan_work = (double)nq * (double)n * (double)m;
     return PQS_OK;
-  };
-  // ---- K5 select (bins, ties by id)
-  uint64_t* gk = nullptr;
-  int64_t* gi = nullptr;
-  PQS_TRY(scratch(ctx, S_KEYS, (size_t)(nq * cap), &gk));
-  PQS_TRY(scratch(ctx, S_IDS, (size_t)(nq * cap), &gi));
-  SelArgs s{};
-  s.src = SEL_CAND_BIN;
-  s.nq = nq;
-  s.r = r;
-  s.cand = cand;
-  s.cand_cnt = cnt;
-  s.cap = cap;
-  s.ids = db->ids;
-  s.id_base = db->id_base;
-  s.out_b = d_bins;
-  s.out_i = d_ids;
-  s.out_c = d_count;
-  s.gkeys = gk;
-  s.gids = gi;
-  s.gcap = cap;
-  std::vector<int> hcnt(nq);
-  bool used_tc = false;
-  PQS_TRY(scan_timer_begin(ctx));
-  if (st > 0 && ctx->scan4_engine != 1) {
-    const int rc = scan_tc();
-    if (rc == PQS_OK) {
-      used_tc = true;
-    } else if (rc == PQS_ERR_UNSUPPORTED) {
-      if (ctx->scan4_engine == 2)
-        return set_err(ctx, PQS_ERR_UNSUPPORTED, "tcgen05 Quick ADC scan: unsupported shape (needs m <= 16)");
-      PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nq, ctx->stream));
-    } else {
-      return rc;
-    }
   }
-  if (!used_tc) PQS_TRY(scan_prmt());
-  PQS_TRY(scan_timer_end(ctx));
-  ctx->last_scan_launches = second ? 2 : 1;
-  PQS_TRY(launch_select(ctx, s));
-  // one synchronisation: candidate counts (+ the tcgen05 record-overflow flag)
-  int ovf = 0;
-  PQS_CUDA(ctx, cudaMemcpyAsync(hcnt.data(), cnt, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
-  if (used_tc) PQS_CUDA(ctx, cudaMemcpyAsync(&ovf, d_ovf, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-  PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  if (ovf) {  // a CTA record list overflowed: redo the scan on the PRMT engine
-    PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nq, ctx->stream));
-    PQS_TRY(scan_timer_begin(ctx));
-    PQS_TRY(scan_prmt());
-    PQS_TRY(scan_timer_end(ctx));
-    PQS_TRY(launch_select(ctx, s));
-    PQS_CUDA(ctx, cudaMemcpyAsync(hcnt.data(), cnt, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
-    PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  }
-  ctx->last_evals = nq * n;
 
-  // ---- overflow check -> exact dense fallback for those queries
-  PQS_TRY(scan_timer_collect(ctx));
-  std::vector<int> over;
-  int64_t mx = 0, ctot = 0;
-  for (int64_t q = 0; q < nq; ++q) {
-    mx = std::max<int64_t>(mx, hcnt[q]);
-    ctot += hcnt[q];
-    if (hcnt[q] > cap || hcnt[q] < r_eff || ctx->force_fallback) over.push_back((int)q);
-  }
-  ctx->last_max_cand = mx;
-  ctx->last_cand_total = ctot;
-  ctx->last_overflow = (int64_t)over.size();
-  if (!over.empty()) {
-    const int64_t B = std::max<int64_t>(1, std::min<int64_t>((int64_t)over.size(), (int64_t)(1ll << 30) / std::max<int64_t>(n, 1)));
-    int* d_qmap = nullptr;
-    uint8_t* qt_sub = nullptr;
-    uint8_t* dense = nullptr;
-    PQS_TRY(scratch(ctx, S_MISC, (size_t)over.size(), &d_qmap));
-    PQS_TRY(scratch(ctx, S_QTABLES, (size_t)(B * m * 16), &qt_sub));
-    PQS_TRY(scratch(ctx, S_DENSE, (size_t)(B * n), &dense));
-    PQS_CUDA(ctx, cudaMemcpyAsync(d_qmap, over.data(), sizeof(int) * over.size(), cudaMemcpyHostToDevice, ctx->stream));
-    for (int64_t b0 = 0; b0 < (int64_t)over.size(); b0 += B) {
-      const int64_t nb = std::min<int64_t>(B, (int64_t)over.size() - b0);
-      gather_rows_u8_kernel<<<(unsigned)cdiv(nb * m * 16, 256), 256, 0, ctx->stream>>>(d_qt, d_qmap + b0, nb,
-                                                                                     (int64_t)m * 16, qt_sub);
+  int device_phase() {
+    n = db->n;
+    m = db->m;
+    // ---- K9: params + quantized tables
+    const int64_t n_src = db->prefix ? db->n_prefix : n;
+    const int64_t n_init = std::min<int64_t>(init_count, n_src);
+    unsigned long long* pscratch = nullptr;
+    if (n_init > 2048) PQS_TRY(scratch(ctx, S_PREFIX, (size_t)(nq * n_init), &pscratch));
+    qadc_params_kernel<<<(unsigned)nq, SCAN4_THREADS, 0, ctx->stream>>>(*db, d_tables, nq, init_count, r, pscratch,
+                                                                       n_init, d_qt, d_qmm);
+    PQS_LAUNCHED(ctx);
+
+    // ---- threshold: exact when every code fits the candidate buffer.
+    // Otherwise certified thresholds from the first st tiles (the "prefix"):
+    //   1. t0 = the r-th smallest bin of the first s0 tiles (histogram pass);
+    //   2. the prefix is filtered with t0 (>= the prefix's r-th smallest bin t);
+    //   3. t = the r-th smallest prefix candidate bin (cand_theta_kernel): every
+    //      top-r code has bin <= t, and -- ids increasing in storage order -- a
+    //      code after the prefix needs bin < t (the prefix holds r codes with
+    //      bin <= t and smaller ids), so the rest is filtered with t - 1.
+    PQS_TRY(scratch(ctx, S_THETA, (size_t)(2 * nq), &theta));
+    theta_main = theta + nq;
+    cap = std::min<int64_t>(ctx->cand_cap, std::max<int64_t>(n, 1));
+    r_eff = std::min<int64_t>(r, n);
+    st = 0;  // prefix tiles (TILE4 codes each); 0 = no sample
+    bool b_built = false;  // tcgen05 B tiles (query tables) already built by the histogram pass
+    if (n <= cap) {
+      fill_u8_kernel<<<(unsigned)cdiv(nq, 256), 256, 0, ctx->stream>>>(theta, nq, 127);
       PQS_LAUNCHED(ctx);
-      PQS_TRY(launch_scan4_dense(ctx, db, qt_sub, nb, dense, n));
-      SelArgs f{};
-      f.src = SEL_DENSE_U8;
-      f.nq = nb;
-      f.r = r;
-      f.dense = dense;
-      f.n = n;
-      f.ids = db->ids;
-      f.id_base = db->id_base;
-      f.qmap = d_qmap + b0;
-      f.out_b = d_bins;
-      f.out_i = d_ids;
-      f.out_c = d_count;
-      PQS_TRY(launch_select(ctx, f));
+    } else {
+      const int64_t tmin = cdiv(16 * r_eff, TILE4);
+      // prefix: 1/sample_div of the list, but at least min(1/4 of it, 256 tiles)
+      // -- small lists get a larger prefix (fewer candidates after it)
+      static const int pdiv = getenv("PQS_PREFIX_DIV") ? atoi(getenv("PQS_PREFIX_DIV")) : 4;  // tuning experiments
+      static const int s0div = getenv("PQS_S0_DIV") ? atoi(getenv("PQS_S0_DIV")) : 2;
+      st = std::max<int64_t>(cdiv(db->ntiles, ctx->sample_div), std::min<int64_t>(cdiv(db->ntiles, pdiv), 1024 / pdiv));
+      st = std::min<int64_t>(std::max<int64_t>(st, tmin), db->ntiles);
+      const int64_t s0 = std::min<int64_t>(std::max<int64_t>(cdiv(st, s0div), tmin), st);
+      unsigned int* ghist = nullptr;
+      PQS_TRY(scratch(ctx, S_IVF_WORK3, (size_t)(nq * 128), &ghist));
+      PQS_CUDA(ctx, cudaMemsetAsync(ghist, 0, sizeof(unsigned int) * nq * 128, ctx->stream));
+      // the histogram of the first s0 tiles: tcgen05 when the filter will run there
+      const int64_t nh = std::min<int64_t>(s0 * TILE4, n);
+      unsigned int pad1 = 0;
+      int hrc = PQS_ERR_UNSUPPORTED;
+      if (ctx->scan4_engine != 1 && cdiv(nq, 256) < ctx->sm_count) {
+        hrc = launch_hist_tc(ctx, db, d_qt, nq, nh, ghist);
+        if (hrc != PQS_OK && hrc != PQS_ERR_UNSUPPORTED) return hrc;
+        if (hrc == PQS_OK) {
+          pad1 = (unsigned int)(cdiv(nh, 256) * 256 - nh);
+          b_built = true;
+        }
+      }
+      if (hrc != PQS_OK) {
+        Scan4Args a{};
+        a.parts = 4;
+        a.words = db->words4;
+        a.n = n;
+        a.m = m;
+        a.qt = d_qt;
+        a.nq = nq;
+        a.nvt = s0;
+        a.tile_off = 0;
+        a.tile_step = 1;
+        a.ghist = ghist;
+        PQS_TRY(launch_scan4<MODE_HIST>(ctx, db->mp, a, nq));
+      }
+      theta4_final_kernel<<<(unsigned)cdiv(nq, 128), 128, 0, ctx->stream>>>(ghist, nq, (int)r_eff, pad1, theta);
+      PQS_LAUNCHED(ctx);
     }
+
+    // ---- K4 filtered scan
+    PQS_TRY(scratch(ctx, S_CAND, (size_t)(nq * cap), &cand));
+    PQS_TRY(scratch(ctx, S_CAND_CNT, (size_t)nq, &cnt));
+    PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nq, ctx->stream));
+    t1 = st > 0 ? st : db->ntiles;  // end of the first range
+    second = st > 0 && st < db->ntiles;
+    PQS_TRY(scratch(ctx, S_TC_OVF, 1, &d_ovf));
+    PQS_CUDA(ctx, cudaMemsetAsync(d_ovf, 0, sizeof(int), ctx->stream));
+    used_tc = false;
+    PQS_TRY(scan_timer_begin(ctx));
+    if (st > 0 && ctx->scan4_engine != 1) {
+      // tcgen05 engine (128-code tiles); UNSUPPORTED for shapes outside it
+      const int64_t nt128 = cdiv(n, 128);
+      const int64_t p128 = std::min<int64_t>(t1 * (TILE4 / 128), nt128);
+      int rc = launch_scan4_tc(ctx, db, d_qt, theta, nq, 0, p128, !b_built, cand, cnt, cap, d_ovf);
+      if (rc == PQS_OK && second) {
+        PQS_TRY(main_theta());
+        rc = launch_scan4_tc(ctx, db, d_qt, theta_main, nq, p128, nt128, false, cand, cnt, cap, d_ovf);
+      }
+      if (rc == PQS_OK) {
+        used_tc = true;
+        ctx->last_scan_engine = 2;
+        ctx->last_scan_work = 2.0 * (double)cdiv(nq, 256) * 256.0 * (double)nt128 * 128.0 * 256.0;
+      } else if (rc == PQS_ERR_UNSUPPORTED) {
+        if (ctx->scan4_engine == 2)
+          return set_err(ctx, PQS_ERR_UNSUPPORTED, "tcgen05 Quick ADC scan: unsupported shape (needs m <= 16)");
+        PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nq, ctx->stream));
+      } else {
+        return rc;
+      }
+    }
+    if (!used_tc) PQS_TRY(scan_prmt());
+    PQS_TRY(scan_timer_end(ctx));
+    ctx->last_scan_launches = second ? 2 : 1;
+
+    // ---- K5 select (bins, ties by id)
+    uint64_t* gk = nullptr;
+    int64_t* gi = nullptr;
+    PQS_TRY(scratch(ctx, S_KEYS, (size_t)(nq * cap), &gk));
+    PQS_TRY(scratch(ctx, S_IDS, (size_t)(nq * cap), &gi));
+    sel = SelArgs{};
+    sel.src = SEL_CAND_BIN;
+    sel.nq = nq;
+    sel.r = r;
+    sel.cand = cand;
+    sel.cand_cnt = cnt;
+    sel.cap = cap;
+    sel.ids = db->ids;
+    sel.id_base = db->id_base;
+    sel.out_b = d_bins;
+    sel.out_i = d_ids;
+    sel.out_c = d_count;
+    sel.gkeys = gk;
+    sel.gids = gi;
+    sel.gcap = cap;
+    PQS_TRY(launch_select(ctx, sel));
+    // candidate counts + the tcgen05 record-overflow flag into pinned host memory
+    PQS_CUDA(ctx, cudaMemcpyAsync(ctx->h_cnt, cnt, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
+    PQS_CUDA(ctx, cudaMemcpyAsync(ctx->h_cnt + nq, d_ovf, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    return PQS_OK;
   }
-  return PQS_OK;
+
+  int host_phase() {
+    const int* hcnt = ctx->h_cnt;
+    if (used_tc && ctx->h_cnt[nq]) {  // a CTA record list overflowed: redo the scan on the PRMT engine
+      PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nq, ctx->stream));
+      PQS_TRY(scan_timer_begin(ctx));
+      PQS_TRY(scan_prmt());
+      PQS_TRY(scan_timer_end(ctx));
+      PQS_TRY(launch_select(ctx, sel));
+      PQS_CUDA(ctx, cudaMemcpyAsync(ctx->h_cnt, cnt, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
+      PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    ctx->last_evals = nq * n;
+    // ---- overflow check -> exact dense fallback for those queries
+    PQS_TRY(scan_timer_collect(ctx));
+    std::vector<int> over;
+    int64_t mx = 0, ctot = 0;
+    for (int64_t q = 0; q < nq; ++q) {
+      mx = std::max<int64_t>(mx, hcnt[q]);
+      ctot += hcnt[q];
+      if (hcnt[q] > cap || hcnt[q] < r_eff || ctx->force_fallback) over.push_back((int)q);
+    }
+    ctx->last_max_cand = mx;
+    ctx->last_cand_total = ctot;
+    ctx->last_overflow = (int64_t)over.size();
+    if (!over.empty()) {
+      const int64_t B =
+          std::max<int64_t>(1, std::min<int64_t>((int64_t)over.size(), (int64_t)(1ll << 30) / std::max<int64_t>(n, 1)));
+      int* d_qmap = nullptr;
+      uint8_t* qt_sub = nullptr;
+      uint8_t* dense = nullptr;
+      PQS_TRY(scratch(ctx, S_MISC, (size_t)over.size(), &d_qmap));
+      PQS_TRY(scratch(ctx, S_QTABLES, (size_t)(B * m * 16), &qt_sub));
+      PQS_TRY(scratch(ctx, S_DENSE, (size_t)(B * n), &dense));
+      PQS_CUDA(ctx, cudaMemcpyAsync(d_qmap, over.data(), sizeof(int) * over.size(), cudaMemcpyHostToDevice,
+                                    ctx->stream));
+      for (int64_t b0 = 0; b0 < (int64_t)over.size(); b0 += B) {
+        const int64_t nb = std::min<int64_t>(B, (int64_t)over.size() - b0);
+        gather_rows_u8_kernel<<<(unsigned)cdiv(nb * m * 16, 256), 256, 0, ctx->stream>>>(d_qt, d_qmap + b0, nb,
+                                                                                       (int64_t)m * 16, qt_sub);
+        PQS_LAUNCHED(ctx);
+        PQS_TRY(launch_scan4_dense(ctx, db, qt_sub, nb, dense, n));
+        SelArgs f{};
+        f.src = SEL_DENSE_U8;
+        f.nq = nb;
+        f.r = r;
+        f.dense = dense;
+        f.n = n;
+        f.ids = db->ids;
+        f.id_base = db->id_base;
+        f.qmap = d_qmap + b0;
+        f.out_b = d_bins;
+        f.out_i = d_ids;
+        f.out_c = d_count;
+        PQS_TRY(launch_select(ctx, f));
+      }
+    }
+    return PQS_OK;
+  }
+};
+
+}  // namespace
+
+int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t nq, int init_count, int r,
+                  uint8_t* d_bins, int64_t* d_ids, int32_t* d_count, uint8_t* d_qt, double* d_qmm) {
+  // pinned landing buffer for the counts (+ overflow flag); growing it drops the graph
+  if (ctx->h_cnt_cap < nq + 1) {
+    if (ctx->h_cnt) {
+      PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+      cudaFreeHost(ctx->h_cnt);
+      ctx->h_cnt = nullptr;
+    }
+    PQS_CUDA(ctx, cudaHostAlloc((void**)&ctx->h_cnt, sizeof(int) * (size_t)(nq + 1), cudaHostAllocDefault));
+    ctx->h_cnt_cap = nq + 1;
+    ctx->scratch_epoch++;
+  }
+  QadcRun run{ctx, db, d_tables, nq, init_count, r, d_bins, d_qt, d_ids, d_count, d_qmm};
+  const std::vector<int64_t> key = {(int64_t)(uintptr_t)db, db->n, (int64_t)(uintptr_t)db->prefix, db->n_prefix,
+                                    (int64_t)(uintptr_t)d_tables, nq, init_count, r, ctx->cand_cap, ctx->sample_div,
+                                    ctx->scan4_engine, ctx->tc_chunk_tiles, (int64_t)(uintptr_t)d_bins,
+                                    (int64_t)(uintptr_t)d_ids, (int64_t)(uintptr_t)d_count, (int64_t)(uintptr_t)d_qt,
+                                    (int64_t)(uintptr_t)d_qmm, (int64_t)(uintptr_t)ctx->h_cnt};
+  static const bool no_graph = getenv("PQS_NO_GRAPH") != nullptr || getenv("PQS_TC_DEBUG") != nullptr;
+  auto& g = ctx->qg;
+  if (!no_graph && g.exec && g.key == key && g.epoch == ctx->scratch_epoch) {
+    // replay: the plan is the captured one (it only depends on the key)
+    PQS_CUDA(ctx, cudaGraphLaunch(g.exec, ctx->stream));
+    ctx->launches += g.launches;
+    run.n = db->n;
+    run.m = db->m;
+    run.cap = std::min<int64_t>(ctx->cand_cap, std::max<int64_t>(db->n, 1));
+    run.r_eff = std::min<int64_t>(r, db->n);
+    run.used_tc = g.used_tc != 0;
+    run.second = g.second != 0;
+    ctx->last_scan_engine = run.used_tc ? 2 : 1;
+    ctx->last_scan_work = g.scan_work;
+    ctx->last_scan_launches = run.second ? 2 : 1;
+    // buffers for a possible host-phase redo (same scratch layout: the epoch matched)
+    PQS_TRY(scratch(ctx, S_THETA, (size_t)(2 * nq), &run.theta));
+    run.theta_main = run.theta + nq;
+    PQS_TRY(scratch(ctx, S_CAND, (size_t)(nq * run.cap), &run.cand));
+    PQS_TRY(scratch(ctx, S_CAND_CNT, (size_t)nq, &run.cnt));
+    if (run.used_tc) {  // the PRMT redo needs the prefix split
+      const int64_t tmin = cdiv(16 * run.r_eff, TILE4);
+      static const int pdiv = getenv("PQS_PREFIX_DIV") ? atoi(getenv("PQS_PREFIX_DIV")) : 4;
+      int64_t st = std::max<int64_t>(cdiv(db->ntiles, ctx->sample_div), std::min<int64_t>(cdiv(db->ntiles, pdiv), 1024 / pdiv));
+      st = std::min<int64_t>(std::max<int64_t>(st, tmin), db->ntiles);
+      run.st = run.n <= run.cap ? 0 : st;
+      run.t1 = run.st > 0 ? run.st : db->ntiles;
+      uint64_t* gk = nullptr;
+      int64_t* gi = nullptr;
+      PQS_TRY(scratch(ctx, S_KEYS, (size_t)(nq * run.cap), &gk));
+      PQS_TRY(scratch(ctx, S_IDS, (size_t)(nq * run.cap), &gi));
+      run.sel.src = SEL_CAND_BIN;
+      run.sel.nq = nq;
+      run.sel.r = r;
+      run.sel.cand = run.cand;
+      run.sel.cand_cnt = run.cnt;
+      run.sel.cap = run.cap;
+      run.sel.ids = db->ids;
+      run.sel.id_base = db->id_base;
+      run.sel.out_b = d_bins;
+      run.sel.out_i = d_ids;
+      run.sel.out_c = d_count;
+      run.sel.gkeys = gk;
+      run.sel.gids = gi;
+      run.sel.gcap = run.cap;
+    }
+  } else if (!no_graph && g.seen == key && g.epoch == ctx->scratch_epoch) {
+    // second identical call (scratch already sized): capture the device phase on the
+    // context's own stream and launch the graph on the caller's stream
+    if (g.exec) {
+      cudaGraphExecDestroy(g.exec);
+      g.exec = nullptr;
+    }
+    cudaStream_t user = ctx->stream;
+    PQS_CUDA(ctx, cudaStreamSynchronize(user));
+    ctx->stream = ctx->own_stream;
+    const int64_t l0 = ctx->launches, e0 = ctx->scratch_epoch;
+    cudaGraph_t graph = nullptr;
+    int rc = PQS_OK;
+    if (cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      rc = PQS_ERR_CUDA;
+    } else {
+      rc = run.device_phase();
+      const cudaError_t ce = cudaStreamEndCapture(ctx->stream, &graph);
+      if (rc == PQS_OK && ce != cudaSuccess) rc = PQS_ERR_CUDA;
+    }
+    ctx->stream = user;
+    cudaGetLastError();
+    if (rc == PQS_OK && graph && ctx->scratch_epoch == e0 &&
+        cudaGraphInstantiate(&g.exec, graph, 0) == cudaSuccess) {
+      g.key = key;
+      g.epoch = ctx->scratch_epoch;
+      g.launches = ctx->launches - l0;
+      g.used_tc = run.used_tc;
+      g.second = run.second;
+      g.scan_work = ctx->last_scan_work;
+      if (graph) cudaGraphDestroy(graph);
+      PQS_CUDA(ctx, cudaGraphLaunch(g.exec, ctx->stream));
+    } else {  // not capturable here: run it directly (and do not try again for this key)
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      g.exec = nullptr;
+      g.seen.clear();
+      ctx->launches = l0;
+      PQS_TRY(run.device_phase());
+    }
+  } else {
+    PQS_TRY(run.device_phase());
+    g.seen = key;
+    g.epoch = ctx->scratch_epoch;
+  }
+  PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return run.host_phase();
 }

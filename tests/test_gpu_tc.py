@@ -65,3 +65,29 @@ def test_tc_odd_sizes(data):
     pr = _search(books, codes[:n], qs[:37], 1, r=20)
     for a, b in zip(tc, pr):
         np.testing.assert_array_equal(a, b)
+
+
+def test_graph_replay_matches_direct(data):
+    """The Quick ADC device phase is captured as a CUDA graph on the second
+    identical call and replayed afterwards: replays with new query batches of
+    the same shape (and host/device io) equal the uncaptured result."""
+    import torch
+
+    books, codes, qs = data
+    pq = P.ProductQuantizer(16, 4, 64, books)
+    ctx = P.Context(0)
+    db = P.DeviceCodes(codes, 4, ctx=ctx)
+    dq = P.DeviceQuantizer(pq, ctx)
+    rng = np.random.default_rng(9)
+    batches = [qs + rng.normal(0, 3, qs.shape).astype(np.float32) for _ in range(4)]
+    got = [db.qadc_search(dq, b, 200, 100, want_tables=True) for b in batches]       # run, capture, replay, replay
+    got.append(db.qadc_search(dq, torch.from_numpy(batches[1]).cuda(), 200, 100, want_tables=True))
+    ref_ctx = P.Context(0)
+    ref_db = P.DeviceCodes(codes, 4, ctx=ref_ctx)
+    ref_dq = P.DeviceQuantizer(pq, ref_ctx)
+    for k, b in enumerate(batches + [batches[1]]):
+        want = ref_db.qadc_search(ref_dq, b, 200, 100, want_tables=True)
+        ref_db = P.DeviceCodes(codes, 4, ctx=ref_ctx)   # new handle: never replays
+        for u, v in zip(got[k], want):
+            u = u.cpu().numpy() if hasattr(u, "cpu") else u
+            np.testing.assert_array_equal(u, v)
