@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
   extern __shared__ __align__(16) unsigned char tsm[];
   float* su = (float*)tsm;                                   // [m*k]
   unsigned int* keys = (unsigned int*)(su + (size_t)m * k);  // [ma*spl]
-  __shared__ unsigned int hist[256];
+  __shared__ KthU32Shared ksh;
   __shared__ unsigned int s_prefix, s_k, s_valid;
   const int64_t q = blockIdx.x;
   for (int i = threadIdx.x; i < m * k; i += blockDim.x) su[i] = U[q * (int64_t)m * k + i];
@@ -350,46 +350,13 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
     if (threadIdx.x == 0) theta[q] = __int_as_float(0x7f800000);
     return;
   }
-  for (int shift = 24; shift >= 0; shift -= 8) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    const unsigned prefix = s_prefix;
-    for (int i = threadIdx.x; i < ns; i += blockDim.x) {
-      const unsigned key = keys[i];
-      if (key == 0xFFFFFFFFu) continue;
-      const bool match = (shift == 24) ? true : ((key ^ prefix) >> (shift + 8)) == 0;
-      if (match) atomicAdd(&hist[(key >> shift) & 255u], 1u);
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {  // lane-parallel digit search: each lane owns 8 bins
-      const int lane = threadIdx.x;
-      unsigned int s8 = 0;
-#pragma unroll
-      for (int bb = 0; bb < 8; ++bb) s8 += hist[lane * 8 + bb];
-      unsigned int incl = s8;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      const unsigned int kk = s_k, excl = incl - s8;
-      if (kk >= excl && kk < incl) {
-        unsigned int cc = excl;
-        int d = lane * 8;
-        for (int bb = 0; bb < 8; ++bb) {
-          const unsigned int h = hist[lane * 8 + bb];
-          if (kk < cc + h) {
-            d = lane * 8 + bb;
-            break;
-          }
-          cc += h;
-        }
-        s_k = kk - cc;
-        s_prefix = prefix | ((unsigned)d << shift);
-      }
-    }
-    __syncthreads();
-  }
+  auto get = [&](int64_t i, unsigned int& v) {
+    v = keys[i];
+    return v != 0xFFFFFFFFu;
+  };
+  const unsigned int kth = block_kth_u32(ns, get, (unsigned)(r - 1), ksh);
+  if (threadIdx.x == 0) s_prefix = kth;
+  __syncthreads();
   if (threadIdx.x == 0) {
     const double t = (double)fkey_inv(s_prefix) + 2.0 * (double)aerr[q];
     float f = (float)t;
@@ -617,8 +584,8 @@ __global__ void __launch_bounds__(CT_THREADS) ivf_cand_theta_kernel(const uint64
                                                                     int r, const float* __restrict__ aerr,
                                                                     uint64_t* __restrict__ out, int* __restrict__ cnt2) {
   __shared__ unsigned int keys[CT_SMEM];
-  __shared__ unsigned int hist[256];
-  __shared__ unsigned int s_prefix, s_k;
+  __shared__ KthU32Shared ksh;
+  __shared__ unsigned int s_prefix;
   __shared__ int s_n;
   const int64_t q = blockIdx.x;
   const int64_t M = min((int64_t)cand_cnt[q], cap);
@@ -628,50 +595,14 @@ __global__ void __launch_bounds__(CT_THREADS) ivf_cand_theta_kernel(const uint64
   float th2 = __int_as_float(0x7f800000);
   if (cand_cnt[q] <= cap && M > r && M <= CT_SMEM) {
     for (int i = threadIdx.x; i < M; i += blockDim.x) keys[i] = fkey(aq[i]);
-    if (threadIdx.x == 0) {
-      s_prefix = 0;
-      s_k = (unsigned)(r - 1);
-    }
     __syncthreads();
-    for (int shift = 24; shift >= 0; shift -= 8) {
-      for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
-      __syncthreads();
-      const unsigned prefix = s_prefix;
-      for (int i = threadIdx.x; i < M; i += blockDim.x) {
-        const unsigned key = keys[i];
-        const bool match = (shift == 24) ? true : ((key ^ prefix) >> (shift + 8)) == 0;
-        if (match) atomicAdd(&hist[(key >> shift) & 255u], 1u);
-      }
-      __syncthreads();
-      if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        unsigned int s8 = 0;
-#pragma unroll
-        for (int bb = 0; bb < 8; ++bb) s8 += hist[lane * 8 + bb];
-        unsigned int incl = s8;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += t;
-        }
-        const unsigned int kk = s_k, excl = incl - s8;
-        if (kk >= excl && kk < incl) {
-          unsigned int cc = excl;
-          int d = lane * 8;
-          for (int bb = 0; bb < 8; ++bb) {
-            const unsigned int h = hist[lane * 8 + bb];
-            if (kk < cc + h) {
-              d = lane * 8 + bb;
-              break;
-            }
-            cc += h;
-          }
-          s_k = kk - cc;
-          s_prefix = prefix | ((unsigned)d << shift);
-        }
-      }
-      __syncthreads();
-    }
+    auto get = [&](int64_t i, unsigned int& v) {
+      v = keys[i];
+      return true;
+    };
+    const unsigned int kth = block_kth_u32(M, get, (unsigned)(r - 1), ksh);
+    if (threadIdx.x == 0) s_prefix = kth;
+    __syncthreads();
     const double t = (double)fkey_inv(s_prefix) + 2.0 * (double)aerr[q];
     float f = (float)t;
     if ((double)f < t) f = nextafterf(f, __int_as_float(0x7f800000));
@@ -1021,7 +952,8 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
   s.gcap = cap;
   PQS_TRY(launch_select(ctx, s));
   // overflow / sanity check against the exact probed totals
-  std::vector<int> hcnt(nq);
+  std::vector<int> hcnt(nq), hcnt2(nq);
+  PQS_CUDA(ctx, cudaMemcpyAsync(hcnt2.data(), cnt2, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
   std::vector<int64_t> hcells(nq * ma);
   PQS_CUDA(ctx, cudaMemcpyAsync(hcnt.data(), cnt, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
   PQS_CUDA(ctx, cudaMemcpyAsync(hcells.data(), cells, sizeof(int64_t) * nq * ma, cudaMemcpyDeviceToHost, ctx->stream));
@@ -1048,6 +980,11 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
   ctx->last_scan_work = (double)total_evals * (double)m;
   ctx->last_max_cand = mx;
   ctx->last_cand_total = ctot;
+  {
+    int64_t rt = 0;
+    for (int64_t q = 0; q < nq; ++q) rt += hcnt2[q];
+    ctx->last_rerank_total = rt;
+  }
   ctx->last_overflow = (int64_t)over.size();
   if (!over.empty()) {
     const int64_t fcap = std::max<int64_t>(worst_total, 1);

@@ -80,6 +80,7 @@ struct pqs_ctx {
   int64_t last_scan_ns = 0;
   int64_t last_scan_launches = 0;
   int64_t last_cand_total = 0;
+  int64_t last_rerank_total = 0;  // candidates left for the exact re-score after tightening
   int64_t last_scan_engine = 0;
   double last_scan_work = 0;
   cudaEvent_t scan_ev[2] = {nullptr, nullptr};

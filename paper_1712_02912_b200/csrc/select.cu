@@ -59,9 +59,16 @@ __device__ __forceinline__ double adc_exact(const float* __restrict__ T, const u
   const int c = (int)(idx % TILE8);
   const uint8_t* base = codes8 + tile * (int64_t)m * TILE8 + c;
   double acc = 0.0;
-  for (int j = 0; j < m; ++j) {
-    const int code = base[(int64_t)j * TILE8];
-    acc = __dadd_rn(acc, (double)__ldg(T + (int64_t)j * k + code));
+  for (int j0 = 0; j0 < m; j0 += 8) {  // 8 components' codes and entries in flight, then the ordered sum
+    int code[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) code[u] = j0 + u < m ? base[(int64_t)(j0 + u) * TILE8] : 0;
+    float t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = j0 + u < m ? __ldg(T + (int64_t)(j0 + u) * k + code[u]) : 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (j0 + u < m) acc = __dadd_rn(acc, (double)t[u]);
   }
   return acc;
 }
