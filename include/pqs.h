@@ -99,6 +99,12 @@ void pqs_pq_destroy(pqs_pq* pq);
  *       default ids = arange(n), scan.py:170-171).                         */
 int pqs_db_create(pqs_ctx* ctx, const uint8_t* codes, int64_t n, int m, int b,
                   const int64_t* ids, int64_t id_base, int io, pqs_db** out);
+/* code list straight from a PQL1 file payload (scan.py:290-359, save_codes):
+ * b_file <= 4 -> (m+1)/2 nibble-packed bytes per code (even component low),
+ * unpacked on the device; 4 < b_file <= 8 -> one byte per component.
+ * layout_b = 4 (Quick ADC, even m, components < 16) or 8 (float ADC).    */
+int pqs_db_create_packed(pqs_ctx* ctx, const uint8_t* payload, int64_t n, int m, int b_file,
+                         int layout_b, const int64_t* ids, int64_t id_base, int io, pqs_db** out);
 /* Quick ADC under sharding: qmax must come from the first init_count codes of
  * the GLOBAL list (quickadc.py:130-137).  Supplies them (uint8 (n_prefix, m)). */
 int pqs_db_set_prefix(pqs_ctx* ctx, pqs_db* db, const uint8_t* prefix_codes, int64_t n_prefix,

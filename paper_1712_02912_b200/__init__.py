@@ -32,6 +32,17 @@ from .scan import (  # noqa: F401
     transpose_blocks,
 )
 from .quantizer import encode  # noqa: F401
+from .formats import (  # noqa: F401
+    FormatError,
+    load_codes,
+    load_codes_device,
+    load_ivf,
+    load_ivf_device,
+    load_quantizer,
+    save_codes,
+    save_ivf,
+    save_quantizer,
+)
 from .quickadc import qadc_block, qadc_scan, quantize, quantize_tables_4bit, quantized_distances  # noqa: F401
 from .ivf import KERNELS, default_r2, query_ivf, query_ivf_batch  # noqa: F401
 from .engine import DeviceCodes, DeviceIvf, DeviceQuantizer, merge_topr  # noqa: F401

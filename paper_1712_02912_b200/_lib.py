@@ -59,6 +59,7 @@ SIGNATURES = {
     "pqs_pq_destroy": (None, [_p]),
     "pqs_db_create": (_i, [_p, _p, _i64, _i, _i, _p, _i64, _i, ctypes.POINTER(_p)]),
     "pqs_db_set_prefix": (_i, [_p, _p, _p, _i64, _i]),
+    "pqs_db_create_packed": (_i, [_p, _p, _i64, _i, _i, _i, _p, _i64, _i, ctypes.POINTER(_p)]),
     "pqs_db_destroy": (None, [_p]),
     "pqs_compute_tables": (_i, [_p, _p, _p, _i64, _p, _i]),
     "pqs_scan_distances": (_i, [_p, _p, _p, _i64, _i, _p, _i]),

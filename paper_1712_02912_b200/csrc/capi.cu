@@ -16,6 +16,7 @@
 int build_db4(pqs_ctx* ctx, pqs_db* db, const uint8_t* d_codes);
 int build_db8(pqs_ctx* ctx, pqs_db* db, const uint8_t* d_codes);
 int device_max_u8(pqs_ctx* ctx, const uint8_t* d, int64_t count, int* out);
+int launch_unpack_nibbles(pqs_ctx* ctx, const uint8_t* d_packed, int64_t n, int m, uint8_t* d_out);
 int launch_encode(pqs_ctx* ctx, const pqs_pq* pq, const float* d_x, int64_t n, const float* d_coarse,
                   const int64_t* d_cells, uint8_t* d_out);
 int launch_quantize(pqs_ctx* ctx, double qmin, double qmax, const double* d_v, int64_t n, uint8_t* d_out);
@@ -364,6 +365,62 @@ int pqs_db_create(pqs_ctx* ctx, const uint8_t* codes, int64_t n, int m, int b, c
   if (tmp) cudaFree(tmp);
   *out = db;
   return PQS_OK;
+}
+
+// code list straight from a PQL1 payload (scan.py:290-359): b_file <= 4 ->
+// nibble-packed (m+1)/2 bytes per code, unpacked on the device; 4 < b_file <= 8
+// -> one byte per component.  layout_b selects the device layout (4 or 8).
+int pqs_db_create_packed(pqs_ctx* ctx, const uint8_t* payload, int64_t n, int m, int b_file, int layout_b,
+                         const int64_t* ids, int64_t id_base, int io, pqs_db** out) {
+  if (!ctx || !out) return PQS_ERR_INVALID;
+  *out = nullptr;
+  PQS_TRY(check_io(ctx, io));
+  PQS_CHECK(ctx, n >= 0 && m >= 1, "bad code list shape");
+  PQS_CHECK(ctx, b_file >= 1 && b_file <= 8, "device code lists hold b <= 8 components");
+  if (b_file > 4) return pqs_db_create(ctx, payload, n, m, layout_b, ids, id_base, io, out);
+  PQS_CUDA(ctx, cudaSetDevice(ctx->device));
+  const size_t pbytes = (size_t)n * ((m + 1) / 2);
+  uint8_t* dp = nullptr;
+  uint8_t* dc = nullptr;
+  if (cudaMalloc(&dc, std::max<size_t>((size_t)n * m, 16)) != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(ctx, PQS_ERR_NOMEM, "unpack allocation failed");
+  }
+  const uint8_t* src = payload;
+  if (io == PQS_IO_HOST && pbytes) {
+    if (cudaMalloc(&dp, pbytes) != cudaSuccess) {
+      cudaFree(dc);
+      cudaGetLastError();
+      return set_err(ctx, PQS_ERR_NOMEM, "staging allocation failed");
+    }
+    int st = upload(ctx, dp, payload, pbytes);
+    if (st != PQS_OK) {
+      cudaFree(dp);
+      cudaFree(dc);
+      return st;
+    }
+    src = dp;
+  }
+  int st = launch_unpack_nibbles(ctx, src, n, m, dc);
+  // ids follow the caller's io; codes are now on the device
+  if (st == PQS_OK && io == PQS_IO_HOST && ids && n) {
+    // pqs_db_create takes one io for codes and ids: stage the ids too
+    int64_t* di = nullptr;
+    if (cudaMalloc(&di, (size_t)n * 8) != cudaSuccess) {
+      st = set_err(ctx, PQS_ERR_NOMEM, "id staging failed");
+    } else {
+      st = upload(ctx, di, ids, (size_t)n * 8);
+      if (st == PQS_OK) st = pqs_db_create(ctx, dc, n, m, layout_b, di, id_base, PQS_IO_DEVICE, out);
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(di);
+    }
+  } else if (st == PQS_OK) {
+    st = pqs_db_create(ctx, dc, n, m, layout_b, ids, id_base, PQS_IO_DEVICE, out);
+  }
+  cudaStreamSynchronize(ctx->stream);
+  if (dp) cudaFree(dp);
+  cudaFree(dc);
+  return st;
 }
 
 int pqs_db_set_prefix(pqs_ctx* ctx, pqs_db* db, const uint8_t* prefix, int64_t n_prefix, int io) {

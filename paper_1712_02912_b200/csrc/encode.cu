@@ -111,7 +111,26 @@ __global__ void build_db8_kernel(const uint8_t* __restrict__ codes, int64_t n, i
   out[o] = i < n ? codes[i * m + j] : (uint8_t)0;
 }
 
+// PQL1 payload with b <= 4 (scan.py:293-316): (m+1)/2 bytes per code, even
+// component in the low nibble, odd component in the high nibble
+__global__ void unpack_nibbles_kernel(const uint8_t* __restrict__ packed, int64_t n, int m,
+                                      uint8_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n * m) return;
+  const int64_t c = i / m;
+  const int j = (int)(i - c * m);
+  const uint8_t v = packed[c * ((m + 1) / 2) + (j >> 1)];
+  out[i] = (j & 1) ? (uint8_t)(v >> 4) : (uint8_t)(v & 15);
+}
+
 }  // namespace
+
+int launch_unpack_nibbles(pqs_ctx* ctx, const uint8_t* d_packed, int64_t n, int m, uint8_t* d_out) {
+  if (n == 0) return PQS_OK;
+  unpack_nibbles_kernel<<<(unsigned)cdiv(n * m, 256), 256, 0, ctx->stream>>>(d_packed, n, m, d_out);
+  PQS_LAUNCHED(ctx);
+  return PQS_OK;
+}
 
 int device_max_u8(pqs_ctx* ctx, const uint8_t* d, int64_t count, int* out) {
   *out = 0;

@@ -233,6 +233,32 @@ def g_encode():
     save("encode.npz", **out)
 
 
+def g_formats():
+    """PQZ1 / PQL1 (b = 4 packed nibbles, b = 8) / IVF1 files written by the reference."""
+    from pqscan import save_codes, save_ivf, save_quantizer
+
+    rng = np.random.default_rng(707)
+    x = mixture(rng, 3000, 32, 8, 128.0, 16.0, 0.0, 255.0)
+    pq8 = train_pq(x[:2000], 4, 8, TrainConfig(kmeans_iters=2, seed=4))
+    pq4 = train_pq(x[:2000], 8, 4, TrainConfig(kmeans_iters=2, seed=5))
+    save_quantizer(os.path.join(OUT, "fmt_pq8.pqz"), pq8)
+    save_quantizer(os.path.join(OUT, "fmt_pq4.pqz"), pq4)
+    c8 = encode(pq8, x[:777])
+    c4 = encode(pq4, x[:555])
+    ids = rng.permutation(5000)[:777].astype(np.int64)
+    save_codes(os.path.join(OUT, "fmt_codes8.pql"), CodeList(c8, ids), 8)
+    save_codes(os.path.join(OUT, "fmt_codes4.pql"), CodeList(c4), 4)
+    c3 = rng.integers(0, 8, (101, 5)).astype(np.uint8)             # odd m, b = 3 (nibble packed)
+    save_codes(os.path.join(OUT, "fmt_codes3.pql"), CodeList(c3), 3)
+    idx = build_ivf(x[:2500], K=16, m=4, b=8, cfg=TrainConfig(kmeans_iters=2, seed=6))
+    save_ivf(os.path.join(OUT, "fmt_index.ivf"), idx)
+    save("formats.npz", pq8_books=pq8.codebooks, pq4_books=pq4.codebooks, codes8=c8, ids8=ids, codes4=c4, codes3=c3,
+         ivf_coarse=idx.coarse, ivf_books=idx.pq.codebooks,
+         ivf_sizes=np.array([l.n for l in idx.lists], np.int64),
+         ivf_codes=np.concatenate([l.codes for l in idx.lists]),
+         ivf_ids=np.concatenate([l.ids for l in idx.lists]))
+
+
 if __name__ == "__main__":
     print("pqscan from", pqscan.__file__)
     g_tables()
@@ -241,3 +267,4 @@ if __name__ == "__main__":
     g_quantize()
     g_ivf()
     g_encode()
+    g_formats()
