@@ -53,7 +53,9 @@ def query_ivf(index: IvfIndex, query: np.ndarray, ma: int, r: int, kernel: str =
     if kernel != "adc":
         raise NotImplementedError(f"kernel={kernel!r} is outside the device ADC scan path")
     dev = device_index(index)
-    d, i, c = dev.search(query.astype(np.float32)[None, :], int(ma), int(r))
+    from .quantizer import as_f32_exact
+
+    d, i, c = dev.search(as_f32_exact(query, "query_ivf")[None, :], int(ma), int(r))
     n = int(c[0])
     return NeighborSet.from_pairs(r, d[0, :n], i[0, :n])
 

@@ -41,7 +41,9 @@ def compute_tables(pq: ProductQuantizer, query: np.ndarray) -> LookupTables:
     if query.ndim != 1 or query.shape[0] != pq.d:
         raise ValueError(f"query must have shape ({pq.d},)")
     dq = _device_quantizer(pq)
-    return LookupTables(dq.compute_tables(query.astype(np.float32)[None, :])[0])
+    from .quantizer import as_f32_exact
+
+    return LookupTables(dq.compute_tables(as_f32_exact(query, "compute_tables")[None, :])[0])
 
 
 def compute_tables_batch(pq: ProductQuantizer, queries: np.ndarray) -> np.ndarray:
