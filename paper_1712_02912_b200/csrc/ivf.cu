@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
   extern __shared__ __align__(16) unsigned char tsm[];
   float* su = (float*)tsm;                                   // [m*k]
   unsigned int* keys = (unsigned int*)(su + (size_t)m * k);  // [ma*spl]
-  __shared__ KthU32Shared ksh;
+  __shared__ unsigned int hist[256];
   __shared__ unsigned int s_prefix, s_k, s_valid;
   const int64_t q = blockIdx.x;
   for (int i = threadIdx.x; i < m * k; i += blockDim.x) su[i] = U[q * (int64_t)m * k + i];
@@ -350,13 +350,46 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
     if (threadIdx.x == 0) theta[q] = __int_as_float(0x7f800000);
     return;
   }
-  auto get = [&](int64_t i, unsigned int& v) {
-    v = keys[i];
-    return v != 0xFFFFFFFFu;
-  };
-  const unsigned int kth = block_kth_u32(ns, get, (unsigned)(r - 1), ksh);
-  if (threadIdx.x == 0) s_prefix = kth;
-  __syncthreads();
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const unsigned prefix = s_prefix;
+    for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+      const unsigned key = keys[i];
+      if (key == 0xFFFFFFFFu) continue;
+      const bool match = (shift == 24) ? true : ((key ^ prefix) >> (shift + 8)) == 0;
+      if (match) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // lane-parallel digit search: each lane owns 8 bins
+      const int lane = threadIdx.x;
+      unsigned int s8 = 0;
+#pragma unroll
+      for (int bb = 0; bb < 8; ++bb) s8 += hist[lane * 8 + bb];
+      unsigned int incl = s8;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const unsigned int kk = s_k, excl = incl - s8;
+      if (kk >= excl && kk < incl) {
+        unsigned int cc = excl;
+        int d = lane * 8;
+        for (int bb = 0; bb < 8; ++bb) {
+          const unsigned int h = hist[lane * 8 + bb];
+          if (kk < cc + h) {
+            d = lane * 8 + bb;
+            break;
+          }
+          cc += h;
+        }
+        s_k = kk - cc;
+        s_prefix = prefix | ((unsigned)d << shift);
+      }
+    }
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
     const double t = (double)fkey_inv(s_prefix) + 2.0 * (double)aerr[q];
     float f = (float)t;
@@ -409,15 +442,15 @@ __global__ void pair_fill_kernel(const int64_t* __restrict__ cells, const double
   pa[o] = (float)pdist[i];
 }
 
-// One CTA per inverted list; the queries probing it are processed 16 at a
-// time ("slots"): their U tables are staged in shared memory interleaved as
-// [j*k + entry][slot] (row stride 17 words), a half-warp evaluates one code
-// for all 16 slots (lane = slot, the code's bytes are a broadcast read), so
-// the 16 lookups of one table row hit 16 consecutive banks.  Survivors are
+// One CTA per inverted list (two resident per SM); the queries probing it are
+// processed 8 at a time ("slots"): their U tables are staged in shared memory
+// interleaved as [j*k + entry][slot] (row stride 9 words), a quarter-warp
+// evaluates one code for all 8 slots (lane = slot, the code's bytes are a
+// broadcast read), so the 8 lookups of one table row hit 8 consecutive banks.  Survivors are
 // staged per slot in shared memory and appended to the query's candidate
 // list with one global reservation per (list, slot).
-constexpr int LQ = 16;
-constexpr int LROW = 17;           // padded row stride (words) of the slot-interleaved tables
+constexpr int LQ = 8;
+constexpr int LROW = LQ + 1;       // padded row stride (words) of the slot-interleaved tables
 constexpr int LIST_THREADS = 512;
 constexpr int LCH = 1024;          // codes per chunk
 constexpr int LSTAGE = 256;        // staged survivors per slot
@@ -443,7 +476,7 @@ __device__ __forceinline__ void cp_async4_stream(void* smem, const void* gmem, u
 }
 
 template <int MT, int KT>  // compile-time (m, k), or (0, 0) for runtime values
-__global__ void __launch_bounds__(LIST_THREADS) ivf_list_kernel(
+__global__ void __launch_bounds__(LIST_THREADS, 2) ivf_list_kernel(
     const float* __restrict__ U, const int64_t* __restrict__ starts, const int* __restrict__ pq,
     const float* __restrict__ pa, const int64_t* __restrict__ offsets, const uint8_t* __restrict__ codes,
     const float* __restrict__ V, int m_rt, int k_rt, const float* __restrict__ theta, uint64_t* __restrict__ cand,
@@ -466,7 +499,7 @@ __global__ void __launch_bounds__(LIST_THREADS) ivf_list_kernel(
   const int mk = m * k;
   const int mw = (m + 3) / 4;   // code words per code
   const int slot = threadIdx.x & (LQ - 1);
-  const int hw = threadIdx.x >> 4, nhw = blockDim.x >> 4;
+  const int hw = threadIdx.x / LQ, nhw = blockDim.x / LQ;
   const float* su_s = su + slot;
   for (int64_t g0 = p0; g0 < p1; g0 += LQ) {
     const int ns = (int)min((int64_t)LQ, p1 - g0);
@@ -584,8 +617,8 @@ __global__ void __launch_bounds__(CT_THREADS) ivf_cand_theta_kernel(const uint64
                                                                     int r, const float* __restrict__ aerr,
                                                                     uint64_t* __restrict__ out, int* __restrict__ cnt2) {
   __shared__ unsigned int keys[CT_SMEM];
-  __shared__ KthU32Shared ksh;
-  __shared__ unsigned int s_prefix;
+  __shared__ unsigned int hist[256];
+  __shared__ unsigned int s_prefix, s_k;
   __shared__ int s_n;
   const int64_t q = blockIdx.x;
   const int64_t M = min((int64_t)cand_cnt[q], cap);
@@ -595,14 +628,50 @@ __global__ void __launch_bounds__(CT_THREADS) ivf_cand_theta_kernel(const uint64
   float th2 = __int_as_float(0x7f800000);
   if (cand_cnt[q] <= cap && M > r && M <= CT_SMEM) {
     for (int i = threadIdx.x; i < M; i += blockDim.x) keys[i] = fkey(aq[i]);
+    if (threadIdx.x == 0) {
+      s_prefix = 0;
+      s_k = (unsigned)(r - 1);
+    }
     __syncthreads();
-    auto get = [&](int64_t i, unsigned int& v) {
-      v = keys[i];
-      return true;
-    };
-    const unsigned int kth = block_kth_u32(M, get, (unsigned)(r - 1), ksh);
-    if (threadIdx.x == 0) s_prefix = kth;
-    __syncthreads();
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      const unsigned prefix = s_prefix;
+      for (int i = threadIdx.x; i < M; i += blockDim.x) {
+        const unsigned key = keys[i];
+        const bool match = (shift == 24) ? true : ((key ^ prefix) >> (shift + 8)) == 0;
+        if (match) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        unsigned int s8 = 0;
+#pragma unroll
+        for (int bb = 0; bb < 8; ++bb) s8 += hist[lane * 8 + bb];
+        unsigned int incl = s8;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const unsigned int kk = s_k, excl = incl - s8;
+        if (kk >= excl && kk < incl) {
+          unsigned int cc = excl;
+          int d = lane * 8;
+          for (int bb = 0; bb < 8; ++bb) {
+            const unsigned int h = hist[lane * 8 + bb];
+            if (kk < cc + h) {
+              d = lane * 8 + bb;
+              break;
+            }
+            cc += h;
+          }
+          s_k = kk - cc;
+          s_prefix = prefix | ((unsigned)d << shift);
+        }
+      }
+      __syncthreads();
+    }
     const double t = (double)fkey_inv(s_prefix) + 2.0 * (double)aerr[q];
     float f = (float)t;
     if ((double)f < t) f = nextafterf(f, __int_as_float(0x7f800000));

@@ -419,7 +419,7 @@ int launch_scan8(pqs_ctx* ctx, Scan8Args a) {
 __global__ void theta8_kernel(const uint32_t* __restrict__ sample, int64_t ns, int r, int m,
                               const int* __restrict__ e0, const double* __restrict__ slack, int* __restrict__ e1,
                               uint32_t* __restrict__ theta) {
-  __shared__ seldev::KthU32Shared ksh;
+  __shared__ unsigned int hist[256];
   __shared__ unsigned int s_prefix, s_k, s_valid;
   const int64_t q = blockIdx.x;
   const uint32_t* row = sample + q * ns;
@@ -440,13 +440,29 @@ __global__ void theta8_kernel(const uint32_t* __restrict__ sample, int64_t ns, i
     }
     return;
   }
-  auto get = [&](int64_t i, unsigned int& v) {
-    v = row[i];
-    return v != 0xFFFFFFFFu;
-  };
-  const unsigned int kth = seldev::block_kth_u32(ns, get, (unsigned)(r - 1), ksh);
-  if (threadIdx.x == 0) s_prefix = kth;
-  __syncthreads();
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const unsigned prefix = s_prefix;
+    for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
+      const uint32_t v = row[i];
+      if (v == 0xFFFFFFFFu) continue;
+      const bool match = (shift == 24) ? true : ((v ^ prefix) >> (shift + 8)) == 0;
+      if (match) atomicAdd(&hist[(v >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned c = 0, kk = s_k;
+      int d = 0;
+      for (; d < 256; ++d) {
+        if (kk < c + hist[d]) break;
+        c += hist[d];
+      }
+      s_k = kk - c;
+      s_prefix = prefix | ((unsigned)d << shift);
+    }
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
     const double Dp = ldexp((double)s_prefix + (double)m, -e0[q]) + slack[q];
     const double target = 65536.0 * (m > 8 ? m / 8.0 : 1.0);

@@ -188,105 +188,4 @@ static __device__ void bitonic_sort(uint64_t* K, int64_t* I, int P) {
 }
 
 
-// ---------------------------------------------------------------------------
-// k-th smallest (0-based) of the valid u32 keys of a block: get(i, v) -> bool
-// (valid) for i < M.  MSD radix select with 8-bit digits starting at the
-// highest bit where the keys differ (min/max pass), warp-aggregated shared
-// histogram updates (__match_any_sync: a skewed digit costs one atomic per
-// warp, not 32) into 8 sub-histograms, lane-parallel digit search.  Requires
-// k < number of valid keys; every thread of the block must call it.
-struct KthU32Shared {
-  unsigned int wh[8][256];
-  unsigned int red[SEL_MAX_WARPS][2];
-  unsigned int prefix, k, vmin, vmax;
-};
-
-template <class Get>
-__device__ unsigned int block_kth_u32(int64_t M, Get get, unsigned int k, KthU32Shared& sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  unsigned int lo = 0xFFFFFFFFu, hi = 0u;
-  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
-    unsigned int v;
-    if (get(i, v)) {
-      lo = min(lo, v);
-      hi = max(hi, v);
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-  }
-  if (lane == 0) {
-    sh.red[warp][0] = lo;
-    sh.red[warp][1] = hi;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned int a = 0xFFFFFFFFu, b = 0u;
-    for (int w = 0; w < nw; ++w) {
-      a = min(a, sh.red[w][0]);
-      b = max(b, sh.red[w][1]);
-    }
-    sh.vmin = a;
-    sh.vmax = b;
-    sh.k = k;
-  }
-  __syncthreads();
-  const unsigned int vmin = sh.vmin, vmax = sh.vmax;
-  if (vmin == vmax) return vmin;
-  const int hib = 31 - __clz((int)(vmin ^ vmax));
-  int shift = (hib / 8) * 8;
-  if (threadIdx.x == 0) sh.prefix = shift + 8 >= 32 ? 0u : (vmin >> (shift + 8)) << (shift + 8);
-  __syncthreads();
-  for (; shift >= 0; shift -= 8) {
-    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&sh.wh[0][0])[i] = 0;
-    __syncthreads();
-    const unsigned int prefix = sh.prefix;
-    unsigned int* h = sh.wh[warp & 7];
-    for (int64_t base = 0; base < M; base += blockDim.x) {
-      const int64_t i = base + threadIdx.x;
-      unsigned int v = 0;
-      bool ok = i < M && get(i, v);
-      ok = ok && (shift + 8 >= 32 || ((v ^ prefix) >> (shift + 8)) == 0);
-      const unsigned int d = ok ? (v >> shift) & 255u : 256u;
-      const unsigned int grp = __match_any_sync(0xffffffffu, d);
-      if (ok && lane == __ffs(grp) - 1) atomicAdd(&h[d], (unsigned int)__popc(grp));
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {  // lane-parallel digit search: each lane owns 8 bins
-      unsigned int c8[8], s8 = 0;
-#pragma unroll
-      for (int bb = 0; bb < 8; ++bb) {
-        unsigned int t = 0;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) t += sh.wh[w][lane * 8 + bb];
-        c8[bb] = t;
-        s8 += t;
-      }
-      unsigned int incl = s8;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      const unsigned int kk = sh.k, excl = incl - s8;
-      if (kk >= excl && kk < incl) {
-        unsigned int cc = excl;
-        int d = lane * 8;
-        for (int bb = 0; bb < 8; ++bb) {
-          if (kk < cc + c8[bb]) {
-            d = lane * 8 + bb;
-            break;
-          }
-          cc += c8[bb];
-        }
-        sh.k = kk - cc;
-        sh.prefix = prefix | ((unsigned int)d << shift);
-      }
-    }
-    __syncthreads();
-  }
-  return sh.prefix;
-}
-
 }  // namespace seldev
