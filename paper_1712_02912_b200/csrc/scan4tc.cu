@@ -34,8 +34,10 @@ namespace {
 constexpr int TC_M = 128;          // codes per tile (TMEM lanes)
 constexpr int TC_N = 256;          // queries per group (TMEM columns per accumulator)
 constexpr int TC_K = 256;          // one-hot width (16 components x 16 values)
-constexpr int A_BYTES = TC_M * TC_K;     // 32 KB
-constexpr int B_BYTES = TC_N * TC_K;     // 64 KB
+constexpr int TC_KB = TC_K + 32;   // + one K step carrying the per-query threshold (A: ones, B: -(theta+1))
+constexpr int A_BYTES = TC_M * TC_KB;    // 36 KB
+constexpr int B_BYTES = TC_N * TC_KB;    // 72 KB per 256-query group
+constexpr int B_ONEHOT_BYTES = TC_N * TC_K;  // its first 64 KB: the quantized tables
 constexpr int LBO_A = (TC_M / 8) * 128;  // byte distance between K-chunks of A (2048)
 constexpr int LBO_B = (TC_N / 8) * 128;  // ... of B (4096)
 constexpr int TC_THREADS = 13 * 32;      // 8 epilogue + 4 producer + 1 MMA warp
@@ -110,7 +112,8 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
 }
 
 // instruction descriptor: u8 x u8 -> s32, K-major A and B, M=128, N=256
-constexpr uint32_t IDESC = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(TC_N >> 3) << 17) |
+// A unsigned (one-hot), B signed (tables <= 127 and the negative threshold column)
+constexpr uint32_t IDESC = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(TC_N >> 3) << 17) |
                            ((uint32_t)(TC_M >> 4) << 24);
 
 __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate) {
@@ -148,7 +151,7 @@ struct Scan4TcArgs {
   const uint32_t* words;   // 4-bit quad layout (mp = 16: 8 words per quad)
   int64_t n;
   const uint8_t* bglob;    // [nqg][B_BYTES] canonical B tiles
-  const int* nthr;         // [nqg][128] packed per-column-pair biases (build_bias_kernel)
+  const uint16_t* nadd;    // [nqg][256] per column: S = D + nadd (the threshold folded into B, build_bias_kernel)
   int64_t nq, nqg, ntiles; // ntiles of TC_M codes in this launch's range
   int64_t tile0;           // first tile of the range
   uint64_t* rec;           // [gridDim][rec_cap] (q << 40 | bin << 32 | idx)
@@ -167,8 +170,8 @@ __device__ __forceinline__ unsigned long long gtime() {
 __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smtc[];
   uint8_t* sB = smtc;                           // 64 KB (one query group)
-  uint8_t* sA = smtc + B_BYTES;                 // 2 x 32 KB
-  uint32_t* sTh = reinterpret_cast<uint32_t*>(smtc + B_BYTES + 2 * A_BYTES);  // [2 buffers][128] biases
+  uint8_t* sA = smtc + B_BYTES;                 // 2 x 36 KB
+  uint16_t* sAdd = reinterpret_cast<uint16_t*>(smtc + B_BYTES + 2 * A_BYTES);  // [2 buffers][256]
   uint32_t* stage = reinterpret_cast<uint32_t*>(smtc + B_BYTES + 2 * A_BYTES + 2 * TC_N * 2);
   __shared__ __align__(8) uint64_t bar_b[2], bar_afull[2], bar_aempty[2], bar_accfull[2], bar_accempty[2];
   __shared__ uint32_t s_tmem;
@@ -224,7 +227,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
             }
             mbar_expect_tx(&bar_b[bb], (uint32_t)(B_BYTES + TC_N * 2));
             bulk_g2s(sB, a.bglob + g * (int64_t)B_BYTES, B_BYTES, &bar_b[bb]);
-            bulk_g2s(sTh + bb * (TC_N / 2), a.nthr + g * (TC_N / 2), TC_N * 2, &bar_b[bb]);
+            bulk_g2s(sAdd + bb * TC_N, a.nadd + g * TC_N, TC_N * 2, &bar_b[bb]);
             mbar_wait(&bar_b[bb], 0);
             cur_g = g;
           }
@@ -240,7 +243,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
           const uint32_t a_base = smem_u32(sA + ab * A_BYTES);
           const uint32_t b_base = smem_u32(sB);
 #pragma unroll
-          for (int s = 0; s < TC_K / 32; ++s) {
+          for (int s = 0; s < TC_KB / 32; ++s) {
             const uint64_t da = make_desc(a_base + (uint32_t)(2 * s) * LBO_A, LBO_A, 128);
             const uint64_t db = make_desc(b_base + (uint32_t)(2 * s) * LBO_B, LBO_B, 128);
             mma_i8(d_tmem, da, db, s > 0 ? 1u : 0u);
@@ -253,6 +256,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
       // ---------------- one-hot producers: thread = code row ----------------
       const int row = (warp - EPI_WARPS) * 32 + lane;  // 0..127
       const uint32_t row_off = (uint32_t)(row >> 3) * 128u + (uint32_t)(row & 7) * 16u;
+      // threshold K step (chunks 16, 17): ones against B's -(theta+1) column block; constant per row
+      for (int bufi = 0; bufi < 2; ++bufi) {
+        *reinterpret_cast<uint4*>(sA + bufi * A_BYTES + row_off + 16 * LBO_A) =
+            make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+        *reinterpret_cast<uint4*>(sA + bufi * A_BYTES + row_off + 17 * LBO_A) = make_uint4(0u, 0u, 0u, 0u);
+      }
       for (int64_t w = w0; w < w1; ++w) {
         const int64_t it = w - w0;
         const int ab = (int)(it & 1);
@@ -337,55 +346,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
         tc_fence_after();
         const int64_t tile = a.tile0 + tile_of(w);
         const bool cvalid = tile * TC_M + row < a.n;
-        const uint32_t* bias = sTh + (gi & 1) * (TC_N / 2);
+        const uint16_t* nadd = sAdd + (gi & 1) * TC_N;
         const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(ab * TC_N);
         const uint32_t itag = (uint32_t)it << 15;
 #pragma unroll 1
         for (int c0 = half * (TC_N / 2); c0 < (half + 1) * (TC_N / 2) && !(a.dbg_mode & 1); c0 += 64) {
           uint32_t v[64];
           TMEM_LD64(tbase + (uint32_t)c0, v);
-          uint32_t bs[32];
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            const uint4 b4 = *reinterpret_cast<const uint4*>(bias + c0 / 2 + i);  // broadcast
-            bs[i] = b4.x;
-            bs[i + 1] = b4.y;
-            bs[i + 2] = b4.z;
-            bs[i + 3] = b4.w;
-          }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          // D = S - (theta + 1) per query column: a survivor is a negative D
+          uint32_t orv = 0;
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {  // two 32-column halves of the load
-            const int cc = c0 + 32 * hh;
-            uint32_t x[16];
-            uint32_t allm = 0xFFFFFFFFu;
+          for (int i = 0; i < 64; ++i) orv |= v[i];
+          if ((orv & 0x80000000u) && cvalid) {  // lane-local, rare
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              // two query columns per word (S <= 2032 fits 16 bits); bit 15 clear <=> S <= theta
-              x[i] = __byte_perm(v[32 * hh + 2 * i], v[32 * hh + 2 * i + 1], 0x5410) + bs[16 * hh + i];
-              allm &= x[i];
-            }
-            if ((allm & 0x80008000u) != 0x80008000u && cvalid) {  // lane-local, rare
-              // hit mask: bit i <- column 2i, bit 16+i <- column 2i+1 (flag = bit 15 clear);
-              // the packed words go to a per-thread stash for the dynamic reads below
+            for (int hh = 0; hh < 2; ++hh) {  // two 32-column halves of the load
+              const int cc = c0 + 32 * hh;
+              // hit mask: bit i <- column cc+2i, bit 16+i <- column cc+2i+1 (sign of D, |D| < 2^15);
+              // the packed D pairs go to a per-thread stash for the dynamic reads below
               uint32_t mask = 0;
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
-                mask |= (~x[i] >> (15 - i)) & (0x00010001u << i);
-                my_x[i * (EPI_WARPS * 32)] = x[i];
+                const uint32_t x = __byte_perm(v[32 * hh + 2 * i], v[32 * hh + 2 * i + 1], 0x5410);
+                mask |= (x >> (15 - i)) & (0x00010001u << i);
+                my_x[i * (EPI_WARPS * 32)] = x;
               }
               const uint32_t base = itag | ((uint32_t)cc << 7);
               while (mask) {
-                const int b = __ffs(mask) - 1;
+                const int bi = __ffs(mask) - 1;
                 mask &= mask - 1;
-                const int i = b & 15, h = b >> 4;
-                const uint32_t pk = my_x[i * (EPI_WARPS * 32)] - bias[cc / 2 + i];  // packed sums (no lane carry)
-                const uint32_t S = (pk >> (16 * h)) & 0xFFFFu;
+                const int i = bi & 15, h = bi >> 4;
+                const int col = cc + 2 * i + h;
+                const int D = (int)(int16_t)(my_x[i * (EPI_WARPS * 32)] >> (16 * h));
+                const uint32_t S = (uint32_t)(D + (int)nadd[col]);
                 my_stage[ncand * (EPI_WARPS * 32)] = base + ((uint32_t)(2 * i + h) << 7) + min(S, 127u);
                 ++ncand;
               }
+              if (ncand > ESTAGE - 32) flush();  // rare
             }
-            if (ncand > ESTAGE - 32) flush();  // rare
           }
         }
         tc_fence_before();
@@ -447,8 +445,8 @@ __device__ __forceinline__ void mma_i8_h(uint32_t tmem_d, uint64_t da, uint64_t 
 __global__ void __launch_bounds__(H_THREADS, 1) scan4tc_hist_kernel(HistTcArgs a) {
   extern __shared__ __align__(1024) uint8_t smh[];
   uint8_t* sG = smh;                                    // 64 KB: query tables of one group
-  uint8_t* sO = smh + B_BYTES;                          // 64 KB: one-hot of 256 codes
-  unsigned int* hist = reinterpret_cast<unsigned int*>(smh + B_BYTES + HO_BYTES);  // [64][256]
+  uint8_t* sO = smh + B_ONEHOT_BYTES;                   // 64 KB: one-hot of 256 codes
+  unsigned int* hist = reinterpret_cast<unsigned int*>(smh + B_ONEHOT_BYTES + HO_BYTES);  // [64][256]
   __shared__ __align__(8) uint64_t bar_g, bar_ofull, bar_oempty, bar_accfull[2], bar_accempty[2];
   __shared__ uint32_t s_tmem;
 
@@ -490,8 +488,8 @@ __global__ void __launch_bounds__(H_THREADS, 1) scan4tc_hist_kernel(HistTcArgs a
           if (g != cur_g) {
             ++gi;
             if (it > 0) mbar_wait(&bar_oempty, (uint32_t)((it - 1) & 1));  // all MMAs on the old tables done
-            mbar_expect_tx(&bar_g, (uint32_t)B_BYTES);
-            bulk_g2s(sG, a.bglob + g * (int64_t)B_BYTES, B_BYTES, &bar_g);
+            mbar_expect_tx(&bar_g, (uint32_t)B_ONEHOT_BYTES);
+            bulk_g2s(sG, a.bglob + g * (int64_t)B_BYTES, B_ONEHOT_BYTES, &bar_g);
             mbar_wait(&bar_g, (uint32_t)(gi & 1));
             cur_g = g;
           }
@@ -624,19 +622,32 @@ __global__ void build_b_kernel(const uint8_t* __restrict__ qt, int64_t nq, int m
   *reinterpret_cast<uint4*>(bglob + g * (int64_t)B_BYTES + (int64_t)j * LBO_B + (n >> 3) * 128 + (n & 7) * 16) = v;
 }
 
-// packed 16-bit lane biases of the column pair (2i, 2i+1): S + (0x7FFF - theta)
-// has bit 15 clear iff S <= theta; padding queries and THETA_NONE (255) get
-// 0x8000 (never clear)
-__global__ void build_bias_kernel(const uint8_t* __restrict__ theta, int64_t nq, int64_t npairs,
-                                  int* __restrict__ nthr) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= npairs) return;
-  const int64_t q0 = 2 * i, q1 = q0 + 1;
-  const uint32_t t0 = q0 < nq ? theta[q0] : 255u, t1 = q1 < nq ? theta[q1] : 255u;
-  // 127 admits every sum (bin = min(S, 127)): bias 0 keeps bit 15 clear
-  const uint32_t b0 = t0 == 255u ? 0x8000u : (t0 == 127u ? 0u : 0x7FFFu - t0);
-  const uint32_t b1 = t1 == 255u ? 0x8000u : (t1 == 127u ? 0u : 0x7FFFu - t1);
-  nthr[i] = (int)(b0 | (b1 << 16));
+// The threshold K step of every group's B tile (chunks 16, 17) and the
+// per-column offset back to S: D = S + sum_t B[n][256 + t] with the A side all
+// ones over t < 16 -- theta <= 126: -(theta + 1) (D < 0 <=> S <= theta);
+// theta 127 admits every sum: -2048 (16 x -128 <= -S for S <= 2032);
+// THETA_NONE (255) and padding queries: 0 (D >= 0, never a survivor).
+__global__ void build_bias_kernel(const uint8_t* __restrict__ theta, int64_t nq, int64_t nqg,
+                                  uint8_t* __restrict__ bglob, uint16_t* __restrict__ nadd) {
+  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // one per (group, n)
+  if (gid >= nqg * TC_N) return;
+  const int n = (int)(gid % TC_N);
+  const int64_t g = gid / TC_N;
+  const int64_t q = g * TC_N + n;
+  const uint32_t t = q < nq ? theta[q] : 255u;
+  uint32_t w0 = 0, wrest = 0, add = 0;
+  if (t == 127u) {
+    w0 = 0x80808080u;
+    wrest = 0x80808080u;
+    add = 2048;
+  } else if (t != 255u) {
+    w0 = (uint32_t)(uint8_t)(int8_t)(-(int)(t + 1));
+    add = t + 1;
+  }
+  uint8_t* dst = bglob + g * (int64_t)B_BYTES + (n >> 3) * 128 + (n & 7) * 16;
+  *reinterpret_cast<uint4*>(dst + 16 * LBO_B) = make_uint4(w0, wrest, wrest, wrest);
+  *reinterpret_cast<uint4*>(dst + 17 * LBO_B) = make_uint4(0u, 0u, 0u, 0u);
+  nadd[gid] = (uint16_t)add;
 }
 
 // per-CTA survivor records -> per-query candidate lists (bin << 32 | idx).
@@ -727,11 +738,11 @@ int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const u
     if (nqg > 1 && cdiv(total, std::min<int64_t>(nctas_max, total)) >= ntiles) return PQS_ERR_UNSUPPORTED;
   }
   uint8_t* bglob = nullptr;
-  int* nthr = nullptr;
+  uint16_t* nadd = nullptr;
   uint64_t* rec = nullptr;
   int* rec_cnt = nullptr;
   PQS_TRY(scratch(ctx, S_TC_B, (size_t)(nqg * B_BYTES), &bglob));
-  PQS_TRY(scratch(ctx, S_TC_TH, (size_t)(nqg * TC_N / 2), &nthr));
+  PQS_TRY(scratch(ctx, S_TC_TH, (size_t)(nqg * TC_N), &nadd));
   // survivors per CTA: expect ~nq*cap_used/nctas; size generously
   const int64_t rec_cap = std::max<int64_t>(1 << 16, cdiv(nq * std::min<int64_t>(cap, 8192), nctas_max) * 2);
   PQS_TRY(scratch(ctx, S_TC_REC, (size_t)(nctas_max * rec_cap), &rec));
@@ -740,7 +751,7 @@ int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const u
     build_b_kernel<<<(unsigned)cdiv(nqg * TC_N * 16, 256), 256, 0, ctx->stream>>>(d_qt, nq, db->m, nqg, bglob);
     PQS_LAUNCHED(ctx);
   }
-  build_bias_kernel<<<(unsigned)cdiv(nqg * TC_N / 2, 256), 256, 0, ctx->stream>>>(d_theta, nq, nqg * TC_N / 2, nthr);
+  build_bias_kernel<<<(unsigned)cdiv(nqg * TC_N, 256), 256, 0, ctx->stream>>>(d_theta, nq, nqg, bglob, nadd);
   PQS_LAUNCHED(ctx);
   const size_t smem =
       (size_t)B_BYTES + 2 * (size_t)A_BYTES + 2 * TC_N * 2 + (size_t)(ESTAGE + 16) * EPI_WARPS * 32 * 4;
@@ -757,7 +768,7 @@ int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const u
     a.words = db->words4;
     a.n = db->n;
     a.bglob = bglob;
-    a.nthr = nthr;
+    a.nadd = nadd;
     a.nq = nq;
     a.nqg = nqg;
     a.ntiles = ntiles;
@@ -810,7 +821,7 @@ int launch_hist_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, int64_t 
   a.nqg = nqg;
   a.ntiles = ntiles;
   a.ghist = ghist;
-  const size_t smem = (size_t)B_BYTES + HO_BYTES + (size_t)H_PAIRS * TC_N * 4;
+  const size_t smem = (size_t)B_ONEHOT_BYTES + HO_BYTES + (size_t)H_PAIRS * TC_N * 4;
   PQS_CUDA(ctx, cudaFuncSetAttribute(scan4tc_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t nctas = std::min<int64_t>((int64_t)ctx->sm_count, total);
   scan4tc_hist_kernel<<<(unsigned)nctas, H_THREADS, smem, ctx->stream>>>(a);
