@@ -166,6 +166,14 @@ int pqs_ivf_probe(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_
                   int64_t* out_cells, double* out_dist, int io);
 int pqs_ivf_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_t nq, int ma,
                    int r, double* out_dist, int64_t* out_ids, int32_t* out_count, int io);
+/* ---- query_ivf kernel='quick-adc' (ivf.py:185-190): per probed list the
+ * Quick ADC scan (quickadc.py:104-141, init_count = min(init_count, list
+ * size)), its r best by (bin, id) rescaled (quickadc.py:50-54) and merged by
+ * (distance, id).  b == 4, even m <= 64; init_count >= 1.  Outputs as
+ * pqs_ivf_search (out_dist = rescaled fp64 distances).                    */
+int pqs_ivf_qadc_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_t nq,
+                        int ma, int r, int init_count, double* out_dist, int64_t* out_ids,
+                        int32_t* out_count, int io);
 
 /* ---- encode (quantizer.py:308-325, nearest _dist.py:24-39): per sub-space
  * the nearest centroid by the fp64 cdist sum, ties to the lowest index.

@@ -320,9 +320,11 @@ def encode(codebooks: np.ndarray, x: np.ndarray, coarse: np.ndarray | None = Non
 
 
 def query_ivf(coarse: np.ndarray, codebooks: np.ndarray, lists_codes, lists_ids,
-              query: np.ndarray, ma: int, r: int):
-    """ivf.py:148-196, kernel='adc': probe the ma nearest cells, scan each
-    list against the fp64 residual's tables, merge by (distance, id)."""
+              query: np.ndarray, ma: int, r: int, kernel: str = "adc", init_count: int = 200):
+    """ivf.py:148-196, kernels 'adc' and 'quick-adc': probe the ma nearest
+    cells, scan each list against the fp64 residual's tables ('adc': exact
+    ADC, ivf.py:181-184; 'quick-adc': qadc_scan with min(init_count, n) and
+    its bins rescaled, ivf.py:185-190), merge by (distance, id)."""
     K = coarse.shape[0]
     if not 1 <= ma <= K:
         raise ValueError(f"ma must be in [1, {K}]")
@@ -337,7 +339,12 @@ def query_ivf(coarse: np.ndarray, codebooks: np.ndarray, lists_codes, lists_ids,
             continue
         residual = q64 - np.asarray(coarse[int(cell)], np.float32).astype(np.float64)
         tables = compute_tables(codebooks, residual)
-        d, ids = scan(codes, lists_ids[int(cell)], tables, r)
+        if kernel == "quick-adc":
+            bins, ids, _, qmin, qmax = qadc_scan(codes, lists_ids[int(cell)], tables,
+                                                 min(init_count, codes.shape[0]), r)
+            d = rescale(bins, qmin, qmax)
+        else:
+            d, ids = scan(codes, lists_ids[int(cell)], tables, r)
         for dist, ident in zip(d.tolist(), ids.tolist()):
             merged.push(dist, ident)
     items = merged.items()

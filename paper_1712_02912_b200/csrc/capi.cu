@@ -716,6 +716,33 @@ int pqs_ivf_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64
   return finish(ctx, io);
 }
 
+int pqs_ivf_qadc_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_t nq, int ma, int r,
+                        int init_count, double* out_dist, int64_t* out_ids, int32_t* out_count, int io) {
+  if (!ctx || !ivf) return PQS_ERR_INVALID;
+  PQS_TRY(check_io(ctx, io));
+  PQS_CHECK(ctx, ma >= 1 && ma <= ivf->K, "ma must be in [1, K]");
+  PQS_CHECK(ctx, r >= 1, "r must be >= 1");
+  PQS_CHECK(ctx, ivf->k == 16 && ivf->m % 2 == 0, "quick-adc kernel requires b=4 and even m");
+  PQS_CHECK(ctx, init_count >= 1, "init_count must be >= 1");
+  if (r > MAX_R) return set_err(ctx, PQS_ERR_UNSUPPORTED, "r > 4096 is not supported by the device select");
+  if (ivf->m > 64) return set_err(ctx, PQS_ERR_UNSUPPORTED, "quick-adc IVF kernel supports m <= 64");
+  if (nq == 0) return PQS_OK;
+  PQS_CUDA(ctx, cudaSetDevice(ctx->device));
+  const float* dq = nullptr;
+  double* dd = nullptr;
+  int64_t* di = nullptr;
+  int32_t* dc = nullptr;
+  PQS_TRY(stage_in(ctx, S_QUERIES, queries, (size_t)nq * ivf->d, io, &dq));
+  PQS_TRY(stage_out(ctx, S_OUT_D, out_dist, (size_t)nq * r, io, &dd));
+  PQS_TRY(stage_out(ctx, S_OUT_I, out_ids, (size_t)nq * r, io, &di));
+  PQS_TRY(stage_out(ctx, S_OUT_C, out_count, (size_t)nq, io, &dc));
+  PQS_TRY(run_ivf_qadc_search(ctx, ivf, dq, nq, ma, r, init_count, dd, di, dc));
+  PQS_TRY(copy_out(ctx, out_dist, dd, (size_t)nq * r, io));
+  PQS_TRY(copy_out(ctx, out_ids, di, (size_t)nq * r, io));
+  PQS_TRY(copy_out(ctx, out_count, dc, (size_t)nq, io));
+  return finish(ctx, io);
+}
+
 // ---------------------------------------------------------------- merge
 int pqs_merge_topr(pqs_ctx* ctx, int G, const double* dists, const int64_t* ids, const int32_t* counts, int64_t nq,
                    int r_in, int r, double* out_dist, int64_t* out_ids, int32_t* out_count, int io) {

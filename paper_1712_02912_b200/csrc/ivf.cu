@@ -25,6 +25,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -520,6 +522,9 @@ __global__ void __launch_bounds__(LIST_THREADS, 2) ivf_list_kernel(
     }
     const int q = s_q[slot];
     const float A = s_a[slot], th = s_th[slot];
+    // idle slots (ns < LQ) read unstaged table rows: whatever they sum to
+    // (even -inf) must not emit
+    const bool live = slot < ns;
     for (int64_t cb = b; cb < e; cb += LCH) {
       const int nc = (int)min((int64_t)LCH, e - cb);
       __syncthreads();
@@ -565,7 +570,7 @@ __global__ void __launch_bounds__(LIST_THREADS, 2) ivf_list_kernel(
           const uint8_t* cd = (const uint8_t*)scode + i * m;
           for (int j = 0; j < m; ++j) acc += su_s[(j * k + cd[j]) * LROW];
         }
-        if (acc <= th) {
+        if (live && acc <= th) {
           const int pos = atomicAdd(&s_cnt[slot], 1);
           const uint32_t off = (uint32_t)(cb - b + i);
           if (pos < LSTAGE) {
@@ -1041,6 +1046,10 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
     ctot += hcnt[q];
     const int64_t r_eff = std::min<int64_t>(r, tot);
     if (hcnt[q] > cap || hcnt[q] < r_eff || ctx->force_fallback) {
+      static const bool dbg = getenv("PQS_DEBUG") != nullptr;
+      if (dbg)
+        fprintf(stderr, "pqs ivf: query %lld falls back: %d candidates (cap %lld, r_eff %lld, probed %lld)\n",
+                (long long)q, hcnt[q], (long long)cap, (long long)r_eff, (long long)tot);
       over.push_back((int)q);
       worst_total = std::max(worst_total, tot);
     }

@@ -232,6 +232,18 @@ __host__ __device__ inline float fkey_inv(uint32_t k) {
 
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+#ifdef __CUDACC__
+// fastscan.py:48-57 in fp64: 127 at or above qmax, else floor((v-qmin)*scale)
+// clamped to [0, 126]; 0 everywhere when the span is empty.
+__device__ __forceinline__ uint8_t quantize1(double v, double qmin, double qmax, double scale) {
+  if (scale == 0.0) return 0;
+  if (v >= qmax) return 127;
+  double f = floor(__dmul_rn(__dsub_rn(v, qmin), scale));
+  f = f < 0.0 ? 0.0 : (f > 126.0 ? 126.0 : f);
+  return (uint8_t)f;
+}
+#endif
+
 // ---------------------------------------------------------------------------
 // launchers (defined in the .cu files)
 // ---------------------------------------------------------------------------
@@ -302,3 +314,6 @@ int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* ivf, const float* d_queries, int6
                   int64_t* d_cells, double* d_dist);
 int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* d_queries, int64_t nq, int ma,
                    int r, double* d_dist, int64_t* d_ids, int32_t* d_count);
+// ivf_qadc.cu
+int run_ivf_qadc_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* d_queries, int64_t nq, int ma,
+                        int r, int init_count, double* d_dist, int64_t* d_ids, int32_t* d_count);

@@ -77,16 +77,6 @@ __device__ __forceinline__ int code4_at(const pqs_db& db, const uint32_t* __rest
   return (int)((sel >> (4 * (i & 3))) & 15u);
 }
 
-// fastscan.py:48-57 in fp64: 127 at or above qmax, else floor((v-qmin)*scale)
-// clamped to [0, 126]; 0 everywhere when the span is empty.
-__device__ __forceinline__ uint8_t quantize1(double v, double qmin, double qmax, double scale) {
-  if (scale == 0.0) return 0;
-  if (v >= qmax) return 127;
-  double f = floor(__dmul_rn(__dsub_rn(v, qmin), scale));
-  f = f < 0.0 ? 0.0 : (f > 126.0 ? 126.0 : f);
-  return (uint8_t)f;
-}
-
 __global__ void quantize_kernel(const double* __restrict__ v, int64_t n, double qmin, double qmax, double scale,
                                 uint8_t* __restrict__ out) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;

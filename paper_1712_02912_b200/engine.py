@@ -282,7 +282,9 @@ class DeviceIvf:
                                                   ptr(dist), _io(self.ctx, q, cells)), "ivf_probe")
         return cells, dist
 
-    def search(self, queries, ma: int, r: int):
+    def search(self, queries, ma: int, r: int, kernel: str = "adc", init_count: int = 200):
+        """Batched query_ivf: kernel 'adc' (exact fp64 distances) or 'quick-adc'
+        (per-list Quick ADC bins rescaled to fp64, ivf.py:185-190)."""
         q = _host_f32(queries, 2, "queries")
         if q.shape[1] != self.d:
             raise ValueError(f"query must have shape ({self.d},)")
@@ -290,8 +292,16 @@ class DeviceIvf:
         d = _empty((nq, r), np.float64, q)
         i = _empty((nq, r), np.int64, q)
         c = _empty((nq,), np.int32, q)
-        self.ctx.check(self.ctx.lib.pqs_ivf_search(self.ctx.handle, self.handle, ptr(q), nq, int(ma), int(r), ptr(d),
-                                                   ptr(i), ptr(c), _io(self.ctx, q, d)), "ivf_search")
+        io = _io(self.ctx, q, d)
+        if kernel == "adc":
+            st = self.ctx.lib.pqs_ivf_search(self.ctx.handle, self.handle, ptr(q), nq, int(ma), int(r), ptr(d),
+                                             ptr(i), ptr(c), io)
+        elif kernel == "quick-adc":
+            st = self.ctx.lib.pqs_ivf_qadc_search(self.ctx.handle, self.handle, ptr(q), nq, int(ma), int(r),
+                                                  int(init_count), ptr(d), ptr(i), ptr(c), io)
+        else:
+            raise ValueError(f"unknown device IVF kernel {kernel!r}")
+        self.ctx.check(st, "ivf_search")
         return d, i, c
 
     def __del__(self):

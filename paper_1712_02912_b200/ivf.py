@@ -1,10 +1,11 @@
-"""Drop-in for `pqscan.ivf.query_ivf` (ivf.py:148-196), kernel='adc', on the GPU.
+"""Drop-in for `pqscan.ivf.query_ivf` (ivf.py:148-196), kernels 'adc' and
+'quick-adc', on the GPU.
 
 Probes (nearest_k, _dist.py:42-67) and the list scans run in libpqs.so
 (K7 probe GEMM + exact fp64 re-score, K8 list-major filtered scan, K6 exact
-residual-table rerank, K5 select).  The index is uploaded once and cached on
-the IvfIndex object.  The 'quick-adc' and 'derived' kernels are outside the
-device scan path (not in any BASELINE config).
+residual-table rerank, K5 select; kernel='quick-adc': the per-list Quick ADC of ivf_qadc.cu).  The
+index is uploaded once and cached on the IvfIndex object.  The 'derived'
+kernel (derived.py two-pass search) is outside the device scan path.
 """
 
 from __future__ import annotations
@@ -35,7 +36,7 @@ def device_index(index: IvfIndex) -> DeviceIvf:
 
 def query_ivf(index: IvfIndex, query: np.ndarray, ma: int, r: int, kernel: str = "adc",
               init_count: int = 200, r2: int | None = None) -> NeighborSet:
-    """ivf.py:148-196 with kernel='adc'."""
+    """ivf.py:148-196 with kernel='adc' or 'quick-adc'."""
     kernel = kernel.replace("_", "-")
     if kernel not in KERNELS:
         raise ValueError(f"kernel must be one of {KERNELS}")
@@ -50,16 +51,26 @@ def query_ivf(index: IvfIndex, query: np.ndarray, ma: int, r: int, kernel: str =
     query = np.asarray(query, dtype=np.float64)
     if query.shape != (index.d,):
         raise ValueError(f"query must have shape ({index.d},)")
-    if kernel != "adc":
-        raise NotImplementedError(f"kernel={kernel!r} is outside the device ADC scan path")
+    if kernel == "derived":
+        raise NotImplementedError("kernel='derived' (derived.py two-pass search) is outside the device scan path")
     dev = device_index(index)
     from .quantizer import as_f32_exact
 
-    d, i, c = dev.search(as_f32_exact(query, "query_ivf")[None, :], int(ma), int(r))
+    if kernel == "quick-adc" and init_count < 1:
+        # qadc_scan raises at the first non-empty probed list (quickadc.py:123-124)
+        cells, _ = dev.probe(as_f32_exact(query, "query_ivf")[None, :], int(ma))
+        if any(index.lists[int(c)].n for c in cells[0]):
+            raise ValueError("init_count must be >= 1")
+        return NeighborSet(r)
+
+    d, i, c = dev.search(as_f32_exact(query, "query_ivf")[None, :], int(ma), int(r), kernel=kernel,
+                         init_count=int(init_count))
     n = int(c[0])
     return NeighborSet.from_pairs(r, d[0, :n], i[0, :n])
 
 
-def query_ivf_batch(index: IvfIndex, queries: np.ndarray, ma: int, r: int):
+def query_ivf_batch(index: IvfIndex, queries: np.ndarray, ma: int, r: int, kernel: str = "adc",
+                    init_count: int = 200):
     """Batched query_ivf: (nq, d) -> (dist (nq, r), ids (nq, r), count (nq,))."""
-    return device_index(index).search(queries, int(ma), int(r))
+    kernel = kernel.replace("_", "-")
+    return device_index(index).search(queries, int(ma), int(r), kernel=kernel, init_count=int(init_count))

@@ -205,6 +205,51 @@ def g_ivf():
     save("ivf.npz", **out)
 
 
+def g_ivf_qadc():
+    """query_ivf kernel='quick-adc' (ivf.py:185-190): a built 8x4 index (ids
+    ascending per list) and a hand-made one with permuted ids, a small code
+    alphabet (heavy bin ties), empty and tiny lists; init_count below r,
+    between r and the list sizes, and above every list size."""
+    from pqscan import IvfIndex, ProductQuantizer
+
+    rng = np.random.default_rng(808)
+    base = mixture(rng, 3000, 32, 16, 128.0, 16.0, 0.0, 255.0)
+    idx = build_ivf(base, K=24, m=8, b=4, cfg=TrainConfig(kmeans_iters=5, seed=7))
+    qs = base[rng.choice(3000, 6, replace=False)] + rng.normal(0, 6, (6, 32)).astype(np.float32)
+    out = {}
+
+    def dump(tag, index, settings):
+        out[f"{tag}_coarse"] = index.coarse
+        out[f"{tag}_codebooks"] = index.pq.codebooks
+        out[f"{tag}_list_sizes"] = np.array([lst.n for lst in index.lists], dtype=np.int64)
+        out[f"{tag}_list_codes"] = np.concatenate([lst.codes for lst in index.lists]).reshape(-1, index.pq.m)
+        out[f"{tag}_list_ids"] = np.concatenate([lst.ids for lst in index.lists])
+        for ma, r, ic in settings:
+            d = np.full((len(qs), r), np.nan)
+            i = np.full((len(qs), r), -1, dtype=np.int64)
+            for qi, q in enumerate(qs):
+                dd, ii, _ = items_arrays(query_ivf(index, q, ma=ma, r=r, kernel="quick-adc", init_count=ic), r)
+                d[qi], i[qi] = dd, ii
+            out[f"{tag}_ma{ma}_r{r}_i{ic}_dist"] = d
+            out[f"{tag}_ma{ma}_r{r}_i{ic}_ids"] = i
+
+    dump("built", idx, [(1, 20, 200), (4, 50, 30), (8, 100, 200), (24, 10, 5000)])
+    # hand-made index: permuted ids, codes from a 3-symbol alphabet -> many equal bins
+    K = 6
+    coarse = base[rng.choice(3000, K, replace=False)]
+    pq = ProductQuantizer(m=8, b=4, d=32, codebooks=idx.pq.codebooks)
+    sizes = [700, 0, 3, 150, 1, 400]
+    perm = rng.permutation(10_000)[: sum(sizes)].astype(np.int64)
+    lists, o = [], 0
+    for sz in sizes:
+        codes = rng.integers(0, 3, (sz, 8)).astype(np.uint8)
+        lists.append(CodeList(codes, perm[o:o + sz]))
+        o += sz
+    dump("ties", IvfIndex(coarse=coarse, pq=pq, lists=lists), [(6, 100, 200), (3, 40, 1), (2, 250, 64)])
+    out["queries"] = qs
+    save("ivf_qadc.npz", **out)
+
+
 def g_encode():
     """encode (plain and IVF-residual) incl. exact centroid ties."""
     rng = np.random.default_rng(606)
@@ -261,10 +306,15 @@ def g_formats():
 
 if __name__ == "__main__":
     print("pqscan from", pqscan.__file__)
+    if len(sys.argv) > 1:            # regenerate selected fixtures only
+        for name in sys.argv[1:]:
+            globals()[f"g_{name}"]()
+        sys.exit(0)
     g_tables()
     g_scan()
     g_quick_adc()
     g_quantize()
     g_ivf()
+    g_ivf_qadc()
     g_encode()
     g_formats()

@@ -116,3 +116,30 @@ def test_encode_golden(golden, tag):
     np.testing.assert_array_equal(O.encode(books, x, g[f"{tag}_coarse"], g[f"{tag}_cells"]),
                                   g[f"{tag}_rescodes"])
     assert (g[f"{tag}_codes"][:50] == 0).all()  # tied duplicate centroid -> lowest index
+
+
+QADC_IVF = [("built", 1, 20, 200), ("built", 4, 50, 30), ("built", 8, 100, 200), ("built", 24, 10, 5000),
+            ("ties", 6, 100, 200), ("ties", 3, 40, 1), ("ties", 2, 250, 64)]
+
+
+def qadc_ivf_lists(g, tag):
+    sizes = g[f"{tag}_list_sizes"]
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    codes = [g[f"{tag}_list_codes"][offs[c]:offs[c + 1]] for c in range(len(sizes))]
+    ids = [g[f"{tag}_list_ids"][offs[c]:offs[c + 1]] for c in range(len(sizes))]
+    return codes, ids
+
+
+@pytest.mark.parametrize("tag,ma,r,ic", QADC_IVF)
+def test_ivf_quick_adc_query(golden, tag, ma, r, ic):
+    """query_ivf kernel='quick-adc' (ivf.py:185-190) vs the reference's outputs."""
+    g = golden("ivf_qadc.npz")
+    codes, ids = qadc_ivf_lists(g, tag)
+    key = f"{tag}_ma{ma}_r{r}_i{ic}"
+    for qi, q in enumerate(g["queries"]):
+        d, i = O.query_ivf(g[f"{tag}_coarse"], g[f"{tag}_codebooks"], codes, ids, q, ma, r,
+                           kernel="quick-adc", init_count=ic)
+        n = len(d)
+        np.testing.assert_array_equal(d, g[f"{key}_dist"][qi][:n])
+        np.testing.assert_array_equal(i, g[f"{key}_ids"][qi][:n])
+        assert np.all(g[f"{key}_ids"][qi][n:] == -1)
