@@ -74,15 +74,17 @@ __global__ void v_kernel(const float* __restrict__ coarse, const float* __restri
   if ((threadIdx.x & 31) == 0) atomicMax((int*)vmax_out, __float_as_int(vmax));
 }
 
-// per-query tables U[q][j][i] = ||C_ji||^2 - 2 <q_j, C_ji> (fp64 -> fp32)
+// per-query tables U[q][i][j] = ||C_ji||^2 - 2 <q_j, C_ji> (fp64 -> fp32),
+// entry-major ([i * m + j]): the list scan's shared-memory row of (entry i,
+// component j) then sits in bank window j mod 4 (see ivf_list_kernel)
 __global__ void utables_kernel(const float* __restrict__ queries, const float* __restrict__ books, int64_t nq, int m,
                                int k, int dsub, float* __restrict__ U) {
   const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (gid >= nq * m * (int64_t)k) return;
-  const int i = (int)(gid % k);
-  const int64_t t = gid / k;
-  const int j = (int)(t % m);
-  const int64_t q = t / m;
+  const int j = (int)(gid % m);
+  const int64_t t = gid / m;
+  const int i = (int)(t % k);
+  const int64_t q = t / k;
   const float* qv = queries + q * (int64_t)m * dsub + (int64_t)j * dsub;
   const float* cb = books + ((int64_t)j * k + i) * dsub;
   double nn = 0.0, dot = 0.0;
@@ -103,7 +105,7 @@ __global__ void ivf_bound_kernel(const float* __restrict__ U, const double* __re
   double s = 0.0;
   for (int j = warp; j < m; j += nw) {
     float mx = 0.f;
-    for (int i = lane; i < k; i += 32) mx = fmaxf(mx, fabsf(U[(q * m + j) * (int64_t)k + i]));
+    for (int i = lane; i < k; i += 32) mx = fmaxf(mx, fabsf(U[(q * k + i) * (int64_t)m + j]));
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     s += (double)mx;
   }
@@ -316,7 +318,7 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
     const int64_t* __restrict__ offsets, const uint8_t* __restrict__ codes, const float* __restrict__ V, int ma,
     int spl, int m, int k, int r, const float* __restrict__ aerr, float* __restrict__ theta) {
   extern __shared__ __align__(16) unsigned char tsm[];
-  float* su = (float*)tsm;                                   // [m*k]
+  float* su = (float*)tsm;                                   // [k][m]
   unsigned int* keys = (unsigned int*)(su + (size_t)m * k);  // [ma*spl]
   __shared__ unsigned int hist[256];
   __shared__ unsigned int s_prefix, s_k, s_valid;
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
       if (b + i < e) {
         const int64_t pos = b + i;
         float acc = (float)pdist[q * ma + p] + V[pos];
-        for (int j = 0; j < m; ++j) acc += su[j * k + codes[pos * m + j]];
+        for (int j = 0; j < m; ++j) acc += su[codes[pos * m + j] * m + j];
         key = fkey(acc);
         ++valid;
       }
@@ -446,13 +448,17 @@ __global__ void pair_fill_kernel(const int64_t* __restrict__ cells, const double
 
 // One CTA per inverted list (two resident per SM); the queries probing it are
 // processed 8 at a time ("slots"): their U tables are staged in shared memory
-// interleaved as [j*k + entry][slot] (row stride 9 words), a quarter-warp
+// interleaved as [entry*m + j][slot] (row stride 8 words), a quarter-warp
 // evaluates one code for all 8 slots (lane = slot, the code's bytes are a
-// broadcast read), so the 8 lookups of one table row hit 8 consecutive banks.  Survivors are
-// staged per slot in shared memory and appended to the query's candidate
-// list with one global reservation per (list, slot).
+// broadcast read), so the 8 lookups of one table row hit the 8 banks of
+// window (row mod 4) = (j mod 4) when m % 4 == 0.  The four quarter-warps of
+// a warp visit the components in rotated orders (quarter-warp w reads
+// component (t + w) mod m at step t), so one warp-wide lookup touches four
+// distinct windows: conflict-free for any codes.  Survivors are staged per
+// slot in shared memory and appended to the query's candidate list with one
+// global reservation per (list, slot).
 constexpr int LQ = 8;
-constexpr int LROW = LQ + 1;       // padded row stride (words) of the slot-interleaved tables
+constexpr int LROW = LQ;           // row stride (words) of the slot-interleaved tables
 constexpr int LIST_THREADS = 512;
 constexpr int LCH = 1024;          // codes per chunk
 constexpr int LSTAGE = 256;        // staged survivors per slot
@@ -475,6 +481,12 @@ __device__ __forceinline__ void cp_async4_stream(void* smem, const void* gmem, u
                    (uint32_t)__cvta_generic_to_shared(smem)),
                "l"(gmem), "l"(pol)
                : "memory");
+}
+
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
 }
 
 template <int MT, int KT>  // compile-time (m, k), or (0, 0) for runtime values
@@ -503,6 +515,14 @@ __global__ void __launch_bounds__(LIST_THREADS, 2) ivf_list_kernel(
   const int slot = threadIdx.x & (LQ - 1);
   const int hw = threadIdx.x / LQ, nhw = blockDim.x / LQ;
   const float* su_s = su + slot;
+  // rotated lookups (MT % 4 == 0): byte offset of component (t + qw) mod MT
+  // within an entry's block of MT rows, and the entry stride as a shift
+  const int qw = (threadIdx.x >> 3) & 3;
+  constexpr int eshift = MT > 0 ? 31 - __builtin_clz(MT * LROW * 4) : 0;
+  uint32_t jb[MT > 0 ? MT : 1];  // shared-window byte addresses
+#pragma unroll
+  for (int t = 0; t < (MT > 0 ? MT : 1); ++t)
+    jb[t] = (uint32_t)__cvta_generic_to_shared(su_s) + (MT > 0 ? ((t + qw) % (MT > 0 ? MT : 1)) * LROW * 4 : 0);
   for (int64_t g0 = p0; g0 < p1; g0 += LQ) {
     const int ns = (int)min((int64_t)LQ, p1 - g0);
     __syncthreads();
@@ -514,11 +534,17 @@ __global__ void __launch_bounds__(LIST_THREADS, 2) ivf_list_kernel(
       s_cnt[threadIdx.x] = 0;
     }
     __syncthreads();
-    // stage the tables: row-contiguous global reads, stride-17 shared writes
-    // (conflict-free), asynchronous copies (completed with the first code chunk)
-    for (int idx = threadIdx.x; idx < ns * mk; idx += LIST_THREADS) {
-      const int sl = idx / mk, i = idx - sl * mk;
-      cp_async4(su + i * LROW + sl, U + (int64_t)s_q[sl] * mk + i);
+    // stage the tables (asynchronous, completed with the first code chunk):
+    // a warp copies runs of 8 consecutive entries (one 32 B sector) of 4
+    // slots' tables; shared writes are 2-way conflicted at most
+    {
+      static_assert(LQ == 8 && LIST_THREADS % 64 == 0, "staging map assumes 8 slots");
+      const int u = threadIdx.x & 7, g8 = threadIdx.x >> 3, sl = g8 & 7;
+      if (sl < ns) {
+        const float* src = U + (int64_t)s_q[sl] * mk;
+        // 64 threads per slot: 8 runs of 8 consecutive entries per step
+        for (int i = (g8 >> 3) * 8 + u; i < mk; i += 64) cp_async4(su + i * LROW + sl, src + i);
+      }
     }
     const int q = s_q[slot];
     const float A = s_a[slot], th = s_th[slot];
@@ -543,19 +569,25 @@ __global__ void __launch_bounds__(LIST_THREADS, 2) ivf_list_kernel(
       for (int i = hw; i < nc; i += nhw) {
         float acc = A + sv[i];
         if (MT > 0 && (MT & 3) == 0) {
-          // pairwise (tree) sum: the filter bound holds for any summation order
-          float part[MT >= 4 ? MT / 4 : 1];
+          // rotated component order (conflict-free windows); the sum is
+          // pairwise -- the filter bound holds for any summation order
+          constexpr int W = MT >= 4 ? MT / 4 : 1;
+          uint32_t cw[W], rot[W];
 #pragma unroll
-          for (int w = 0; w < MT / 4; ++w) {
-            const uint32_t cw = scode[i * (MT / 4) + w];  // broadcast
+          for (int w = 0; w < W; ++w) cw[w] = scode[i * W + w];  // broadcast
+#pragma unroll
+          for (int w = 0; w < W; ++w) rot[w] = __funnelshift_r(cw[w], cw[(w + 1) % W], 8 * qw);
+          float part[W];
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
             float t4[4];
 #pragma unroll
             for (int t = 0; t < 4; ++t)
-              t4[t] = su_s[((4 * w + t) * KT + (int)__byte_perm(cw, 0u, 0x4440 + t)) * LROW];
+              t4[t] = lds_f32(jb[4 * w + t] + (__byte_perm(rot[w], 0u, 0x4440 + t) << eshift));
             part[w] = (t4[0] + t4[1]) + (t4[2] + t4[3]);
           }
 #pragma unroll
-          for (int w = 1; w < MT / 4; ++w) part[0] += part[w];
+          for (int w = 1; w < W; ++w) part[0] += part[w];
           acc += part[0];
         } else if ((m & 3) == 0) {
           for (int w = 0; w < mw; ++w) {
@@ -563,12 +595,12 @@ __global__ void __launch_bounds__(LIST_THREADS, 2) ivf_list_kernel(
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
               const int j = 4 * w + t;
-              acc += su_s[(j * k + (int)((cw >> (8 * t)) & 255u)) * LROW];
+              acc += su_s[((int)((cw >> (8 * t)) & 255u) * m + j) * LROW];
             }
           }
         } else {
           const uint8_t* cd = (const uint8_t*)scode + i * m;
-          for (int j = 0; j < m; ++j) acc += su_s[(j * k + cd[j]) * LROW];
+          for (int j = 0; j < m; ++j) acc += su_s[(cd[j] * m + j) * LROW];
         }
         if (live && acc <= th) {
           const int pos = atomicAdd(&s_cnt[slot], 1);
