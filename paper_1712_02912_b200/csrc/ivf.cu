@@ -40,7 +40,7 @@ using namespace seldev;
 
 // ------------------------------------------------------------ index build
 __global__ void cnorm_kernel(const float* __restrict__ coarse, int64_t K, int d, double* __restrict__ cnorm,
-                             float* __restrict__ gnorm) {
+                             float* __restrict__ gnorm, float* __restrict__ cnormf) {
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= K) return;
   double s = 0.0;
@@ -50,6 +50,7 @@ __global__ void cnorm_kernel(const float* __restrict__ coarse, int64_t K, int d,
   }
   cnorm[c] = s;
   gnorm[c] = (float)sqrt(s);
+  cnormf[c] = (float)s;
 }
 
 // V[pos] = 2 sum_j <g_cj, C_j[code_j]>, fp64 -> fp32; one CTA per list
@@ -126,12 +127,14 @@ __global__ void ivf_bound_kernel(const float* __restrict__ U, const double* __re
 struct ProbeArgs {
   const float* dots;     // (nqb, K) fp32 q.c
   const double* cnorm;   // (K,)
+  const float* cnormf;   // (K,) fp32 ||c||^2 (approximate keys)
   const float* gnorm;    // (K,) ||c|| fp32
   float gmax;
   const float* queries;  // (nq, d), batch-offset applied
   const float* coarse;   // (K, d)
   int64_t K;
   int d, ma;
+  int tf32;              // dots from a TF32 tensor-core GEMM (wider certified bound)
   int64_t q0;            // global index of batch row 0
   int64_t* out_cells;    // (nq, ma)
   double* out_dist;      // (nq, ma)
@@ -166,9 +169,21 @@ __global__ void __launch_bounds__(PROBE_THREADS) probe_select_kernel(ProbeArgs a
   __syncthreads();
   // certified bound on |approx - exact|: fp32 dot (any order) error <= gamma_d ||q|| ||c||
   const double u = 5.9604644775390625e-08;
-  const double gam = a.d * u / (1.0 - a.d * u);
-  const double eps = 2.0 * gam * s_qn * (double)a.gmax * 1.01 + 1e-9 * (s_qn * s_qn + (double)a.gmax * a.gmax);
-  auto approx = [&](int64_t c) { return a.cnorm[c] - 2.0 * (double)dots[c]; };
+  // fp32 GEMM: |fl(q.c) - q.c| <= gamma_d ||q|| ||c|| (any summation order).
+  // TF32 tensor cores: operands keep 10 mantissa bits (truncation: relative
+  // error < 2^-10 each, products exact), fp32 accumulation taken as <= 2^-22
+  // per add -- (2^-9 + 2^-19 + d 2^-22) ||q|| ||c||, i.e. ~2x the
+  // round-to-nearest operand error.
+  const double gam = a.tf32 ? (1.953125e-3 + 1.9073486328125e-06 + a.d * 2.384185791015625e-07)
+                            : a.d * u / (1.0 - a.d * u);
+  // approximate keys in fp32: approx = fl(fl(||c||^2) - 2 q.c) (2 q.c exact)
+  // adds <= u (||c||^2 + |approx|) <= 2u (gmax^2 + ||q|| gmax) to the GEMM error
+  const double gm = (double)a.gmax;
+  const double eps = 2.0 * gam * s_qn * gm * 1.01 + 2.0 * u * 1.01 * (gm * gm + s_qn * gm) +
+                     1e-9 * (s_qn * s_qn + gm * gm);
+  auto approx = [&](int64_t c) -> float { return a.cnormf[c] - 2.f * dots[c]; };
+  auto akey = [](float f) -> uint64_t { return (uint64_t)fkey(f); };           // 32-bit: <= 4 radix passes
+  auto akey_inv = [](uint64_t k) -> double { return (double)fkey_inv((uint32_t)k); };
   double thr = 1e300;
   if (ma < K) {
     // certified cut from a strided sample of S >= ma cells: its ma-th smallest
@@ -176,29 +191,41 @@ __global__ void __launch_bounds__(PROBE_THREADS) probe_select_kernel(ProbeArgs a
     // every true probe has approx <= that + 2 eps (one pass over the dots,
     // ~ma * K / S cells re-scored exactly)
     const int64_t S = K < PROBE_SMEM_CAP ? K : PROBE_SMEM_CAP;
-    for (int64_t i = threadIdx.x; i < S; i += blockDim.x) ck[i] = dkey(approx(i * K / S));
+    for (int64_t i = threadIdx.x; i < S; i += blockDim.x) ck[i] = akey(approx(i * K / S));
     __syncthreads();
     auto getk = [&](int64_t i, uint64_t& v) {
       v = ck[i];
       return true;
     };
     block_radix_select(S, getk, (unsigned long long)(ma - 1), sh);
-    thr = dkey_inv(sh.prefix) + 2.0 * eps;
+    thr = akey_inv(sh.prefix) + 2.0 * eps;
     __syncthreads();
   }
   // gather the cells with approx <= thr (approximate keys first)
-  for (int64_t c = threadIdx.x; c < K; c += blockDim.x) {
-    const double ap = approx(c);
-    if (ap <= thr) {
+  auto gather = [&](float ap, int64_t c) {
+    if ((double)ap <= thr) {
       const int p = atomicAdd(&s_cnt, 1);
       if (p < PROBE_SMEM_CAP) {
-        ck[p] = dkey(ap);
+        ck[p] = akey(ap);
         ci[p] = c;
       } else {
-        a.gkeys[ql * K + p] = dkey(ap);
+        a.gkeys[ql * K + p] = akey(ap);
         a.gids[ql * K + p] = c;
       }
     }
+  };
+  if ((K & 3) == 0) {  // 16-byte loads of the dots row and the norms
+    const float4* d4 = reinterpret_cast<const float4*>(dots);
+    const float4* n4 = reinterpret_cast<const float4*>(a.cnormf);
+    for (int64_t c4 = threadIdx.x; c4 < K / 4; c4 += blockDim.x) {
+      const float4 dv = d4[c4], nv = __ldg(n4 + c4);
+      gather(nv.x - 2.f * dv.x, 4 * c4);
+      gather(nv.y - 2.f * dv.y, 4 * c4 + 1);
+      gather(nv.z - 2.f * dv.z, 4 * c4 + 2);
+      gather(nv.w - 2.f * dv.w, 4 * c4 + 3);
+    }
+  } else {
+    for (int64_t c = threadIdx.x; c < K; c += blockDim.x) gather(approx(c), c);
   }
   __syncthreads();
   const int64_t M = s_cnt;
@@ -221,13 +248,13 @@ __global__ void __launch_bounds__(PROBE_THREADS) probe_select_kernel(ProbeArgs a
         return true;
       };
       block_radix_select(M, getk2, (unsigned long long)(ma - 1), sh);
-      thr2 = dkey_inv(sh.prefix) + 2.0 * eps;
+      thr2 = akey_inv(sh.prefix) + 2.0 * eps;
       __syncthreads();
     }
     // exact fp64 distance (sequential, as scipy cdist) of the cells within
     // thr2; the others get the largest key (never selected: >= ma are exact)
     for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
-      if (dkey_inv(AK[i]) <= thr2) {
+      if (akey_inv(AK[i]) <= thr2) {
         const float* g = a.coarse + AI[i] * (int64_t)a.d;
         double s2 = 0.0;
         for (int t0 = 0; t0 < a.d; t0 += 8) {
@@ -318,12 +345,15 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
     const int64_t* __restrict__ offsets, const uint8_t* __restrict__ codes, const float* __restrict__ V, int ma,
     int spl, int m, int k, int r, const float* __restrict__ aerr, float* __restrict__ theta) {
   extern __shared__ __align__(16) unsigned char tsm[];
-  float* su = (float*)tsm;                                   // [k][m]
+  float* su = (float*)tsm;                                   // [m][k] (lanes read random entries of one row)
   unsigned int* keys = (unsigned int*)(su + (size_t)m * k);  // [ma*spl]
   __shared__ unsigned int hist[256];
   __shared__ unsigned int s_prefix, s_k, s_valid;
   const int64_t q = blockIdx.x;
-  for (int i = threadIdx.x; i < m * k; i += blockDim.x) su[i] = U[q * (int64_t)m * k + i];
+  for (int i = threadIdx.x; i < m * k; i += blockDim.x) {
+    const int e = i / m, j = i - e * m;
+    su[j * k + e] = U[q * (int64_t)m * k + i];
+  }
   if (threadIdx.x == 0) {
     s_prefix = 0;
     s_k = (unsigned)(r - 1);
@@ -341,7 +371,7 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
       if (b + i < e) {
         const int64_t pos = b + i;
         float acc = (float)pdist[q * ma + p] + V[pos];
-        for (int j = 0; j < m; ++j) acc += su[codes[pos * m + j] * m + j];
+        for (int j = 0; j < m; ++j) acc += su[j * k + codes[pos * m + j]];
         key = fkey(acc);
         ++valid;
       }
@@ -483,6 +513,11 @@ __device__ __forceinline__ void cp_async4_stream(void* smem, const void* gmem, u
                : "memory");
 }
 
+__device__ __forceinline__ float2 lds_f32x2(uint32_t addr) {
+  float2 v;
+  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ float lds_f32(uint32_t addr) {
   float v;
   asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
@@ -519,6 +554,12 @@ __global__ void __launch_bounds__(LIST_THREADS, 2) ivf_list_kernel(
   // within an entry's block of MT rows, and the entry stride as a shift
   const int qw = (threadIdx.x >> 3) & 3;
   constexpr int eshift = MT > 0 ? 31 - __builtin_clz(MT * LROW * 4) : 0;
+  constexpr bool PAIR = MT == 8 && KT == 256;
+  const int qw2 = (threadIdx.x >> 2) & 3;
+  uint32_t jb2[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t)
+    jb2[t] = (uint32_t)__cvta_generic_to_shared(su) + 8 * (threadIdx.x & 3) + ((t + qw2) & 7) * LROW * 4;
   uint32_t jb[MT > 0 ? MT : 1];  // shared-window byte addresses
 #pragma unroll
   for (int t = 0; t < (MT > 0 ? MT : 1); ++t)
@@ -551,6 +592,10 @@ __global__ void __launch_bounds__(LIST_THREADS, 2) ivf_list_kernel(
     // idle slots (ns < LQ) read unstaged table rows: whatever they sum to
     // (even -inf) must not emit
     const bool live = slot < ns;
+    const int ps0 = 2 * (threadIdx.x & 3);  // PAIR: this lane's slots ps0, ps0 + 1
+    const int q0 = s_q[ps0], q1 = s_q[ps0 + 1];
+    const float A0 = s_a[ps0], A1 = s_a[ps0 + 1], th0 = s_th[ps0], th1 = s_th[ps0 + 1];
+    const bool live0 = ps0 < ns, live1 = ps0 + 1 < ns;
     for (int64_t cb = b; cb < e; cb += LCH) {
       const int nc = (int)min((int64_t)LCH, e - cb);
       __syncthreads();
@@ -566,6 +611,41 @@ __global__ void __launch_bounds__(LIST_THREADS, 2) ivf_list_kernel(
       for (int i = threadIdx.x; i < nc; i += blockDim.x) cp_async4_stream(sv + i, V + cb + i, pol);
       cp_async_wait_all();
       __syncthreads();
+      auto emit = [&](int sl, int qs, float acc, int i) {
+        const int pos = atomicAdd(&s_cnt[sl], 1);
+        const uint32_t off = (uint32_t)(cb - b + i);
+        if (pos < LSTAGE) {
+          sst[sl * LSTAGE + pos] = off;
+          ssa[sl * LSTAGE + pos] = acc;
+        } else {  // stage full: direct append
+          const int gp = atomicAdd(cand_cnt + qs, 1);
+          if (gp < cap) {
+            cand[(int64_t)qs * cap + gp] = ((uint64_t)c << 32) | (uint64_t)(uint32_t)(b + off);
+            cand_apx[(int64_t)qs * cap + gp] = acc;
+          }
+        }
+      };
+      if constexpr (PAIR) {
+        // 4 lanes per code, two slots per lane (one 8-byte lookup = the
+        // entries of slots 2l, 2l+1): 8 codes per warp, each half-warp's four
+        // codes in distinct bank windows (rotation by code index mod 4)
+        for (int i = threadIdx.x >> 2; i < nc; i += LIST_THREADS / 4) {
+          const uint32_t c0 = scode[2 * i], c1 = scode[2 * i + 1];  // broadcast to the 4 lanes
+          const uint32_t r0 = __funnelshift_r(c0, c1, 8 * qw2), r1 = __funnelshift_r(c1, c0, 8 * qw2);
+          float2 t8[8];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) t8[t] = lds_f32x2(jb2[t] + (__byte_perm(r0, 0u, 0x4440 + t) << eshift));
+#pragma unroll
+          for (int t = 0; t < 4; ++t) t8[4 + t] = lds_f32x2(jb2[4 + t] + (__byte_perm(r1, 0u, 0x4440 + t) << eshift));
+          const float vv = sv[i];
+          const float s0 = ((t8[0].x + t8[1].x) + (t8[2].x + t8[3].x)) + ((t8[4].x + t8[5].x) + (t8[6].x + t8[7].x));
+          const float s1 = ((t8[0].y + t8[1].y) + (t8[2].y + t8[3].y)) + ((t8[4].y + t8[5].y) + (t8[6].y + t8[7].y));
+          const float acc0 = (A0 + vv) + s0, acc1 = (A1 + vv) + s1;
+          if (live0 && acc0 <= th0) emit(ps0, q0, acc0, i);
+          if (live1 && acc1 <= th1) emit(ps0 + 1, q1, acc1, i);
+        }
+        continue;
+      }
       for (int i = hw; i < nc; i += nhw) {
         float acc = A + sv[i];
         if (MT > 0 && (MT & 3) == 0) {
@@ -602,20 +682,7 @@ __global__ void __launch_bounds__(LIST_THREADS, 2) ivf_list_kernel(
           const uint8_t* cd = (const uint8_t*)scode + i * m;
           for (int j = 0; j < m; ++j) acc += su_s[(cd[j] * m + j) * LROW];
         }
-        if (live && acc <= th) {
-          const int pos = atomicAdd(&s_cnt[slot], 1);
-          const uint32_t off = (uint32_t)(cb - b + i);
-          if (pos < LSTAGE) {
-            sst[slot * LSTAGE + pos] = off;
-            ssa[slot * LSTAGE + pos] = acc;
-          } else {  // stage full: direct append
-            const int gp = atomicAdd(cand_cnt + q, 1);
-            if (gp < cap) {
-              cand[(int64_t)q * cap + gp] = ((uint64_t)c << 32) | (uint64_t)(uint32_t)(b + off);
-              cand_apx[(int64_t)q * cap + gp] = acc;
-            }
-          }
-        }
+        if (live && acc <= th) emit(slot, q, acc, i);
       }
     }
     __syncthreads();
@@ -847,7 +914,7 @@ int ivf_create_impl(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t
   iv->max_list = mx;
   const int d = pq->d;
   auto al = [&](void** p, size_t bytes) { return cudaMalloc(p, std::max<size_t>(bytes, 16)) == cudaSuccess; };
-  bool ok = al((void**)&iv->coarse, (size_t)K * d * 4) && al((void**)&iv->cnorm, (size_t)K * 8) &&
+  bool ok = al((void**)&iv->coarse, (size_t)K * d * 4) && al((void**)&iv->cnorm, (size_t)K * 8) && al((void**)&iv->cnormf, (size_t)K * 4) &&
             al((void**)&iv->books, (size_t)pq->m * pq->k * pq->dsub * 4) && al((void**)&iv->offsets, (size_t)(K + 1) * 8) &&
             al((void**)&iv->codes, (size_t)n * pq->m) && al((void**)&iv->ids, (size_t)n * 8) &&
             al((void**)&iv->gnorm, (size_t)K * 4 /* gnorm */ + 16) && al((void**)&iv->vtab, (size_t)n * 4) &&
@@ -871,7 +938,7 @@ int ivf_create_impl(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t
     }
   }
   PQS_CUDA(ctx, cudaMemsetAsync(iv->vmax, 0, 16, ctx->stream));
-  cnorm_kernel<<<(unsigned)cdiv(K, 256), 256, 0, ctx->stream>>>(iv->coarse, K, d, iv->cnorm, iv->gnorm);
+  cnorm_kernel<<<(unsigned)cdiv(K, 256), 256, 0, ctx->stream>>>(iv->coarse, K, d, iv->cnorm, iv->gnorm, iv->cnormf);
   PQS_LAUNCHED(ctx);
   v_kernel<<<(unsigned)K, 256, 0, ctx->stream>>>(iv->coarse, iv->books, iv->offsets, iv->codes, iv->m, iv->k, iv->dsub,
                                                  d, iv->vtab, iv->vmax);
@@ -892,6 +959,7 @@ void ivf_destroy_impl(pqs_ivf* iv) {
   cudaFree(iv->coarse);
   cudaFree(iv->gnorm);
   cudaFree(iv->cnorm);
+  cudaFree(iv->cnormf);
   cudaFree(iv->books);
   cudaFree(iv->offsets);
   cudaFree(iv->codes);
@@ -914,6 +982,10 @@ int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int64
   PQS_TRY(scratch(ctx, S_IDS, (size_t)(QB * K), &gi));
   cublasHandle_t h;
   PQS_TRY(get_cublas(ctx, &h));
+  // TF32 tensor-core GEMM by default (the probe sets stay exact: every cell
+  // within the certified bound is re-scored in fp64); PQS_PROBE_FP32=1 keeps
+  // the pedantic fp32 SIMT GEMM
+  static const int tf32 = getenv("PQS_PROBE_FP32") ? 0 : 1;
   int P = 1;
   while (P < ma) P <<= 1;
   if (P < 2) P = 2;
@@ -928,6 +1000,7 @@ int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int64
     // C(K, nb) = A(K, d) * B(d, nb) with A = coarse row-major seen as (d x K)
     // col-major transposed, B = queries row-major seen as (d x nb) col-major.
     const float alpha = 1.f, beta = 0.f;
+    cublasSetMathMode(h, tf32 ? CUBLAS_TF32_TENSOR_OP_MATH : CUBLAS_PEDANTIC_MATH);
     if (cublasSgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)K, (int)nb, d, &alpha, iv->coarse, d, d_queries + q0 * d, d,
                     &beta, dots, (int)K) != CUBLAS_STATUS_SUCCESS)
       return set_err(ctx, PQS_ERR_CUDA, "cublasSgemm failed");
@@ -935,6 +1008,8 @@ int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int64
     ProbeArgs a{};
     a.dots = dots;
     a.cnorm = iv->cnorm;
+    a.cnormf = iv->cnormf;
+    a.tf32 = tf32;
     a.gnorm = iv->gnorm;
     a.gmax = iv->gmax;
     a.queries = d_queries + q0 * d;

@@ -127,6 +127,7 @@ struct pqs_ivf {
   float* gnorm = nullptr;         // (K,) ||c|| (fp32, for the probe error bound)
   float gmax = 0.f;               // max ||c||
   double* cnorm = nullptr;        // (K,) fp64 ||c||^2
+  float* cnormf = nullptr;        // (K,) fp32 ||c||^2 (probe keys)
   float* vtab = nullptr;          // (n,) V = 2 sum_j <c_j, C_j[code_j]> per stored code
   float* vmax = nullptr;          // (1,) max |V|
   float* books = nullptr;         // (m, k, dsub)

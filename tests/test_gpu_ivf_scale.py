@@ -55,3 +55,18 @@ def test_ivf_search_vs_oracle(index):
         assert c[qi] == len(od)
         np.testing.assert_array_equal(d[qi, :c[qi]], od)
         np.testing.assert_array_equal(i[qi, :c[qi]], oi)
+
+
+def test_probe_sets_exact_many_queries(index):
+    """K7 probes (TF32 GEMM + certified fp64 re-score) == nearest_k
+    (_dist.py:42-67) for all 300 queries: same cells, same order, same fp64
+    distances -- incl. the cfg3 geometry (queries inside a mixture component
+    tiled by many centroids)."""
+    books, coarse, sizes, codes, ids, queries = index
+    pq = P.ProductQuantizer(8, 8, 128, books)
+    ivf = P.DeviceIvf.from_arrays(pq, coarse, sizes, codes, ids)
+    for ma in (1, 64, 300):
+        cells, dist = ivf.probe(queries, ma)
+        oc, od = O.nearest_k(queries.astype(np.float64), coarse.cpu().numpy().astype(np.float64), ma)
+        np.testing.assert_array_equal(cells, oc)
+        np.testing.assert_array_equal(dist, od)
