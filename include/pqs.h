@@ -166,6 +166,15 @@ int pqs_ivf_probe(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_
                   int64_t* out_cells, double* out_dist, int io);
 int pqs_ivf_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_t nq, int ma,
                    int r, double* out_dist, int64_t* out_ids, int32_t* out_count, int io);
+/* ---- PQ Fast Scan statistics (fast_scan, fastscan.py:328-386): the number
+ * of codes whose exact distance the reference's pruned scan evaluates
+ * (ScanStats.checked; pruned = n - checked).  db: the grouped database's
+ * codes in storage order (GroupedDatabase.reconstruct_codes, b == 8, m ==
+ * 8); tables (nq, 8, 256) float32; n_init = ceil(init * n) in [1, n].  The
+ * neighbour set equals pqs_adc_scan's (fast_scan is exact).              */
+int pqs_fastscan_checked(pqs_ctx* ctx, const pqs_db* db, const float* tables, int64_t nq,
+                         int64_t n_init, int r, int64_t* out_checked, int io);
+
 /* ---- query_ivf kernel='quick-adc' (ivf.py:185-190): per probed list the
  * Quick ADC scan (quickadc.py:104-141, init_count = min(init_count, list
  * size)), its r best by (bin, id) rescaled (quickadc.py:50-54) and merged by

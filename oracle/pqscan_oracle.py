@@ -112,12 +112,19 @@ class NeighborMerge:
         self.r = r
         self._heap: list = []
 
-    def push(self, distance: float, ident: int) -> None:
+    def push(self, distance: float, ident: int) -> bool:
         entry = (-float(distance), -int(ident))
         if len(self._heap) < self.r:
             heapq.heappush(self._heap, entry)
-        elif entry > self._heap[0]:
+            return True
+        if entry > self._heap[0]:
             heapq.heappushpop(self._heap, entry)
+            return True
+        return False
+
+    def worst(self) -> float:
+        """scan.py:102-107: the r-th best distance, inf while fewer are held."""
+        return float("inf") if len(self._heap) < self.r else -self._heap[0][0]
 
     def items(self):
         return sorted((-d, -i) for d, i in self._heap)
@@ -361,3 +368,65 @@ def merge_shards(dists_list, ids_list, r: int):
     d = np.concatenate([np.asarray(x, np.float64) for x in dists_list])
     i = np.concatenate([np.asarray(x, np.int64) for x in ids_list])
     return select_best(d, i, r)
+
+
+# --------------------------------------------------------------------------
+# PQ Fast Scan  (fastscan.py:208-386)
+# --------------------------------------------------------------------------
+
+def group_order(codes: np.ndarray) -> np.ndarray:
+    """fastscan.py:208-219: stable order by the high nibbles of components 0-3."""
+    highs = (np.asarray(codes)[:, :4] >> 4).astype(np.uint32)
+    key_val = (highs[:, 0] << 12) | (highs[:, 1] << 8) | (highs[:, 2] << 4) | highs[:, 3]
+    return np.argsort(key_val, kind="stable")
+
+
+def fast_scan(codes: np.ndarray, ids: np.ndarray, tables: np.ndarray, init: float, r: int):
+    """fastscan.py:328-386 on codes in grouped storage order: the sequential
+    pruned scan.  Returns (dists, ids, checked, pruned)."""
+    import math
+
+    tables = np.asarray(tables, dtype=np.float32)
+    ids = np.asarray(ids, dtype=np.int64)
+    n = codes.shape[0]
+    merged = NeighborMerge(r)
+    if n == 0:
+        return np.empty(0), np.empty(0, np.int64), 0, 0
+    n_init = math.ceil(init * n)
+    prefix_d = scan_distances(tables, codes[:n_init])
+    checked, pruned = n_init, 0
+    order = np.lexsort((ids[:n_init], prefix_d))
+    for pos in order[: min(r, n_init)]:
+        merged.push(float(prefix_d[pos]), int(ids[pos]))
+    qmax = float(np.partition(prefix_d, r - 1)[r - 1]) if n_init >= r else float(prefix_d.max())
+    qmin = float(tables.min())
+    qmax = max(qmax, qmin)
+    qt = quantize(qmin, qmax, tables)
+    mins = qt[4:8].reshape(4, 16, 16).min(axis=2)                 # fastscan.py:258-260
+    start = n_init
+    while start < n:
+        stop = min(start + 1024, n)
+        chunk = codes[start:stop]
+        worst = merged.worst()
+        threshold = int(quantize(qmin, qmax, np.array([worst]))[0])
+        idx = chunk.astype(np.int64)                               # _lower_bounds_all, fastscan.py:300-310
+        acc = qt[0][idx[:, 0]].astype(np.int16)
+        for j in range(1, 4):
+            acc += qt[j][idx[:, j]]
+        for j in range(4, 8):
+            acc += mins[j - 4][idx[:, j] >> 4]
+        lb = np.minimum(acc, BINS)
+        keep = lb <= threshold
+        pruned += int(np.count_nonzero(~keep))
+        kept = np.flatnonzero(keep)
+        if kept.size:
+            d = scan_distances(tables, chunk[kept])
+            checked += kept.size
+            kid = ids[start:stop][kept]
+            for pos in np.lexsort((kid, d)):
+                if not merged.push(float(d[pos]), int(kid[pos])):
+                    break
+        start = stop
+    items = merged.items()
+    return (np.array([p[0] for p in items], dtype=np.float64), np.array([p[1] for p in items], dtype=np.int64),
+            checked, pruned)

@@ -44,6 +44,21 @@ from .formats import (  # noqa: F401
     save_quantizer,
 )
 from .quickadc import qadc_block, qadc_scan, quantize, quantize_tables_4bit, quantized_distances  # noqa: F401
+from .fastscan import (  # noqa: F401
+    GroupedDatabase,
+    ScanStats,
+    SmallTables,
+    build_small_tables,
+    compute_quant_params,
+    fast_scan,
+    group_codes,
+    group_key,
+    load_grouped,
+    lower_bound,
+    pack_code,
+    relabel_codes,
+    save_grouped,
+)
 from .ivf import KERNELS, default_r2, query_ivf, query_ivf_batch  # noqa: F401
 from .engine import DeviceCodes, DeviceIvf, DeviceQuantizer, merge_topr  # noqa: F401
 from ._lib import Context, default_context, load_library  # noqa: F401

@@ -743,6 +743,25 @@ int pqs_ivf_qadc_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, 
   return finish(ctx, io);
 }
 
+int pqs_fastscan_checked(pqs_ctx* ctx, const pqs_db* db, const float* tables, int64_t nq, int64_t n_init, int r,
+                         int64_t* out_checked, int io) {
+  if (!ctx || !db) return PQS_ERR_INVALID;
+  PQS_TRY(check_io(ctx, io));
+  PQS_CHECK(ctx, db->b == 8 && db->m == 8, "fast scan requires m=8, b=8 lookup tables");
+  PQS_CHECK(ctx, r >= 1, "r must be >= 1");
+  PQS_CHECK(ctx, db->n >= 1, "empty code list");
+  PQS_CHECK(ctx, n_init >= 1 && n_init <= db->n, "n_init must be in [1, n]");
+  if (nq == 0) return PQS_OK;
+  PQS_CUDA(ctx, cudaSetDevice(ctx->device));
+  const float* dt = nullptr;
+  int64_t* dc = nullptr;
+  PQS_TRY(stage_in(ctx, S_TABLES, tables, (size_t)nq * 8 * 256, io, &dt));
+  PQS_TRY(stage_out(ctx, S_OUT_I, out_checked, (size_t)nq, io, &dc));
+  PQS_TRY(run_fastscan_checked(ctx, db, dt, nq, n_init, r, dc));
+  PQS_TRY(copy_out(ctx, out_checked, dc, (size_t)nq, io));
+  return finish(ctx, io);
+}
+
 // ---------------------------------------------------------------- merge
 int pqs_merge_topr(pqs_ctx* ctx, int G, const double* dists, const int64_t* ids, const int32_t* counts, int64_t nq,
                    int r_in, int r, double* out_dist, int64_t* out_ids, int32_t* out_count, int io) {

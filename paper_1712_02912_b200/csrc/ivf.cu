@@ -77,24 +77,47 @@ __global__ void v_kernel(const float* __restrict__ coarse, const float* __restri
 
 // per-query tables U[q][i][j] = ||C_ji||^2 - 2 <q_j, C_ji> (fp64 -> fp32),
 // entry-major ([i * m + j]): the list scan's shared-memory row of (entry i,
-// component j) then sits in bank window j mod 4 (see ivf_list_kernel)
-__global__ void utables_kernel(const float* __restrict__ queries, const float* __restrict__ books, int64_t nq, int m,
-                               int k, int dsub, float* __restrict__ U) {
-  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (gid >= nq * m * (int64_t)k) return;
-  const int j = (int)(gid % m);
-  const int64_t t = gid / m;
-  const int i = (int)(t % k);
-  const int64_t q = t / k;
-  const float* qv = queries + q * (int64_t)m * dsub + (int64_t)j * dsub;
-  const float* cb = books + ((int64_t)j * k + i) * dsub;
-  double nn = 0.0, dot = 0.0;
-  for (int s = 0; s < dsub; ++s) {
-    const double cv = (double)cb[s];
-    nn += cv * cv;
-    dot += (double)qv[s] * cv;
+// component j) then sits in bank window j mod 4 (see ivf_list_kernel).
+// One CTA per UQ queries, thread = entry i: each codebook row is loaded once
+// per CTA, the UQ tables are built in shared memory and written out with
+// coalesced 16-byte stores.
+constexpr int UQ = 8;
+__global__ void __launch_bounds__(256) utables_kernel(const float* __restrict__ queries,
+                                                      const float* __restrict__ books, int64_t nq, int m, int k,
+                                                      int dsub, float* __restrict__ U) {
+  extern __shared__ __align__(16) float usm[];  // [UQ][k * m] tables, then [UQ][d] queries
+  const int d = m * dsub, mk = m * k;
+  float* sq = usm + (size_t)UQ * mk;
+  const int64_t q0 = (int64_t)blockIdx.x * UQ;
+  const int nqb = (int)min((int64_t)UQ, nq - q0);
+  for (int t = threadIdx.x; t < nqb * d; t += blockDim.x) sq[t] = queries[q0 * d + t];
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    for (int j = 0; j < m; ++j) {
+      const float* cb = books + ((int64_t)j * k + i) * dsub;
+      double nn = 0.0;
+      double dot[UQ];
+#pragma unroll
+      for (int u = 0; u < UQ; ++u) dot[u] = 0.0;
+      for (int s2 = 0; s2 < dsub; ++s2) {
+        const double cv = (double)__ldg(cb + s2);
+        nn += cv * cv;
+#pragma unroll
+        for (int u = 0; u < UQ; ++u) dot[u] += (double)sq[u * d + j * dsub + s2] * cv;
+      }
+#pragma unroll
+      for (int u = 0; u < UQ; ++u) usm[u * mk + i * m + j] = (float)(nn - 2.0 * dot[u]);
+    }
   }
-  U[gid] = (float)(nn - 2.0 * dot);
+  __syncthreads();
+  float* out = U + q0 * mk;
+  if ((mk & 3) == 0) {
+    const float4* s4 = reinterpret_cast<const float4*>(usm);
+    float4* o4 = reinterpret_cast<float4*>(out);
+    for (int t = threadIdx.x; t < nqb * mk / 4; t += blockDim.x) o4[t] = s4[t];
+  } else {
+    for (int t = threadIdx.x; t < nqb * mk; t += blockDim.x) out[t] = usm[t];
+  }
 }
 
 // per query: E_q = certified bound of |filter distance - exact distance|
@@ -1043,7 +1066,12 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
   float* aerr = nullptr;
   PQS_TRY(scratch(ctx, S_TABLES, (size_t)(nq * m * k), &U));
   PQS_TRY(scratch(ctx, S_AERR, (size_t)nq, &aerr));
-  utables_kernel<<<(unsigned)cdiv(nq * m * k, 256), 256, 0, ctx->stream>>>(d_queries, iv->books, nq, m, k, iv->dsub, U);
+  {
+    const size_t usz = ((size_t)UQ * m * k + (size_t)UQ * iv->d) * 4;
+    PQS_CHECK(ctx, usz <= 200 * 1024, "IVF query tables: m * k too large");
+    PQS_CUDA(ctx, cudaFuncSetAttribute(utables_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usz));
+    utables_kernel<<<(unsigned)cdiv(nq, UQ), 256, usz, ctx->stream>>>(d_queries, iv->books, nq, m, k, iv->dsub, U);
+  }
   PQS_LAUNCHED(ctx);
   ivf_bound_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(U, pdist, nq, ma, m, k, iv->vmax, aerr);
   PQS_LAUNCHED(ctx);

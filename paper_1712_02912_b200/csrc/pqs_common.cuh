@@ -315,6 +315,9 @@ int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* ivf, const float* d_queries, int6
                   int64_t* d_cells, double* d_dist);
 int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* d_queries, int64_t nq, int ma,
                    int r, double* d_dist, int64_t* d_ids, int32_t* d_count);
+// fastscan.cu
+int run_fastscan_checked(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t nq, int64_t n_init,
+                         int r, int64_t* d_checked);
 // ivf_qadc.cu
 int run_ivf_qadc_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* d_queries, int64_t nq, int ma,
                         int r, int init_count, double* d_dist, int64_t* d_ids, int32_t* d_count);

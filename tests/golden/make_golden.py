@@ -250,6 +250,35 @@ def g_ivf_qadc():
     save("ivf_qadc.npz", **out)
 
 
+def g_fastscan():
+    """fast_scan (fastscan.py:328-386) on a grouped 8x8 database: neighbour
+    sets and ScanStats for several (init, r); a PQG1 file."""
+    from pqscan import fast_scan, group_codes, save_grouped
+
+    rng = np.random.default_rng(909)
+    x = mixture(rng, 24000, 32, 24, 128.0, 16.0, 0.0, 255.0)
+    pq = train_pq(x[:6000], 8, 8, TrainConfig(kmeans_iters=4, seed=8))
+    codes = encode(pq, x[:20000])
+    ids = rng.permutation(50_000)[:20000].astype(np.int64)
+    grouped = group_codes(CodeList(codes, ids))
+    qs = x[20000:20006] + rng.normal(0, 4, (6, 32)).astype(np.float32)
+    out = dict(codebooks=pq.codebooks, codes=codes, ids=ids, queries=qs,
+               g_keys=grouped.keys, g_offsets=grouped.offsets, g_counts=grouped.counts,
+               g_packed=grouped.packed, g_ids=grouped.ids)
+    for init, r in [(0.01, 100), (0.05, 10), (0.001, 1), (1.0, 50), (0.0002, 300)]:
+        tag = f"i{init}_r{r}"
+        d = np.full((len(qs), r), np.nan)
+        i = np.full((len(qs), r), -1, dtype=np.int64)
+        st = np.zeros((len(qs), 3), dtype=np.int64)
+        for qi, q in enumerate(qs):
+            nset, stats = fast_scan(grouped, compute_tables(pq, q), init, r)
+            d[qi], i[qi], _ = items_arrays(nset, r)
+            st[qi] = (stats.total, stats.checked, stats.pruned)
+        out[f"{tag}_dist"], out[f"{tag}_ids"], out[f"{tag}_stats"] = d, i, st
+    save_grouped(os.path.join(OUT, "fmt_grouped.pqg"), group_codes(CodeList(codes[:300], ids[:300])))
+    save("fastscan.npz", **out)
+
+
 def g_encode():
     """encode (plain and IVF-residual) incl. exact centroid ties."""
     rng = np.random.default_rng(606)
@@ -316,5 +345,6 @@ if __name__ == "__main__":
     g_quantize()
     g_ivf()
     g_ivf_qadc()
+    g_fastscan()
     g_encode()
     g_formats()
