@@ -453,10 +453,13 @@ def run_ivf(args):
                 "d2h_bytes_per_step": nq * r * 16 + nq * 4},
         "gpu_launches": launches,
         "candidates": {"max_per_query": cand_max, "mean_per_query": cand_tot / nq,
-                       "reranked_per_query": ctx.stat(_lib.STAT_LAST_RERANK_TOTAL) / nq},
+                       "reranked_per_query": ctx.stat(_lib.STAT_LAST_RERANK_TOTAL) / nq,
+                       "list_scan_slot_utilization": (ctx.stat(_lib.STAT_LAST_EVALS) /
+                                                      max(1, ctx.stat(_lib.STAT_LAST_SLOT_EVALS)))},
         "clocks": clk,
         "roofline": {"bound": "lut", "achieved": lut_rate, "peak": lut_peak, "unit": "Glookup/s",
-                     "frac": lut_rate / lut_peak, "traffic": None,
+                     "frac": lut_rate / lut_peak, "traffic": _ncu_traffic("ivf_list_kernel"),
+                     "traffic_note": "DRAM bytes of one list-scan launch from the committed ncu capture (profiles/r01_ivf_cfg3.md); the excess over the algorithmic bytes is the per-(list, query) staging of the 8 KB query tables",
                      "kernel": "ivf_list_kernel (list-major, smem LUT)",
                      "per_unit": f"{m} table lookups per probed (query, code); {evals_step:.3e} per launch",
                      "peak_source": f"shared-memory LUT rate {sm_count} SM x 32 lookups/clk x {f_mhz:.0f} MHz",
@@ -473,6 +476,13 @@ def run_ivf(args):
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def _ncu_traffic(kernel: str):
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(kernel, {}).get("bytes")
+    except (OSError, ValueError):
+        return None
 
 
 def main():

@@ -72,7 +72,8 @@ enum pqs_stat {
   PQS_STAT_LAST_CAND_TOTAL = 7,    /* sum over queries of the candidates of the last search */
   PQS_STAT_LAST_SCAN_ENGINE = 8,   /* 1 PRMT scan4, 2 tcgen05 scan4, 3 scan8, 4 IVF list scan */
   PQS_STAT_LAST_SCAN_WORK = 9,     /* work units of that kernel: tcgen05 -> int8 MMA ops; others -> table lookups */
-  PQS_STAT_LAST_RERANK_TOTAL = 10  /* float / IVF: candidates re-scored exactly after the bound tightening (sum over queries) */
+  PQS_STAT_LAST_RERANK_TOTAL = 10, /* float / IVF: candidates re-scored exactly after the bound tightening (sum over queries) */
+  PQS_STAT_LAST_SLOT_EVALS = 11    /* IVF list scan: (slot, code) evaluations incl. idle slots of partly filled 8-query groups */
 };
 
 int pqs_api_version(void);

@@ -39,6 +39,7 @@ STAT_LAST_CAND_TOTAL = 7
 STAT_LAST_SCAN_ENGINE = 8
 STAT_LAST_SCAN_WORK = 9
 STAT_LAST_RERANK_TOTAL = 10
+STAT_LAST_SLOT_EVALS = 11
 
 _p = ctypes.c_void_p
 _i = ctypes.c_int

@@ -251,6 +251,7 @@ int pqs_ctx_get_stat(pqs_ctx* ctx, int stat, int64_t* out) {
     case PQS_STAT_LAST_SCAN_ENGINE: *out = ctx->last_scan_engine; return PQS_OK;
     case PQS_STAT_LAST_SCAN_WORK: *out = (int64_t)ctx->last_scan_work; return PQS_OK;
     case PQS_STAT_LAST_RERANK_TOTAL: *out = ctx->last_rerank_total; return PQS_OK;
+    case PQS_STAT_LAST_SLOT_EVALS: *out = ctx->last_slot_evals; return PQS_OK;
   }
   return set_err(ctx, PQS_ERR_INVALID, "unknown stat");
 }

@@ -1191,6 +1191,14 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
   }
   ctx->last_evals = total_evals;
   ctx->last_scan_work = (double)total_evals * (double)m;
+  {
+    std::vector<int> pc((size_t)K, 0);
+    for (int64_t c : hcells)
+      if (c >= 0) ++pc[(size_t)c];
+    int64_t se = 0;
+    for (int64_t c = 0; c < K; ++c) se += (iv->h_offsets[c + 1] - iv->h_offsets[c]) * (int64_t)LQ * ((pc[c] + LQ - 1) / LQ);
+    ctx->last_slot_evals = se;
+  }
   ctx->last_max_cand = mx;
   ctx->last_cand_total = ctot;
   {

@@ -82,6 +82,7 @@ struct pqs_ctx {
   int64_t last_cand_total = 0;
   int64_t last_rerank_total = 0;  // candidates left for the exact re-score after tightening
   int64_t last_scan_engine = 0;
+  int64_t last_slot_evals = 0;    // IVF list scan: slot-evaluations incl. idle slots
   double last_scan_work = 0;
   cudaEvent_t scan_ev[2] = {nullptr, nullptr};
   Scratch scratch[S_NSLOTS];

@@ -162,13 +162,29 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(SelArgs a, int sort
       __syncthreads();
       for (int64_t i = threadIdx.x; i < M; i += blockDim.x) atomicAdd(&sh.hist[es.K[i]], 1u);
       __syncthreads();
-      if (threadIdx.x == 0) {
-        unsigned long long c = 0;
-        int b = 0;
-        for (; b < 127 && c + sh.hist[b] <= (unsigned long long)(r_eff - 1); ++b) c += sh.hist[b];
-        sh.prefix = (unsigned long long)b;
-        sh.less = c;
-        sh.eq = sh.hist[b];
+      if (threadIdx.x < 32) {
+        // warp-parallel cut: lane l owns bins 4l..4l+3; the cut bin is the
+        // first whose inclusive count reaches r_eff (every bin is < 128)
+        const int lane = threadIdx.x;
+        unsigned int h[4], s4 = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s4 += (h[u] = sh.hist[4 * lane + u]);
+        unsigned int incl = s4;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const unsigned long long re = (unsigned long long)r_eff;
+        const unsigned int excl = incl - s4;
+        if (excl < re && incl >= re) {
+          unsigned int c = excl;
+          int u = 0;
+          while (c + h[u] < re) c += h[u++];
+          sh.prefix = (unsigned long long)(4 * lane + u);
+          sh.less = c;
+          sh.eq = h[u];
+        }
       }
       __syncthreads();
     } else {
