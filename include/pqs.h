@@ -176,6 +176,20 @@ int pqs_ivf_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64
 int pqs_fastscan_checked(pqs_ctx* ctx, const pqs_db* db, const float* tables, int64_t nq,
                          int64_t n_init, int r, int64_t* out_checked, int io);
 
+/* ---- derived-quantizer two-pass search: search_two_pass (derived.py:402-409)
+ * over a b == 8 list; full: the DerivedPQ's quantizer (m, 2^b), derived: its
+ * 2^bbar codebooks as a quantizer handle (same m, d).  r2 >= 1 candidates
+ * for the exact rerank (default_r2, ivf.py:51-53).  Outputs as
+ * pqs_adc_search (exact fp64 distances of the reranked codes).           */
+int pqs_derived_search(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* full, const pqs_pq* derived,
+                       const float* queries, int64_t nq, int r, int64_t r2, double* out_dist,
+                       int64_t* out_ids, int32_t* out_count, int io);
+/* ---- query_ivf kernel='derived' (ivf.py:191-195): search_two_pass per
+ * probed list on the residual, merged by (distance, id).                 */
+int pqs_ivf_derived_search(pqs_ctx* ctx, const pqs_ivf* ivf, const pqs_pq* derived,
+                           const float* queries, int64_t nq, int ma, int r, int64_t r2,
+                           double* out_dist, int64_t* out_ids, int32_t* out_count, int io);
+
 /* ---- query_ivf kernel='quick-adc' (ivf.py:185-190): per probed list the
  * Quick ADC scan (quickadc.py:104-141, init_count = min(init_count, list
  * size)), its r best by (bin, id) rescaled (quickadc.py:50-54) and merged by

@@ -430,3 +430,77 @@ def fast_scan(codes: np.ndarray, ids: np.ndarray, tables: np.ndarray, init: floa
     items = merged.items()
     return (np.array([p[0] for p in items], dtype=np.float64), np.array([p[1] for p in items], dtype=np.int64),
             checked, pruned)
+
+
+# --------------------------------------------------------------------------
+# Derived quantizers: two-pass search  (derived.py:129-409)
+# --------------------------------------------------------------------------
+
+def quantize_255(qmin: float, qmax: float, values) -> np.ndarray:
+    """derived.py:143-154."""
+    v = np.asarray(values, dtype=np.float64)
+    span = qmax - qmin
+    if span <= 0.0:
+        return np.zeros(v.shape, dtype=np.uint8)
+    bins = np.clip(np.floor((v - qmin) * (255 / span)), 0, 254)
+    return np.where(v >= qmax, 255, bins).astype(np.uint8)
+
+
+def search_two_pass(full_books: np.ndarray, derived_books: np.ndarray, codes: np.ndarray, ids: np.ndarray,
+                    query: np.ndarray, r: int, r2: int):
+    """derived.py:402-409 restated: compact tables (129-140), 255-bin
+    quantization with qmax = max ADC of the first min(r2, n) codes' low bits
+    (180-198), the admission rule of scan_candidates (294-326) and the exact
+    rerank of the admitted codes (362-399)."""
+    codes = np.asarray(codes)
+    ids = np.asarray(ids, dtype=np.int64)
+    n = codes.shape[0]
+    if n == 0:
+        raise ValueError("empty code list")
+    kbar = derived_books.shape[1]
+    compact = compute_tables(derived_books, query)
+    low = (codes.astype(np.int64) & (kbar - 1))
+    qmin = float(compact.min())
+    qmax = max(float(scan_distances(compact, low[: min(r2, n)]).max()), qmin)
+    qt = quantize_255(qmin, qmax, compact)
+    acc = np.zeros(n, dtype=np.int32)
+    for j in range(qt.shape[0]):
+        acc = np.minimum(acc + qt[j][low[:, j]], 255)
+    d = acc.astype(np.uint8)
+    smalls = d <= 254
+    if int(np.count_nonzero(smalls)) >= r2:
+        hist = np.bincount(d[smalls], minlength=255)
+        bound = int(np.argmax(np.cumsum(hist) >= r2))
+        sel = d <= bound
+    else:
+        # put() in storage order: a d = 255 code is admitted while fewer than
+        # r2 are held (scan_candidates, derived.py:316-323)
+        sel = smalls.copy()
+        held = 0
+        for p in range(n):
+            if smalls[p]:
+                held += 1
+            elif held < r2:
+                sel[p] = True
+                held += 1
+    pick = np.flatnonzero(sel)
+    full = compute_tables(full_books, query)
+    dist = scan_distances(full, codes[pick])
+    return select_best(dist, ids[pick], r)
+
+
+def query_ivf_derived(coarse, full_books, derived_books, lists_codes, lists_ids, query, ma: int, r: int, r2: int):
+    """ivf.py:148-196 with kernel='derived' (191-195)."""
+    q64 = np.asarray(query, dtype=np.float64)
+    cells, _ = nearest_k(q64[None, :], np.asarray(coarse, np.float32).astype(np.float64), ma)
+    merged = NeighborMerge(r)
+    for cell in cells[0]:
+        codes = lists_codes[int(cell)]
+        if codes.shape[0] == 0:
+            continue
+        residual = q64 - np.asarray(coarse[int(cell)], np.float32).astype(np.float64)
+        d, ids = search_two_pass(full_books, derived_books, codes, lists_ids[int(cell)], residual, r, r2)
+        for dist, ident in zip(d.tolist(), ids.tolist()):
+            merged.push(dist, ident)
+    items = merged.items()
+    return (np.array([p[0] for p in items], dtype=np.float64), np.array([p[1] for p in items], dtype=np.int64))

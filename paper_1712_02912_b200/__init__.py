@@ -59,6 +59,15 @@ from .fastscan import (  # noqa: F401
     relabel_codes,
     save_grouped,
 )
+from .derived import (  # noqa: F401
+    CBINS,
+    DerivedPQ,
+    compute_compact_tables,
+    load_derived,
+    load_quantizer_any,
+    save_derived,
+    search_two_pass,
+)
 from .ivf import KERNELS, default_r2, query_ivf, query_ivf_batch  # noqa: F401
 from .engine import DeviceCodes, DeviceIvf, DeviceQuantizer, merge_topr  # noqa: F401
 from ._lib import Context, default_context, load_library  # noqa: F401

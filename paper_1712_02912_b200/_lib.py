@@ -77,6 +77,8 @@ SIGNATURES = {
     "pqs_ivf_search": (_i, [_p, _p, _p, _i64, _i, _i, _p, _p, _p, _i]),
     "pqs_ivf_qadc_search": (_i, [_p, _p, _p, _i64, _i, _i, _i, _p, _p, _p, _i]),
     "pqs_fastscan_checked": (_i, [_p, _p, _p, _i64, _i64, _i, _p, _i]),
+    "pqs_derived_search": (_i, [_p, _p, _p, _p, _p, _i64, _i, _i64, _p, _p, _p, _i]),
+    "pqs_ivf_derived_search": (_i, [_p, _p, _p, _p, _i64, _i, _i, _i64, _p, _p, _p, _i]),
     "pqs_merge_topr": (_i, [_p, _i, _p, _p, _p, _i64, _i, _i, _p, _p, _p, _i]),
 }
 

@@ -763,6 +763,70 @@ int pqs_fastscan_checked(pqs_ctx* ctx, const pqs_db* db, const float* tables, in
   return finish(ctx, io);
 }
 
+int pqs_derived_search(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* full, const pqs_pq* derived,
+                       const float* queries, int64_t nq, int r, int64_t r2, double* out_dist, int64_t* out_ids,
+                       int32_t* out_count, int io) {
+  if (!ctx || !db || !full || !derived) return PQS_ERR_INVALID;
+  PQS_TRY(check_io(ctx, io));
+  PQS_CHECK(ctx, db->n >= 1, "empty code list");
+  PQS_CHECK(ctx, r2 >= 1, "r2 must be >= 1");
+  PQS_CHECK(ctx, r >= 1, "r must be >= 1");
+  PQS_CHECK(ctx, db->b == 8 && db->m == full->m, "derived search needs a b=8 code list matching the quantizer");
+  PQS_CHECK(ctx, derived->m == full->m && derived->d == full->d && derived->k <= full->k,
+            "derived codebooks do not match the full quantizer");
+  PQS_CHECK(ctx, db->max_code < full->k, "code component out of range for the quantizer");
+  if (r > MAX_R) return set_err(ctx, PQS_ERR_UNSUPPORTED, "r > 4096 is not supported by the device select");
+  if (nq == 0) return PQS_OK;
+  PQS_CUDA(ctx, cudaSetDevice(ctx->device));
+  const float* dq = nullptr;
+  float* tf = nullptr;
+  float* tc = nullptr;
+  double* dd = nullptr;
+  int64_t* di = nullptr;
+  int32_t* dc = nullptr;
+  PQS_TRY(stage_in(ctx, S_QUERIES, queries, (size_t)nq * full->d, io, &dq));
+  PQS_TRY(scratch(ctx, S_TABLES, (size_t)nq * full->m * full->k, &tf));
+  PQS_TRY(scratch(ctx, S_TABLES_T, (size_t)nq * derived->m * derived->k, &tc));
+  PQS_TRY(launch_tables_exact(ctx, full, dq, nq, tf));
+  PQS_TRY(launch_tables_exact(ctx, derived, dq, nq, tc));
+  PQS_TRY(stage_out(ctx, S_OUT_D, out_dist, (size_t)nq * r, io, &dd));
+  PQS_TRY(stage_out(ctx, S_OUT_I, out_ids, (size_t)nq * r, io, &di));
+  PQS_TRY(stage_out(ctx, S_OUT_C, out_count, (size_t)nq, io, &dc));
+  PQS_TRY(run_derived_search(ctx, db, tf, full->k, tc, nq, derived->k, r, r2, dd, di, dc));
+  PQS_TRY(copy_out(ctx, out_dist, dd, (size_t)nq * r, io));
+  PQS_TRY(copy_out(ctx, out_ids, di, (size_t)nq * r, io));
+  PQS_TRY(copy_out(ctx, out_count, dc, (size_t)nq, io));
+  return finish(ctx, io);
+}
+
+int pqs_ivf_derived_search(pqs_ctx* ctx, const pqs_ivf* ivf, const pqs_pq* derived, const float* queries, int64_t nq,
+                           int ma, int r, int64_t r2, double* out_dist, int64_t* out_ids, int32_t* out_count,
+                           int io) {
+  if (!ctx || !ivf || !derived) return PQS_ERR_INVALID;
+  PQS_TRY(check_io(ctx, io));
+  PQS_CHECK(ctx, ma >= 1 && ma <= ivf->K, "ma must be in [1, K]");
+  PQS_CHECK(ctx, r >= 1, "r must be >= 1");
+  PQS_CHECK(ctx, r2 >= 1, "r2 must be >= 1");
+  PQS_CHECK(ctx, derived->m == ivf->m && derived->d == ivf->d && derived->k <= ivf->k,
+            "derived codebooks do not match the index quantizer");
+  if (r > MAX_R) return set_err(ctx, PQS_ERR_UNSUPPORTED, "r > 4096 is not supported by the device select");
+  if (nq == 0) return PQS_OK;
+  PQS_CUDA(ctx, cudaSetDevice(ctx->device));
+  const float* dq = nullptr;
+  double* dd = nullptr;
+  int64_t* di = nullptr;
+  int32_t* dc = nullptr;
+  PQS_TRY(stage_in(ctx, S_QUERIES, queries, (size_t)nq * ivf->d, io, &dq));
+  PQS_TRY(stage_out(ctx, S_OUT_D, out_dist, (size_t)nq * r, io, &dd));
+  PQS_TRY(stage_out(ctx, S_OUT_I, out_ids, (size_t)nq * r, io, &di));
+  PQS_TRY(stage_out(ctx, S_OUT_C, out_count, (size_t)nq, io, &dc));
+  PQS_TRY(run_ivf_derived_search(ctx, ivf, derived->books, derived->k, dq, nq, ma, r, r2, dd, di, dc));
+  PQS_TRY(copy_out(ctx, out_dist, dd, (size_t)nq * r, io));
+  PQS_TRY(copy_out(ctx, out_ids, di, (size_t)nq * r, io));
+  PQS_TRY(copy_out(ctx, out_count, dc, (size_t)nq, io));
+  return finish(ctx, io);
+}
+
 // ---------------------------------------------------------------- merge
 int pqs_merge_topr(pqs_ctx* ctx, int G, const double* dists, const int64_t* ids, const int32_t* counts, int64_t nq,
                    int r_in, int r, double* out_dist, int64_t* out_ids, int32_t* out_count, int io) {

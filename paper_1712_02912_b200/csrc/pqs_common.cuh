@@ -319,6 +319,11 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* d_queries, int
 // fastscan.cu
 int run_fastscan_checked(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t nq, int64_t n_init,
                          int r, int64_t* d_checked);
+// derived.cu
+int run_derived_search(pqs_ctx* ctx, const pqs_db* db, const float* d_full, int k, const float* d_compact,
+                       int64_t nq, int kbar, int r, int64_t r2, double* d_dist, int64_t* d_ids, int32_t* d_count);
+int run_ivf_derived_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_dbooks, int kbar, const float* d_queries,
+                           int64_t nq, int ma, int r, int64_t r2, double* d_dist, int64_t* d_ids, int32_t* d_count);
 // ivf_qadc.cu
 int run_ivf_qadc_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* d_queries, int64_t nq, int ma,
                         int r, int init_count, double* d_dist, int64_t* d_ids, int32_t* d_count);

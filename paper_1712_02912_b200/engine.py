@@ -282,7 +282,8 @@ class DeviceIvf:
                                                   ptr(dist), _io(self.ctx, q, cells)), "ivf_probe")
         return cells, dist
 
-    def search(self, queries, ma: int, r: int, kernel: str = "adc", init_count: int = 200):
+    def search(self, queries, ma: int, r: int, kernel: str = "adc", init_count: int = 200, r2: int = 9000,
+               dpq=None):
         """Batched query_ivf: kernel 'adc' (exact fp64 distances) or 'quick-adc'
         (per-list Quick ADC bins rescaled to fp64, ivf.py:185-190)."""
         q = _host_f32(queries, 2, "queries")
@@ -299,6 +300,12 @@ class DeviceIvf:
         elif kernel == "quick-adc":
             st = self.ctx.lib.pqs_ivf_qadc_search(self.ctx.handle, self.handle, ptr(q), nq, int(ma), int(r),
                                                   int(init_count), ptr(d), ptr(i), ptr(c), io)
+        elif kernel == "derived":
+            if dpq is None:
+                raise ValueError("index has no derived quantizer")
+            _, dd = dpq._device()
+            st = self.ctx.lib.pqs_ivf_derived_search(self.ctx.handle, self.handle, dd.handle, ptr(q), nq, int(ma),
+                                                     int(r), int(r2), ptr(d), ptr(i), ptr(c), io)
         else:
             raise ValueError(f"unknown device IVF kernel {kernel!r}")
         self.ctx.check(st, "ivf_search")

@@ -9,7 +9,7 @@ ValueError carrying the byte offset, _binio.py:11-18).  The device loaders
 parse only the headers on the host and hand the code payload to
 `pqs_db_create_packed`, which uploads the packed bytes as they are in the file
 (b <= 4: half the bytes) and unpacks them on the GPU into the scan layouts.
-Derived quantizers (IVF1 with has_derived) are outside the device scan path.
+IVF1 files with a derived quantizer (has_derived) carry a DerivedPQ.
 """
 
 from __future__ import annotations
@@ -173,13 +173,16 @@ def load_codes(path) -> tuple[CodeList, int]:
 
 # ------------------------------------------------------------ IVF1
 def save_ivf(path, index: IvfIndex) -> None:
-    if index.dpq is not None:
-        raise NotImplementedError("derived quantizers are outside the device scan path")
     with open(path, "wb") as f:
         f.write(MAGIC_IVF)
         _write_i32(f, index.K)
-        _write_i32(f, 0)
-        write_quantizer_body(f, index.pq)
+        _write_i32(f, 1 if index.dpq is not None else 0)
+        if index.dpq is not None:
+            from .derived import write_derived_body
+
+            write_derived_body(f, index.dpq)
+        else:
+            write_quantizer_body(f, index.pq)
         _write_array(f, index.coarse, "<f4")
         for lst in index.lists:
             write_codes_body(f, lst, index.pq.b)
@@ -188,18 +191,23 @@ def save_ivf(path, index: IvfIndex) -> None:
 def _read_ivf_head(f: BinaryIO):
     _expect_magic(f, MAGIC_IVF)
     K = _read_i32(f)
+    dpq = None
     if _read_i32(f):
-        raise NotImplementedError("IVF1 with a derived quantizer is outside the device scan path")
-    pq = read_quantizer_body(f)
+        from .derived import read_derived_body
+
+        dpq = read_derived_body(f)
+        pq = dpq.pq
+    else:
+        pq = read_quantizer_body(f)
     coarse = _read_array(f, "<f4", K * pq.d).reshape(K, pq.d)
-    return K, pq, coarse
+    return K, pq, coarse, dpq
 
 
 def load_ivf(path) -> IvfIndex:
     with open(path, "rb") as f:
-        K, pq, coarse = _read_ivf_head(f)
+        K, pq, coarse, dpq = _read_ivf_head(f)
         lists = [read_codes_body(f)[0] for _ in range(K)]
-    return IvfIndex(coarse=coarse, pq=pq, lists=lists)
+    return IvfIndex(coarse=coarse, pq=pq, lists=lists, dpq=dpq)
 
 
 # ------------------------------------------------------------ device handles
@@ -238,7 +246,7 @@ def load_ivf_device(path, ctx=None):
     from .engine import DeviceIvf
 
     with open(path, "rb") as f:
-        K, pq, coarse = _read_ivf_head(f)
+        K, pq, coarse, _dpq = _read_ivf_head(f)
         sizes = np.empty(K, dtype=np.int64)
         codes, ids = [], []
         for c in range(K):

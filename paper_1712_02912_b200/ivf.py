@@ -3,9 +3,9 @@
 
 Probes (nearest_k, _dist.py:42-67) and the list scans run in libpqs.so
 (K7 probe GEMM + exact fp64 re-score, K8 list-major filtered scan, K6 exact
-residual-table rerank, K5 select; kernel='quick-adc': the per-list Quick ADC of ivf_qadc.cu).  The
-index is uploaded once and cached on the IvfIndex object.  The 'derived'
-kernel (derived.py two-pass search) is outside the device scan path.
+residual-table rerank, K5 select; kernel='quick-adc': the per-list Quick ADC of ivf_qadc.cu;
+kernel='derived': the per-list two-pass search of derived.cu).  The index is
+uploaded once and cached on the IvfIndex object.
 """
 
 from __future__ import annotations
@@ -36,7 +36,7 @@ def device_index(index: IvfIndex) -> DeviceIvf:
 
 def query_ivf(index: IvfIndex, query: np.ndarray, ma: int, r: int, kernel: str = "adc",
               init_count: int = 200, r2: int | None = None) -> NeighborSet:
-    """ivf.py:148-196 with kernel='adc' or 'quick-adc'."""
+    """ivf.py:148-196, kernels 'adc', 'quick-adc' and 'derived'."""
     kernel = kernel.replace("_", "-")
     if kernel not in KERNELS:
         raise ValueError(f"kernel must be one of {KERNELS}")
@@ -51,8 +51,6 @@ def query_ivf(index: IvfIndex, query: np.ndarray, ma: int, r: int, kernel: str =
     query = np.asarray(query, dtype=np.float64)
     if query.shape != (index.d,):
         raise ValueError(f"query must have shape ({index.d},)")
-    if kernel == "derived":
-        raise NotImplementedError("kernel='derived' (derived.py two-pass search) is outside the device scan path")
     dev = device_index(index)
     from .quantizer import as_f32_exact
 
@@ -64,7 +62,7 @@ def query_ivf(index: IvfIndex, query: np.ndarray, ma: int, r: int, kernel: str =
         return NeighborSet(r)
 
     d, i, c = dev.search(as_f32_exact(query, "query_ivf")[None, :], int(ma), int(r), kernel=kernel,
-                         init_count=int(init_count))
+                         init_count=int(init_count), r2=(r2 if r2 is not None else default_r2(r)), dpq=index.dpq)
     n = int(c[0])
     return NeighborSet.from_pairs(r, d[0, :n], i[0, :n])
 
@@ -73,4 +71,7 @@ def query_ivf_batch(index: IvfIndex, queries: np.ndarray, ma: int, r: int, kerne
                     init_count: int = 200):
     """Batched query_ivf: (nq, d) -> (dist (nq, r), ids (nq, r), count (nq,))."""
     kernel = kernel.replace("_", "-")
-    return device_index(index).search(queries, int(ma), int(r), kernel=kernel, init_count=int(init_count))
+    if kernel == "derived" and index.dpq is None:
+        raise ValueError("index has no derived quantizer")
+    return device_index(index).search(queries, int(ma), int(r), kernel=kernel, init_count=int(init_count),
+                                      r2=default_r2(r), dpq=index.dpq)

@@ -254,6 +254,8 @@ class IvfIndex:
             raise ValueError("coarse centroids must have shape (K, d)")
         if len(self.lists) != self.coarse.shape[0]:
             raise ValueError("need exactly one inverted list per coarse centroid")
+        if self.dpq is not None and self.dpq.pq is not self.pq:
+            raise ValueError("derived quantizer must wrap the index quantizer")
 
     @property
     def K(self) -> int:

@@ -279,6 +279,42 @@ def g_fastscan():
     save("fastscan.npz", **out)
 
 
+def g_derived():
+    """search_two_pass (derived.py:402-409) on a trained DerivedPQ, query_ivf
+    kernel='derived' on a built index with a derived quantizer, and the
+    PQZ1+derived / IVF1+derived files."""
+    from pqscan import build_ivf, save_derived, save_ivf, search_two_pass, train_derived
+
+    rng = np.random.default_rng(1010)
+    x = mixture(rng, 9000, 32, 16, 128.0, 16.0, 0.0, 255.0)
+    dpq = train_derived(x[:4000], 8, 8, 4, TrainConfig(kmeans_iters=3, seed=11))
+    codes = encode(dpq.pq, x[:6000])
+    ids = rng.permutation(20_000)[:6000].astype(np.int64)
+    qs = x[6000:6005] + rng.normal(0, 4, (5, 32)).astype(np.float32)
+    out = dict(books=dpq.pq.codebooks, derived=dpq.derived, codes=codes, ids=ids, queries=qs)
+    for r, r2 in [(10, 50), (100, 9000), (5, 1), (20, 300), (50, 6000)]:
+        d = np.full((len(qs), r), np.nan)
+        i = np.full((len(qs), r), -1, dtype=np.int64)
+        for qi, q in enumerate(qs):
+            d[qi], i[qi], _ = items_arrays(search_two_pass(dpq, CodeList(codes, ids), q, r, r2), r)
+        out[f"r{r}_r2{r2}_dist"], out[f"r{r}_r2{r2}_ids"] = d, i
+    save_derived(os.path.join(OUT, "fmt_derived.pqz"), dpq)
+    idx = build_ivf(x[:5000], K=12, m=8, b=8, cfg=TrainConfig(kmeans_iters=3, seed=12), bderived=3)
+    out["ivf_coarse"], out["ivf_books"], out["ivf_derived"] = idx.coarse, idx.pq.codebooks, idx.dpq.derived
+    out["ivf_sizes"] = np.array([l.n for l in idx.lists], np.int64)
+    out["ivf_codes"] = np.concatenate([l.codes for l in idx.lists])
+    out["ivf_ids"] = np.concatenate([l.ids for l in idx.lists])
+    for ma, r, r2 in [(3, 20, 100), (12, 50, None), (2, 10, 1)]:
+        d = np.full((len(qs), r), np.nan)
+        i = np.full((len(qs), r), -1, dtype=np.int64)
+        for qi, q in enumerate(qs):
+            d[qi], i[qi], _ = items_arrays(query_ivf(idx, q, ma=ma, r=r, kernel="derived", r2=r2), r)
+        out[f"ivf_ma{ma}_r{r}_r2{r2}_dist"], out[f"ivf_ma{ma}_r{r}_r2{r2}_ids"] = d, i
+    save_ivf(os.path.join(OUT, "fmt_index_derived.ivf"), build_ivf(x[:1500], K=4, m=4, b=6,
+             cfg=TrainConfig(kmeans_iters=2, seed=13), bderived=2))
+    save("derived.npz", **out)
+
+
 def g_encode():
     """encode (plain and IVF-residual) incl. exact centroid ties."""
     rng = np.random.default_rng(606)
@@ -346,5 +382,6 @@ if __name__ == "__main__":
     g_ivf()
     g_ivf_qadc()
     g_fastscan()
+    g_derived()
     g_encode()
     g_formats()
