@@ -996,7 +996,10 @@ int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int64
                   double* d_dist) {
   const int64_t K = iv->K;
   const int d = iv->d;
-  const int64_t QB = std::max<int64_t>(1, std::min<int64_t>(nq, (int64_t)(256ll << 20) / (K * 4)));
+  // query batch: the (QB, K) fp32 dot block is written by the GEMM and read
+  // back by the select; PQS_PROBE_MB sizes it (tuning experiments)
+  static const int64_t probe_mb = getenv("PQS_PROBE_MB") ? atoll(getenv("PQS_PROBE_MB")) : 1024;
+  const int64_t QB = std::max<int64_t>(1, std::min<int64_t>(nq, (probe_mb << 20) / (K * 4)));
   float* dots = nullptr;
   uint64_t* gk = nullptr;
   int64_t* gi = nullptr;
@@ -1076,7 +1079,9 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
   ivf_bound_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(U, pdist, nq, ma, m, k, iv->vmax, aerr);
   PQS_LAUNCHED(ctx);
   // threshold from the sample (the first spl codes of every probed list)
-  const int spl = std::min(256, std::max(1, THETA_SAMPLE_CAP / std::max(ma, 1)));
+  static const int theta_cap = getenv("PQS_THETA_CAP") ? std::min(THETA_SAMPLE_CAP, atoi(getenv("PQS_THETA_CAP")))
+                                                        : THETA_SAMPLE_CAP;  // tuning experiments
+  const int spl = std::min(256, std::max(1, theta_cap / std::max(ma, 1)));
   float* theta = nullptr;
   PQS_TRY(scratch(ctx, S_THETA, (size_t)nq * 4, (uint8_t**)&theta));
   const size_t usm = (size_t)m * k * 4;
