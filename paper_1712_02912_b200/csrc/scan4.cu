@@ -25,6 +25,8 @@
 namespace {
 
 constexpr int SCAN4_THREADS = 256;
+// K9: 128 threads per query CTA so a 1000-query batch is one wave (12 CTAs/SM)
+constexpr int PARAMS_THREADS = 128;
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
   uint32_t d;
@@ -180,32 +182,42 @@ __device__ unsigned long long kth_smallest(const unsigned long long* keys, int64
   return sh.prefix;
 }
 
-// k-th smallest of M <= blockDim.x keys by rank counting (one key per thread,
-// broadcast reads): the key with #less <= k < #less + #equal
+// k-th smallest of a few hundred keys by rank counting (broadcast reads):
+// the key with #less <= k < #less + #equal.  Each thread ranks two keys in
+// one unrolled pass (the shared loads stay in flight).
 __device__ unsigned long long kth_smallest_small(const unsigned long long* keys, int M, int k, ParamShared& sh) {
-  if (threadIdx.x < M) {
-    const unsigned long long v = keys[threadIdx.x];
-    int less = 0, eq = 0;
+  for (int t0 = threadIdx.x; t0 < M; t0 += 2 * blockDim.x) {
+    const int t1 = t0 + blockDim.x;
+    const unsigned long long v0 = keys[t0], v1 = t1 < M ? keys[t1] : ~0ull;
+    int l0 = 0, e0 = 0, l1 = 0, e1 = 0;
+#pragma unroll 8
     for (int i = 0; i < M; ++i) {
       const unsigned long long w = keys[i];
-      less += w < v ? 1 : 0;
-      eq += w == v ? 1 : 0;
+      l0 += w < v0 ? 1 : 0;
+      e0 += w == v0 ? 1 : 0;
+      l1 += w < v1 ? 1 : 0;
+      e1 += w == v1 ? 1 : 0;
     }
-    if (less <= k && k < less + eq) sh.prefix = v;  // every writer holds the same value
+    if (l0 <= k && k < l0 + e0) sh.prefix = v0;  // every writer holds the same value
+    if (t1 < M && l1 <= k && k < l1 + e1) sh.prefix = v1;
   }
   __syncthreads();
   return sh.prefix;
 }
 
-__global__ void __launch_bounds__(SCAN4_THREADS) qadc_params_kernel(
+__global__ void __launch_bounds__(PARAMS_THREADS) qadc_params_kernel(
     pqs_db db, const float* __restrict__ tables, int64_t nq, int init_count, int r,
     unsigned long long* __restrict__ gscratch, int64_t gscratch_ld, uint8_t* __restrict__ qt_out,
     double* __restrict__ qmm_out) {
   __shared__ ParamShared sh;
   __shared__ unsigned long long s_keys[2048];
+  __shared__ float sT[32 * 16];
+  __shared__ __align__(16) uint32_t s_src[2048];  // prefix codes (<= 256 codes: words or bytes)
   const int64_t q = blockIdx.x;
   const int m = db.m;
-  const float* T = tables + q * (int64_t)m * 16;
+  const float* Tg = tables + q * (int64_t)m * 16;
+  for (int i = threadIdx.x; i < m * 16; i += blockDim.x) sT[i] = Tg[i];
+  const float* T = sT;
   // qmin
   float mn = __int_as_float(0x7f800000);
   for (int i = threadIdx.x; i < m * 16; i += blockDim.x) mn = fminf(mn, T[i]);
@@ -222,18 +234,48 @@ __global__ void __launch_bounds__(SCAN4_THREADS) qadc_params_kernel(
   const int64_t n_src = db.prefix ? db.n_prefix : db.n;
   const int64_t n_init = min((int64_t)init_count, n_src);
   unsigned long long* keys = n_init <= 2048 ? s_keys : gscratch + q * gscratch_ld;
-  for (int64_t i = threadIdx.x; i < n_init; i += blockDim.x) {
-    double acc = 0.0;
-    for (int j = 0; j < m; ++j) {
-      const int c = db.prefix ? db.prefix[i * m + j] : code4_at(db, db.words4, i, j);
-      acc = __dadd_rn(acc, (double)T[j * 16 + c]);
+  const int hp = db.mp / 2;
+  if (n_init <= 256) {
+    // stage the prefix codes with one coalesced pass (the per-code decode
+    // below then reads shared memory instead of dependent global loads)
+    if (db.prefix) {  // 16-byte loads (cudaMalloc'd, row-major prefix)
+      const int nb = (int)n_init * m;
+      for (int i = threadIdx.x; i < nb / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(s_src)[i] = reinterpret_cast<const uint4*>(db.prefix)[i];
+      for (int i = (nb & ~15) + threadIdx.x; i < nb; i += blockDim.x) ((uint8_t*)s_src)[i] = db.prefix[i];
+    } else {
+      const int nw = (int)((n_init + 3) / 4) * hp;
+      for (int i = threadIdx.x; i < nw; i += blockDim.x) s_src[i] = db.words4[i];
     }
-    keys[i] = dkey(acc);
+    __syncthreads();
+    for (int i = threadIdx.x; i < (int)n_init; i += blockDim.x) {
+      double acc = 0.0;
+      for (int j = 0; j < m; ++j) {
+        int c;
+        if (db.prefix) {
+          c = ((const uint8_t*)s_src)[i * m + j];
+        } else {
+          const uint32_t w = s_src[(i >> 2) * hp + (j >> 1)];
+          c = (int)((((j & 1) ? (w >> 16) : w) >> (4 * (i & 3))) & 15u);
+        }
+        acc = __dadd_rn(acc, (double)T[j * 16 + c]);
+      }
+      keys[i] = dkey(acc);
+    }
+  } else {
+    for (int64_t i = threadIdx.x; i < n_init; i += blockDim.x) {
+      double acc = 0.0;
+      for (int j = 0; j < m; ++j) {
+        const int c = db.prefix ? db.prefix[i * m + j] : code4_at(db, db.words4, i, j);
+        acc = __dadd_rn(acc, (double)T[j * 16 + c]);
+      }
+      keys[i] = dkey(acc);
+    }
   }
   __syncthreads();
   double qmax;
   const int64_t kq = n_init >= r ? r - 1 : n_init - 1;
-  if (n_init <= SCAN4_THREADS) {
+  if (n_init <= 256) {
     qmax = dkey_inv(kth_smallest_small(keys, (int)n_init, (int)kq, sh));
   } else {
     qmax = dkey_inv(kth_smallest(keys, n_init, (unsigned long long)kq, sh));
@@ -725,7 +767,7 @@ struct QadcRun {
     const int64_t n_init = std::min<int64_t>(init_count, n_src);
     unsigned long long* pscratch = nullptr;
     if (n_init > 2048) PQS_TRY(scratch(ctx, S_PREFIX, (size_t)(nq * n_init), &pscratch));
-    qadc_params_kernel<<<(unsigned)nq, SCAN4_THREADS, 0, ctx->stream>>>(*db, d_tables, nq, init_count, r, pscratch,
+    qadc_params_kernel<<<(unsigned)nq, PARAMS_THREADS, 0, ctx->stream>>>(*db, d_tables, nq, init_count, r, pscratch,
                                                                        n_init, d_qt, d_qmm);
     PQS_LAUNCHED(ctx);
 

@@ -108,12 +108,15 @@ __device__ void materialise(const SelArgs& a, int64_t q, int64_t M, uint64_t* K,
   }
 }
 
-__global__ void __launch_bounds__(SEL_THREADS) select_kernel(SelArgs a, int sortP) {
+// NT threads per query CTA: 128 for candidate lists (a 1000-query batch is
+// one wave at 8 CTAs/SM), 256 for dense rows and merges
+template <int NT>
+__global__ void __launch_bounds__(NT, NT == 128 ? 8 : 1) select_kernel(SelArgs a, int sortP, int scap) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SelShared sh;
   uint64_t* s_keys = (uint64_t*)smem_raw;
-  int64_t* s_ids = (int64_t*)(s_keys + SMEM_CAP);
-  uint64_t* o_keys = (uint64_t*)(s_ids + SMEM_CAP);
+  int64_t* s_ids = (int64_t*)(s_keys + scap);
+  uint64_t* o_keys = (uint64_t*)(s_ids + scap);
   int64_t* o_ids = (int64_t*)(o_keys + sortP);
 
   const int64_t ql = blockIdx.x;
@@ -139,8 +142,8 @@ __global__ void __launch_bounds__(SEL_THREADS) select_kernel(SelArgs a, int sort
 
   ElemSrc es{&a, q, ql, nullptr, nullptr};
   if (a.src != SEL_DENSE_F64 && a.src != SEL_DENSE_U8) {
-    uint64_t* K = M <= SMEM_CAP ? s_keys : a.gkeys + ql * a.gcap;
-    int64_t* I = M <= SMEM_CAP ? s_ids : a.gids + ql * a.gcap;
+    uint64_t* K = M <= scap ? s_keys : a.gkeys + ql * a.gcap;
+    int64_t* I = M <= scap ? s_ids : a.gids + ql * a.gcap;
     materialise(a, q, M, K, I, sh);
     es.K = K;
     es.I = I;
@@ -256,10 +259,13 @@ int launch_select(pqs_ctx* ctx, const SelArgs& a) {
   int P = 1;
   while (P < a.r) P <<= 1;
   if (P < 2) P = 2;
-  const size_t smem = (size_t)SMEM_CAP * 16 + (size_t)P * 16;
-  PQS_CUDA(ctx, cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const bool narrow = a.src == SEL_CAND_BIN || a.src == SEL_CAND_ADC || a.src == SEL_KEYS;
+  const int scap = narrow ? SMEM_CAP / 2 : SMEM_CAP;  // narrow: 18 KB + P -> 8 CTAs/SM
+  const size_t smem = (size_t)scap * 16 + (size_t)P * 16;
+  auto kern = narrow ? select_kernel<128> : select_kernel<SEL_THREADS>;
+  PQS_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)((size_t)SMEM_CAP * 16 + (size_t)MAX_R * 16)));
-  select_kernel<<<nql, SEL_THREADS, smem, ctx->stream>>>(a, P);
+  kern<<<nql, narrow ? 128 : SEL_THREADS, smem, ctx->stream>>>(a, P, scap);
   PQS_LAUNCHED(ctx);
   return PQS_OK;
 }
