@@ -394,7 +394,15 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
       if (b + i < e) {
         const int64_t pos = b + i;
         float acc = (float)pdist[q * ma + p] + V[pos];
-        for (int j = 0; j < m; ++j) acc += su[j * k + codes[pos * m + j]];
+        if (m == 8) {  // one 8-byte load per sampled code
+          const uint2 cw = *reinterpret_cast<const uint2*>(codes + pos * 8);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc += su[j * k + ((cw.x >> (8 * j)) & 255u)];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc += su[(4 + j) * k + ((cw.y >> (8 * j)) & 255u)];
+        } else {
+          for (int j = 0; j < m; ++j) acc += su[j * k + codes[pos * m + j]];
+        }
         key = fkey(acc);
         ++valid;
       }
