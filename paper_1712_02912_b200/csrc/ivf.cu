@@ -53,6 +53,29 @@ __global__ void cnorm_kernel(const float* __restrict__ coarse, int64_t K, int d,
   cnormf[c] = (float)s;
 }
 
+// index build: nearest of P pivot cells for every cell (fp32; only orders the
+// list scan so that lists probed by nearby queries run close in time)
+__global__ void pivot_assign_kernel(const float* __restrict__ coarse, int64_t K, int d, int P, int* __restrict__ out) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= K) return;
+  const float* x = coarse + c * d;
+  float best = __int_as_float(0x7f800000);
+  int arg = 0;
+  for (int p = 0; p < P; ++p) {
+    const float* y = coarse + ((int64_t)p * K / P) * d;
+    float s = 0.f;
+    for (int t = 0; t < d; ++t) {
+      const float df = x[t] - __ldg(y + t);
+      s = fmaf(df, df, s);
+    }
+    if (s < best) {
+      best = s;
+      arg = p;
+    }
+  }
+  out[c] = arg;
+}
+
 // V[pos] = 2 sum_j <g_cj, C_j[code_j]>, fp64 -> fp32; one CTA per list
 __global__ void v_kernel(const float* __restrict__ coarse, const float* __restrict__ books,
                          const int64_t* __restrict__ offsets, const uint8_t* __restrict__ codes, int m, int k,
@@ -560,7 +583,7 @@ __global__ void __launch_bounds__(LIST_THREADS, 2) ivf_list_kernel(
     const float* __restrict__ U, const int64_t* __restrict__ starts, const int* __restrict__ pq,
     const float* __restrict__ pa, const int64_t* __restrict__ offsets, const uint8_t* __restrict__ codes,
     const float* __restrict__ V, int m_rt, int k_rt, const float* __restrict__ theta, uint64_t* __restrict__ cand,
-    float* __restrict__ cand_apx, int* __restrict__ cand_cnt, int64_t cap) {
+    float* __restrict__ cand_apx, int* __restrict__ cand_cnt, int64_t cap, const int* __restrict__ order) {
   const int m = MT > 0 ? MT : m_rt;
   const int k = KT > 0 ? KT : k_rt;
   extern __shared__ __align__(16) unsigned char lsm[];
@@ -571,7 +594,7 @@ __global__ void __launch_bounds__(LIST_THREADS, 2) ivf_list_kernel(
   float* ssa = (float*)(sst + LQ * LSTAGE);                        // [LQ][LSTAGE] filter distances
   __shared__ int s_cnt[LQ], s_q[LQ];
   __shared__ float s_a[LQ], s_th[LQ];
-  const int64_t c = blockIdx.x;
+  const int64_t c = order ? order[blockIdx.x] : blockIdx.x;  // spatially grouped list order (query-table reuse in L2)
   const int64_t p0 = starts[c], p1 = starts[c + 1];
   if (p0 == p1) return;
   const int64_t b = offsets[c], e = offsets[c + 1];
@@ -975,6 +998,25 @@ int ivf_create_impl(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t
                                                  d, iv->vtab, iv->vmax);
   PQS_LAUNCHED(ctx);
   PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  // list scan order: cells grouped by their nearest of P = sqrt(K) pivot cells
+  // (PQS_LIST_ORDER=0 keeps cell order)
+  static const int use_order = getenv("PQS_LIST_ORDER") ? atoi(getenv("PQS_LIST_ORDER")) : 1;
+  if (use_order && K >= 1024) {
+    int P = 1;
+    while ((int64_t)P * P < K) ++P;
+    int* asg = nullptr;
+    PQS_CUDA(ctx, cudaMalloc(&asg, sizeof(int) * K));
+    pivot_assign_kernel<<<(unsigned)cdiv(K, 128), 128, 0, ctx->stream>>>(iv->coarse, K, d, P, asg);
+    PQS_LAUNCHED(ctx);
+    std::vector<int> ha((size_t)K), ord((size_t)K);
+    const int dl = download(ctx, ha.data(), asg, sizeof(int) * K);
+    cudaFree(asg);
+    PQS_TRY(dl);
+    for (int64_t c = 0; c < K; ++c) ord[c] = (int)c;
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return ha[x] < ha[y]; });
+    PQS_CUDA(ctx, cudaMalloc(&iv->list_order, sizeof(int) * K));
+    PQS_TRY(upload(ctx, iv->list_order, ord.data(), sizeof(int) * K));
+  }
   // gmax on host
   std::vector<float> gn(K);
   PQS_TRY(download(ctx, gn.data(), iv->gnorm, (size_t)K * 4));
@@ -997,6 +1039,7 @@ void ivf_destroy_impl(pqs_ivf* iv) {
   cudaFree(iv->ids);
   cudaFree(iv->vtab);
   cudaFree(iv->vmax);
+  if (iv->list_order) cudaFree(iv->list_order);
   delete iv;
 }
 
@@ -1132,7 +1175,7 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
   PQS_CUDA(ctx, cudaFuncSetAttribute(list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
   PQS_TRY(scan_timer_begin(ctx));
   list_kernel<<<(unsigned)K, LIST_THREADS, lsm, ctx->stream>>>(U, starts, pq_, pa, iv->offsets, iv->codes, iv->vtab,
-                                                              m, k, theta, cand, capx, cnt, cap);
+                                                              m, k, theta, cand, capx, cnt, cap, iv->list_order);
   PQS_LAUNCHED(ctx);
   PQS_TRY(scan_timer_end(ctx));
   ctx->last_scan_launches = 1;

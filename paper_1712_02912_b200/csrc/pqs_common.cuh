@@ -137,6 +137,7 @@ struct pqs_ivf {
   uint8_t* codes = nullptr;       // (n, m) row-major, list order
   int64_t* ids = nullptr;         // (n,)
   int64_t max_list = 0;
+  int* list_order = nullptr;      // (K,) list-scan order (cells grouped by nearest pivot) or null
 };
 
 // ---------------------------------------------------------------------------
