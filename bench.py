@@ -649,7 +649,7 @@ def main():
         roofline = {"bound": "tensor", "achieved": achieved, "peak": i8_peak, "unit": "TOP/s (int8)",
                     "frac": achieved / i8_peak,
                     "traffic": traffic_db.get("scan4tc_kernel", {}).get("bytes"),
-                    "traffic_note": "DRAM bytes of the filter launches of one search from the committed ncu capture (profiles/r01_scan4tc_cfg1.md)",
+                    "traffic_note": "DRAM bytes of the filter launches of one search from the committed ncu capture (profiles/r01_final_cfg1.md)",
                     "kernel": "scan4tc_kernel (tcgen05.mma kind::i8, M=128 N=256 K=256 per tile)",
                     "per_unit": "2 x 256 int8 MACs per (query, code) over 256-query groups and 128-code tiles "
                                 f"({work:.3e} ops per launch)",
