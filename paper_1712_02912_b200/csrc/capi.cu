@@ -323,6 +323,7 @@ int pqs_db_create(pqs_ctx* ctx, const uint8_t* codes, int64_t n, int m, int b, c
     cudaStreamSynchronize(ctx->stream);
     if (tmp) cudaFree(tmp);
     if (db->codes8) cudaFree(db->codes8);
+    if (db->codes_rm) cudaFree(db->codes_rm);
     if (db->words4) cudaFree(db->words4);
     if (db->ids) cudaFree(db->ids);
     delete db;
@@ -345,6 +346,9 @@ int pqs_db_create(pqs_ctx* ctx, const uint8_t* codes, int64_t n, int m, int b, c
         return fail(PQS_ERR_NOMEM, "code allocation failed");
       const int s = build_db8(ctx, db, d_codes);
       if (s != PQS_OK) return fail(s, ctx->err);
+      if (cudaMalloc(&db->codes_rm, (size_t)n * m) != cudaSuccess) return fail(PQS_ERR_NOMEM, "code allocation failed");
+      if (cudaMemcpyAsync(db->codes_rm, d_codes, (size_t)n * m, cudaMemcpyDeviceToDevice, ctx->stream) != cudaSuccess)
+        return fail(PQS_ERR_CUDA, "code copy failed");
     }
   } else {
     int mp = 2;
@@ -449,6 +453,7 @@ int pqs_db_set_prefix(pqs_ctx* ctx, pqs_db* db, const uint8_t* prefix, int64_t n
 void pqs_db_destroy(pqs_db* db) {
   if (!db) return;
   if (db->codes8) cudaFree(db->codes8);
+  if (db->codes_rm) cudaFree(db->codes_rm);
   if (db->words4) cudaFree(db->words4);
   if (db->ids) cudaFree(db->ids);
   if (db->prefix) cudaFree(db->prefix);

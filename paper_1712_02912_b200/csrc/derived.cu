@@ -463,6 +463,7 @@ int run_derived_search(pqs_ctx* ctx, const pqs_db* db, const float* d_full, int 
   s.cap = cap;
   s.tables = d_full;
   s.codes8 = db->codes8;
+  s.codes_rm = db->codes_rm;
   s.m = m;
   s.k = k;
   s.ids = db->ids;

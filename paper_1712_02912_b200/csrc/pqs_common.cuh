@@ -114,6 +114,7 @@ struct pqs_db {
   int max_code = 0;       // largest stored component value
   int64_t ntiles = 0;
   uint8_t* codes8 = nullptr;    // b==8 tile-transposed
+  uint8_t* codes_rm = nullptr;  // b==8 row-major copy (n, m): exact re-score reads one row per candidate
   uint32_t* words4 = nullptr;   // b==4 quad words (ntiles*QUADS4, mp/2)
   int64_t* ids = nullptr;       // explicit ids or nullptr
   int64_t id_base = 0;
@@ -290,6 +291,7 @@ struct SelArgs {
   // rerank (SEL_CAND_ADC)
   const float* tables = nullptr;  // (nq, m, k)
   const uint8_t* codes8 = nullptr;
+  const uint8_t* codes_rm = nullptr;  // optional row-major codes (faster exact re-score)
   int m = 0, k = 0;
   // precomputed ids (SEL_KEYS; keys in cand)
   const int64_t* pids = nullptr;

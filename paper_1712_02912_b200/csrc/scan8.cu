@@ -617,6 +617,7 @@ int run_adc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t 
   s.id_base = db->id_base;
   s.tables = d_tables;
   s.codes8 = db->codes8;
+  s.codes_rm = db->codes_rm;
   s.m = m;
   s.k = k;
   s.out_d = d_dist;

@@ -73,6 +73,40 @@ __device__ __forceinline__ double adc_exact(const float* __restrict__ T, const u
   return acc;
 }
 
+// the same sum from a row-major code row: all m code bytes and table entries
+// of a 16-component block are in flight before the ordered fp64 sum
+__device__ __forceinline__ double adc_exact_rm(const float* __restrict__ T, const uint8_t* __restrict__ row, int m,
+                                               int k) {
+  double acc = 0.0;
+  for (int j0 = 0; j0 < m; j0 += 16) {
+    uint32_t w[4];
+    if ((m & 15) == 0) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(row + j0));
+      w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+    } else if ((m & 7) == 0) {
+      const uint2 v0 = __ldg(reinterpret_cast<const uint2*>(row + j0));
+      const uint2 v1 = j0 + 8 < m ? __ldg(reinterpret_cast<const uint2*>(row + j0 + 8)) : make_uint2(0u, 0u);
+      w[0] = v0.x, w[1] = v0.y, w[2] = v1.x, w[3] = v1.y;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint32_t x = 0;
+        for (int b = 0; b < 4; ++b)
+          if (j0 + 4 * u + b < m) x |= (uint32_t)row[j0 + 4 * u + b] << (8 * b);
+        w[u] = x;
+      }
+    }
+    float t[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      t[u] = j0 + u < m ? __ldg(T + (int64_t)(j0 + u) * k + ((w[u >> 2] >> (8 * (u & 3))) & 255u)) : 0.f;
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      if (j0 + u < m) acc = __dadd_rn(acc, (double)t[u]);
+  }
+  return acc;
+}
+
 __device__ void materialise(const SelArgs& a, int64_t q, int64_t M, uint64_t* K, int64_t* I,
                             SelShared& sh) {
   if (a.src == SEL_KEYS) {
@@ -90,7 +124,8 @@ __device__ void materialise(const SelArgs& a, int64_t q, int64_t M, uint64_t* K,
       const int64_t idx = (int64_t)(uint32_t)e;
       uint64_t key;
       if (a.src == SEL_CAND_BIN) key = min(e >> 32, (uint64_t)127);  // bin = min(sum, 127)
-      else key = dkey(adc_exact(T, a.codes8, a.m, a.k, idx));
+      else key = dkey(a.codes_rm ? adc_exact_rm(T, a.codes_rm + idx * a.m, a.m, a.k)
+                                 : adc_exact(T, a.codes8, a.m, a.k, idx));
       K[i] = key;
       I[i] = map_id(a, idx);
     }
