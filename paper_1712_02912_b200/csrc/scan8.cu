@@ -420,18 +420,27 @@ __global__ void theta8_kernel(const uint32_t* __restrict__ sample, int64_t ns, i
                               const int* __restrict__ e0, const double* __restrict__ slack, int* __restrict__ e1,
                               uint32_t* __restrict__ theta) {
   __shared__ unsigned int hist[256];
-  __shared__ unsigned int s_prefix, s_k, s_valid;
+  __shared__ unsigned int s_prefix, s_k, s_valid, s_vmax;
   const int64_t q = blockIdx.x;
   const uint32_t* row = sample + q * ns;
   if (threadIdx.x == 0) {
     s_prefix = 0;
     s_k = (unsigned)(r - 1);
     s_valid = 0;
+    s_vmax = 0;
   }
   __syncthreads();
-  unsigned int valid = 0;
-  for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) valid += row[i] != 0xFFFFFFFFu ? 1u : 0u;
+  unsigned int valid = 0, vmax = 0;
+  for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
+    const uint32_t v = row[i];
+    if (v != 0xFFFFFFFFu) {
+      ++valid;
+      vmax = max(vmax, v);
+    }
+  }
   atomicAdd(&s_valid, valid);
+  for (int o = 16; o > 0; o >>= 1) vmax = max(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(&s_vmax, vmax);
   __syncthreads();
   if (s_valid < (unsigned)r) {
     if (threadIdx.x == 0) {
@@ -440,28 +449,43 @@ __global__ void theta8_kernel(const uint32_t* __restrict__ sample, int64_t ns, i
     }
     return;
   }
-  for (int shift = 24; shift >= 0; shift -= 8) {
+  // MSD radix select over the significant bits only: the first digit is the
+  // top 8 bits below the largest value's leading one (all 256 bins in use,
+  // no hot-bin atomics), then 8-bit digits down to bit 0
+  for (int top = 32 - __clz((int)s_vmax); top > 0;) {
+    const int width = top < 8 ? top : 8, shift = top - width;
     for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     const unsigned prefix = s_prefix;
     for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
       const uint32_t v = row[i];
       if (v == 0xFFFFFFFFu) continue;
-      const bool match = (shift == 24) ? true : ((v ^ prefix) >> (shift + 8)) == 0;
-      if (match) atomicAdd(&hist[(v >> shift) & 255u], 1u);
+      const bool match = top >= 32 ? true : ((v ^ prefix) >> top) == 0;
+      if (match) atomicAdd(&hist[(v >> shift) & ((1u << width) - 1u)], 1u);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned c = 0, kk = s_k;
-      int d = 0;
-      for (; d < 256; ++d) {
-        if (kk < c + hist[d]) break;
-        c += hist[d];
+    if (threadIdx.x < 32) {  // warp-parallel digit search: lane l owns bins 8l..8l+7
+      const int lane = threadIdx.x;
+      unsigned h8[8], s8 = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) s8 += (h8[u] = hist[8 * lane + u]);
+      unsigned incl = s8;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
       }
-      s_k = kk - c;
-      s_prefix = prefix | ((unsigned)d << shift);
+      const unsigned kk = s_k, excl = incl - s8;
+      if (kk >= excl && kk < incl) {
+        unsigned c = excl;
+        int u = 0;
+        while (kk >= c + h8[u]) c += h8[u++];
+        s_k = kk - c;
+        s_prefix = prefix | ((unsigned)(8 * lane + u) << shift);
+      }
     }
     __syncthreads();
+    top = shift;
   }
   if (threadIdx.x == 0) {
     const double Dp = ldexp((double)s_prefix + (double)m, -e0[q]) + slack[q];
