@@ -93,21 +93,25 @@ __device__ void block_radix_select(int64_t M, Get get, unsigned long long k, Sel
     return;
   }
   const int hib = 63 - __clzll((long long)(vmin ^ vmax));
-  int shift = (hib / 8) * 8;
+  // digits of up to 8 bits from the highest differing bit down: the first
+  // digit spans the top 8 varying bits, so all 256 bins are in use (no
+  // hot-bin atomics); bits above hib are common to every key (the prefix)
+  int top = hib + 1;
   if (threadIdx.x == 0) {
-    const int s = shift + 8;
-    sh.prefix = s >= 64 ? 0ull : (vmin >> s) << s;
+    sh.prefix = top >= 64 ? 0ull : (vmin >> top) << top;
     sh.k = k;
     sh.less = 0;
   }
   __syncthreads();
-  for (; shift >= 0; shift -= 8) {
+  while (top > 0) {
+    const int width = top < 8 ? top : 8, shift = top - width;
+    const unsigned long long dmask = (1ull << width) - 1ull;
     for (int i = threadIdx.x; i < 256; i += blockDim.x) sh.hist[i] = 0;
     __syncthreads();
     const unsigned long long prefix = sh.prefix;
     for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
       uint64_t v;
-      if (get(i, v) && match_above(v, prefix, shift + 8)) atomicAdd(&sh.hist[(v >> shift) & 255u], 1u);
+      if (get(i, v) && match_above(v, prefix, top)) atomicAdd(&sh.hist[(v >> shift) & dmask], 1u);
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -141,6 +145,7 @@ __device__ void block_radix_select(int64_t M, Get get, unsigned long long k, Sel
       }
     }
     __syncthreads();
+    top = shift;
   }
 }
 
