@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
   float* su = (float*)tsm;                                   // [m][k] (lanes read random entries of one row)
   unsigned int* keys = (unsigned int*)(su + (size_t)m * k);  // [ma*spl]
   __shared__ unsigned int hist[256];
-  __shared__ unsigned int s_prefix, s_k, s_valid;
+  __shared__ unsigned int s_prefix, s_k, s_valid, s_kmin, s_kmax;
   const int64_t q = blockIdx.x;
   for (int i = threadIdx.x; i < m * k; i += blockDim.x) {
     const int e = i / m, j = i - e * m;
@@ -404,10 +404,12 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
     s_prefix = 0;
     s_k = (unsigned)(r - 1);
     s_valid = 0;
+    s_kmin = 0xFFFFFFFFu;
+    s_kmax = 0u;
   }
   __syncthreads();
   const int ns = ma * spl;
-  unsigned int valid = 0;
+  unsigned int valid = 0, kmin = 0xFFFFFFFFu, kmax = 0u;
   for (int s2 = threadIdx.x; s2 < ns; s2 += blockDim.x) {
     const int p = s2 / spl, i = s2 - p * spl;
     const int64_t c = cells[q * ma + p];
@@ -428,25 +430,43 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
         }
         key = fkey(acc);
         ++valid;
+        kmin = min(kmin, key);
+        kmax = max(kmax, key);
       }
     }
     keys[s2] = key;
   }
   atomicAdd(&s_valid, valid);
+  for (int o = 16; o > 0; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&s_kmin, kmin);
+    atomicMax(&s_kmax, kmax);
+  }
   __syncthreads();
   if (s_valid < (unsigned)r) {
     if (threadIdx.x == 0) theta[q] = __int_as_float(0x7f800000);
     return;
   }
-  for (int shift = 24; shift >= 0; shift -= 8) {
+  // digits from the highest bit where the keys differ (fkeys share their
+  // sign/exponent bits: a fixed 24-bit first shift would pile them into a
+  // few hot bins); the common high bits seed the prefix
+  const unsigned kdiff = s_kmin ^ s_kmax;
+  int top = kdiff ? 32 - __clz((int)kdiff) : 0;
+  if (threadIdx.x == 0) s_prefix = top >= 32 ? 0u : (s_kmin >> top) << top;
+  __syncthreads();
+  for (; top > 0;) {
+    const int width = top < 8 ? top : 8, shift = top - width;
     for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     const unsigned prefix = s_prefix;
     for (int i = threadIdx.x; i < ns; i += blockDim.x) {
       const unsigned key = keys[i];
       if (key == 0xFFFFFFFFu) continue;
-      const bool match = (shift == 24) ? true : ((key ^ prefix) >> (shift + 8)) == 0;
-      if (match) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+      const bool match = top >= 32 ? true : ((key ^ prefix) >> top) == 0;
+      if (match) atomicAdd(&hist[(key >> shift) & ((1u << width) - 1u)], 1u);
     }
     __syncthreads();
     if (threadIdx.x < 32) {  // lane-parallel digit search: each lane owns 8 bins
@@ -477,6 +497,7 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
       }
     }
     __syncthreads();
+    top = shift;
   }
   if (threadIdx.x == 0) {
     const double t = (double)fkey_inv(s_prefix) + 2.0 * (double)aerr[q];
