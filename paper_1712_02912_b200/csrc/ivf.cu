@@ -190,12 +190,14 @@ struct ProbeArgs {
 
 constexpr int PROBE_THREADS = 512;
 constexpr int PROBE_SMEM_CAP = 4096;
+constexpr int PROBE_QMAX = 1024;  // queries up to this d are staged in shared memory
 
 __global__ void __launch_bounds__(PROBE_THREADS) probe_select_kernel(ProbeArgs a, int sortP) {
   extern __shared__ __align__(16) unsigned char psm[];
   __shared__ SelShared sh;
   __shared__ int s_cnt;
   __shared__ double s_qn;
+  __shared__ __align__(16) float s_q[PROBE_QMAX];
   uint64_t* ck = (uint64_t*)psm;                 // candidates (PROBE_SMEM_CAP)
   int64_t* ci = (int64_t*)(ck + PROBE_SMEM_CAP);
   uint64_t* ok = (uint64_t*)(ci + PROBE_SMEM_CAP);
@@ -206,13 +208,22 @@ __global__ void __launch_bounds__(PROBE_THREADS) probe_select_kernel(ProbeArgs a
   const float* qv = a.queries + ql * (int64_t)a.d;
   const int64_t K = a.K;
   const int ma = a.ma;
-  if (threadIdx.x == 0) {
+  // the query in shared memory (the exact re-score reads it per cell) and its
+  // norm by a warp reduction (only feeds the error bound: any order)
+  const bool q_in_smem = a.d <= PROBE_QMAX;
+  if (q_in_smem)
+    for (int t = threadIdx.x; t < a.d; t += blockDim.x) s_q[t] = qv[t];
+  if (threadIdx.x < 32) {
     double s = 0.0;
-    for (int t = 0; t < a.d; ++t) s += (double)qv[t] * (double)qv[t];
-    s_qn = sqrt(s);
-    s_cnt = 0;
+    for (int t = threadIdx.x; t < a.d; t += 32) s += (double)qv[t] * (double)qv[t];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) {
+      s_qn = sqrt(s);
+      s_cnt = 0;
+    }
   }
   __syncthreads();
+  const float* qx = q_in_smem ? s_q : qv;
   // certified bound on |approx - exact|: fp32 dot (any order) error <= gamma_d ||q|| ||c||
   const double u = 5.9604644775390625e-08;
   // fp32 GEMM: |fl(q.c) - q.c| <= gamma_d ||q|| ||c|| (any summation order).
@@ -237,6 +248,7 @@ __global__ void __launch_bounds__(PROBE_THREADS) probe_select_kernel(ProbeArgs a
     // every true probe has approx <= that + 2 eps (one pass over the dots,
     // ~ma * K / S cells re-scored exactly)
     const int64_t S = K < PROBE_SMEM_CAP ? K : PROBE_SMEM_CAP;
+#pragma unroll 4
     for (int64_t i = threadIdx.x; i < S; i += blockDim.x) ck[i] = akey(approx(i * K / S));
     __syncthreads();
     auto getk = [&](int64_t i, uint64_t& v) {
@@ -263,12 +275,29 @@ __global__ void __launch_bounds__(PROBE_THREADS) probe_select_kernel(ProbeArgs a
   if ((K & 3) == 0) {  // 16-byte loads of the dots row and the norms
     const float4* d4 = reinterpret_cast<const float4*>(dots);
     const float4* n4 = reinterpret_cast<const float4*>(a.cnormf);
-    for (int64_t c4 = threadIdx.x; c4 < K / 4; c4 += blockDim.x) {
-      const float4 dv = d4[c4], nv = __ldg(n4 + c4);
-      gather(nv.x - 2.f * dv.x, 4 * c4);
-      gather(nv.y - 2.f * dv.y, 4 * c4 + 1);
-      gather(nv.z - 2.f * dv.z, 4 * c4 + 2);
-      gather(nv.w - 2.f * dv.w, 4 * c4 + 3);
+    // four 16-byte loads of the dots row in flight per thread (the row
+    // streams from DRAM; the gather's atomics would otherwise serialise them)
+    const int64_t K4 = K / 4, bd = blockDim.x;
+    for (int64_t c0 = threadIdx.x; c0 < K4; c0 += 4 * bd) {
+      float4 dv[4], nv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t c4 = c0 + u * bd;
+        if (c4 < K4) {
+          dv[u] = __ldcs(d4 + c4);
+          nv[u] = __ldg(n4 + c4);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t c4 = c0 + u * bd;
+        if (c4 < K4) {
+          gather(nv[u].x - 2.f * dv[u].x, 4 * c4);
+          gather(nv[u].y - 2.f * dv[u].y, 4 * c4 + 1);
+          gather(nv[u].z - 2.f * dv[u].z, 4 * c4 + 2);
+          gather(nv[u].w - 2.f * dv[u].w, 4 * c4 + 3);
+        }
+      }
     }
   } else {
     for (int64_t c = threadIdx.x; c < K; c += blockDim.x) gather(approx(c), c);
@@ -303,17 +332,24 @@ __global__ void __launch_bounds__(PROBE_THREADS) probe_select_kernel(ProbeArgs a
       if (akey_inv(AK[i]) <= thr2) {
         const float* g = a.coarse + AI[i] * (int64_t)a.d;
         double s2 = 0.0;
-        for (int t0 = 0; t0 < a.d; t0 += 8) {
-          float qa[8], ga[8];
+        // 32 coordinates of the cell row in flight (16-byte loads when the
+        // rows are 16-byte aligned), then the sequential fp64 sum (scipy order)
+        for (int t0 = 0; t0 < a.d; t0 += 32) {
+          float ga[32];
+          if ((a.d & 3) == 0 && t0 + 32 <= a.d) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            qa[u] = t0 + u < a.d ? qv[t0 + u] : 0.f;
-            ga[u] = t0 + u < a.d ? g[t0 + u] : 0.f;
+            for (int u = 0; u < 8; ++u) {
+              const float4 v = __ldg(reinterpret_cast<const float4*>(g + t0) + u);
+              ga[4 * u] = v.x, ga[4 * u + 1] = v.y, ga[4 * u + 2] = v.z, ga[4 * u + 3] = v.w;
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < 32; ++u) ga[u] = t0 + u < a.d ? __ldg(g + t0 + u) : 0.f;
           }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < 32; ++u) {
             if (t0 + u < a.d) {
-              const double df = __dsub_rn((double)qa[u], (double)ga[u]);
+              const double df = __dsub_rn((double)qx[t0 + u], (double)ga[u]);
               s2 = __dadd_rn(s2, __dmul_rn(df, df));
             }
           }
