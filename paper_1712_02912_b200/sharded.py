@@ -29,18 +29,24 @@ def shard_range(n_total: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def all_gather_results(dist, ids, cnt, group=None):
-    """Gather (G, nq, r) dist/ids and (G, nq) counts from every rank."""
+    """Gather (G, nq, r) dist/ids and (G, nq) counts from every rank with ONE
+    collective: each rank packs [fp64 distance bits | ids | count] into an
+    (nq, 2r + 1) int64 block (the per-step exchange is latency-, not
+    bandwidth-bound, so one all-gather instead of three)."""
     import torch
     import torch.distributed as dist_
 
     world = dist_.get_world_size(group)
-    gd = [torch.empty_like(dist) for _ in range(world)]
-    gi = [torch.empty_like(ids) for _ in range(world)]
-    gc = [torch.empty_like(cnt) for _ in range(world)]
-    dist_.all_gather(gd, dist, group=group)
-    dist_.all_gather(gi, ids, group=group)
-    dist_.all_gather(gc, cnt, group=group)
-    return torch.stack(gd), torch.stack(gi), torch.stack(gc)
+    nq, r = dist.shape
+    packed = torch.cat([dist.to(torch.float64).contiguous().view(torch.int64), ids.to(torch.int64),
+                        cnt.to(torch.int64).reshape(nq, 1)], dim=1).contiguous()
+    out = torch.empty((world * nq, packed.shape[1]), dtype=torch.int64, device=packed.device)
+    dist_.all_gather_into_tensor(out, packed, group=group)  # rank blocks concatenated along dim 0
+    out = out.view(world, nq, packed.shape[1])
+    gd = out[:, :, :r].contiguous().view(torch.float64)
+    gi = out[:, :, r:2 * r].contiguous()
+    gc = out[:, :, 2 * r].to(cnt.dtype).contiguous()
+    return gd, gi, gc
 
 
 class ShardedSearch:
