@@ -48,6 +48,23 @@ def _empty(shape, dtype, like):
     return np.empty(shape, dtype=dtype)
 
 
+def _check_out(out, shapes, dtypes, like):
+    """Validate caller-provided output arrays (same side as `like`, C-contiguous)."""
+    if len(out) != len(shapes):
+        raise ValueError("out must hold one array per result")
+    for o, shp, dt in zip(out, shapes, dtypes):
+        if _is_device(o) != _is_device(like):
+            raise ValueError("out arrays must live on the same side (host / device) as the queries")
+        if tuple(o.shape) != tuple(shp):
+            raise ValueError(f"out array of shape {tuple(o.shape)}, expected {tuple(shp)}")
+        if _is_device(o):
+            if not o.is_contiguous() or str(o.dtype) != "torch." + np.dtype(dt).name:
+                raise ValueError("out tensors must be contiguous with the result dtypes")
+        elif o.dtype != np.dtype(dt) or not o.flags["C_CONTIGUOUS"]:
+            raise ValueError("out arrays must be C-contiguous with the result dtypes")
+    return out
+
+
 def _host_f32(a, ndim, what):
     if _is_device(a):
         if a.dtype.__str__() != "torch.float32" or not a.is_contiguous():
@@ -176,13 +193,17 @@ class DeviceCodes:
                                                  ptr(i), ptr(c), _io(self.ctx, t, d)), "adc_scan")
         return d, i, c
 
-    def adc_search(self, dq: DeviceQuantizer, queries, r: int):
-        """Batched compute_tables + scan: (nq, d) queries -> (dist, ids, count)."""
+    def adc_search(self, dq: DeviceQuantizer, queries, r: int, out=None):
+        """Batched compute_tables + scan: (nq, d) queries -> (dist, ids, count);
+        out: optional caller-owned output arrays as in qadc_search."""
         q = _host_f32(queries, 2, "queries")
         nq = q.shape[0]
-        d = _empty((nq, r), np.float64, q)
-        i = _empty((nq, r), np.int64, q)
-        c = _empty((nq,), np.int32, q)
+        if out is not None:
+            d, i, c = _check_out(out, ((nq, r), (nq, r), (nq,)), (np.float64, np.int64, np.int32), q)
+        else:
+            d = _empty((nq, r), np.float64, q)
+            i = _empty((nq, r), np.int64, q)
+            c = _empty((nq,), np.int32, q)
         self.ctx.check(self.ctx.lib.pqs_adc_search(self.ctx.handle, self.handle, dq.handle, ptr(q), nq, int(r), ptr(d),
                                                    ptr(i), ptr(c), _io(self.ctx, q, d)), "adc_search")
         return d, i, c
@@ -205,12 +226,19 @@ class DeviceCodes:
                        "qadc_scan")
         return bins, i, c, qt, qmm
 
-    def qadc_search(self, dq: DeviceQuantizer, queries, init_count: int, r: int, want_tables: bool = False):
+    def qadc_search(self, dq: DeviceQuantizer, queries, init_count: int, r: int, want_tables: bool = False,
+                    out=None):
+        """Batched compute_tables + qadc_scan.  out: optional caller-owned
+        (bins uint8 (nq, r), ids int64 (nq, r), count int32 (nq,)) arrays on
+        the queries' side (e.g. pinned host buffers reused across calls)."""
         q = _host_f32(queries, 2, "queries")
         nq = q.shape[0]
-        bins = _empty((nq, r), np.uint8, q)
-        i = _empty((nq, r), np.int64, q)
-        c = _empty((nq,), np.int32, q)
+        if out is not None:
+            bins, i, c = _check_out(out, ((nq, r), (nq, r), (nq,)), (np.uint8, np.int64, np.int32), q)
+        else:
+            bins = _empty((nq, r), np.uint8, q)
+            i = _empty((nq, r), np.int64, q)
+            c = _empty((nq,), np.int32, q)
         qt = _empty((nq, self.m, 16), np.uint8, q) if want_tables else None
         qmm = _empty((nq, 2), np.float64, q) if want_tables else None
         self.ctx.check(self.ctx.lib.pqs_qadc_search(self.ctx.handle, self.handle, dq.handle, ptr(q), nq,
@@ -283,16 +311,20 @@ class DeviceIvf:
         return cells, dist
 
     def search(self, queries, ma: int, r: int, kernel: str = "adc", init_count: int = 200, r2: int = 9000,
-               dpq=None):
-        """Batched query_ivf: kernel 'adc' (exact fp64 distances) or 'quick-adc'
-        (per-list Quick ADC bins rescaled to fp64, ivf.py:185-190)."""
+               dpq=None, out=None):
+        """Batched query_ivf: kernel 'adc' (exact fp64 distances), 'quick-adc'
+        (per-list Quick ADC bins rescaled to fp64, ivf.py:185-190) or 'derived'
+        (ivf.py:191-195).  out: optional caller-owned (dist, ids, count) arrays."""
         q = _host_f32(queries, 2, "queries")
         if q.shape[1] != self.d:
             raise ValueError(f"query must have shape ({self.d},)")
         nq = q.shape[0]
-        d = _empty((nq, r), np.float64, q)
-        i = _empty((nq, r), np.int64, q)
-        c = _empty((nq,), np.int32, q)
+        if out is not None:
+            d, i, c = _check_out(out, ((nq, r), (nq, r), (nq,)), (np.float64, np.int64, np.int32), q)
+        else:
+            d = _empty((nq, r), np.float64, q)
+            i = _empty((nq, r), np.int64, q)
+            c = _empty((nq,), np.int32, q)
         io = _io(self.ctx, q, d)
         if kernel == "adc":
             st = self.ctx.lib.pqs_ivf_search(self.ctx.handle, self.handle, ptr(q), nq, int(ma), int(r), ptr(d),

@@ -259,3 +259,34 @@ def test_merge_equals_unsharded(data4):
     np.testing.assert_array_equal(mc, fc)
     np.testing.assert_array_equal(mi, fi)
     np.testing.assert_array_equal(md.astype(np.uint8), fb)
+
+
+def test_search_into_caller_buffers():
+    """qadc_search / adc_search write into caller-owned (pinned) host buffers
+    exactly what they return otherwise; bad buffers are refused."""
+    import torch
+
+    rng = np.random.default_rng(12)
+    x = mixture(rng, 20000, 32, comps=16)
+    books4 = kmeans_books(x[:4000], 8, 16, iters=3)
+    books8 = kmeans_books(x[:4000], 4, 256, iters=2)
+    qs = x[:9] + 1.0
+    db4 = P.DeviceCodes(encode(books4, x), 4)
+    dq4 = P.DeviceQuantizer(P.ProductQuantizer(8, 4, 32, books4))
+    ref = db4.qadc_search(dq4, qs, 200, 50)
+    out = (torch.empty((9, 50), dtype=torch.uint8).pin_memory().numpy(),
+           torch.empty((9, 50), dtype=torch.int64).pin_memory().numpy(),
+           torch.empty((9,), dtype=torch.int32).pin_memory().numpy())
+    got = db4.qadc_search(dq4, qs, 200, 50, out=out)
+    for a, b in zip(ref[:3], got[:3]):
+        np.testing.assert_array_equal(a, b)
+    assert got[0] is out[0]
+    db8 = P.DeviceCodes(encode(books8, x), 8)
+    dq8 = P.DeviceQuantizer(P.ProductQuantizer(4, 8, 32, books8))
+    ref8 = db8.adc_search(dq8, qs, 20)
+    out8 = (np.empty((9, 20)), np.empty((9, 20), np.int64), np.empty(9, np.int32))
+    got8 = db8.adc_search(dq8, qs, 20, out=out8)
+    for a, b in zip(ref8, got8):
+        np.testing.assert_array_equal(a, b)
+    with pytest.raises(ValueError):
+        db8.adc_search(dq8, qs, 20, out=(np.empty((9, 20), np.float32), out8[1], out8[2]))
