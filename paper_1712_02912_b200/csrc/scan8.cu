@@ -353,16 +353,21 @@ __global__ void __launch_bounds__(SCAN8_THREADS, 1) scan8_kernel(Scan8Args a) {
         const int mcur = min(mc, m - ch * mc);
         const uint32_t tbase = smem_u32(sm8 + b * tab_bytes) + 2u * lane;
         const uint8_t* cb = code_base + b * code_bytes + warp * C8;
+        // component pairs outermost: all C8 partial sums stay in fixed registers
+        int jj = 0;
+        for (; jj + 1 < mcur; jj += 2) {
 #pragma unroll
-        for (int v = 0; v < C8 / 16; ++v) {
-          const uint8_t* cv = cb + v * 16;
-          int jj = 0;
-          for (; jj + 1 < mcur; jj += 2)
+          for (int v = 0; v < C8 / 16; ++v) {
+            const uint8_t* cv = cb + v * 16;
             lookup16x2(tbase + (uint32_t)jj * row_bytes, *reinterpret_cast<const uint4*>(cv + jj * TILE8),
                        tbase + (uint32_t)(jj + 1) * row_bytes,
                        *reinterpret_cast<const uint4*>(cv + (jj + 1) * TILE8), part + v * 16);
-          if (jj < mcur)
-            lookup16(tbase + (uint32_t)jj * row_bytes, *reinterpret_cast<const uint4*>(cv + jj * TILE8),
+          }
+        }
+        if (jj < mcur) {
+#pragma unroll
+          for (int v = 0; v < C8 / 16; ++v)
+            lookup16(tbase + (uint32_t)jj * row_bytes, *reinterpret_cast<const uint4*>(cb + v * 16 + jj * TILE8),
                      part + v * 16);
         }
         if (ch == nch - 1) {
