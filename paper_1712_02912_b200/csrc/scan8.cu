@@ -370,11 +370,6 @@ __global__ void __launch_bounds__(SCAN8_THREADS, 1) scan8_kernel(Scan8Args a) {
             lookup16(tbase + (uint32_t)jj * row_bytes, *reinterpret_cast<const uint4*>(cb + v * 16 + jj * TILE8),
                      part + v * 16);
         }
-        if (ch == nch - 1) {
-          emit(part, tile * TILE8 + warp * C8, vi * TILE8 + warp * C8);
-#pragma unroll
-          for (int c = 0; c < C8; ++c) part[c] = 0u;
-        }
         __syncthreads();
         if (threadIdx.x == 0 && s + 2 < S) {
           int64_t w2;
@@ -383,6 +378,11 @@ __global__ void __launch_bounds__(SCAN8_THREADS, 1) scan8_kernel(Scan8Args a) {
           issue_at(b, w2, ch2);
         }
       }
+      // the epilogue reads registers and the stage area only, so it runs after
+      // the chunk loop: the lookup loop carries no epilogue register pressure
+      emit(part, tile * TILE8 + warp * C8, vi * TILE8 + warp * C8);
+#pragma unroll
+      for (int c = 0; c < C8; ++c) part[c] = 0u;
     }
   }
   flush();
