@@ -321,21 +321,30 @@ __global__ void __launch_bounds__(SCAN8_THREADS, 1) scan8_kernel(Scan8Args a) {
       mbar_wait(&bars[b], (uint32_t)((s >> 1) & 1));
       const uint32_t tbase = smem_u32(sm8) + 2u * lane;
       const uint8_t* cb = code_base + b * code_bytes + warp * C8;
-      for (int v = 0; v < C8 / 16; ++v) {
-        uint32_t acc[16];
+      // component pairs outermost over all C8 codes of the warp (64 sums in
+      // fixed registers); the epilogue runs once per tile after the barrier
+      uint32_t acc[C8];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) acc[e] = 0u;
-        const uint8_t* cv = cb + v * 16;
-        int jj = 0;
-        for (; jj + 1 < m; jj += 2)
+      for (int e = 0; e < C8; ++e) acc[e] = 0u;
+      int jj = 0;
+      for (; jj + 1 < m; jj += 2) {
+#pragma unroll
+        for (int v = 0; v < C8 / 16; ++v) {
+          const uint8_t* cv = cb + v * 16;
           lookup16x2(tbase + (uint32_t)jj * row_bytes, *reinterpret_cast<const uint4*>(cv + jj * TILE8),
                      tbase + (uint32_t)(jj + 1) * row_bytes, *reinterpret_cast<const uint4*>(cv + (jj + 1) * TILE8),
-                     acc);
-        if (jj < m) lookup16(tbase + (uint32_t)jj * row_bytes, *reinterpret_cast<const uint4*>(cv + jj * TILE8), acc);
-        emit(acc, tile * TILE8 + warp * C8 + v * 16, vi * TILE8 + warp * C8 + v * 16);
+                     acc + v * 16);
+        }
+      }
+      if (jj < m) {
+#pragma unroll
+        for (int v = 0; v < C8 / 16; ++v)
+          lookup16(tbase + (uint32_t)jj * row_bytes, *reinterpret_cast<const uint4*>(cb + v * 16 + jj * TILE8),
+                   acc + v * 16);
       }
       __syncthreads();
       if (threadIdx.x == 0 && s + 2 < S) issue_at(b, w + 2, 0);
+      emit(acc, tile * TILE8 + warp * C8, vi * TILE8 + warp * C8);
     }
   } else {
     uint32_t part[C8];
