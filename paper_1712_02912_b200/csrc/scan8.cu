@@ -110,25 +110,42 @@ __global__ void tables_u16_stats_kernel(const float* __restrict__ tables, int64_
   }
 }
 
-// t'[qg][j][c][lane] = min(65535, floor((T - o_j) * 2^e_q)); exact in fp64
-__global__ void tables_u16_kernel(const float* __restrict__ tables, const float* __restrict__ off,
-                                  const int* __restrict__ ex, int64_t nq, int m, int k, uint16_t* __restrict__ tt) {
-  const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t total = cdiv(nq, 32) * m * (int64_t)k * 32;
-  if (gid >= total) return;
-  const int lane = (int)(gid & 31);
-  int64_t t = gid >> 5;
-  const int c = (int)(t % k);
-  t /= k;
-  const int j = (int)(t % m);
-  const int64_t q = (t / m) * 32 + lane;
-  uint16_t v = 0;
-  if (q < nq) {
-    const double d = ((double)tables[(q * m + j) * (int64_t)k + c] - (double)off[q * m + j]);
-    const double f = floor(ldexp(d, ex[q]));
-    v = f >= 65535.0 ? (uint16_t)65535 : (uint16_t)f;
+// t'[qg][j][c][lane] = min(65535, floor((T - o_j) * 2^e_q)); exact in fp64.
+// One CTA per (query group, component): the 32 queries' rows of k entries are
+// read coalesced and transposed through shared memory, so the [c][lane]
+// output is written coalesced too
+constexpr int TU16_THREADS = 256;
+__global__ void __launch_bounds__(TU16_THREADS) tables_u16_t_kernel(const float* __restrict__ tables,
+                                                                   const float* __restrict__ off,
+                                                                   const int* __restrict__ ex, int64_t nq, int m,
+                                                                   int k, uint16_t* __restrict__ tt) {
+  __shared__ float st[32][257];  // k <= 256
+  __shared__ double so[32];
+  __shared__ int se[32];
+  const int64_t qg = blockIdx.x / m;
+  const int j = (int)(blockIdx.x - qg * m);
+  if (threadIdx.x < 32) {
+    const int64_t q = qg * 32 + threadIdx.x;
+    so[threadIdx.x] = q < nq ? (double)off[q * m + j] : 0.0;
+    se[threadIdx.x] = q < nq ? ex[q] : 0;
   }
-  tt[gid] = v;
+  for (int i = threadIdx.x; i < 32 * k; i += TU16_THREADS) {
+    const int l = i / k, c = i - l * k;
+    const int64_t q = qg * 32 + l;
+    st[l][c] = q < nq ? tables[(q * m + j) * (int64_t)k + c] : 0.f;
+  }
+  __syncthreads();
+  uint16_t* dst = tt + (qg * m + j) * (int64_t)k * 32;
+  for (int i = threadIdx.x; i < 32 * k; i += TU16_THREADS) {
+    const int l = i & 31, c = i >> 5;
+    uint16_t v = 0;
+    if (qg * 32 + l < nq) {
+      const double d = (double)st[l][c] - so[l];
+      const double f = floor(ldexp(d, se[l]));
+      v = f >= 65535.0 ? (uint16_t)65535 : (uint16_t)f;
+    }
+    dst[i] = v;
+  }
 }
 
 // --------------------------------------------------------------- K3 kernel
@@ -576,7 +593,7 @@ int run_adc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t 
   tables_u16_stats_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(d_tables, nq, m, k, off, e0, slack);
   PQS_LAUNCHED(ctx);
   const int64_t tt_total = cdiv(nq, 32) * m * (int64_t)k * 32;
-  tables_u16_kernel<<<(unsigned)cdiv(tt_total, 256), 256, 0, ctx->stream>>>(d_tables, off, e0, nq, m, k, tt);
+  tables_u16_t_kernel<<<(unsigned)(cdiv(nq, 32) * m), TU16_THREADS, 0, ctx->stream>>>(d_tables, off, e0, nq, m, k, tt);
   PQS_LAUNCHED(ctx);
 
   const int64_t cap = std::min<int64_t>(ctx->cand_cap, n);
@@ -607,7 +624,7 @@ int run_adc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t 
     theta8_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(sample, ns, (int)r_eff, m, e0, slack, e1, theta);
     PQS_LAUNCHED(ctx);
     // rebuild the tables at the filter scale e1
-    tables_u16_kernel<<<(unsigned)cdiv(tt_total, 256), 256, 0, ctx->stream>>>(d_tables, off, e1, nq, m, k, tt);
+    tables_u16_t_kernel<<<(unsigned)(cdiv(nq, 32) * m), TU16_THREADS, 0, ctx->stream>>>(d_tables, off, e1, nq, m, k, tt);
     PQS_LAUNCHED(ctx);
   }
 
