@@ -17,7 +17,15 @@ $(OUT_DIR)/obj/%.o: $(SRC_DIR)/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(LIB): $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcublas -Xlinker -rpath,/usr/local/cuda/lib64
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -Xlinker -rpath,/usr/local/cuda/lib64
+
+PEAKS    := tools/bin/pqs_peaks
+
+peaks: $(PEAKS)
+
+$(PEAKS): tools/peaks.cu
+	@mkdir -p tools/bin
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -o $@ $<
 
 ptxas: $(SRCS)
 	@for f in $(SRCS); do $(NVCC) $(NVFLAGS) -Xptxas -v -c $$f -o /dev/null 2>&1 | grep -E "Compiling|registers|spill" ; done
@@ -25,4 +33,4 @@ ptxas: $(SRCS)
 clean:
 	rm -rf $(OUT_DIR)
 
-.PHONY: all clean ptxas
+.PHONY: all clean ptxas peaks

@@ -24,6 +24,12 @@
  *     one set with pqs_ctx_set_stream).  A context is single-writer, like
  *     the reference NeighborSet; separate contexts may run
  *     concurrently.
+ *   - Query (and vector) rows: every entry point that takes them as
+ *     `const float*` has a `_f64` twin taking `const double*`.  The reference
+ *     computes from float64(query) (ProductQuantizer.rotate,
+ *     quantizer.py:85-89; query_ivf ivf.py:170; encode quantizer.py:319-323),
+ *     so the exact kernels read the rows in fp64 either way; float32 rows are
+ *     widened exactly, float64 rows are used as given.
  *   - Results are (nq, r) row-major arrays ascending by (distance, id);
  *     out_count[q] = number of valid entries (min(r, candidates)); unused
  *     slots hold distance +inf (bins 255) and id -1.
@@ -37,7 +43,7 @@
 extern "C" {
 #endif
 
-#define PQS_API_VERSION 2
+#define PQS_API_VERSION 3
 
 typedef struct pqs_ctx pqs_ctx;
 typedef struct pqs_pq pqs_pq;
@@ -116,6 +122,8 @@ void pqs_db_destroy(pqs_db* db);
  * queries (nq, d) float32 -> out_tables (nq, m, k) float32, bit-identical. */
 int pqs_compute_tables(pqs_ctx* ctx, const pqs_pq* pq, const float* queries, int64_t nq,
                        float* out_tables, int io);
+int pqs_compute_tables_f64(pqs_ctx* ctx, const pqs_pq* pq, const double* queries, int64_t nq,
+                           float* out_tables, int io);
 
 /* ---- dense fp64 ADC: scan_distances (scan.py:68-81), b == 8 list
  * tables (nq, m, k) float32 (k <= 256, every code < k) -> out (nq, n)
@@ -130,6 +138,9 @@ int pqs_adc_scan(pqs_ctx* ctx, const pqs_db* db, const float* tables, int64_t nq
 int pqs_adc_search(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* pq, const float* queries,
                    int64_t nq, int r, double* out_dist, int64_t* out_ids, int32_t* out_count,
                    int io);
+int pqs_adc_search_f64(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* pq, const double* queries,
+                       int64_t nq, int r, double* out_dist, int64_t* out_ids, int32_t* out_count,
+                       int io);
 
 /* ---- Quick ADC: qadc_scan (quickadc.py:104-141), b == 4 list, given tables
  * (nq, m, 16) float32.  Outputs bins (nq, r) uint8 ascending by (bin, id),
@@ -142,6 +153,9 @@ int pqs_qadc_scan(pqs_ctx* ctx, const pqs_db* db, const float* tables, int64_t n
 int pqs_qadc_search(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* pq, const float* queries,
                     int64_t nq, int init_count, int r, uint8_t* out_bins, int64_t* out_ids,
                     int32_t* out_count, uint8_t* out_qtables, double* out_qminmax, int io);
+int pqs_qadc_search_f64(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* pq, const double* queries,
+                        int64_t nq, int init_count, int r, uint8_t* out_bins, int64_t* out_ids,
+                        int32_t* out_count, uint8_t* out_qtables, double* out_qminmax, int io);
 
 /* ---- quantize (fastscan.py:48-57): 127-bin fp64 quantization of values
  * (n,) float64 with QuantParams(qmin, qmax) -> out (n,) uint8.            */
@@ -165,8 +179,12 @@ void pqs_ivf_destroy(pqs_ivf* ivf);
  * out_dist (nq, ma) float64 (may be NULL), ascending by (distance, cell).  */
 int pqs_ivf_probe(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_t nq, int ma,
                   int64_t* out_cells, double* out_dist, int io);
+int pqs_ivf_probe_f64(pqs_ctx* ctx, const pqs_ivf* ivf, const double* queries, int64_t nq, int ma,
+                      int64_t* out_cells, double* out_dist, int io);
 int pqs_ivf_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_t nq, int ma,
                    int r, double* out_dist, int64_t* out_ids, int32_t* out_count, int io);
+int pqs_ivf_search_f64(pqs_ctx* ctx, const pqs_ivf* ivf, const double* queries, int64_t nq, int ma,
+                       int r, double* out_dist, int64_t* out_ids, int32_t* out_count, int io);
 /* ---- PQ Fast Scan statistics (fast_scan, fastscan.py:328-386): the number
  * of codes whose exact distance the reference's pruned scan evaluates
  * (ScanStats.checked; pruned = n - checked).  db: the grouped database's
@@ -184,11 +202,17 @@ int pqs_fastscan_checked(pqs_ctx* ctx, const pqs_db* db, const float* tables, in
 int pqs_derived_search(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* full, const pqs_pq* derived,
                        const float* queries, int64_t nq, int r, int64_t r2, double* out_dist,
                        int64_t* out_ids, int32_t* out_count, int io);
+int pqs_derived_search_f64(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* full, const pqs_pq* derived,
+                           const double* queries, int64_t nq, int r, int64_t r2, double* out_dist,
+                           int64_t* out_ids, int32_t* out_count, int io);
 /* ---- query_ivf kernel='derived' (ivf.py:191-195): search_two_pass per
  * probed list on the residual, merged by (distance, id).                 */
 int pqs_ivf_derived_search(pqs_ctx* ctx, const pqs_ivf* ivf, const pqs_pq* derived,
                            const float* queries, int64_t nq, int ma, int r, int64_t r2,
                            double* out_dist, int64_t* out_ids, int32_t* out_count, int io);
+int pqs_ivf_derived_search_f64(pqs_ctx* ctx, const pqs_ivf* ivf, const pqs_pq* derived,
+                               const double* queries, int64_t nq, int ma, int r, int64_t r2,
+                               double* out_dist, int64_t* out_ids, int32_t* out_count, int io);
 
 /* ---- query_ivf kernel='quick-adc' (ivf.py:185-190): per probed list the
  * Quick ADC scan (quickadc.py:104-141, init_count = min(init_count, list
@@ -198,6 +222,9 @@ int pqs_ivf_derived_search(pqs_ctx* ctx, const pqs_ivf* ivf, const pqs_pq* deriv
 int pqs_ivf_qadc_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_t nq,
                         int ma, int r, int init_count, double* out_dist, int64_t* out_ids,
                         int32_t* out_count, int io);
+int pqs_ivf_qadc_search_f64(pqs_ctx* ctx, const pqs_ivf* ivf, const double* queries, int64_t nq,
+                            int ma, int r, int init_count, double* out_dist, int64_t* out_ids,
+                            int32_t* out_count, int io);
 
 /* ---- encode (quantizer.py:308-325, nearest _dist.py:24-39): per sub-space
  * the nearest centroid by the fp64 cdist sum, ties to the lowest index.
@@ -207,6 +234,8 @@ int pqs_ivf_qadc_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, 
  * both NULL for plain PQ.                                                  */
 int pqs_encode(pqs_ctx* ctx, const pqs_pq* pq, const float* x, int64_t n, const float* coarse,
                int64_t K, const int64_t* cells, uint8_t* out_codes, int io);
+int pqs_encode_f64(pqs_ctx* ctx, const pqs_pq* pq, const double* x, int64_t n, const float* coarse,
+                   int64_t K, const int64_t* cells, uint8_t* out_codes, int io);
 
 /* ---- sharded merge: top-r of the union of G per-shard top-r lists by
  * (distance, id) -- NeighborSet.push semantics (scan.py:109-118).

@@ -81,6 +81,11 @@ SIGNATURES = {
     "pqs_ivf_derived_search": (_i, [_p, _p, _p, _p, _i64, _i, _i, _i64, _p, _p, _p, _i]),
     "pqs_merge_topr": (_i, [_p, _i, _p, _p, _p, _i64, _i, _i, _p, _p, _p, _i]),
 }
+# float64 twins of the query-taking entry points (same arguments; queries double*)
+F64_TWINS = ("pqs_compute_tables", "pqs_adc_search", "pqs_qadc_search", "pqs_ivf_probe", "pqs_ivf_search",
+             "pqs_ivf_qadc_search", "pqs_derived_search", "pqs_ivf_derived_search", "pqs_encode")
+for _n in F64_TWINS:
+    SIGNATURES[_n + "_f64"] = SIGNATURES[_n]
 
 _lib = None
 _lib_lock = threading.Lock()

@@ -5,6 +5,8 @@
 // kernel pipelines in tables.cu / scan4.cu / scan8.cu / select.cu / ivf.cu.
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -17,7 +19,7 @@ int build_db4(pqs_ctx* ctx, pqs_db* db, const uint8_t* d_codes);
 int build_db8(pqs_ctx* ctx, pqs_db* db, const uint8_t* d_codes);
 int device_max_u8(pqs_ctx* ctx, const uint8_t* d, int64_t count, int* out);
 int launch_unpack_nibbles(pqs_ctx* ctx, const uint8_t* d_packed, int64_t n, int m, uint8_t* d_out);
-int launch_encode(pqs_ctx* ctx, const pqs_pq* pq, const float* d_x, int64_t n, const float* d_coarse,
+int launch_encode(pqs_ctx* ctx, const pqs_pq* pq, QVec d_x, int64_t n, const float* d_coarse,
                   const int64_t* d_cells, uint8_t* d_out);
 int launch_quantize(pqs_ctx* ctx, double qmin, double qmax, const double* d_v, int64_t n, uint8_t* d_out);
 int ivf_create_impl(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t K, const int64_t* list_sizes,
@@ -102,6 +104,24 @@ int download(pqs_ctx* ctx, void* dst, const void* src, size_t bytes) {
 namespace {
 
 // input staging: device pointer as-is, host pointer copied into a scratch slot
+template <class T>
+int stage_in(pqs_ctx* ctx, int slot, const T* p, size_t count, int io, const T** out);
+
+// query rows (float32 or float64, as the caller passed them) -> device QVec
+int stage_q(pqs_ctx* ctx, const void* p, size_t count, int io, int f64, QVec* out) {
+  out->f64 = f64;
+  if (f64) {
+    const double* d = nullptr;
+    PQS_TRY(stage_in(ctx, S_QUERIES, (const double*)p, count, io, &d));
+    out->p = d;
+  } else {
+    const float* d = nullptr;
+    PQS_TRY(stage_in(ctx, S_QUERIES, (const float*)p, count, io, &d));
+    out->p = d;
+  }
+  return PQS_OK;
+}
+
 template <class T>
 int stage_in(pqs_ctx* ctx, int slot, const T* p, size_t count, int io, const T** out) {
   if (io == PQS_IO_DEVICE) {
@@ -319,6 +339,7 @@ int pqs_db_create(pqs_ctx* ctx, const uint8_t* codes, int64_t n, int m, int b, c
     }
   }
   pqs_db* db = new pqs_db();
+  db->gen = next_db_generation();
   auto fail = [&](int code, const std::string& msg) {
     cudaStreamSynchronize(ctx->stream);
     if (tmp) cudaFree(tmp);
@@ -437,6 +458,7 @@ int pqs_db_set_prefix(pqs_ctx* ctx, pqs_db* db, const uint8_t* prefix, int64_t n
   if (db->prefix) cudaFree(db->prefix);
   db->prefix = nullptr;
   db->n_prefix = 0;
+  db->gen = next_db_generation();
   PQS_CUDA(ctx, cudaMalloc(&db->prefix, (size_t)n_prefix * db->m));
   PQS_TRY(upload(ctx, db->prefix, prefix, (size_t)n_prefix * db->m));
   int maxc = 0;
@@ -447,11 +469,13 @@ int pqs_db_set_prefix(pqs_ctx* ctx, pqs_db* db, const uint8_t* prefix, int64_t n
     return set_err(ctx, PQS_ERR_INVALID, "component out of range for b=4");
   }
   db->n_prefix = n_prefix;
+  db->gen = next_db_generation();
   return PQS_OK;
 }
 
 void pqs_db_destroy(pqs_db* db) {
   if (!db) return;
+  db->gen = -1;
   if (db->codes8) cudaFree(db->codes8);
   if (db->codes_rm) cudaFree(db->codes_rm);
   if (db->words4) cudaFree(db->words4);
@@ -461,19 +485,27 @@ void pqs_db_destroy(pqs_db* db) {
 }
 
 // ---------------------------------------------------------------- tables
-int pqs_compute_tables(pqs_ctx* ctx, const pqs_pq* pq, const float* queries, int64_t nq, float* out_tables, int io) {
+static int compute_tables_impl(pqs_ctx* ctx, const pqs_pq* pq, const void* queries, int f64, int64_t nq,
+                               float* out_tables, int io) {
   if (!ctx || !pq) return PQS_ERR_INVALID;
   PQS_TRY(check_io(ctx, io));
   PQS_CHECK(ctx, nq >= 0, "nq must be >= 0");
   PQS_CUDA(ctx, cudaSetDevice(ctx->device));
-  const float* dq = nullptr;
+  QVec dq;
   float* dt = nullptr;
   const size_t tcount = (size_t)nq * pq->m * pq->k;
-  PQS_TRY(stage_in(ctx, S_QUERIES, queries, (size_t)nq * pq->d, io, &dq));
+  PQS_TRY(stage_q(ctx, queries, (size_t)nq * pq->d, io, f64, &dq));
   PQS_TRY(stage_out(ctx, S_TABLES, out_tables, tcount, io, &dt));
   PQS_TRY(launch_tables_exact(ctx, pq, dq, nq, dt));
   PQS_TRY(copy_out(ctx, out_tables, dt, tcount, io));
   return finish(ctx, io);
+}
+int pqs_compute_tables(pqs_ctx* ctx, const pqs_pq* pq, const float* queries, int64_t nq, float* out_tables, int io) {
+  return compute_tables_impl(ctx, pq, queries, 0, nq, out_tables, io);
+}
+int pqs_compute_tables_f64(pqs_ctx* ctx, const pqs_pq* pq, const double* queries, int64_t nq, float* out_tables,
+                           int io) {
+  return compute_tables_impl(ctx, pq, queries, 1, nq, out_tables, io);
 }
 
 // ---------------------------------------------------------------- float ADC
@@ -528,8 +560,8 @@ int pqs_adc_scan(pqs_ctx* ctx, const pqs_db* db, const float* tables, int64_t nq
   return adc_common(ctx, db, dt, nq, k, r, out_dist, out_ids, out_count, io);
 }
 
-int pqs_adc_search(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* pq, const float* queries, int64_t nq, int r,
-                   double* out_dist, int64_t* out_ids, int32_t* out_count, int io) {
+static int adc_search_impl(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* pq, const void* queries, int f64, int64_t nq,
+                           int r, double* out_dist, int64_t* out_ids, int32_t* out_count, int io) {
   if (!ctx || !db || !pq) return PQS_ERR_INVALID;
   PQS_TRY(check_io(ctx, io));
   PQS_CHECK(ctx, r >= 1, "r must be >= 1");
@@ -539,12 +571,20 @@ int pqs_adc_search(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* pq, const float
   if (r > MAX_R) return set_err(ctx, PQS_ERR_UNSUPPORTED, "r > 4096 is not supported by the device select");
   if (nq == 0) return PQS_OK;
   PQS_CUDA(ctx, cudaSetDevice(ctx->device));
-  const float* dq = nullptr;
+  QVec dq;
   float* dt = nullptr;
-  PQS_TRY(stage_in(ctx, S_QUERIES, queries, (size_t)nq * pq->d, io, &dq));
+  PQS_TRY(stage_q(ctx, queries, (size_t)nq * pq->d, io, f64, &dq));
   PQS_TRY(scratch(ctx, S_TABLES, (size_t)nq * pq->m * pq->k, &dt));
   PQS_TRY(launch_tables_exact(ctx, pq, dq, nq, dt));
   return adc_common(ctx, db, dt, nq, pq->k, r, out_dist, out_ids, out_count, io);
+}
+int pqs_adc_search(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* pq, const float* queries, int64_t nq, int r,
+                   double* out_dist, int64_t* out_ids, int32_t* out_count, int io) {
+  return adc_search_impl(ctx, db, pq, queries, 0, nq, r, out_dist, out_ids, out_count, io);
+}
+int pqs_adc_search_f64(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* pq, const double* queries, int64_t nq, int r,
+                       double* out_dist, int64_t* out_ids, int32_t* out_count, int io) {
+  return adc_search_impl(ctx, db, pq, queries, 1, nq, r, out_dist, out_ids, out_count, io);
 }
 
 // ---------------------------------------------------------------- Quick ADC
@@ -594,21 +634,33 @@ int pqs_qadc_scan(pqs_ctx* ctx, const pqs_db* db, const float* tables, int64_t n
   return qadc_common(ctx, db, dt, nq, init_count, r, out_bins, out_ids, out_count, out_qt, out_qmm, io);
 }
 
-int pqs_qadc_search(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* pq, const float* queries, int64_t nq,
-                    int init_count, int r, uint8_t* out_bins, int64_t* out_ids, int32_t* out_count, uint8_t* out_qt,
-                    double* out_qmm, int io) {
+static int qadc_search_impl(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* pq, const void* queries, int f64,
+                            int64_t nq, int init_count, int r, uint8_t* out_bins, int64_t* out_ids,
+                            int32_t* out_count, uint8_t* out_qt, double* out_qmm, int io) {
   if (!ctx || !db || !pq) return PQS_ERR_INVALID;
   PQS_TRY(check_io(ctx, io));
   PQS_TRY(qadc_validate(ctx, db, init_count, r));
   PQS_CHECK(ctx, pq->k == 16 && pq->m == db->m, "tables do not match the code list shape");
   if (nq == 0) return PQS_OK;
   PQS_CUDA(ctx, cudaSetDevice(ctx->device));
-  const float* dq = nullptr;
+  QVec dq;
   float* dt = nullptr;
-  PQS_TRY(stage_in(ctx, S_QUERIES, queries, (size_t)nq * pq->d, io, &dq));
+  PQS_TRY(stage_q(ctx, queries, (size_t)nq * pq->d, io, f64, &dq));
   PQS_TRY(scratch(ctx, S_TABLES, (size_t)nq * pq->m * 16, &dt));
   PQS_TRY(launch_tables_exact(ctx, pq, dq, nq, dt));
   return qadc_common(ctx, db, dt, nq, init_count, r, out_bins, out_ids, out_count, out_qt, out_qmm, io);
+}
+int pqs_qadc_search(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* pq, const float* queries, int64_t nq,
+                    int init_count, int r, uint8_t* out_bins, int64_t* out_ids, int32_t* out_count, uint8_t* out_qt,
+                    double* out_qmm, int io) {
+  return qadc_search_impl(ctx, db, pq, queries, 0, nq, init_count, r, out_bins, out_ids, out_count, out_qt, out_qmm,
+                          io);
+}
+int pqs_qadc_search_f64(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* pq, const double* queries, int64_t nq,
+                        int init_count, int r, uint8_t* out_bins, int64_t* out_ids, int32_t* out_count,
+                        uint8_t* out_qt, double* out_qmm, int io) {
+  return qadc_search_impl(ctx, db, pq, queries, 1, nq, init_count, r, out_bins, out_ids, out_count, out_qt, out_qmm,
+                          io);
 }
 
 int pqs_quantize(pqs_ctx* ctx, double qmin, double qmax, const double* values, int64_t n, uint8_t* out, int io) {
@@ -652,8 +704,8 @@ int pqs_ivf_create(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t 
 }
 
 // ---------------------------------------------------------------- encode
-int pqs_encode(pqs_ctx* ctx, const pqs_pq* pq, const float* x, int64_t n, const float* coarse, int64_t K,
-               const int64_t* cells, uint8_t* out_codes, int io) {
+static int encode_impl(pqs_ctx* ctx, const pqs_pq* pq, const void* x, int f64, int64_t n, const float* coarse,
+                       int64_t K, const int64_t* cells, uint8_t* out_codes, int io) {
   if (!ctx || !pq) return PQS_ERR_INVALID;
   PQS_TRY(check_io(ctx, io));
   PQS_CHECK(ctx, n >= 0, "n must be >= 0");
@@ -662,11 +714,11 @@ int pqs_encode(pqs_ctx* ctx, const pqs_pq* pq, const float* x, int64_t n, const 
   PQS_CHECK(ctx, coarse == nullptr || K >= 1, "K must be >= 1");
   if (n == 0) return PQS_OK;
   PQS_CUDA(ctx, cudaSetDevice(ctx->device));
-  const float* dx = nullptr;
+  QVec dx;
   const float* dg = nullptr;
   const int64_t* dc = nullptr;
   uint8_t* dout = nullptr;
-  PQS_TRY(stage_in(ctx, S_QUERIES, x, (size_t)n * pq->d, io, &dx));
+  PQS_TRY(stage_q(ctx, x, (size_t)n * pq->d, io, f64, &dx));
   if (coarse) {
     PQS_TRY(stage_in(ctx, S_IVF_WORK, coarse, (size_t)K * pq->d, io, &dg));
     PQS_TRY(stage_in(ctx, S_PROBE, cells, (size_t)n, io, &dc));
@@ -676,20 +728,28 @@ int pqs_encode(pqs_ctx* ctx, const pqs_pq* pq, const float* x, int64_t n, const 
   PQS_TRY(copy_out(ctx, out_codes, dout, (size_t)n * pq->m, io));
   return finish(ctx, io);
 }
+int pqs_encode(pqs_ctx* ctx, const pqs_pq* pq, const float* x, int64_t n, const float* coarse, int64_t K,
+               const int64_t* cells, uint8_t* out_codes, int io) {
+  return encode_impl(ctx, pq, x, 0, n, coarse, K, cells, out_codes, io);
+}
+int pqs_encode_f64(pqs_ctx* ctx, const pqs_pq* pq, const double* x, int64_t n, const float* coarse, int64_t K,
+                   const int64_t* cells, uint8_t* out_codes, int io) {
+  return encode_impl(ctx, pq, x, 1, n, coarse, K, cells, out_codes, io);
+}
 
 void pqs_ivf_destroy(pqs_ivf* ivf) { ivf_destroy_impl(ivf); }
 
-int pqs_ivf_probe(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_t nq, int ma, int64_t* out_cells,
-                  double* out_dist, int io) {
+static int ivf_probe_impl(pqs_ctx* ctx, const pqs_ivf* ivf, const void* queries, int f64, int64_t nq, int ma,
+                          int64_t* out_cells, double* out_dist, int io) {
   if (!ctx || !ivf) return PQS_ERR_INVALID;
   PQS_TRY(check_io(ctx, io));
   PQS_CHECK(ctx, ma >= 1 && ma <= ivf->K, "ma must be in [1, K]");
   if (nq == 0) return PQS_OK;
   PQS_CUDA(ctx, cudaSetDevice(ctx->device));
-  const float* dq = nullptr;
+  QVec dq;
   int64_t* dc = nullptr;
   double* dd = nullptr;
-  PQS_TRY(stage_in(ctx, S_QUERIES, queries, (size_t)nq * ivf->d, io, &dq));
+  PQS_TRY(stage_q(ctx, queries, (size_t)nq * ivf->d, io, f64, &dq));
   PQS_TRY(stage_out(ctx, S_OUT_I, out_cells, (size_t)nq * ma, io, &dc));
   PQS_TRY(stage_out(ctx, S_OUT_D, out_dist, (size_t)nq * ma, io, &dd));
   PQS_TRY(run_ivf_probe(ctx, ivf, dq, nq, ma, dc, dd));
@@ -697,9 +757,17 @@ int pqs_ivf_probe(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_
   PQS_TRY(copy_out(ctx, out_dist, dd, (size_t)nq * ma, io));
   return finish(ctx, io);
 }
+int pqs_ivf_probe(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_t nq, int ma, int64_t* out_cells,
+                  double* out_dist, int io) {
+  return ivf_probe_impl(ctx, ivf, queries, 0, nq, ma, out_cells, out_dist, io);
+}
+int pqs_ivf_probe_f64(pqs_ctx* ctx, const pqs_ivf* ivf, const double* queries, int64_t nq, int ma,
+                      int64_t* out_cells, double* out_dist, int io) {
+  return ivf_probe_impl(ctx, ivf, queries, 1, nq, ma, out_cells, out_dist, io);
+}
 
-int pqs_ivf_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_t nq, int ma, int r,
-                   double* out_dist, int64_t* out_ids, int32_t* out_count, int io) {
+static int ivf_search_impl(pqs_ctx* ctx, const pqs_ivf* ivf, const void* queries, int f64, int64_t nq, int ma, int r,
+                           double* out_dist, int64_t* out_ids, int32_t* out_count, int io) {
   if (!ctx || !ivf) return PQS_ERR_INVALID;
   PQS_TRY(check_io(ctx, io));
   PQS_CHECK(ctx, ma >= 1 && ma <= ivf->K, "ma must be in [1, K]");
@@ -707,11 +775,11 @@ int pqs_ivf_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64
   if (r > MAX_R) return set_err(ctx, PQS_ERR_UNSUPPORTED, "r > 4096 is not supported by the device select");
   if (nq == 0) return PQS_OK;
   PQS_CUDA(ctx, cudaSetDevice(ctx->device));
-  const float* dq = nullptr;
+  QVec dq;
   double* dd = nullptr;
   int64_t* di = nullptr;
   int32_t* dc = nullptr;
-  PQS_TRY(stage_in(ctx, S_QUERIES, queries, (size_t)nq * ivf->d, io, &dq));
+  PQS_TRY(stage_q(ctx, queries, (size_t)nq * ivf->d, io, f64, &dq));
   PQS_TRY(stage_out(ctx, S_OUT_D, out_dist, (size_t)nq * r, io, &dd));
   PQS_TRY(stage_out(ctx, S_OUT_I, out_ids, (size_t)nq * r, io, &di));
   PQS_TRY(stage_out(ctx, S_OUT_C, out_count, (size_t)nq, io, &dc));
@@ -721,9 +789,18 @@ int pqs_ivf_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64
   PQS_TRY(copy_out(ctx, out_count, dc, (size_t)nq, io));
   return finish(ctx, io);
 }
+int pqs_ivf_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_t nq, int ma, int r,
+                   double* out_dist, int64_t* out_ids, int32_t* out_count, int io) {
+  return ivf_search_impl(ctx, ivf, queries, 0, nq, ma, r, out_dist, out_ids, out_count, io);
+}
+int pqs_ivf_search_f64(pqs_ctx* ctx, const pqs_ivf* ivf, const double* queries, int64_t nq, int ma, int r,
+                       double* out_dist, int64_t* out_ids, int32_t* out_count, int io) {
+  return ivf_search_impl(ctx, ivf, queries, 1, nq, ma, r, out_dist, out_ids, out_count, io);
+}
 
-int pqs_ivf_qadc_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_t nq, int ma, int r,
-                        int init_count, double* out_dist, int64_t* out_ids, int32_t* out_count, int io) {
+static int ivf_qadc_search_impl(pqs_ctx* ctx, const pqs_ivf* ivf, const void* queries, int f64, int64_t nq, int ma,
+                                int r, int init_count, double* out_dist, int64_t* out_ids, int32_t* out_count,
+                                int io) {
   if (!ctx || !ivf) return PQS_ERR_INVALID;
   PQS_TRY(check_io(ctx, io));
   PQS_CHECK(ctx, ma >= 1 && ma <= ivf->K, "ma must be in [1, K]");
@@ -734,11 +811,11 @@ int pqs_ivf_qadc_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, 
   if (ivf->m > 64) return set_err(ctx, PQS_ERR_UNSUPPORTED, "quick-adc IVF kernel supports m <= 64");
   if (nq == 0) return PQS_OK;
   PQS_CUDA(ctx, cudaSetDevice(ctx->device));
-  const float* dq = nullptr;
+  QVec dq;
   double* dd = nullptr;
   int64_t* di = nullptr;
   int32_t* dc = nullptr;
-  PQS_TRY(stage_in(ctx, S_QUERIES, queries, (size_t)nq * ivf->d, io, &dq));
+  PQS_TRY(stage_q(ctx, queries, (size_t)nq * ivf->d, io, f64, &dq));
   PQS_TRY(stage_out(ctx, S_OUT_D, out_dist, (size_t)nq * r, io, &dd));
   PQS_TRY(stage_out(ctx, S_OUT_I, out_ids, (size_t)nq * r, io, &di));
   PQS_TRY(stage_out(ctx, S_OUT_C, out_count, (size_t)nq, io, &dc));
@@ -747,6 +824,14 @@ int pqs_ivf_qadc_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, 
   PQS_TRY(copy_out(ctx, out_ids, di, (size_t)nq * r, io));
   PQS_TRY(copy_out(ctx, out_count, dc, (size_t)nq, io));
   return finish(ctx, io);
+}
+int pqs_ivf_qadc_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_t nq, int ma, int r,
+                        int init_count, double* out_dist, int64_t* out_ids, int32_t* out_count, int io) {
+  return ivf_qadc_search_impl(ctx, ivf, queries, 0, nq, ma, r, init_count, out_dist, out_ids, out_count, io);
+}
+int pqs_ivf_qadc_search_f64(pqs_ctx* ctx, const pqs_ivf* ivf, const double* queries, int64_t nq, int ma, int r,
+                            int init_count, double* out_dist, int64_t* out_ids, int32_t* out_count, int io) {
+  return ivf_qadc_search_impl(ctx, ivf, queries, 1, nq, ma, r, init_count, out_dist, out_ids, out_count, io);
 }
 
 int pqs_fastscan_checked(pqs_ctx* ctx, const pqs_db* db, const float* tables, int64_t nq, int64_t n_init, int r,
@@ -768,9 +853,9 @@ int pqs_fastscan_checked(pqs_ctx* ctx, const pqs_db* db, const float* tables, in
   return finish(ctx, io);
 }
 
-int pqs_derived_search(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* full, const pqs_pq* derived,
-                       const float* queries, int64_t nq, int r, int64_t r2, double* out_dist, int64_t* out_ids,
-                       int32_t* out_count, int io) {
+static int derived_search_impl(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* full, const pqs_pq* derived,
+                               const void* queries, int f64, int64_t nq, int r, int64_t r2, double* out_dist,
+                               int64_t* out_ids, int32_t* out_count, int io) {
   if (!ctx || !db || !full || !derived) return PQS_ERR_INVALID;
   PQS_TRY(check_io(ctx, io));
   PQS_CHECK(ctx, db->n >= 1, "empty code list");
@@ -783,13 +868,13 @@ int pqs_derived_search(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* full, const
   if (r > MAX_R) return set_err(ctx, PQS_ERR_UNSUPPORTED, "r > 4096 is not supported by the device select");
   if (nq == 0) return PQS_OK;
   PQS_CUDA(ctx, cudaSetDevice(ctx->device));
-  const float* dq = nullptr;
+  QVec dq;
   float* tf = nullptr;
   float* tc = nullptr;
   double* dd = nullptr;
   int64_t* di = nullptr;
   int32_t* dc = nullptr;
-  PQS_TRY(stage_in(ctx, S_QUERIES, queries, (size_t)nq * full->d, io, &dq));
+  PQS_TRY(stage_q(ctx, queries, (size_t)nq * full->d, io, f64, &dq));
   PQS_TRY(scratch(ctx, S_TABLES, (size_t)nq * full->m * full->k, &tf));
   PQS_TRY(scratch(ctx, S_TABLES_T, (size_t)nq * derived->m * derived->k, &tc));
   PQS_TRY(launch_tables_exact(ctx, full, dq, nq, tf));
@@ -803,10 +888,20 @@ int pqs_derived_search(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* full, const
   PQS_TRY(copy_out(ctx, out_count, dc, (size_t)nq, io));
   return finish(ctx, io);
 }
+int pqs_derived_search(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* full, const pqs_pq* derived,
+                       const float* queries, int64_t nq, int r, int64_t r2, double* out_dist, int64_t* out_ids,
+                       int32_t* out_count, int io) {
+  return derived_search_impl(ctx, db, full, derived, queries, 0, nq, r, r2, out_dist, out_ids, out_count, io);
+}
+int pqs_derived_search_f64(pqs_ctx* ctx, const pqs_db* db, const pqs_pq* full, const pqs_pq* derived,
+                           const double* queries, int64_t nq, int r, int64_t r2, double* out_dist, int64_t* out_ids,
+                           int32_t* out_count, int io) {
+  return derived_search_impl(ctx, db, full, derived, queries, 1, nq, r, r2, out_dist, out_ids, out_count, io);
+}
 
-int pqs_ivf_derived_search(pqs_ctx* ctx, const pqs_ivf* ivf, const pqs_pq* derived, const float* queries, int64_t nq,
-                           int ma, int r, int64_t r2, double* out_dist, int64_t* out_ids, int32_t* out_count,
-                           int io) {
+static int ivf_derived_search_impl(pqs_ctx* ctx, const pqs_ivf* ivf, const pqs_pq* derived, const void* queries,
+                                   int f64, int64_t nq, int ma, int r, int64_t r2, double* out_dist,
+                                   int64_t* out_ids, int32_t* out_count, int io) {
   if (!ctx || !ivf || !derived) return PQS_ERR_INVALID;
   PQS_TRY(check_io(ctx, io));
   PQS_CHECK(ctx, ma >= 1 && ma <= ivf->K, "ma must be in [1, K]");
@@ -817,11 +912,11 @@ int pqs_ivf_derived_search(pqs_ctx* ctx, const pqs_ivf* ivf, const pqs_pq* deriv
   if (r > MAX_R) return set_err(ctx, PQS_ERR_UNSUPPORTED, "r > 4096 is not supported by the device select");
   if (nq == 0) return PQS_OK;
   PQS_CUDA(ctx, cudaSetDevice(ctx->device));
-  const float* dq = nullptr;
+  QVec dq;
   double* dd = nullptr;
   int64_t* di = nullptr;
   int32_t* dc = nullptr;
-  PQS_TRY(stage_in(ctx, S_QUERIES, queries, (size_t)nq * ivf->d, io, &dq));
+  PQS_TRY(stage_q(ctx, queries, (size_t)nq * ivf->d, io, f64, &dq));
   PQS_TRY(stage_out(ctx, S_OUT_D, out_dist, (size_t)nq * r, io, &dd));
   PQS_TRY(stage_out(ctx, S_OUT_I, out_ids, (size_t)nq * r, io, &di));
   PQS_TRY(stage_out(ctx, S_OUT_C, out_count, (size_t)nq, io, &dc));
@@ -830,6 +925,16 @@ int pqs_ivf_derived_search(pqs_ctx* ctx, const pqs_ivf* ivf, const pqs_pq* deriv
   PQS_TRY(copy_out(ctx, out_ids, di, (size_t)nq * r, io));
   PQS_TRY(copy_out(ctx, out_count, dc, (size_t)nq, io));
   return finish(ctx, io);
+}
+int pqs_ivf_derived_search(pqs_ctx* ctx, const pqs_ivf* ivf, const pqs_pq* derived, const float* queries, int64_t nq,
+                           int ma, int r, int64_t r2, double* out_dist, int64_t* out_ids, int32_t* out_count,
+                           int io) {
+  return ivf_derived_search_impl(ctx, ivf, derived, queries, 0, nq, ma, r, r2, out_dist, out_ids, out_count, io);
+}
+int pqs_ivf_derived_search_f64(pqs_ctx* ctx, const pqs_ivf* ivf, const pqs_pq* derived, const double* queries,
+                               int64_t nq, int ma, int r, int64_t r2, double* out_dist, int64_t* out_ids,
+                               int32_t* out_count, int io) {
+  return ivf_derived_search_impl(ctx, ivf, derived, queries, 1, nq, ma, r, r2, out_dist, out_ids, out_count, io);
 }
 
 // ---------------------------------------------------------------- merge

@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(DV_THREADS) dv_collect_kernel(const uint8_t* _
 // list; the list's r best (exact distance, id) go to the query's candidate
 // row (one reservation), merged by K5.
 struct DvIvfArgs {
-  const float* queries;
+  QVec queries;
   const float* coarse;
   const float* books;     // (m, k, dsub)
   const float* dbooks;    // (m, kbar, dsub)
@@ -245,11 +245,11 @@ struct DvShared {
   unsigned long long kstar, istar;
 };
 
-__device__ __forceinline__ double table_entry(const float* qv, const float* g, const float* cb, int j, int dsub) {
+__device__ __forceinline__ double table_entry(QVec qv, const float* g, const float* cb, int j, int dsub) {
   double t = 0.0;
   for (int s = 0; s < dsub; ++s) {
     const int dd = j * dsub + s;
-    const double rr = __dsub_rn((double)__ldg(qv + dd), (double)__ldg(g + dd));
+    const double rr = __dsub_rn(qv.at(dd), (double)__ldg(g + dd));
     const double df = __dsub_rn(rr, (double)__ldg(cb + s));
     t = __dadd_rn(t, __dmul_rn(df, df));
   }
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(DV_THREADS) dv_ivf_kernel(DvIvfArgs a) {
   if (c < 0) return;
   const int64_t lb = a.offsets[c], n = a.offsets[c + 1] - lb;
   if (n == 0) return;  // ivf.py:176-177
-  const float* qv = a.queries + (a.q0 + ql) * (int64_t)a.d;
+  const QVec qv = a.queries.offset((a.q0 + ql) * (int64_t)a.d);
   const float* g = a.coarse + c * (int64_t)a.d;
   const uint8_t* lc = a.codes + lb * (int64_t)m;
   const int64_t* li = a.ids + lb;
@@ -487,7 +487,7 @@ int run_derived_search(pqs_ctx* ctx, const pqs_db* db, const float* d_full, int 
 }
 
 // query_ivf kernel='derived' for a batch of queries
-int run_ivf_derived_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_dbooks, int kbar, const float* d_queries,
+int run_ivf_derived_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_dbooks, int kbar, QVec d_queries,
                            int64_t nq, int ma, int r, int64_t r2, double* d_dist, int64_t* d_ids, int32_t* d_count) {
   const int m = iv->m, k = iv->k;
   const size_t smem = (size_t)m * k * 4 + (size_t)m * kbar * 4 + (size_t)m * kbar;

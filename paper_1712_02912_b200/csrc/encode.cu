@@ -23,7 +23,7 @@ namespace {
 constexpr int ENC_THREADS = 128;
 
 template <int DSUB>
-__global__ void __launch_bounds__(ENC_THREADS) encode_kernel(const float* __restrict__ x, int64_t n, int d,
+__global__ void __launch_bounds__(ENC_THREADS) encode_kernel(QVec x, int64_t n, int d,
                                                              const float* __restrict__ books, int k, int dsub_rt,
                                                              const float* __restrict__ coarse,
                                                              const int64_t* __restrict__ cells, int m,
@@ -36,12 +36,12 @@ __global__ void __launch_bounds__(ENC_THREADS) encode_kernel(const float* __rest
   __syncthreads();
   const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (v >= n) return;
-  const float* xv = x + v * d + (int64_t)j * dsub;
+  const QVec xv = x.offset(v * d + (int64_t)j * dsub);
   const float* gv = coarse ? coarse + cells[v] * d + (int64_t)j * dsub : nullptr;
   if (DSUB > 0) {
     double z[DSUB > 0 ? DSUB : 1];
 #pragma unroll
-    for (int t = 0; t < DSUB; ++t) z[t] = gv ? __dsub_rn((double)xv[t], (double)gv[t]) : (double)xv[t];
+    for (int t = 0; t < DSUB; ++t) z[t] = gv ? __dsub_rn(xv.at(t), (double)gv[t]) : xv.at(t);
     double best = 0.0;
     int bi = 0;
     for (int i = 0; i < k; ++i) {
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(ENC_THREADS) encode_kernel(const float* __rest
       const double* c = cs + i * dsub;
       double acc = 0.0;
       for (int t = 0; t < dsub; ++t) {
-        const double zt = gv ? __dsub_rn((double)xv[t], (double)gv[t]) : (double)xv[t];
+        const double zt = gv ? __dsub_rn(xv.at(t), (double)gv[t]) : xv.at(t);
         const double df = __dsub_rn(zt, c[t]);
         acc = __dadd_rn(acc, __dmul_rn(df, df));
       }
@@ -154,7 +154,7 @@ int build_db8(pqs_ctx* ctx, pqs_db* db, const uint8_t* d_codes) {
   return PQS_OK;
 }
 
-int launch_encode(pqs_ctx* ctx, const pqs_pq* pq, const float* d_x, int64_t n, const float* d_coarse,
+int launch_encode(pqs_ctx* ctx, const pqs_pq* pq, QVec d_x, int64_t n, const float* d_coarse,
                   const int64_t* d_cells, uint8_t* d_out) {
   if (n == 0) return PQS_OK;
   const int k = pq->k, dsub = pq->dsub;

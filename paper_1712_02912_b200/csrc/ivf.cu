@@ -6,12 +6,9 @@
 // (ivf.py:179-183), merge all per-list top-r by (distance, id).
 //
 // B200 design:
-//  K7  probe distances: ||c||^2 - 2 q.c with the q.c products from one fp32
-//      GEMM (cuBLAS, pedantic fp32 math = no TF32); a per-query radix select
-//      finds the ma-th approximate distance, every cell within a certified
-//      fp32 error bound of it is re-scored in exact fp64 (scipy's sequential
-//      order) and the ma best by (distance, cell) are kept -> identical probe
-//      sets and order to nearest_k.
+//  K7  probes: probe.cu (tcgen05 kind::tf32 GEMM with the key and the
+//      certified candidate filter fused into its epilogue, exact fp64
+//      re-score) -> identical probe sets and order to nearest_k.
 //  K8  the residual tables are never materialised per (query, list): with
 //      PQ sub-spaces disjoint, sum_j T_j = ||q-c||^2 + sum_j U_q[j][code_j]
 //      + V[code] where U_q[j][i] = ||C_ji||^2 - 2<q_j, C_ji> (per query) and
@@ -21,7 +18,6 @@
 //      exactly (residual tables in fp64, scan.py:45-56 + 77-81 order) in the
 //      select kernel.  The filter threshold per query comes from a sample
 //      (the first 64 codes of every probed list).
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -105,15 +101,15 @@ __global__ void v_kernel(const float* __restrict__ coarse, const float* __restri
 // per CTA, the UQ tables are built in shared memory and written out with
 // coalesced 16-byte stores.
 constexpr int UQ = 8;
-__global__ void __launch_bounds__(256) utables_kernel(const float* __restrict__ queries,
+__global__ void __launch_bounds__(256) utables_kernel(QVec queries,
                                                       const float* __restrict__ books, int64_t nq, int m, int k,
                                                       int dsub, float* __restrict__ U) {
-  extern __shared__ __align__(16) float usm[];  // [UQ][k * m] tables, then [UQ][d] queries
+  extern __shared__ __align__(16) float usm[];  // [UQ][k * m] tables, then [UQ][d] fp64 queries
   const int d = m * dsub, mk = m * k;
-  float* sq = usm + (size_t)UQ * mk;
+  double* sq = reinterpret_cast<double*>(usm + (size_t)UQ * mk + ((size_t)UQ * mk & 1));
   const int64_t q0 = (int64_t)blockIdx.x * UQ;
   const int nqb = (int)min((int64_t)UQ, nq - q0);
-  for (int t = threadIdx.x; t < nqb * d; t += blockDim.x) sq[t] = queries[q0 * d + t];
+  for (int t = threadIdx.x; t < nqb * d; t += blockDim.x) sq[t] = queries.at(q0 * d + t);
   __syncthreads();
   for (int i = threadIdx.x; i < k; i += blockDim.x) {
     for (int j = 0; j < m; ++j) {
@@ -126,7 +122,7 @@ __global__ void __launch_bounds__(256) utables_kernel(const float* __restrict__ 
         const double cv = (double)__ldg(cb + s2);
         nn += cv * cv;
 #pragma unroll
-        for (int u = 0; u < UQ; ++u) dot[u] += (double)sq[u * d + j * dsub + s2] * cv;
+        for (int u = 0; u < UQ; ++u) dot[u] += sq[u * d + j * dsub + s2] * cv;
       }
 #pragma unroll
       for (int u = 0; u < UQ; ++u) usm[u * mk + i * m + j] = (float)(nn - 2.0 * dot[u]);
@@ -166,250 +162,6 @@ __global__ void ivf_bound_kernel(const float* __restrict__ U, const double* __re
     const double B = amax + (double)vmax[0] + usum;
     const double u = 5.9604644775390625e-08;
     aerr[q] = (float)((m + 6) * u * 1.05 * B + 1e-30);
-  }
-}
-
-// ------------------------------------------------------------ K7 probes
-struct ProbeArgs {
-  const float* dots;     // (nqb, K) fp32 q.c
-  const double* cnorm;   // (K,)
-  const float* cnormf;   // (K,) fp32 ||c||^2 (approximate keys)
-  const float* gnorm;    // (K,) ||c|| fp32
-  float gmax;
-  const float* queries;  // (nq, d), batch-offset applied
-  const float* coarse;   // (K, d)
-  int64_t K;
-  int d, ma;
-  int tf32;              // dots from a TF32 tensor-core GEMM (wider certified bound)
-  int64_t q0;            // global index of batch row 0
-  int64_t* out_cells;    // (nq, ma)
-  double* out_dist;      // (nq, ma)
-  uint64_t* gkeys;       // (nqb, K) scratch
-  int64_t* gids;
-};
-
-constexpr int PROBE_THREADS = 512;
-constexpr int PROBE_SMEM_CAP = 4096;
-constexpr int PROBE_QMAX = 1024;  // queries up to this d are staged in shared memory
-
-__global__ void __launch_bounds__(PROBE_THREADS) probe_select_kernel(ProbeArgs a, int sortP) {
-  extern __shared__ __align__(16) unsigned char psm[];
-  __shared__ SelShared sh;
-  __shared__ int s_cnt;
-  __shared__ double s_qn;
-  __shared__ __align__(16) float s_q[PROBE_QMAX];
-  uint64_t* ck = (uint64_t*)psm;                 // candidates (PROBE_SMEM_CAP)
-  int64_t* ci = (int64_t*)(ck + PROBE_SMEM_CAP);
-  uint64_t* ok = (uint64_t*)(ci + PROBE_SMEM_CAP);
-  int64_t* oi = (int64_t*)(ok + sortP);
-  const int64_t ql = blockIdx.x;
-  const int64_t q = a.q0 + ql;
-  const float* dots = a.dots + ql * a.K;
-  const float* qv = a.queries + ql * (int64_t)a.d;
-  const int64_t K = a.K;
-  const int ma = a.ma;
-  // the query in shared memory (the exact re-score reads it per cell) and its
-  // norm by a warp reduction (only feeds the error bound: any order)
-  const bool q_in_smem = a.d <= PROBE_QMAX;
-  if (q_in_smem)
-    for (int t = threadIdx.x; t < a.d; t += blockDim.x) s_q[t] = qv[t];
-  if (threadIdx.x < 32) {
-    double s = 0.0;
-    for (int t = threadIdx.x; t < a.d; t += 32) s += (double)qv[t] * (double)qv[t];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) {
-      s_qn = sqrt(s);
-      s_cnt = 0;
-    }
-  }
-  __syncthreads();
-  const float* qx = q_in_smem ? s_q : qv;
-  // certified bound on |approx - exact|: fp32 dot (any order) error <= gamma_d ||q|| ||c||
-  const double u = 5.9604644775390625e-08;
-  // fp32 GEMM: |fl(q.c) - q.c| <= gamma_d ||q|| ||c|| (any summation order).
-  // TF32 tensor cores: operands keep 10 mantissa bits (truncation: relative
-  // error < 2^-10 each, products exact), fp32 accumulation taken as <= 2^-22
-  // per add -- (2^-9 + 2^-19 + d 2^-22) ||q|| ||c||, i.e. ~2x the
-  // round-to-nearest operand error.
-  const double gam = a.tf32 ? (1.953125e-3 + 1.9073486328125e-06 + a.d * 2.384185791015625e-07)
-                            : a.d * u / (1.0 - a.d * u);
-  // approximate keys in fp32: approx = fl(fl(||c||^2) - 2 q.c) (2 q.c exact)
-  // adds <= u (||c||^2 + |approx|) <= 2u (gmax^2 + ||q|| gmax) to the GEMM error
-  const double gm = (double)a.gmax;
-  const double eps = 2.0 * gam * s_qn * gm * 1.01 + 2.0 * u * 1.01 * (gm * gm + s_qn * gm) +
-                     1e-9 * (s_qn * s_qn + gm * gm);
-  auto approx = [&](int64_t c) -> float { return a.cnormf[c] - 2.f * dots[c]; };
-  auto akey = [](float f) -> uint64_t { return (uint64_t)fkey(f); };           // 32-bit: <= 4 radix passes
-  auto akey_inv = [](uint64_t k) -> double { return (double)fkey_inv((uint32_t)k); };
-  double thr = 1e300;
-  if (ma < K) {
-    // certified cut from a strided sample of S >= ma cells: its ma-th smallest
-    // approximate distance bounds the ma-th smallest of all K from above, so
-    // every true probe has approx <= that + 2 eps (one pass over the dots,
-    // ~ma * K / S cells re-scored exactly)
-    const int64_t S = K < PROBE_SMEM_CAP ? K : PROBE_SMEM_CAP;
-#pragma unroll 4
-    for (int64_t i = threadIdx.x; i < S; i += blockDim.x) ck[i] = akey(approx(i * K / S));
-    __syncthreads();
-    auto getk = [&](int64_t i, uint64_t& v) {
-      v = ck[i];
-      return true;
-    };
-    block_radix_select(S, getk, (unsigned long long)(ma - 1), sh);
-    thr = akey_inv(sh.prefix) + 2.0 * eps;
-    __syncthreads();
-  }
-  // gather the cells with approx <= thr (approximate keys first)
-  auto gather = [&](float ap, int64_t c) {
-    if ((double)ap <= thr) {
-      const int p = atomicAdd(&s_cnt, 1);
-      if (p < PROBE_SMEM_CAP) {
-        ck[p] = akey(ap);
-        ci[p] = c;
-      } else {
-        a.gkeys[ql * K + p] = akey(ap);
-        a.gids[ql * K + p] = c;
-      }
-    }
-  };
-  if ((K & 3) == 0) {  // 16-byte loads of the dots row and the norms
-    const float4* d4 = reinterpret_cast<const float4*>(dots);
-    const float4* n4 = reinterpret_cast<const float4*>(a.cnormf);
-    // four 16-byte loads of the dots row in flight per thread (the row
-    // streams from DRAM; the gather's atomics would otherwise serialise them)
-    const int64_t K4 = K / 4, bd = blockDim.x;
-    for (int64_t c0 = threadIdx.x; c0 < K4; c0 += 4 * bd) {
-      float4 dv[4], nv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t c4 = c0 + u * bd;
-        if (c4 < K4) {
-          dv[u] = __ldcs(d4 + c4);
-          nv[u] = __ldg(n4 + c4);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t c4 = c0 + u * bd;
-        if (c4 < K4) {
-          gather(nv[u].x - 2.f * dv[u].x, 4 * c4);
-          gather(nv[u].y - 2.f * dv[u].y, 4 * c4 + 1);
-          gather(nv[u].z - 2.f * dv[u].z, 4 * c4 + 2);
-          gather(nv[u].w - 2.f * dv[u].w, 4 * c4 + 3);
-        }
-      }
-    }
-  } else {
-    for (int64_t c = threadIdx.x; c < K; c += blockDim.x) gather(approx(c), c);
-  }
-  __syncthreads();
-  const int64_t M = s_cnt;
-  {
-    uint64_t* AK = M <= PROBE_SMEM_CAP ? ck : a.gkeys + ql * K;
-    int64_t* AI = M <= PROBE_SMEM_CAP ? ci : a.gids + ql * K;
-    if (M > PROBE_SMEM_CAP) {
-      for (int p = threadIdx.x; p < PROBE_SMEM_CAP; p += blockDim.x) {
-        a.gkeys[ql * K + p] = ck[p];
-        a.gids[ql * K + p] = ci[p];
-      }
-      __syncthreads();
-    }
-    // tighten: the ma-th smallest approx among the gathered cells is the
-    // ma-th smallest overall (all cells up to it were gathered)
-    double thr2 = thr;
-    if (ma < M) {
-      auto getk2 = [&](int64_t i, uint64_t& v) {
-        v = AK[i];
-        return true;
-      };
-      block_radix_select(M, getk2, (unsigned long long)(ma - 1), sh);
-      thr2 = akey_inv(sh.prefix) + 2.0 * eps;
-      __syncthreads();
-    }
-    // exact fp64 distance (sequential, as scipy cdist) of the cells within
-    // thr2; the others get the largest key (never selected: >= ma are exact)
-    for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
-      if (akey_inv(AK[i]) <= thr2) {
-        const float* g = a.coarse + AI[i] * (int64_t)a.d;
-        double s2 = 0.0;
-        // 32 coordinates of the cell row in flight (16-byte loads when the
-        // rows are 16-byte aligned), then the sequential fp64 sum (scipy order)
-        for (int t0 = 0; t0 < a.d; t0 += 32) {
-          float ga[32];
-          if ((a.d & 3) == 0 && t0 + 32 <= a.d) {
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const float4 v = __ldg(reinterpret_cast<const float4*>(g + t0) + u);
-              ga[4 * u] = v.x, ga[4 * u + 1] = v.y, ga[4 * u + 2] = v.z, ga[4 * u + 3] = v.w;
-            }
-          } else {
-#pragma unroll
-            for (int u = 0; u < 32; ++u) ga[u] = t0 + u < a.d ? __ldg(g + t0 + u) : 0.f;
-          }
-#pragma unroll
-          for (int u = 0; u < 32; ++u) {
-            if (t0 + u < a.d) {
-              const double df = __dsub_rn((double)qx[t0 + u], (double)ga[u]);
-              s2 = __dadd_rn(s2, __dmul_rn(df, df));
-            }
-          }
-        }
-        AK[i] = dkey(s2);
-      } else {
-        AK[i] = ~0ull;
-      }
-    }
-    __syncthreads();
-  }
-  const uint64_t* KK = M <= PROBE_SMEM_CAP ? ck : a.gkeys + ql * K;
-  const int64_t* II = M <= PROBE_SMEM_CAP ? ci : a.gids + ql * K;
-  unsigned long long kstar = ~0ull;
-  long long istar = 0x7FFFFFFFFFFFFFFFll;
-  bool all_ties = true;
-  const int64_t r_eff = ma < M ? ma : M;
-  if (r_eff < M) {
-    auto getk = [&](int64_t i, uint64_t& v) {
-      v = KK[i];
-      return true;
-    };
-    block_radix_select(M, getk, (unsigned long long)(r_eff - 1), sh);
-    kstar = sh.prefix;
-    const unsigned long long less = sh.less, eq = sh.eq, need = r_eff - less;
-    __syncthreads();
-    if (eq > need) {
-      all_ties = false;
-      auto geti = [&](int64_t i, uint64_t& v) {
-        v = (uint64_t)II[i] ^ 0x8000000000000000ull;
-        return KK[i] == kstar;
-      };
-      block_radix_select(M, geti, need - 1, sh);
-      istar = (long long)(sh.prefix ^ 0x8000000000000000ull);
-      __syncthreads();
-    }
-  }
-  if (threadIdx.x == 0) s_cnt = 0;
-  __syncthreads();
-  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
-    const uint64_t key = KK[i];
-    const int64_t id = II[i];
-    if (key < kstar || (key == kstar && (all_ties || id <= istar))) {
-      const int p = atomicAdd(&s_cnt, 1);
-      if (p < sortP) {
-        ok[p] = key;
-        oi[p] = id;
-      }
-    }
-  }
-  __syncthreads();
-  for (int p = (int)r_eff + threadIdx.x; p < sortP; p += blockDim.x) {
-    ok[p] = ~0ull;
-    oi[p] = 0x7FFFFFFFFFFFFFFFll;
-  }
-  __syncthreads();
-  bitonic_sort(ok, oi, sortP);
-  for (int p = threadIdx.x; p < ma; p += blockDim.x) {
-    a.out_cells[q * ma + p] = p < r_eff ? oi[p] : -1;
-    if (a.out_dist) a.out_dist[q * ma + p] = p < r_eff ? dkey_inv(ok[p]) : __longlong_as_double(0x7FF0000000000000ll);
   }
 }
 
@@ -915,13 +667,13 @@ constexpr int RERANK_THREADS = 256;
 
 __global__ void __launch_bounds__(RERANK_THREADS, 4) ivf_rerank_kernel(
     uint64_t* __restrict__ cand, const int* __restrict__ cand_cnt, int64_t cap, const int64_t* __restrict__ ids,
-    const float* __restrict__ queries, const float* __restrict__ coarse, const float* __restrict__ books,
+    QVec queries, const float* __restrict__ coarse, const float* __restrict__ books,
     const uint8_t* __restrict__ codes, int m, int k, int d, int dsub, int64_t* __restrict__ pids) {
   const int64_t q = blockIdx.x;
   const int64_t M = min((int64_t)cand_cnt[q], cap);
   uint64_t* cq = cand + q * cap;
   int64_t* iq = pids + q * cap;
-  const float* qv = queries + q * (int64_t)d;
+  const QVec qv = queries.offset(q * (int64_t)d);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane >> 3, j0 = lane & 7;
   const int64_t step = (int64_t)gridDim.y * (RERANK_THREADS / 32) * 4;
@@ -942,7 +694,7 @@ __global__ void __launch_bounds__(RERANK_THREADS, 4) ivf_rerank_kernel(
         double t = 0.0;
         for (int s2 = 0; s2 < dsub; ++s2) {
           const int dd = j * dsub + s2;
-          const double rr = __dsub_rn((double)__ldg(qv + dd), (double)__ldg(g + dd));
+          const double rr = __dsub_rn(qv.at(dd), (double)__ldg(g + dd));
           const double df = __dsub_rn(rr, (double)__ldg(cb + s2));
           t = __dadd_rn(t, __dmul_rn(df, df));
         }
@@ -972,27 +724,10 @@ __global__ void ivf_all_kernel(const int64_t* __restrict__ cells_row, int ma, co
   }
 }
 
-struct Cublas {
-  cublasHandle_t h = nullptr;
-  int device = -1;
-};
-Cublas g_cublas[16];
-
-int get_cublas(pqs_ctx* ctx, cublasHandle_t* out) {
-  Cublas& c = g_cublas[ctx->device & 15];
-  if (!c.h) {
-    if (cublasCreate(&c.h) != CUBLAS_STATUS_SUCCESS) return set_err(ctx, PQS_ERR_CUDA, "cublasCreate failed");
-    cublasSetMathMode(c.h, CUBLAS_PEDANTIC_MATH);  // true fp32, no TF32
-    c.device = ctx->device;
-  }
-  cublasSetStream(c.h, ctx->stream);
-  *out = c.h;
-  return PQS_OK;
-}
-
 }  // namespace
 
 void ivf_destroy_impl(pqs_ivf* iv);
+int probe_build_index(pqs_ctx* ctx, pqs_ivf* iv);
 
 // ---------------------------------------------------------------------------
 int device_max_u8(pqs_ctx* ctx, const uint8_t* d, int64_t count, int* out);
@@ -1051,6 +786,14 @@ int ivf_create_impl(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t
   PQS_CUDA(ctx, cudaMemsetAsync(iv->vmax, 0, 16, ctx->stream));
   cnorm_kernel<<<(unsigned)cdiv(K, 256), 256, 0, ctx->stream>>>(iv->coarse, K, d, iv->cnorm, iv->gnorm, iv->cnormf);
   PQS_LAUNCHED(ctx);
+  {
+    const int st = probe_build_index(ctx, iv);
+    if (st != PQS_OK) {
+      cudaGetLastError();
+      ivf_destroy_impl(iv);
+      return st;
+    }
+  }
   v_kernel<<<(unsigned)K, 256, 0, ctx->stream>>>(iv->coarse, iv->books, iv->offsets, iv->codes, iv->m, iv->k, iv->dsub,
                                                  d, iv->vtab, iv->vmax);
   PQS_LAUNCHED(ctx);
@@ -1097,72 +840,11 @@ void ivf_destroy_impl(pqs_ivf* iv) {
   cudaFree(iv->vtab);
   cudaFree(iv->vmax);
   if (iv->list_order) cudaFree(iv->list_order);
+  if (iv->probe_b) cudaFree(iv->probe_b);
   delete iv;
 }
 
-int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int64_t nq, int ma, int64_t* d_cells,
-                  double* d_dist) {
-  const int64_t K = iv->K;
-  const int d = iv->d;
-  // query batch: the (QB, K) fp32 dot block is written by the GEMM and read
-  // back by the select; PQS_PROBE_MB sizes it (tuning experiments)
-  static const int64_t probe_mb = getenv("PQS_PROBE_MB") ? atoll(getenv("PQS_PROBE_MB")) : 1024;
-  const int64_t QB = std::max<int64_t>(1, std::min<int64_t>(nq, (probe_mb << 20) / (K * 4)));
-  float* dots = nullptr;
-  uint64_t* gk = nullptr;
-  int64_t* gi = nullptr;
-  PQS_TRY(scratch(ctx, S_IVF_WORK, (size_t)(QB * K), &dots));
-  PQS_TRY(scratch(ctx, S_KEYS, (size_t)(QB * K), &gk));
-  PQS_TRY(scratch(ctx, S_IDS, (size_t)(QB * K), &gi));
-  cublasHandle_t h;
-  PQS_TRY(get_cublas(ctx, &h));
-  // TF32 tensor-core GEMM by default (the probe sets stay exact: every cell
-  // within the certified bound is re-scored in fp64); PQS_PROBE_FP32=1 keeps
-  // the pedantic fp32 SIMT GEMM
-  static const int tf32 = getenv("PQS_PROBE_FP32") ? 0 : 1;
-  int P = 1;
-  while (P < ma) P <<= 1;
-  if (P < 2) P = 2;
-  PQS_CHECK(ctx, P <= 4096, "ma too large for the device probe select (<= 4096)");
-  const size_t smem = (size_t)PROBE_SMEM_CAP * 16 + (size_t)P * 16;
-  PQS_CUDA(ctx, cudaFuncSetAttribute(probe_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)((size_t)PROBE_SMEM_CAP * 16 + 4096 * 16)));
-  for (int64_t q0 = 0; q0 < nq; q0 += QB) {
-    const int64_t nb = std::min(QB, nq - q0);
-    // dots (nb, K) row-major = queries (nb, d) x coarse^T; column-major view:
-    // dots^T (K x nb) = coarse (K x d, col-major = coarse^T row-major...) use
-    // C(K, nb) = A(K, d) * B(d, nb) with A = coarse row-major seen as (d x K)
-    // col-major transposed, B = queries row-major seen as (d x nb) col-major.
-    const float alpha = 1.f, beta = 0.f;
-    cublasSetMathMode(h, tf32 ? CUBLAS_TF32_TENSOR_OP_MATH : CUBLAS_PEDANTIC_MATH);
-    if (cublasSgemm(h, CUBLAS_OP_T, CUBLAS_OP_N, (int)K, (int)nb, d, &alpha, iv->coarse, d, d_queries + q0 * d, d,
-                    &beta, dots, (int)K) != CUBLAS_STATUS_SUCCESS)
-      return set_err(ctx, PQS_ERR_CUDA, "cublasSgemm failed");
-    ctx->launches++;
-    ProbeArgs a{};
-    a.dots = dots;
-    a.cnorm = iv->cnorm;
-    a.cnormf = iv->cnormf;
-    a.tf32 = tf32;
-    a.gnorm = iv->gnorm;
-    a.gmax = iv->gmax;
-    a.queries = d_queries + q0 * d;
-    a.coarse = iv->coarse;
-    a.K = K;
-    a.d = d;
-    a.ma = ma;
-    a.q0 = q0;
-    a.out_cells = d_cells;
-    a.out_dist = d_dist;
-    a.gkeys = gk;
-    a.gids = gi;
-    probe_select_kernel<<<(unsigned)nb, PROBE_THREADS, smem, ctx->stream>>>(a, P);
-    PQS_LAUNCHED(ctx);
-  }
-  return PQS_OK;
-}
-
-int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int64_t nq, int ma, int r, double* d_dist,
+int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, int ma, int r, double* d_dist,
                    int64_t* d_ids, int32_t* d_count) {
   const int64_t K = iv->K;
   const int m = iv->m, k = iv->k;
@@ -1178,7 +860,7 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
   PQS_TRY(scratch(ctx, S_TABLES, (size_t)(nq * m * k), &U));
   PQS_TRY(scratch(ctx, S_AERR, (size_t)nq, &aerr));
   {
-    const size_t usz = ((size_t)UQ * m * k + (size_t)UQ * iv->d) * 4;
+    const size_t usz = ((size_t)UQ * m * k + 1) * 4 + (size_t)UQ * iv->d * 8;
     PQS_CHECK(ctx, usz <= 200 * 1024, "IVF query tables: m * k too large");
     PQS_CUDA(ctx, cudaFuncSetAttribute(utables_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usz));
     utables_kernel<<<(unsigned)cdiv(nq, UQ), 256, usz, ctx->stream>>>(d_queries, iv->books, nq, m, k, iv->dsub, U);
@@ -1246,7 +928,7 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
   ivf_cand_theta_kernel<<<(unsigned)nq, CT_THREADS, 0, ctx->stream>>>(cand, capx, cnt, cap, r, aerr, cand2, cnt2);
   PQS_LAUNCHED(ctx);
   int64_t* pids = reinterpret_cast<int64_t*>(cand);
-  auto rerank = [&](uint64_t* cd, const int* cc, int64_t cp, const float* qs, int64_t nqr, int64_t* pi) -> int {
+  auto rerank = [&](uint64_t* cd, const int* cc, int64_t cp, QVec qs, int64_t nqr, int64_t* pi) -> int {
     dim3 rg((unsigned)nqr, 8);
     ivf_rerank_kernel<<<rg, RERANK_THREADS, 0, ctx->stream>>>(cd, cc, cp, iv->ids, qs, iv->coarse, iv->books,
                                                               iv->codes, m, k, iv->d, iv->dsub, pi);
@@ -1337,7 +1019,7 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int6
       PQS_LAUNCHED(ctx);
       int64_t* fpi = nullptr;
       PQS_TRY(scratch(ctx, S_PIDS, (size_t)fcap, &fpi));
-      PQS_TRY(rerank(fc, fcnt, fcap, d_queries + (int64_t)qg * iv->d, 1, fpi));
+      PQS_TRY(rerank(fc, fcnt, fcap, d_queries.offset((int64_t)qg * iv->d), 1, fpi));
       SelArgs f = s;
       f.nq = 1;
       f.cand = fc;

@@ -54,7 +54,7 @@ struct QiShared {
 __device__ __forceinline__ uint64_t id_key(int64_t id) { return (uint64_t)id ^ 0x8000000000000000ull; }
 
 __global__ void __launch_bounds__(QI_THREADS) ivf_qadc_kernel(
-    const float* __restrict__ queries, const float* __restrict__ coarse, const float* __restrict__ books,
+    QVec queries, const float* __restrict__ coarse, const float* __restrict__ books,
     const int64_t* __restrict__ offsets, const uint8_t* __restrict__ codes, const int64_t* __restrict__ ids,
     const int64_t* __restrict__ cells, int64_t q0, int ma, int m, int d, int dsub, int init_count, int r,
     uint64_t* __restrict__ cand, int64_t* __restrict__ pids, int* __restrict__ cnt, int64_t cap) {
@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(QI_THREADS) ivf_qadc_kernel(
   const int64_t lb = offsets[c];
   const int64_t n = offsets[c + 1] - lb;
   if (n == 0) return;  // ivf.py:176-177
-  const float* qv = queries + (q0 + ql) * (int64_t)d;
+  const QVec qv = queries.offset((q0 + ql) * (int64_t)d);
   const float* g = coarse + c * (int64_t)d;
   const uint8_t* lc = codes + lb * (int64_t)m;
   const int64_t* li = ids + lb;
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(QI_THREADS) ivf_qadc_kernel(
     double t = 0.0;
     for (int s = 0; s < dsub; ++s) {
       const int dd = j * dsub + s;
-      const double rr = __dsub_rn((double)__ldg(qv + dd), (double)__ldg(g + dd));
+      const double rr = __dsub_rn(qv.at(dd), (double)__ldg(g + dd));
       const double df = __dsub_rn(rr, (double)__ldg(cb + s));
       t = __dadd_rn(t, __dmul_rn(df, df));
     }
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(QI_THREADS) ivf_qadc_kernel(
 // Batched query_ivf(kernel='quick-adc'): probes, per-(query, probe) Quick ADC
 // top-r, K5 merge.  Queries are processed in batches so the candidate rows
 // (ma * r per query) stay within a bounded scratch.
-int run_ivf_qadc_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_queries, int64_t nq, int ma, int r,
+int run_ivf_qadc_search(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, int ma, int r,
                         int init_count, double* d_dist, int64_t* d_ids, int32_t* d_count) {
   const int m = iv->m;
   PQS_CHECK(ctx, iv->k == 16, "the quick-adc kernel requires b = 4 (16-entry tables)");

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -21,6 +22,23 @@ constexpr int TILE8 = 1024;
 constexpr int TILE4 = 1024;
 constexpr int QUADS4 = TILE4 / 4;
 constexpr int MAX_R = 4096;  // largest r the device select handles
+
+// Query (or vector) rows as the caller passed them: float32 or float64.  The
+// reference computes from float64(query) (ProductQuantizer.rotate,
+// quantizer.py:85-89; query_ivf ivf.py:170), so every exact kernel reads
+// the rows through at() in fp64; float32 input is widened exactly.
+struct QVec {
+  const void* p = nullptr;
+  int f64 = 0;
+  __host__ __device__ QVec offset(int64_t i) const {
+    return QVec{f64 ? (const void*)((const double*)p + i) : (const void*)((const float*)p + i), f64};
+  }
+#ifdef __CUDACC__
+  __device__ __forceinline__ double at(int64_t i) const {
+    return f64 ? __ldg((const double*)p + i) : (double)__ldg((const float*)p + i);
+  }
+#endif
+};
 
 struct Scratch {
   void* p = nullptr;
@@ -59,6 +77,7 @@ enum ScratchSlot {
   S_PIDS,     // compacted IVF candidates (then their exact keys)
   S_IVF_APX,  // IVF candidates' filter distances
   S_IVF_CNT2, // IVF compacted candidate counts
+  S_QUERIES32,// float32 copy of float64 queries (probe GEMM operand)
   S_NSLOTS
 };
 
@@ -107,7 +126,16 @@ struct pqs_pq {
   float* books = nullptr;  // device (m, k, dsub)
 };
 
+// every pqs_db gets a process-unique generation number at creation and a new
+// one whenever its device content changes (pqs_db_set_prefix): captured CUDA
+// graphs are keyed on it, never on the (reusable) host address of the handle
+inline int64_t next_db_generation() {
+  static std::atomic<int64_t> g{0};
+  return ++g;
+}
+
 struct pqs_db {
+  int64_t gen = 0;        // next_db_generation() at create / prefix change
   int64_t n = 0;
   int m = 0, b = 0, k = 0;
   int mp = 0;             // b==4: padded component count (2,4,8,16,32)
@@ -139,6 +167,11 @@ struct pqs_ivf {
   int64_t* ids = nullptr;         // (n,)
   int64_t max_list = 0;
   int* list_order = nullptr;      // (K,) list-scan order (cells grouped by nearest pivot) or null
+  // probe GEMM (probe.cu): canonical tf32 B tiles of (-2c, ||c||^2 hi, lo),
+  // 256 cells per tile, dpad = d + 2 rounded up to 8 (0: d + 2 > 256, exact probes)
+  float* probe_b = nullptr;
+  int probe_dpad = 0;
+  int64_t probe_ntiles = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -252,8 +285,7 @@ __device__ __forceinline__ uint8_t quantize1(double v, double qmin, double qmax,
 // launchers (defined in the .cu files)
 // ---------------------------------------------------------------------------
 // tables.cu
-int launch_tables_exact(pqs_ctx* ctx, const pqs_pq* pq, const float* d_queries, int64_t nq,
-                        float* d_tables);
+int launch_tables_exact(pqs_ctx* ctx, const pqs_pq* pq, QVec d_queries, int64_t nq, float* d_tables);
 // scan8.cu
 int launch_scan_distances(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t nq,
                           double* d_out);
@@ -315,9 +347,9 @@ struct SelArgs {
 };
 int launch_select(pqs_ctx* ctx, const SelArgs& a);
 // ivf.cu
-int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* ivf, const float* d_queries, int64_t nq, int ma,
+int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* ivf, QVec d_queries, int64_t nq, int ma,
                   int64_t* d_cells, double* d_dist);
-int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* d_queries, int64_t nq, int ma,
+int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* ivf, QVec d_queries, int64_t nq, int ma,
                    int r, double* d_dist, int64_t* d_ids, int32_t* d_count);
 // fastscan.cu
 int run_fastscan_checked(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t nq, int64_t n_init,
@@ -325,8 +357,8 @@ int run_fastscan_checked(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, 
 // derived.cu
 int run_derived_search(pqs_ctx* ctx, const pqs_db* db, const float* d_full, int k, const float* d_compact,
                        int64_t nq, int kbar, int r, int64_t r2, double* d_dist, int64_t* d_ids, int32_t* d_count);
-int run_ivf_derived_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_dbooks, int kbar, const float* d_queries,
+int run_ivf_derived_search(pqs_ctx* ctx, const pqs_ivf* iv, const float* d_dbooks, int kbar, QVec d_queries,
                            int64_t nq, int ma, int r, int64_t r2, double* d_dist, int64_t* d_ids, int32_t* d_count);
 // ivf_qadc.cu
-int run_ivf_qadc_search(pqs_ctx* ctx, const pqs_ivf* ivf, const float* d_queries, int64_t nq, int ma,
+int run_ivf_qadc_search(pqs_ctx* ctx, const pqs_ivf* ivf, QVec d_queries, int64_t nq, int ma,
                         int r, int init_count, double* d_dist, int64_t* d_ids, int32_t* d_count);

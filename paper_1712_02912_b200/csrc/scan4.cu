@@ -968,7 +968,9 @@ int run_qadc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t
     ctx->scratch_epoch++;
   }
   QadcRun run{ctx, db, d_tables, nq, init_count, r, d_bins, d_qt, d_ids, d_count, d_qmm};
-  const std::vector<int64_t> key = {(int64_t)(uintptr_t)db, db->n, (int64_t)(uintptr_t)db->prefix, db->n_prefix,
+  // db->gen is unique per handle and content version (never reused), so a graph
+  // captured for a destroyed or re-prefixed list can never replay on another
+  const std::vector<int64_t> key = {db->gen, db->n, (int64_t)(uintptr_t)db->prefix, db->n_prefix,
                                     (int64_t)(uintptr_t)d_tables, nq, init_count, r, ctx->cand_cap, ctx->sample_div,
                                     ctx->scan4_engine, ctx->tc_chunk_tiles, (int64_t)(uintptr_t)d_bins,
                                     (int64_t)(uintptr_t)d_ids, (int64_t)(uintptr_t)d_count, (int64_t)(uintptr_t)d_qt,

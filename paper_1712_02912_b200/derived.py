@@ -22,15 +22,16 @@ from typing import BinaryIO
 import numpy as np
 
 from ._lib import ptr
-from .engine import DeviceCodes, DeviceQuantizer, _empty, _host_f32, _io
+from .engine import DeviceCodes, DeviceQuantizer, _empty, _fn, _io, _queries
 from .formats import _read_array, _read_i32, _write_array, _write_i32, read_quantizer_body, write_quantizer_body
-from .types import CodeList, LookupTables, NeighborSet, ProductQuantizer
+from ._cache import device_cached
+from .types import CodeList, LookupTables, NeighborSet, ProductQuantizer, _Sealable, implicit_ids
 
 CBINS = 255  # derived.py:31
 
 
 @dataclass
-class DerivedPQ:
+class DerivedPQ(_Sealable):
     """derived.py:35-62: full b-bit quantizer + per-sub-space 2^bbar derived
     codebooks; the low bbar bits of a full index name its derived cluster."""
 
@@ -45,6 +46,7 @@ class DerivedPQ:
         expect = (self.pq.m, 1 << self.bbar, self.pq.dsub)
         if self.derived.shape != expect:
             raise ValueError(f"derived shape {self.derived.shape}, expected {expect}")
+        self._seal()
 
     @property
     def kbar(self) -> int:
@@ -56,13 +58,11 @@ class DerivedPQ:
 
     def _device(self):
         """(full, derived) device quantizer handles, cached on the object."""
-        key = (self.pq.codebooks.ctypes.data, self.derived.ctypes.data, self.bbar)
-        cache = getattr(self, "_pqs_dev", None)
-        if cache is None or cache[0] != key:
+        def build():
             dq = ProductQuantizer(m=self.pq.m, b=self.bbar, d=self.pq.d, codebooks=self.derived)
-            cache = (key, DeviceQuantizer(self.pq), DeviceQuantizer(dq))
-            object.__setattr__(self, "_pqs_dev", cache)
-        return cache[1], cache[2]
+            return DeviceQuantizer(self.pq), DeviceQuantizer(dq)
+
+        return device_cached(self, "_pqs_dev", (self.pq.codebooks, self.derived, self.bbar), build)
 
 
 def compute_compact_tables(dpq: DerivedPQ, query: np.ndarray) -> LookupTables:
@@ -70,21 +70,14 @@ def compute_compact_tables(dpq: DerivedPQ, query: np.ndarray) -> LookupTables:
     query = np.asarray(query)
     if query.ndim != 1 or query.shape[0] != dpq.pq.d:
         raise ValueError(f"query must have shape ({dpq.pq.d},)")
-    from .quantizer import as_f32_exact
-
     _, dd = dpq._device()
-    return LookupTables(dd.compute_tables(as_f32_exact(query, "compute_compact_tables")[None, :])[0])
+    return LookupTables(dd.compute_tables(query[None, :])[0])
 
 
 def _device_list(db: CodeList) -> DeviceCodes:
-    codes = np.ascontiguousarray(db.codes, dtype=np.uint8)
-    ids = None if getattr(db, "_implicit_ids", False) else db.ids
-    key = (codes.ctypes.data, codes.shape, None if ids is None else ids.ctypes.data)
-    cache = getattr(db, "_pqs_dv", None)
-    if cache is None or cache[0] != key:
-        cache = (key, DeviceCodes(codes, 8, ids=ids))
-        object.__setattr__(db, "_pqs_dv", cache)
-    return cache[1]
+    ids = None if implicit_ids(db) else db.ids
+    return device_cached(db, "_pqs_dv", (db.codes, db.ids),
+                         lambda: DeviceCodes(np.ascontiguousarray(db.codes, dtype=np.uint8), 8, ids=ids))
 
 
 def search_two_pass_batch(dpq: DerivedPQ, db: CodeList, queries, r: int, r2: int):
@@ -97,14 +90,14 @@ def search_two_pass_batch(dpq: DerivedPQ, db: CodeList, queries, r: int, r2: int
         raise ValueError("r must be >= 1")
     full, dd = dpq._device()
     dev = _device_list(db)
-    q = _host_f32(queries, 2, "queries")
+    q, f64 = _queries(queries, 2, "queries")
     nq = q.shape[0]
     d = _empty((nq, r), np.float64, q)
     i = _empty((nq, r), np.int64, q)
     c = _empty((nq,), np.int32, q)
-    dev.ctx.check(dev.ctx.lib.pqs_derived_search(dev.ctx.handle, dev.handle, full.handle, dd.handle, ptr(q), nq,
-                                                 int(r), int(r2), ptr(d), ptr(i), ptr(c), _io(dev.ctx, q, d)),
-                  "derived_search")
+    dev.ctx.check(_fn(dev.ctx, "pqs_derived_search", f64)(dev.ctx.handle, dev.handle, full.handle, dd.handle, ptr(q),
+                                                            nq, int(r), int(r2), ptr(d), ptr(i), ptr(c),
+                                                            _io(dev.ctx, q, d)), "derived_search")
     return d, i, c
 
 
@@ -114,9 +107,7 @@ def search_two_pass(dpq: DerivedPQ, db: CodeList, query: np.ndarray, r: int, r2:
     query = np.asarray(query)
     if query.ndim != 1 or query.shape[0] != dpq.pq.d:
         raise ValueError(f"query must have shape ({dpq.pq.d},)")
-    from .quantizer import as_f32_exact
-
-    d, i, c = search_two_pass_batch(dpq, db, as_f32_exact(query, "search_two_pass")[None, :], r, r2)
+    d, i, c = search_two_pass_batch(dpq, db, query[None, :], r, r2)
     n = int(c[0])
     return NeighborSet.from_pairs(r, d[0, :n], i[0, :n])
 

@@ -65,7 +65,33 @@ def _check_out(out, shapes, dtypes, like):
     return out
 
 
+def _queries(a, ndim, what):
+    """Query / vector rows and whether they are float64.  float32 rows stay
+    float32; every other dtype becomes float64 -- the reference computes from
+    float64(query) (quantizer.py:85-89, ivf.py:170, quantizer.py:319-323), and
+    the *_f64 entry points read it as given (nothing is rounded to float32)."""
+    if _is_device(a):
+        if str(a.dtype) not in ("torch.float32", "torch.float64") or not a.is_contiguous():
+            raise ValueError(f"{what} must be a contiguous float32 or float64 tensor")
+        if a.dim() != ndim:
+            raise ValueError(f"{what} must be {ndim}-D")
+        return a, str(a.dtype) == "torch.float64"
+    a = np.asarray(a)
+    if a.dtype != np.float32:
+        a = a.astype(np.float64)
+    a = np.ascontiguousarray(a)
+    if a.ndim != ndim:
+        raise ValueError(f"{what} must be {ndim}-D")
+    return a, a.dtype == np.float64
+
+
+def _fn(ctx, name, f64):
+    return getattr(ctx.lib, name + "_f64" if f64 else name)
+
+
 def _host_f32(a, ndim, what):
+    """Lookup tables (LookupTables forces float32, scan.py:21-42) and other
+    float32-by-definition inputs."""
     if _is_device(a):
         if a.dtype.__str__() != "torch.float32" or not a.is_contiguous():
             raise ValueError(f"{what} must be a contiguous float32 tensor")
@@ -96,19 +122,19 @@ class DeviceQuantizer:
 
     def compute_tables(self, queries):
         """Batched compute_tables (scan.py:45-56): (nq, d) -> (nq, m, k) fp32."""
-        q = _host_f32(queries, 2, "queries")
+        q, f64 = _queries(queries, 2, "queries")
         if q.shape[1] != self.d:
             raise ValueError(f"queries must have shape (nq, {self.d})")
         out = _empty((q.shape[0], self.m, self.k), np.float32, q)
-        self.ctx.check(self.ctx.lib.pqs_compute_tables(self.ctx.handle, self.handle, ptr(q), q.shape[0], ptr(out),
-                                                       _io(self.ctx, q, out)), "compute_tables")
+        self.ctx.check(_fn(self.ctx, "pqs_compute_tables", f64)(self.ctx.handle, self.handle, ptr(q), q.shape[0],
+                                                                  ptr(out), _io(self.ctx, q, out)), "compute_tables")
         return out
 
     def encode(self, x, coarse=None, cells=None):
         """encode (quantizer.py:308-325) of (n, d) fp32 vectors -> (n, m) uint8,
         bit-identical; with coarse (K, d) and cells (n,) the IVF residuals
         x - coarse[cells] are encoded (build_ivf, ivf.py:137-140)."""
-        x = _host_f32(x, 2, "vectors")
+        x, f64 = _queries(x, 2, "vectors")
         if x.shape[1] != self.d:
             raise ValueError(f"vector dimensionality {x.shape[1]}, expected {self.d}")
         K = 0
@@ -116,12 +142,17 @@ class DeviceQuantizer:
             coarse = _host_f32(coarse, 2, "coarse")
             K = coarse.shape[0]
             if _is_device(cells):
+                if str(cells.dtype) != "torch.int64" or cells.dim() != 1:
+                    raise ValueError("device cells must be a 1-D int64 tensor")
                 cells = cells.contiguous()
             else:
                 cells = np.ascontiguousarray(cells, dtype=np.int64)
+            if tuple(cells.shape) != (x.shape[0],):
+                raise ValueError(f"cells must have shape ({x.shape[0]},)")
         out = _empty((x.shape[0], self.m), np.uint8, x)
-        self.ctx.check(self.ctx.lib.pqs_encode(self.ctx.handle, self.handle, ptr(x), x.shape[0], ptr(coarse), K,
-                                               ptr(cells), ptr(out), _io(self.ctx, x, coarse, cells, out)), "encode")
+        self.ctx.check(_fn(self.ctx, "pqs_encode", f64)(self.ctx.handle, self.handle, ptr(x), x.shape[0], ptr(coarse),
+                                                          K, ptr(cells), ptr(out), _io(self.ctx, x, coarse, cells, out)),
+                       "encode")
         return out
 
     def __del__(self):
@@ -196,7 +227,7 @@ class DeviceCodes:
     def adc_search(self, dq: DeviceQuantizer, queries, r: int, out=None):
         """Batched compute_tables + scan: (nq, d) queries -> (dist, ids, count);
         out: optional caller-owned output arrays as in qadc_search."""
-        q = _host_f32(queries, 2, "queries")
+        q, f64 = _queries(queries, 2, "queries")
         nq = q.shape[0]
         if out is not None:
             d, i, c = _check_out(out, ((nq, r), (nq, r), (nq,)), (np.float64, np.int64, np.int32), q)
@@ -204,8 +235,8 @@ class DeviceCodes:
             d = _empty((nq, r), np.float64, q)
             i = _empty((nq, r), np.int64, q)
             c = _empty((nq,), np.int32, q)
-        self.ctx.check(self.ctx.lib.pqs_adc_search(self.ctx.handle, self.handle, dq.handle, ptr(q), nq, int(r), ptr(d),
-                                                   ptr(i), ptr(c), _io(self.ctx, q, d)), "adc_search")
+        self.ctx.check(_fn(self.ctx, "pqs_adc_search", f64)(self.ctx.handle, self.handle, dq.handle, ptr(q), nq, int(r),
+                                                              ptr(d), ptr(i), ptr(c), _io(self.ctx, q, d)), "adc_search")
         return d, i, c
 
     # -- Quick ADC (b=4) ---------------------------------------------------
@@ -231,7 +262,7 @@ class DeviceCodes:
         """Batched compute_tables + qadc_scan.  out: optional caller-owned
         (bins uint8 (nq, r), ids int64 (nq, r), count int32 (nq,)) arrays on
         the queries' side (e.g. pinned host buffers reused across calls)."""
-        q = _host_f32(queries, 2, "queries")
+        q, f64 = _queries(queries, 2, "queries")
         nq = q.shape[0]
         if out is not None:
             bins, i, c = _check_out(out, ((nq, r), (nq, r), (nq,)), (np.uint8, np.int64, np.int32), q)
@@ -241,9 +272,9 @@ class DeviceCodes:
             c = _empty((nq,), np.int32, q)
         qt = _empty((nq, self.m, 16), np.uint8, q) if want_tables else None
         qmm = _empty((nq, 2), np.float64, q) if want_tables else None
-        self.ctx.check(self.ctx.lib.pqs_qadc_search(self.ctx.handle, self.handle, dq.handle, ptr(q), nq,
-                                                    int(init_count), int(r), ptr(bins), ptr(i), ptr(c), ptr(qt),
-                                                    ptr(qmm), _io(self.ctx, q, bins)), "qadc_search")
+        self.ctx.check(_fn(self.ctx, "pqs_qadc_search", f64)(self.ctx.handle, self.handle, dq.handle, ptr(q), nq,
+                                                               int(init_count), int(r), ptr(bins), ptr(i), ptr(c),
+                                                               ptr(qt), ptr(qmm), _io(self.ctx, q, bins)), "qadc_search")
         return bins, i, c, qt, qmm
 
     def quantized_distances(self, qtables):
@@ -302,12 +333,13 @@ class DeviceIvf:
         self.handle = h
 
     def probe(self, queries, ma: int):
-        q = _host_f32(queries, 2, "queries")
+        q, f64 = _queries(queries, 2, "queries")
         nq = q.shape[0]
         cells = _empty((nq, ma), np.int64, q)
         dist = _empty((nq, ma), np.float64, q)
-        self.ctx.check(self.ctx.lib.pqs_ivf_probe(self.ctx.handle, self.handle, ptr(q), nq, int(ma), ptr(cells),
-                                                  ptr(dist), _io(self.ctx, q, cells)), "ivf_probe")
+        self.ctx.check(_fn(self.ctx, "pqs_ivf_probe", f64)(self.ctx.handle, self.handle, ptr(q), nq, int(ma),
+                                                             ptr(cells), ptr(dist), _io(self.ctx, q, cells)),
+                       "ivf_probe")
         return cells, dist
 
     def search(self, queries, ma: int, r: int, kernel: str = "adc", init_count: int = 200, r2: int = 9000,
@@ -315,7 +347,7 @@ class DeviceIvf:
         """Batched query_ivf: kernel 'adc' (exact fp64 distances), 'quick-adc'
         (per-list Quick ADC bins rescaled to fp64, ivf.py:185-190) or 'derived'
         (ivf.py:191-195).  out: optional caller-owned (dist, ids, count) arrays."""
-        q = _host_f32(queries, 2, "queries")
+        q, f64 = _queries(queries, 2, "queries")
         if q.shape[1] != self.d:
             raise ValueError(f"query must have shape ({self.d},)")
         nq = q.shape[0]
@@ -327,17 +359,17 @@ class DeviceIvf:
             c = _empty((nq,), np.int32, q)
         io = _io(self.ctx, q, d)
         if kernel == "adc":
-            st = self.ctx.lib.pqs_ivf_search(self.ctx.handle, self.handle, ptr(q), nq, int(ma), int(r), ptr(d),
-                                             ptr(i), ptr(c), io)
+            st = _fn(self.ctx, "pqs_ivf_search", f64)(self.ctx.handle, self.handle, ptr(q), nq, int(ma), int(r),
+                                                        ptr(d), ptr(i), ptr(c), io)
         elif kernel == "quick-adc":
-            st = self.ctx.lib.pqs_ivf_qadc_search(self.ctx.handle, self.handle, ptr(q), nq, int(ma), int(r),
-                                                  int(init_count), ptr(d), ptr(i), ptr(c), io)
+            st = _fn(self.ctx, "pqs_ivf_qadc_search", f64)(self.ctx.handle, self.handle, ptr(q), nq, int(ma),
+                                                             int(r), int(init_count), ptr(d), ptr(i), ptr(c), io)
         elif kernel == "derived":
             if dpq is None:
                 raise ValueError("index has no derived quantizer")
             _, dd = dpq._device()
-            st = self.ctx.lib.pqs_ivf_derived_search(self.ctx.handle, self.handle, dd.handle, ptr(q), nq, int(ma),
-                                                     int(r), int(r2), ptr(d), ptr(i), ptr(c), io)
+            st = _fn(self.ctx, "pqs_ivf_derived_search", f64)(self.ctx.handle, self.handle, dd.handle, ptr(q), nq,
+                                                                int(ma), int(r), int(r2), ptr(d), ptr(i), ptr(c), io)
         else:
             raise ValueError(f"unknown device IVF kernel {kernel!r}")
         self.ctx.check(st, "ivf_search")

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import numpy as np
 
+from ._cache import device_cached, freeze
 from .engine import DeviceIvf
 from .types import IvfIndex, NeighborSet
 
@@ -26,12 +27,17 @@ def default_r2(r: int) -> int:
 
 
 def device_index(index: IvfIndex) -> DeviceIvf:
-    key = (index.coarse.ctypes.data, index.coarse.shape, len(index.lists), index.n)
-    cached = index._device.get("ivf")
-    if cached is None or cached[0] != key:
-        cached = (key, DeviceIvf(index))
-        index._device["ivf"] = cached
-    return cached[1]
+    """The index's device copy: rebuilt after any rebinding of a sealed
+    container's field or change to index.lists (mutation epoch); every list's
+    codes/ids are frozen when uploaded (in-place edits raise)."""
+    def build():
+        for lst in index.lists:
+            freeze(lst.codes)
+            freeze(lst.ids)
+        return DeviceIvf(index)
+
+    return device_cached(index, "_pqs_ivf", (index.coarse, index.pq.codebooks, id(index.lists), len(index.lists)),
+                         build)
 
 
 def query_ivf(index: IvfIndex, query: np.ndarray, ma: int, r: int, kernel: str = "adc",
@@ -52,16 +58,14 @@ def query_ivf(index: IvfIndex, query: np.ndarray, ma: int, r: int, kernel: str =
     if query.shape != (index.d,):
         raise ValueError(f"query must have shape ({index.d},)")
     dev = device_index(index)
-    from .quantizer import as_f32_exact
-
     if kernel == "quick-adc" and init_count < 1:
         # qadc_scan raises at the first non-empty probed list (quickadc.py:123-124)
-        cells, _ = dev.probe(as_f32_exact(query, "query_ivf")[None, :], int(ma))
+        cells, _ = dev.probe(query[None, :], int(ma))
         if any(index.lists[int(c)].n for c in cells[0]):
             raise ValueError("init_count must be >= 1")
         return NeighborSet(r)
 
-    d, i, c = dev.search(as_f32_exact(query, "query_ivf")[None, :], int(ma), int(r), kernel=kernel,
+    d, i, c = dev.search(query[None, :], int(ma), int(r), kernel=kernel,
                          init_count=int(init_count), r2=(r2 if r2 is not None else default_r2(r)), dpq=index.dpq)
     n = int(c[0])
     return NeighborSet.from_pairs(r, d[0, :n], i[0, :n])

@@ -86,12 +86,7 @@ def qadc_scan(tlist: TransposedCodeList, tables: LookupTables, init_count: int, 
         raise ValueError("r must be >= 1")
     if tlist.n == 0:
         raise ValueError("empty code list")
-    cache = getattr(tlist, "_pqs_codes", None)
-    if cache is None:
-        cache = detranspose_blocks(tlist)
-        object.__setattr__(tlist, "_pqs_codes", cache)
-    ids = None if getattr(tlist, "_implicit_ids", False) else tlist.ids
-    dev = _device_codes(tlist, cache.codes, ids, 4)
+    dev = _device_codes(tlist, tlist.blocks, 4, lambda _: detranspose_blocks(tlist).codes)
     r_dev = min(r, tlist.n)
     bins, oid, cnt, qt, qmm = dev.qadc_scan(tables.tables[None], int(init_count), r_dev)
     n = int(cnt[0])

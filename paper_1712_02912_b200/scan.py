@@ -13,26 +13,22 @@ from __future__ import annotations
 
 import numpy as np
 
+from ._cache import device_cached
 from .engine import DeviceCodes, DeviceQuantizer
-from .types import BLOCK, CodeList, LookupTables, NeighborSet, ProductQuantizer, TransposedCodeList
+from .types import BLOCK, CodeList, LookupTables, NeighborSet, ProductQuantizer, TransposedCodeList, implicit_ids
 
 
 def _device_quantizer(pq: ProductQuantizer) -> DeviceQuantizer:
-    key = (pq.codebooks.ctypes.data, pq.codebooks.shape)
-    cache = getattr(pq, "_pqs_dev", None)
-    if cache is None or cache[0] != key:
-        cache = (key, DeviceQuantizer(pq))
-        object.__setattr__(pq, "_pqs_dev", cache)
-    return cache[1]
+    return device_cached(pq, "_pqs_dev", (pq.codebooks, pq.rotation), lambda: DeviceQuantizer(pq))
 
 
-def _device_codes(obj, codes: np.ndarray, ids: np.ndarray | None, b: int) -> DeviceCodes:
-    key = (codes.ctypes.data, codes.shape, None if ids is None else (ids.ctypes.data, ids.shape), b)
-    cache = getattr(obj, "_pqs_dev", None)
-    if cache is None or cache[0] != key:
-        cache = (key, DeviceCodes(codes, b, ids=ids))
-        object.__setattr__(obj, "_pqs_dev", cache)
-    return cache[1]
+def _device_codes(obj, source: np.ndarray, b: int, convert=None) -> DeviceCodes:
+    """Device copy of obj's codes (source: the container's own array, frozen;
+    convert: source -> (n, m) uint8 codes) with obj's ids (implicit while
+    they are the container's default arange)."""
+    ids = None if implicit_ids(obj) else obj.ids
+    return device_cached(obj, f"_pqs_dev{b}", (source, obj.ids),
+                         lambda: DeviceCodes(convert(source) if convert else source, b, ids=ids))
 
 
 def compute_tables(pq: ProductQuantizer, query: np.ndarray) -> LookupTables:
@@ -41,9 +37,7 @@ def compute_tables(pq: ProductQuantizer, query: np.ndarray) -> LookupTables:
     if query.ndim != 1 or query.shape[0] != pq.d:
         raise ValueError(f"query must have shape ({pq.d},)")
     dq = _device_quantizer(pq)
-    from .quantizer import as_f32_exact
-
-    return LookupTables(dq.compute_tables(as_f32_exact(query, "compute_tables")[None, :])[0])
+    return LookupTables(dq.compute_tables(query[None, :])[0])
 
 
 def compute_tables_batch(pq: ProductQuantizer, queries: np.ndarray) -> np.ndarray:
@@ -85,9 +79,10 @@ def scan(codelist: CodeList, tables: LookupTables, r: int) -> NeighborSet:
         raise ValueError(f"codes must have shape (n, {tables.m})")
     if codelist.n == 0:
         return NeighborSet(r)
-    codes = _codes_u8(codelist.codes, tables.k)
-    ids = None if getattr(codelist, "_implicit_ids", False) else codelist.ids
-    dev = _device_codes(codelist, codes, ids, 8)
+    codes = codelist.codes
+    if codes.size and int(codes.max()) >= max(tables.k, 1):
+        raise IndexError("code component out of range for the tables")
+    dev = _device_codes(codelist, codes, 8, lambda c: _codes_u8(c, tables.k))
     r_dev = min(r, codelist.n)
     d, i, c = dev.adc_scan(tables.tables[None], r_dev)
     n = int(c[0])
@@ -120,7 +115,7 @@ def transpose_blocks(codelist: CodeList, b: int) -> TransposedCodeList:
         blocks = np.ascontiguousarray(per_block.transpose(0, 2, 1))
     del rows
     out = TransposedCodeList(blocks=blocks, n=n, m=m, b=b, ids=codelist.ids)
-    object.__setattr__(out, "_implicit_ids", getattr(codelist, "_implicit_ids", False))
+    object.__setattr__(out, "_implicit_ids", codelist.__dict__.get("_implicit_ids"))
     return out
 
 

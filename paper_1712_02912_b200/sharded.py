@@ -94,6 +94,8 @@ class ShardedSearch:
         from .engine import DeviceCodes, DeviceQuantizer, merge_topr
 
         lo, hi = shard_range(n_total, world, rank)
+        if codes_local.shape[0] != hi - lo:
+            raise ValueError("codes_local does not match this rank's shard")
         db = DeviceCodes(codes_local, 8, id_base=lo, ctx=ctx)
         dq = DeviceQuantizer(pq, ctx)
 

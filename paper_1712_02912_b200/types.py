@@ -22,12 +22,57 @@ DEFAULT_INIT_COUNT = 200       # quickadc.py:28
 DEFAULT_INIT_COUNT_BILLION = 1000  # quickadc.py:29
 
 
+# ---------------------------------------------------------------------------
+# device-cache coherence.  The drop-in functions upload a container's arrays
+# to the GPU once and reuse the device copy (paper_1712_02912_b200/_cache.py).
+# The reference recomputes from the arrays on every call, so two things would
+# otherwise make results stale: (1) in-place edits of a cached array -- the
+# cache makes every array it uploads read-only, so such edits raise
+# (numpy's "assignment destination is read-only"): refused, loudly; (2)
+# rebinding a field (`codelist.codes = other`, `index.lists[c] = other`) --
+# sealed containers bump a global mutation epoch that every cache key holds.
+_EPOCH = [0]
+
+
+def mutation_epoch() -> int:
+    """Bumped whenever a field of a sealed container is rebound."""
+    return _EPOCH[0]
+
+
+class _Sealable:
+    def __setattr__(self, name, value):
+        if self.__dict__.get("_sealed", False) and not name.startswith("_"):
+            _EPOCH[0] += 1
+        object.__setattr__(self, name, value)
+
+    def _seal(self):
+        object.__setattr__(self, "_sealed", True)
+
+
+class _TrackedList(list):
+    """IvfIndex.lists: a list whose mutations bump the mutation epoch."""
+
+    def _bump(self):
+        _EPOCH[0] += 1
+
+
+for _name in ("__setitem__", "__delitem__", "__iadd__", "__imul__", "append", "extend", "insert", "pop",
+              "remove", "clear", "sort", "reverse"):
+    def _make(fn):
+        def wrapped(self, *a, **k):
+            self._bump()
+            return fn(self, *a, **k)
+        wrapped.__name__ = fn.__name__
+        return wrapped
+    setattr(_TrackedList, _name, _make(getattr(list, _name)))
+
+
 class TrainError(RuntimeError):
     """quantizer.py:21-22."""
 
 
 @dataclass
-class ProductQuantizer:
+class ProductQuantizer(_Sealable):
     """quantizer.py:38-89: m codebooks of 2^b centroids over d/m dims."""
 
     m: int
@@ -51,6 +96,7 @@ class ProductQuantizer:
             self.rotation = np.ascontiguousarray(self.rotation, dtype=np.float32)
             if self.rotation.shape != (self.d, self.d):
                 raise ValueError("rotation must be d x d")
+        self._seal()
 
     @property
     def k(self) -> int:
@@ -87,6 +133,13 @@ class LookupTables:
     @property
     def nbytes(self) -> int:
         return self.tables.nbytes
+
+
+def implicit_ids(obj) -> bool:
+    """True while obj.ids is still the arange the container made itself
+    (CodeList default ids, scan.py:170-171): the device then uses id = index."""
+    imp = obj.__dict__.get("_implicit_ids")
+    return imp is not None and imp is obj.ids
 
 
 class NeighborSet:
@@ -136,7 +189,7 @@ class NeighborSet:
 
 
 @dataclass
-class CodeList:
+class CodeList(_Sealable):
     """scan.py:157-194: codes (n, m) uint8/uint16 with parallel int64 ids."""
 
     codes: np.ndarray
@@ -148,13 +201,17 @@ class CodeList:
             raise ValueError("codes must be 2-D (n, m)")
         if self.codes.dtype not in (np.dtype(np.uint8), np.dtype(np.uint16)):
             raise ValueError("codes must be uint8 or uint16")
-        self._implicit_ids = self.ids is None
+        implicit = self.ids is None
         if self.ids is None:
             self.ids = np.arange(self.codes.shape[0], dtype=np.int64)
         else:
             self.ids = np.ascontiguousarray(self.ids, dtype=np.int64)
         if self.ids.shape != (self.codes.shape[0],):
             raise ValueError("ids length must match codes")
+        # the default arange ids are implicit on the device (id = index) for as
+        # long as this very array is the list's ids (see implicit_ids)
+        self._implicit_ids = self.ids if implicit else None
+        self._seal()
 
     @property
     def n(self) -> int:
@@ -166,7 +223,7 @@ class CodeList:
 
 
 @dataclass
-class TransposedCodeList:
+class TransposedCodeList(_Sealable):
     """scan.py:209-245: codes regrouped into component-major blocks of 16."""
 
     blocks: np.ndarray
@@ -184,6 +241,8 @@ class TransposedCodeList:
             raise ValueError(f"blocks shape {self.blocks.shape}, expected {(nblocks, rows, BLOCK)}")
         if self.ids.shape != (self.n,):
             raise ValueError("ids length must match n")
+        self._implicit_ids = None
+        self._seal()
 
     @property
     def n_blocks(self) -> int:
@@ -239,7 +298,7 @@ class QuantizedTables4:
 
 
 @dataclass
-class IvfIndex:
+class IvfIndex(_Sealable):
     """ivf.py:58-86: coarse centroids, residual quantizer, K inverted lists."""
 
     coarse: np.ndarray
@@ -256,6 +315,13 @@ class IvfIndex:
             raise ValueError("need exactly one inverted list per coarse centroid")
         if self.dpq is not None and self.dpq.pq is not self.pq:
             raise ValueError("derived quantizer must wrap the index quantizer")
+        self.lists = self.lists  # as a _TrackedList
+        self._seal()
+
+    def __setattr__(self, name, value):
+        if name == "lists" and not isinstance(value, _TrackedList):
+            value = _TrackedList(value)
+        super().__setattr__(name, value)
 
     @property
     def K(self) -> int:

@@ -343,6 +343,58 @@ def g_encode():
     save("encode.npz", **out)
 
 
+def g_fp64():
+    """float64 queries / vectors that float32 cannot represent (the reference
+    computes from float64(query): quantizer.py:85-89, ivf.py:170, encode
+    quantizer.py:319-323): tables, scan, qadc_scan, query_ivf ('adc' and
+    'quick-adc'), the probes and encode."""
+    rng = np.random.default_rng(707)
+    base = mixture(rng, 5000, 32, 24, 128.0, 16.0, 0.0, 255.0)
+    qs = (base[rng.choice(5000, 6, replace=False)].astype(np.float64)
+          + rng.normal(0.0, 6.0, (6, 32)))          # fp64, not fp32-representable
+    assert not np.array_equal(qs.astype(np.float32).astype(np.float64), qs)
+    out = dict(queries=qs)
+    pq8 = train_pq(base[:3000], 4, 8, TrainConfig(kmeans_iters=4, seed=4))
+    codes8 = encode(pq8, base)
+    out.update(pq8_books=pq8.codebooks, codes8=codes8)
+    pq4 = train_pq(base[:3000], 8, 4, TrainConfig(kmeans_iters=4, seed=5))
+    codes4 = encode(pq4, base)
+    out.update(pq4_books=pq4.codebooks, codes4=codes4)
+    tl = transpose_blocks(CodeList(codes4), 4)
+    t8, s_d, s_i, q_b, q_i = [], [], [], [], []
+    for q in qs:
+        t = compute_tables(pq8, q)
+        t8.append(t.tables)
+        d, i, _ = items_arrays(scan(CodeList(codes8), t, 20), 20)
+        s_d.append(d)
+        s_i.append(i)
+        nset, _ = qadc_scan(tl, compute_tables(pq4, q), 200, 30)
+        d, i, _ = items_arrays(nset, 30)
+        q_b.append(d)
+        q_i.append(i)
+    out.update(tables8=np.stack(t8), scan_dist=np.stack(s_d), scan_ids=np.stack(s_i), qadc_bins=np.stack(q_b),
+               qadc_ids=np.stack(q_i))
+    idx = build_ivf(base, K=32, m=4, b=8, cfg=TrainConfig(kmeans_iters=6, seed=2))
+    out.update(coarse=idx.coarse, ivf_books=idx.pq.codebooks,
+               list_sizes=np.array([lst.n for lst in idx.lists], dtype=np.int64),
+               list_codes=np.concatenate([lst.codes for lst in idx.lists]),
+               list_ids=np.concatenate([lst.ids for lst in idx.lists]))
+    d, i = zip(*[items_arrays(query_ivf(idx, q, ma=5, r=25), 25)[:2] for q in qs])
+    out.update(ivf_dist=np.stack(d), ivf_ids=np.stack(i))
+    cells, cd = nearest_k(qs, idx.coarse.astype(np.float64), 7)
+    out.update(probe_cells=cells, probe_dist=cd)
+    idx4 = build_ivf(base, K=16, m=8, b=4, cfg=TrainConfig(kmeans_iters=4, seed=3))
+    out.update(coarse4=idx4.coarse, ivf4_books=idx4.pq.codebooks,
+               list4_sizes=np.array([lst.n for lst in idx4.lists], dtype=np.int64),
+               list4_codes=np.concatenate([lst.codes for lst in idx4.lists]),
+               list4_ids=np.concatenate([lst.ids for lst in idx4.lists]))
+    d, i = zip(*[items_arrays(query_ivf(idx4, q, ma=3, r=15, kernel="quick-adc", init_count=50), 15)[:2] for q in qs])
+    out.update(ivfq_dist=np.stack(d), ivfq_ids=np.stack(i))
+    xs = base[:200].astype(np.float64) + rng.normal(0.0, 1e-3, (200, 32))
+    out.update(enc_x=xs, enc_codes=encode(pq8, xs))
+    save("fp64.npz", **out)
+
+
 def g_formats():
     """PQZ1 / PQL1 (b = 4 packed nibbles, b = 8) / IVF1 files written by the reference."""
     from pqscan import save_codes, save_ivf, save_quantizer
@@ -384,4 +436,5 @@ if __name__ == "__main__":
     g_fastscan()
     g_derived()
     g_encode()
+    g_fp64()
     g_formats()

@@ -40,7 +40,27 @@ def test_python_binding_covers_header():
 def test_api_version():
     from paper_1712_02912_b200 import _lib
 
-    assert _lib.load_library().pqs_api_version() == 2
+    assert _lib.load_library().pqs_api_version() == 3
+
+
+def test_f64_twins():
+    """Every query-taking entry point has a float64 twin (the reference
+    computes from float64(query), quantizer.py:85-89)."""
+    fns = set(header_functions())
+    from paper_1712_02912_b200 import _lib
+
+    for name in _lib.F64_TWINS:
+        assert name in fns and name + "_f64" in fns, name
+
+
+def test_no_library_gemm_linked():
+    """The probe GEMM is hand-written tcgen05 (probe.cu): libpqs.so links no cuBLAS."""
+    import subprocess
+
+    from paper_1712_02912_b200 import _lib
+
+    out = subprocess.run(["ldd", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "cublas" not in out
 
 
 def test_no_device_fails_loudly():

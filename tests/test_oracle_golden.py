@@ -143,3 +143,39 @@ def test_ivf_quick_adc_query(golden, tag, ma, r, ic):
         np.testing.assert_array_equal(d, g[f"{key}_dist"][qi][:n])
         np.testing.assert_array_equal(i, g[f"{key}_ids"][qi][:n])
         assert np.all(g[f"{key}_ids"][qi][n:] == -1)
+
+
+def _split(sizes, codes, ids):
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    return ([codes[offs[c]:offs[c + 1]] for c in range(len(sizes))],
+            [ids[offs[c]:offs[c + 1]] for c in range(len(sizes))])
+
+
+def test_fp64_queries(golden):
+    """float64 queries float32 cannot represent: the reference computes from
+    float64(query) (quantizer.py:85-89, ivf.py:170) -- the oracle too."""
+    g = golden("fp64.npz")
+    qs = g["queries"]
+    assert qs.dtype == np.float64
+    ids = np.arange(g["codes8"].shape[0])
+    lc, li = _split(g["list_sizes"], g["list_codes"], g["list_ids"])
+    lc4, li4 = _split(g["list4_sizes"], g["list4_codes"], g["list4_ids"])
+    for qi, q in enumerate(qs):
+        t = O.compute_tables(g["pq8_books"], q)
+        np.testing.assert_array_equal(t.view(np.uint32), g["tables8"][qi].view(np.uint32))
+        d, i = O.scan(g["codes8"], ids, t, 20)
+        np.testing.assert_array_equal(d, g["scan_dist"][qi])
+        np.testing.assert_array_equal(i, g["scan_ids"][qi])
+        b, i, _, _, _ = O.qadc_scan(g["codes4"], ids, O.compute_tables(g["pq4_books"], q), 200, 30)
+        np.testing.assert_array_equal(b, g["qadc_bins"][qi])
+        np.testing.assert_array_equal(i, g["qadc_ids"][qi])
+        d, i = O.query_ivf(g["coarse"], g["ivf_books"], lc, li, q, 5, 25)
+        np.testing.assert_array_equal(d, g["ivf_dist"][qi])
+        np.testing.assert_array_equal(i, g["ivf_ids"][qi])
+        d, i = O.query_ivf(g["coarse4"], g["ivf4_books"], lc4, li4, q, 3, 15, kernel="quick-adc", init_count=50)
+        np.testing.assert_array_equal(d, g["ivfq_dist"][qi])
+        np.testing.assert_array_equal(i, g["ivfq_ids"][qi])
+    cells, dist = O.nearest_k(qs, g["coarse"].astype(np.float64), 7)
+    np.testing.assert_array_equal(cells, g["probe_cells"])
+    np.testing.assert_array_equal(dist, g["probe_dist"])
+    np.testing.assert_array_equal(O.encode(g["pq8_books"], g["enc_x"]), g["enc_codes"])
