@@ -35,7 +35,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "pqs_common.cuh"
 #include "select_dev.cuh"
@@ -169,11 +171,11 @@ struct ProbeGemmArgs {
   int tstride;
   // MIN: per (query, 128-cell group of the visited tiles) minimum key
   float* gmin;           // (nq, 2 * ntiles_pass)
-  // FILTER
+  // FILTER: per-CTA record lists (q_local << 32 | cell), bucketed afterwards
   const float* theta;    // (nq,)
-  uint64_t* cand;        // (nq, cap) fkey(key) << 32 | cell
-  int* cnt;              // (nq,)
-  int64_t cap;
+  uint64_t* rec;         // (gridDim, rec_cap)
+  int* rec_cnt;          // (gridDim,) records produced (may exceed rec_cap: overflow)
+  int64_t rec_cap;
 };
 
 template <int MODE>  // 0 MIN, 1 FILTER
@@ -181,6 +183,7 @@ __global__ void __launch_bounds__(P_THREADS, 1) probe_gemm_kernel(ProbeGemmArgs 
   extern __shared__ __align__(1024) uint8_t psm[];
   __shared__ __align__(8) uint64_t bar_a, bar_adone, bar_full[3], bar_empty[3], bar_accfull[2], bar_accempty[2];
   __shared__ uint32_t s_tmem;
+  __shared__ int s_rec;
   const int nstages = a.dpad <= 192 ? 3 : 2;
   uint8_t* sA = psm;                                     // PM x dpad fp32
   uint8_t* sB = psm + (size_t)a.dpad * PM * 4;           // nstages x (4 K steps of a B tile)
@@ -201,6 +204,7 @@ __global__ void __launch_bounds__(P_THREADS, 1) probe_gemm_kernel(ProbeGemmArgs 
       tc::mbar_init(&bar_accfull[i], 1);
       tc::mbar_init(&bar_accempty[i], P_EPI_WARPS);
     }
+    s_rec = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tc::tmem_alloc(&s_tmem, 512);
@@ -313,15 +317,31 @@ __global__ void __launch_bounds__(P_THREADS, 1) probe_gemm_kernel(ProbeGemmArgs 
           for (int i = 1; i < 64; ++i) lm = fminf(lm, __uint_as_float(v[i]));
           if (MODE == 0) {
             mn = fminf(mn, lm);
-          } else if (lm <= th) {  // rare: append this query's hits
-#pragma unroll 1
-            for (int i = 0; i < 64; ++i) {
-              const float key = __uint_as_float(v[i]);
-              const int64_t cell = cell0 + c0 + i;
-              if (key <= th && cell < a.K) {
-                const int p = atomicAdd(a.cnt + q, 1);
-                if (p < a.cap) a.cand[q * a.cap + p] = ((uint64_t)fkey(key) << 32) | (uint64_t)(uint32_t)cell;
-              }
+          } else if (__any_sync(0xffffffffu, lm <= th)) {
+            // rare: this warp's hits -> the CTA's record list; one shared
+            // atomic per warp reserves the slots (no global round trip on
+            // the accumulator's critical path)
+            const int64_t cb = cell0 + c0;
+            uint64_t mask = 0;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) mask |= (uint64_t)(__uint_as_float(v[i]) <= th) << i;
+            if (cb + 64 > a.K) mask &= cb >= a.K ? 0ull : (~0ull >> (64 - (a.K - cb)));
+            const int nh = __popcll(mask);
+            int incl = nh;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int t = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= o) incl += t;
+            }
+            int base = 0;
+            if (lane == 31 && incl) base = atomicAdd(&s_rec, incl);
+            base = __shfl_sync(0xffffffffu, base, 31) + incl - nh;
+            const uint64_t qtag = (uint64_t)q << 32;
+            while (mask) {
+              const int i = __ffsll((long long)mask) - 1;
+              mask &= mask - 1;
+              if (base < a.rec_cap) a.rec[(int64_t)blockIdx.x * a.rec_cap + base] = qtag | (uint64_t)(uint32_t)(cb + i);
+              ++base;
             }
           }
         }
@@ -334,9 +354,43 @@ __global__ void __launch_bounds__(P_THREADS, 1) probe_gemm_kernel(ProbeGemmArgs 
   }
   tc::fence_before();
   __syncthreads();
+  if (MODE == 1 && threadIdx.x == 0) a.rec_cnt[blockIdx.x] = s_rec;
   if (warp == 0) {
     tc::fence_after();
     tc::tmem_dealloc(tmem, 512);
+  }
+}
+
+// per-CTA records -> per-query candidate rows: shared histogram over the
+// batch's queries, one global reservation per (region, query), scatter;
+// *ovf set when a region overflowed its capacity (the host re-runs larger)
+__global__ void __launch_bounds__(1024) probe_bucket_kernel(const uint64_t* __restrict__ rec,
+                                                            const int* __restrict__ rec_cnt, int64_t rec_cap,
+                                                            int64_t nq, uint64_t* __restrict__ cand,
+                                                            int* __restrict__ cnt, int64_t cap,
+                                                            int* __restrict__ ovf) {
+  extern __shared__ int bsm[];
+  int* hist = bsm;        // [nq]
+  int* basev = bsm + nq;  // [nq]
+  const int b = blockIdx.x;
+  if (threadIdx.x == 0 && rec_cnt[b] > rec_cap) atomicOr(ovf, 1);
+  const int n = (int)min((int64_t)rec_cnt[b], rec_cap);
+  const uint64_t* r = rec + (int64_t)b * rec_cap;
+  for (int64_t i = threadIdx.x; i < nq; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&hist[r[i] >> 32], 1);
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < nq; i += blockDim.x) {
+    const int h = hist[i];
+    basev[i] = h ? atomicAdd(cnt + i, h) : 0;
+    hist[i] = 0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint64_t x = r[i];
+    const int64_t q = (int64_t)(x >> 32);
+    const int pos = basev[q] + atomicAdd(&hist[q], 1);
+    if (pos < cap) cand[q * cap + pos] = x & 0xFFFFFFFFull;
   }
 }
 
@@ -363,7 +417,8 @@ __global__ void __launch_bounds__(256) probe_theta_kernel(const float* __restric
 }
 
 // ---------------------------------------------------------------- final
-constexpr int PF_THREADS = 512;
+constexpr int PF_THREADS = 256;
+constexpr int PF_SMEM_CAP = 1024;   // candidates staged in shared memory (more: in place in global scratch)
 
 struct ProbeFinalArgs {
   QVec queries;          // batch-offset applied
@@ -371,32 +426,62 @@ struct ProbeFinalArgs {
   const uint64_t* cand;  // (nb, cap)
   const int* cnt;
   int64_t cap;
-  const double* eps;
   int64_t K;
   int d, ma;
   int all_exact;         // 1: every query takes the exact streaming path
   int64_t q0;            // global index of batch row 0
+  uint64_t* gkeys;       // (nb, cap) scratch for rows beyond PF_SMEM_CAP
+  int64_t* gids;
   int64_t* out_cells;    // (nq, ma)
   double* out_dist;
 };
 
-// exact fp64 squared distance, scipy cdist order (sequential over t)
+// exact fp64 squared distance, scipy cdist order (sequential over t).  The
+// centroid row streams through registers 32 coordinates at a time with the
+// next chunk's loads issued before the current chunk's (dependent) fp64 sum,
+// so one L2 round trip is exposed per row instead of one per chunk.
+__device__ __forceinline__ void load_chunk(const float* g, int t0, int d, float (&ga)[32]) {
+  if ((d & 3) == 0 && t0 + 32 <= d) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(g + t0) + u);
+      ga[4 * u] = v.x, ga[4 * u + 1] = v.y, ga[4 * u + 2] = v.z, ga[4 * u + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < 32; ++u) ga[u] = t0 + u < d ? __ldg(g + t0 + u) : 0.f;
+  }
+}
 __device__ __forceinline__ double exact_dist(const double* qx, const float* g, int d) {
   double s = 0.0;
-  for (int t = 0; t < d; ++t) {
-    const double df = __dsub_rn(qx[t], (double)__ldg(g + t));
-    s = __dadd_rn(s, __dmul_rn(df, df));
+  float cur[32], nxt[32];
+  load_chunk(g, 0, d, cur);
+  for (int t0 = 0; t0 < d; t0 += 32) {
+    if (t0 + 32 < d) load_chunk(g, t0 + 32, d, nxt);
+#pragma unroll
+    for (int u = 0; u < 32; ++u) {
+      if (t0 + u < d) {
+        const double df = __dsub_rn(qx[t0 + u], (double)cur[u]);
+        s = __dadd_rn(s, __dmul_rn(df, df));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 32; ++u) cur[u] = nxt[u];
   }
   return s;
 }
 
+// Per query: every candidate (all keys <= theta, a superset of the exact
+// probe set) re-scored exactly, the ma smallest by (distance, cell) selected
+// and sorted.  A row that overflowed its capacity (or all_exact) streams all
+// K cells instead, recomputing the distance in every radix pass.
 __global__ void __launch_bounds__(PF_THREADS) probe_final_kernel(ProbeFinalArgs a, int sortP) {
   extern __shared__ __align__(16) unsigned char fsm[];
   __shared__ SelShared sh;
   __shared__ int s_cnt;
-  uint64_t* ck = (uint64_t*)fsm;                 // cap keys
-  int64_t* ci = (int64_t*)(ck + a.cap);          // cap cells
-  uint64_t* ok = (uint64_t*)(ci + a.cap);        // sortP
+  uint64_t* ck = (uint64_t*)fsm;                 // PF_SMEM_CAP keys
+  int64_t* ci = (int64_t*)(ck + PF_SMEM_CAP);    // PF_SMEM_CAP cells
+  uint64_t* ok = (uint64_t*)(ci + PF_SMEM_CAP);  // sortP
   int64_t* oi = (int64_t*)(ok + sortP);
   double* qx = (double*)(oi + sortP);            // d (fp64 query)
   const int64_t ql = blockIdx.x, q = a.q0 + ql;
@@ -405,100 +490,59 @@ __global__ void __launch_bounds__(PF_THREADS) probe_final_kernel(ProbeFinalArgs 
   const int64_t raw = a.all_exact ? a.cap + 1 : (int64_t)a.cnt[ql];
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();
+  const bool streaming = raw > a.cap;
+  const int64_t M = streaming ? a.K : raw;
+  uint64_t* KK = ck;
+  int64_t* II = ci;
+  if (!streaming) {
+    if (M > PF_SMEM_CAP) {
+      KK = a.gkeys + ql * a.cap;
+      II = a.gids + ql * a.cap;
+    }
+    const uint64_t* cr = a.cand + ql * a.cap;
+    for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+      const int64_t c = (int64_t)(uint32_t)cr[i];
+      II[i] = c;
+      KK[i] = dkey(exact_dist(qx, a.coarse + c * a.d, a.d));
+    }
+    __syncthreads();
+  }
+  auto key_of = [&](int64_t i, uint64_t& v) {
+    v = streaming ? dkey(exact_dist(qx, a.coarse + i * a.d, a.d)) : KK[i];
+    return true;
+  };
+  auto id_of = [&](int64_t i) -> int64_t { return streaming ? i : II[i]; };
   unsigned long long kstar = ~0ull;
   long long istar = 0x7FFFFFFFFFFFFFFFll;
   bool all_ties = true;
-  int64_t r_eff = 0;
-  if (raw <= a.cap) {
-    // ---- fast path: the candidate row holds every key <= theta
-    const int64_t M = raw;
-    const uint64_t* cr = a.cand + ql * a.cap;
-    for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
-      const uint64_t e = cr[i];
-      ck[i] = e >> 32;
-      ci[i] = (int64_t)(uint32_t)e;
-    }
+  const int64_t r_eff = ma < M ? ma : M;
+  if (r_eff < M) {
+    block_radix_select(M, key_of, (unsigned long long)(r_eff - 1), sh);
+    kstar = sh.prefix;
+    const unsigned long long less = sh.less, eq = sh.eq, need = r_eff - less;
     __syncthreads();
-    double thr2 = 1e300;
-    if (ma < M) {
-      auto getk = [&](int64_t i, uint64_t& v) {
-        v = ck[i];
-        return true;
+    if (eq > need) {
+      all_ties = false;
+      auto geti = [&](int64_t i, uint64_t& v) {
+        uint64_t kv;
+        key_of(i, kv);
+        v = (uint64_t)id_of(i) ^ 0x8000000000000000ull;
+        return kv == kstar;
       };
-      block_radix_select(M, getk, (unsigned long long)(ma - 1), sh);
-      thr2 = (double)fkey_inv((uint32_t)sh.prefix) + 2.0 * a.eps[ql];
+      block_radix_select(M, geti, need - 1, sh);
+      istar = (long long)(sh.prefix ^ 0x8000000000000000ull);
       __syncthreads();
     }
-    for (int64_t i = threadIdx.x; i < M; i += blockDim.x)
-      ck[i] = (double)fkey_inv((uint32_t)ck[i]) <= thr2 ? dkey(exact_dist(qx, a.coarse + ci[i] * a.d, a.d)) : ~0ull;
-    __syncthreads();
-    r_eff = ma < M ? ma : M;
-    if (r_eff < M) {
-      auto getk = [&](int64_t i, uint64_t& v) {
-        v = ck[i];
-        return true;
-      };
-      block_radix_select(M, getk, (unsigned long long)(r_eff - 1), sh);
-      kstar = sh.prefix;
-      const unsigned long long less = sh.less, eq = sh.eq, need = r_eff - less;
-      __syncthreads();
-      if (eq > need) {
-        all_ties = false;
-        auto geti = [&](int64_t i, uint64_t& v) {
-          v = (uint64_t)ci[i] ^ 0x8000000000000000ull;
-          return ck[i] == kstar;
-        };
-        block_radix_select(M, geti, need - 1, sh);
-        istar = (long long)(sh.prefix ^ 0x8000000000000000ull);
-        __syncthreads();
-      }
-    }
-    for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
-      const uint64_t key = ck[i];
-      if (key < kstar || (key == kstar && (all_ties || ci[i] <= istar))) {
-        const int p = atomicAdd(&s_cnt, 1);
-        if (p < sortP) {
-          ok[p] = key;
-          oi[p] = ci[i];
-        }
-      }
-    }
-  } else {
-    // ---- exact streaming path over all K cells (overflow / unsupported d):
-    // the distance is recomputed in every radix pass instead of stored
-    const int64_t K = a.K;
-    auto getd = [&](int64_t c, uint64_t& v) {
-      v = dkey(exact_dist(qx, a.coarse + c * a.d, a.d));
-      return true;
-    };
-    r_eff = ma < K ? ma : K;
-    if (r_eff < K) {
-      block_radix_select(K, getd, (unsigned long long)(r_eff - 1), sh);
-      kstar = sh.prefix;
-      const unsigned long long less = sh.less, eq = sh.eq, need = r_eff - less;
-      __syncthreads();
-      if (eq > need) {
-        all_ties = false;
-        auto geti = [&](int64_t c, uint64_t& v) {
-          uint64_t dv;
-          getd(c, dv);
-          v = (uint64_t)c ^ 0x8000000000000000ull;
-          return dv == kstar;
-        };
-        block_radix_select(K, geti, need - 1, sh);
-        istar = (long long)(sh.prefix ^ 0x8000000000000000ull);
-        __syncthreads();
-      }
-    }
-    for (int64_t c = threadIdx.x; c < K; c += blockDim.x) {
-      uint64_t key;
-      getd(c, key);
-      if (key < kstar || (key == kstar && (all_ties || c <= istar))) {
-        const int p = atomicAdd(&s_cnt, 1);
-        if (p < sortP) {
-          ok[p] = key;
-          oi[p] = c;
-        }
+  }
+  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+    uint64_t key;
+    key_of(i, key);
+    const int64_t id = id_of(i);
+    if (key < kstar || (key == kstar && (all_ties || id <= istar))) {
+      const int p = atomicAdd(&s_cnt, 1);
+      if (p < sortP) {
+        ok[p] = key;
+        oi[p] = id;
       }
     }
   }
@@ -544,13 +588,13 @@ int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, i
   if (P < 2) P = 2;
   PQS_CHECK(ctx, P <= 4096, "ma too large for the device probe select (<= 4096)");
   static const int64_t cap_env = getenv("PQS_PROBE_CAP") ? atoll(getenv("PQS_PROBE_CAP")) : 0;  // testing
-  const int64_t cap = cap_env > 0 ? std::min<int64_t>(cap_env, 4096) : 4096;
+  const int64_t cap = cap_env > 0 ? std::min<int64_t>(cap_env, 4096) : 2048;
   const bool tc_path = iv->probe_b != nullptr && getenv("PQS_PROBE_EXACT") == nullptr;
-  const size_t fsmem = (size_t)cap * 16 + (size_t)P * 16 + (size_t)d * 8;
+  const size_t fsmem = (size_t)PF_SMEM_CAP * 16 + (size_t)P * 16 + (size_t)d * 8;
   PQS_CHECK(ctx, fsmem <= 200 * 1024, "probe: d too large for the shared-memory query stage");
   PQS_CUDA(ctx, cudaFuncSetAttribute(probe_final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
   // query batches of QB (multiple of PM): candidate rows QB x cap
-  const int64_t QB = std::min<int64_t>(cdiv(nq, PM) * PM, 4096);
+  const int64_t QB = std::min<int64_t>(cdiv(nq, PM) * PM, 8192);
   double* eps = nullptr;
   PQS_TRY(scratch(ctx, S_AERR, (size_t)QB * 2, (float**)&eps));
   uint64_t* cand = nullptr;
@@ -562,12 +606,17 @@ int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, i
   const int64_t ntiles = iv->probe_ntiles;
   // pass 1 visits every tstride-th tile: >= 2 ma groups of 128 cells
   int tstride = 1;
+  static const int ts_env = getenv("PQS_PROBE_TSTRIDE") ? atoi(getenv("PQS_PROBE_TSTRIDE")) : 2;  // tuning
   if (tc_path) {
     const int64_t groups = 2 * ntiles;
-    tstride = (int)std::max<int64_t>(1, std::min<int64_t>(4, groups / std::max<int64_t>(1, 2 * (int64_t)ma)));
+    tstride = (int)std::max<int64_t>(1, std::min<int64_t>(ts_env, groups / std::max<int64_t>(1, 2 * (int64_t)ma)));
   }
   const int64_t ntp1 = cdiv(ntiles, tstride);
+  uint64_t* gk = nullptr;
+  int64_t* gi = nullptr;
   if (tc_path) {
+    PQS_TRY(scratch(ctx, S_KEYS, (size_t)(QB * cap), &gk));
+    PQS_TRY(scratch(ctx, S_IDS, (size_t)(QB * cap), &gi));
     PQS_TRY(scratch(ctx, S_CAND, (size_t)(QB * cap), &cand));
     PQS_TRY(scratch(ctx, S_CAND_CNT, (size_t)QB, &cnt));
     PQS_TRY(scratch(ctx, S_IVF_WORK, (size_t)(QB * dpad), &A));
@@ -575,6 +624,8 @@ int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, i
     PQS_TRY(scratch(ctx, S_THETA, (size_t)QB * 4, (uint8_t**)&theta));
   }
   const size_t gsmem = (size_t)dpad * PM * 4 + (size_t)(dpad <= 192 ? 3 : 2) * PSTEPS_PER_STAGE * PB_STEP;
+  const size_t bsmem = (size_t)QB * 2 * sizeof(int);
+  PQS_CUDA(ctx, cudaFuncSetAttribute(probe_bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
   for (int64_t q0 = 0; q0 < nq; q0 += QB) {
     const int64_t nb = std::min(QB, nq - q0);
     const QVec qb = d_queries.offset(q0 * d);
@@ -605,9 +656,6 @@ int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, i
       g.nblocks = nblocks;
       g.gmin = gmin;
       g.theta = theta;
-      g.cand = cand;
-      g.cnt = cnt;
-      g.cap = cap;
       // pass 1: group minima over the strided tiles
       g.ntiles_pass = ntp1;
       g.tstride = tstride;
@@ -618,22 +666,67 @@ int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, i
       PQS_LAUNCHED(ctx);
       probe_theta_kernel<<<(unsigned)nb, 256, 0, ctx->stream>>>(gmin, 2 * ntp1, ma, eps, theta);
       PQS_LAUNCHED(ctx);
-      // pass 2: every tile, keys <= theta appended
-      PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nb, ctx->stream));
+      // pass 2: every tile, keys <= theta -> per-CTA records -> candidate rows
       g.ntiles_pass = ntiles;
       g.tstride = 1;
-      probe_gemm_kernel<1><<<(unsigned)std::min<int64_t>(ctx->sm_count, nblocks * ntiles), P_THREADS, gsmem,
-                             ctx->stream>>>(g);
-      PQS_LAUNCHED(ctx);
+      const int64_t nct = std::min<int64_t>(ctx->sm_count, nblocks * ntiles);
+      int64_t rec_cap = std::max<int64_t>(16384, cdiv(nb * 1024, nct));
+      for (int attempt = 0;; ++attempt) {
+        uint64_t* rec = nullptr;
+        int* rec_cnt = nullptr;
+        PQS_TRY(scratch(ctx, S_TC_REC, (size_t)(nct * rec_cap), &rec));
+        PQS_TRY(scratch(ctx, S_TC_RECCNT, (size_t)nct + 1, &rec_cnt));
+        int* ovf = rec_cnt + nct;
+        g.rec = rec;
+        g.rec_cnt = rec_cnt;
+        g.rec_cap = rec_cap;
+        PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nb, ctx->stream));
+        PQS_CUDA(ctx, cudaMemsetAsync(ovf, 0, sizeof(int), ctx->stream));
+        probe_gemm_kernel<1><<<(unsigned)nct, P_THREADS, gsmem, ctx->stream>>>(g);
+        PQS_LAUNCHED(ctx);
+        probe_bucket_kernel<<<(unsigned)nct, 1024, bsmem, ctx->stream>>>(rec, rec_cnt, rec_cap, nb, cand, cnt, cap,
+                                                                         ovf);
+        PQS_LAUNCHED(ctx);
+        int h_ovf = 0;
+        PQS_TRY(download(ctx, &h_ovf, ovf, sizeof(int)));
+        if (!h_ovf) break;
+        PQS_CHECK(ctx, attempt < 6, "probe: candidate records overflow");
+        rec_cap *= 4;
+      }
       f.cand = cand;
       f.cnt = cnt;
-      f.eps = eps;
+      f.gkeys = gk;
+      f.gids = gi;
       f.all_exact = 0;
     } else {
       f.all_exact = 1;
     }
     probe_final_kernel<<<(unsigned)nb, PF_THREADS, fsmem, ctx->stream>>>(f, P);
     PQS_LAUNCHED(ctx);
+    static const bool dbg = getenv("PQS_PROBE_DEBUG") != nullptr;
+    if (dbg && tc_path) {
+      std::vector<int> hc((size_t)nb);
+      std::vector<float> ht((size_t)nb), hg((size_t)(2 * ntp1) * 4);
+      std::vector<double> he((size_t)nb);
+      PQS_TRY(download(ctx, hc.data(), cnt, sizeof(int) * nb));
+      PQS_TRY(download(ctx, ht.data(), theta, sizeof(float) * nb));
+      PQS_TRY(download(ctx, he.data(), eps, sizeof(double) * nb));
+      PQS_TRY(download(ctx, hg.data(), gmin, sizeof(float) * 2 * ntp1 * 4));
+      int64_t tot = 0, mx = 0, over = 0;
+      for (int64_t i = 0; i < nb; ++i) {
+        tot += hc[i];
+        mx = std::max<int64_t>(mx, hc[i]);
+        over += hc[i] > cap;
+      }
+      fprintf(stderr, "probe batch q0=%lld nb=%lld tstride=%d groups=%lld: candidates mean %.1f max %lld overflow %lld\n",
+              (long long)q0, (long long)nb, tstride, (long long)(2 * ntp1), (double)tot / nb, (long long)mx,
+              (long long)over);
+      for (int i = 0; i < 4 && i < nb; ++i) {
+        float mn = 1e38f;
+        for (int64_t g2 = 0; g2 < 2 * ntp1; ++g2) mn = std::min(mn, hg[(size_t)i * 2 * ntp1 + g2]);
+        fprintf(stderr, "  q%d: cnt %d theta %.6g eps %.6g min group %.6g\n", i, hc[i], ht[i], he[i], mn);
+      }
+    }
   }
   return PQS_OK;
 }

@@ -52,8 +52,9 @@ def test_encode_device_tensors_and_oracle():
     np.testing.assert_array_equal(got[:3000].cpu().numpy(), want)
     with pytest.raises(ValueError):
         P.encode(pq, x[:, :95])
-    with pytest.raises(NotImplementedError):
-        P.encode(pq, x[:2].astype(np.float64) + 1e-12)
+    # float64 rows are encoded from their float64 values (quantizer.py:319-323)
+    x64 = x[:500].astype(np.float64) + 1e-4 * np.random.default_rng(9).normal(size=(500, 96))
+    np.testing.assert_array_equal(P.encode(pq, x64), O.encode(books, x64))
 
 
 def test_device_built_codes_equal_host_built():
