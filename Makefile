@@ -20,6 +20,14 @@ $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -Xlinker -rpath,/usr/local/cuda/lib64
 
 PEAKS    := tools/bin/pqs_peaks
+ORACLE_C := oracle/lib/libpqs_oracle.so
+
+# C restatement of the reference's Quick ADC steps (test infrastructure only)
+oracle: $(ORACLE_C)
+
+$(ORACLE_C): oracle/qadc_oracle.c
+	@mkdir -p oracle/lib
+	gcc -O2 -shared -fPIC -o $@ $<
 
 peaks: $(PEAKS)
 
@@ -33,4 +41,4 @@ ptxas: $(SRCS)
 clean:
 	rm -rf $(OUT_DIR)
 
-.PHONY: all clean ptxas peaks
+.PHONY: all clean ptxas peaks oracle

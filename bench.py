@@ -1,23 +1,28 @@
 #!/usr/bin/env python3
 """Benchmark: ADC distance evals/s (codes x queries) on B200.
 
-Default workload (N=1): BASELINE.json configs[1] -- Quick ADC, PQ 16x4 over a
-seeded d=128 Gaussian-mixture stand-in, N=1,000,000 codes, 1,000 queries,
-top-100, init_count 200.  A "step" is one pass of the hot path over the
-whole query batch: tables -> Quick ADC params -> threshold sample -> PRMT
-scan -> (bin, id) top-100 for all 1,000 queries.
+Default workload: BASELINE.json configs[4] -- billion-scale sharded Quick
+ADC (PQ 16x4, d=96 decaying-variance Gaussian, L2-normalised), one 125M-code
+shard per GPU (1e9 codes at N=8), 10,000 queries, top-100, init_count 1000
+with the GLOBAL prefix.  N=1 is the largest single-GPU configuration and the
+unit of the north-star scaling target; N=8 is exactly BASELINE cfg4.  A
+"step" is one pass of the hot path over the whole query batch: tables ->
+Quick ADC params -> threshold sample -> tcgen05 filtered scan -> (bin, id)
+top-100 for all 10,000 queries (-> all-gather + merge at N > 1).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg0..cfg4]
                   [--impl ours|reference]
 
 N > 1 (torchrun, one rank per GPU): weak scaling -- every rank owns its own
-1M-code shard of one global list (ids offset by rank), all ranks scan the
-same queries with the GLOBAL Quick ADC prefix, the per-rank top-100 lists are
+shard of one global list (ids offset by rank), all ranks scan the same
+queries with the GLOBAL Quick ADC prefix, the per-rank top-100 lists are
 all-gathered over NCCL and merged on the device (pqs_merge_topr).
 
---impl reference: the reference's CPU path of the same workload on the
-host's cores (the oracle port of pqscan, oracle/pqscan_oracle.py, in a fork
-process pool), rank 0 only.
+--impl reference: the reference's own CPU implementation of the path --
+`pqscan` installed unmodified from /root/reference into baseline/_ref (pip
+--target; the oracle port oracle/pqscan_oracle.py only if that install is
+absent) -- in a fork process pool over the host's cores, rank 0 only; every
+step times all queries of a fixed-size sample of the same workload.
 """
 
 from __future__ import annotations
@@ -44,7 +49,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg1", choices=["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--config", default="cfg4", choices=["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"])
     ap.add_argument("--n-per-gpu", type=int, default=None, help="override the per-GPU code count (cfg4)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-s", type=float, default=20.0, help="CPU work budget of the baseline sample")
@@ -136,50 +141,125 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU baseline
-_CPU = {}
-
-
-def _cpu_query(qi):
-    from oracle import pqscan_oracle as O
-
-    d = _CPU
-    t = O.compute_tables(d["books"], d["queries"][qi])
-    if d["b"] == 4:
-        O.qadc_scan(d["codes"], d["ids"], t, d["init"], d["r"])
-    else:
-        O.scan(d["codes"], d["ids"], t, d["r"])
-    return qi
-
-
+# The reference CPU path: pqscan itself when baseline/_ref holds the pip
+# --target install of /root/reference (kind "reference"), else the oracle
+# port (kind "port").  Fork process pool over all host cores (threads do not
+# scale: GIL, SURVEY finding 8), the data inherited copy-on-write; per-query
+# timing as cli._run_timed (cli.py:266-276).
+_REF = {}
 CPU_CODE_SAMPLE = 4_000_000
 
 
-def cpu_baseline(cfg, books, codes, queries, budget_s: float, n_full: int | None = None):
-    """Oracle port of the reference CPU path, fork process pool over all host
-    cores (threads do not scale: GIL, SURVEY finding 8)."""
+def _ref_module():
+    p = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(p, "pqscan")):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+        import pqscan
+
+        return pqscan, "reference"
+    from oracle import pqscan_oracle as O
+
+    return O, "port"
+
+
+def _ref_setup(cfg, books, codes=None, queries=None, ivf=None):
+    """Build the reference's own containers once (parent process, untimed)."""
+    mod, kind = _ref_module()
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    _REF.clear()
+    _REF.update(mod=mod, kind=kind, b=cfg["b"], r=cfg["r"], init=cfg.get("init_count", 200), queries=queries,
+                books=books)
+    if kind == "reference":
+        pq = mod.ProductQuantizer(m=cfg["m"], b=cfg["b"], d=cfg["d"], codebooks=books)
+        _REF["pq"] = pq
+        if ivf is not None:
+            coarse, sizes, lcodes, lids = ivf
+            offs = np.concatenate([[0], np.cumsum(sizes)])
+            lists = [mod.CodeList(lcodes[offs[c]:offs[c + 1]], lids[offs[c]:offs[c + 1]]) for c in range(len(sizes))]
+            _REF["index"] = mod.IvfIndex(coarse=coarse, pq=pq, lists=lists)
+        elif cfg["b"] == 4:
+            _REF["tlist"] = mod.transpose_blocks(mod.CodeList(codes), 4)
+        else:
+            _REF["codelist"] = mod.CodeList(codes)
+    else:
+        if ivf is not None:
+            coarse, sizes, lcodes, lids = ivf
+            offs = np.concatenate([[0], np.cumsum(sizes)])
+            _REF.update(coarse=coarse, lists_codes=[lcodes[offs[c]:offs[c + 1]] for c in range(len(sizes))],
+                        lists_ids=[lids[offs[c]:offs[c + 1]] for c in range(len(sizes))])
+        else:
+            _REF.update(codes=codes, ids=np.arange(codes.shape[0], dtype=np.int64))
+    if ivf is not None:
+        _REF.update(ivf=True, ma=cfg["nprobe"])
+    return kind
+
+
+def _ref_query(qi):
+    """One reference query (forked worker); returns its wall time."""
+    d = _REF
+    q = d["queries"][qi % d["queries"].shape[0]]
+    mod = d["mod"]
+    t0 = time.perf_counter()
+    if d["kind"] == "reference":
+        if d.get("ivf"):
+            mod.query_ivf(d["index"], q, d["ma"], d["r"])
+        elif d["b"] == 4:
+            mod.qadc_scan(d["tlist"], mod.compute_tables(d["pq"], q), d["init"], d["r"])
+        else:
+            mod.scan(d["codelist"], mod.compute_tables(d["pq"], q), d["r"])
+    else:
+        if d.get("ivf"):
+            mod.query_ivf(d["coarse"], d["books"], d["lists_codes"], d["lists_ids"], q, d["ma"], d["r"])
+        elif d["b"] == 4:
+            mod.qadc_scan(d["codes"], d["ids"], mod.compute_tables(d["books"], q), d["init"], d["r"])
+        else:
+            mod.scan(d["codes"], d["ids"], mod.compute_tables(d["books"], q), d["r"])
+    return time.perf_counter() - t0
+
+
+def ref_run(evals_of, steps: int, warmup: int, step_budget_s: float):
+    """Time the reference path: `warmup` + `steps` steps, each a fixed sample
+    of queries (cores x per-core, sized from one warm-up query so a step takes
+    ~step_budget_s) run in the fork pool; every query of a step is inside its
+    wall-clock window.  evals_of(list of query indices) -> evaluations."""
     import multiprocessing as mp
 
     cores = len(os.sched_getaffinity(0))
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    _CPU.update(books=books, codes=codes, queries=queries, ids=np.arange(codes.shape[0], dtype=np.int64),
-                b=cfg["b"], init=cfg.get("init_count", 200), r=cfg["r"])
-    t0 = time.perf_counter()
-    _cpu_query(0)  # warm-up (cli._run_timed, cli.py:266-276)
-    per_q = time.perf_counter() - t0
-    nq = int(max(cores, min(queries.shape[0], round(budget_s / max(per_q, 1e-3)))))
-    nq = min(queries.shape[0], max(cores, (nq // cores) * cores))
+    single = _ref_query(0)                       # warm-up query (cli._run_timed)
+    per_core = max(1, int(step_budget_s / max(single, 1e-3)))
+    qps = cores * per_core
+    nq = _REF["queries"].shape[0]
+    vals, walls, per_q = [], [], []
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
-        t0 = time.perf_counter()
-        pool.map(_cpu_query, range(nq), chunksize=1)
-        wall = time.perf_counter() - t0
-    evals = nq * codes.shape[0]
-    return {"value": evals / wall, "unit": "evals/s", "cores": cores, "kind": "port",
-            "sample": f"{nq} of {queries.shape[0]} queries over "
-                      + (f"all {codes.shape[0]} codes" if n_full is None else
-                         f"the first {codes.shape[0]} of {n_full} codes (evals/s is per (query, code))")
-                      + f" (oracle/pqscan_oracle.py, fork pool x{cores}); single-core {per_q * 1e3:.1f} ms/query"}
+        for s in range(warmup + steps):
+            idx = [(1 + s * qps + i) % nq for i in range(qps)]
+            t0 = time.perf_counter()
+            times = pool.map(_ref_query, idx, chunksize=1)
+            wall = time.perf_counter() - t0
+            if s >= warmup:
+                vals.append(evals_of(idx) / wall)
+                walls.append(wall)
+                per_q.extend(times)
+    return {"value": statistics.median(vals), "cores": cores, "queries_per_step": qps,
+            "ms_per_step": statistics.median(walls) * 1e3, "single_core_ms_per_query": statistics.median(per_q) * 1e3}
+
+
+def cpu_baseline(cfg, books, codes, queries, budget_s: float, n_full: int | None = None, steps: int = 1):
+    """The reference CPU path on a bounded sample (see ref_run)."""
+    kind = _ref_setup(cfg, books, codes, queries)
+    n = codes.shape[0]
+    res = ref_run(lambda idx: len(idx) * n, steps, 0, budget_s / max(steps, 1))
+    what = "pqscan (the reference, baseline/_ref)" if kind == "reference" else "oracle/pqscan_oracle.py (port)"
+    return {"value": res["value"], "unit": "evals/s", "cores": res["cores"], "kind": kind,
+            "sample": f"{res['queries_per_step']} queries per step over "
+                      + (f"all {n} codes" if n_full is None else
+                         f"the first {n} of the shard's {n_full} codes (evals/s is per (query, code))")
+                      + f"; {what}, fork pool x{res['cores']}; single-core median "
+                        f"{res['single_core_ms_per_query']:.1f} ms/query",
+            "ms_per_step": res["ms_per_step"]}
 
 
 # ------------------------------------------------------------------ driver
@@ -194,39 +274,49 @@ def metric_name(cfg_name):
     return "ADC distance evals/sec (codes x queries)"
 
 
+def _ref_line(args, world, cfg_name, cfg, res, kind, sample, dtype, config):
+    return {
+        "impl": "reference", "metric": metric_name(cfg_name), "value": res["value"], "unit": "evals/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+        "data": "synthetic (seeded stand-in for the BASELINE config; see DESIGN.md)",
+        "config": config,
+        "cpu_baseline": {"value": res["value"], "unit": "evals/s", "cores": res["cores"], "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": res["value"], "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    n_full = None
+    step_s = max(0.5, args.cpu_sample_s / max(args.steps + args.warmup, 1))
     if args.config == "cfg3":
         # the index is built on the GPU (data preparation, untimed); the timed
-        # path is the oracle's query_ivf on the host cores
+        # path is the reference's query_ivf on the host cores
         import torch
 
         import paper_1712_02912_b200 as P
 
         ctx = P.Context(0)
         cfg, books, coarse, sizes, codes, ids, queries = make_ivf(args, ctx, torch.device("cuda", 0))
-        vals = []
-        for s in range(args.warmup + args.steps):
-            base = cpu_baseline_ivf(books, coarse.cpu().numpy(), sizes, codes.cpu().numpy(), ids.cpu().numpy(),
-                                    queries, cfg["nprobe"], cfg["r"],
-                                    max(2.0, args.cpu_sample_s / max(args.steps, 1)))
-            if s >= args.warmup:
-                vals.append(base["value"])
-        value = statistics.median(vals)
-        print(json.dumps({
-            "impl": "reference", "metric": metric_name("cfg3"), "value": value, "unit": "evals/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded stand-in; index built on the GPU, untimed)",
-            "config": {"workload": "IVFADC K=65536, residual PQ 8x8, nprobe 64", "baseline_config_index": 3},
-            "cpu_baseline": {"value": value, "unit": "evals/s", "cores": base["cores"], "kind": "port",
-                             "sample": base["sample"]},
-            "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
-            flush=True)
+        coarse_h, codes_h, ids_h = coarse.cpu().numpy(), codes.cpu().numpy(), ids.cpu().numpy()
+        del ctx
+        kind = _ref_setup(cfg, books, queries=queries, ivf=(coarse_h, sizes, codes_h, ids_h))
+        from oracle import pqscan_oracle as O
+
+        def evals_of(idx):  # exact evaluation count: sizes of the probed lists (untimed, after the step)
+            cells, _ = O.nearest_k(queries[idx].astype(np.float64), coarse_h.astype(np.float64), cfg["nprobe"])
+            return float(np.asarray(sizes)[cells].sum())
+
+        res = ref_run(evals_of, args.steps, args.warmup, step_s)
+        sample = (f"{res['queries_per_step']} of {queries.shape[0]} queries per step, nprobe {cfg['nprobe']}, full "
+                  f"index; single-core median {res['single_core_ms_per_query']:.1f} ms/query")
+        line = _ref_line(args, world, "cfg3", cfg, res, kind, sample, "f64",
+                         {"workload": "IVFADC K=65536, residual PQ 8x8, nprobe 64", "baseline_config_index": 3})
+        print(json.dumps(line), flush=True)
         return
+    n_full = None
     if args.config == "cfg4":
         # host-generated sample of a shard (same distribution; the full shard
         # is GPU-generated in the "ours" arm); evals/s is per (query, code)
@@ -237,25 +327,15 @@ def run_reference(args):
         books, codes, queries = G.make_exhaustive("cfg4", n=CPU_CODE_SAMPLE)
     else:
         cfg, books, codes, queries, _ = make_data(args.config, 0)
-    base = None
-    vals = []
-    for s in range(args.warmup + args.steps):
-        base = cpu_baseline(cfg, books, codes, queries, budget_s=max(2.0, args.cpu_sample_s / max(args.steps, 1)),
-                            n_full=n_full)
-        if s >= args.warmup:
-            vals.append(base["value"])
-    value = statistics.median(vals)
-    line = {
-        "impl": "reference", "metric": metric_name(args.config), "value": value, "unit": "evals/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": (n_full or codes.shape[0]) * queries.shape[0] / value * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8" if cfg["b"] == 4 else "f64",
-        "data": "synthetic (seeded stand-in for the BASELINE config; see DESIGN.md)",
-        "config": config_dict(args.config, cfg, world, args.n_per_gpu),
-        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": base["cores"], "kind": "port",
-                         "sample": base["sample"]},
-        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
+    kind = _ref_setup(cfg, books, codes, queries)
+    n = codes.shape[0]
+    res = ref_run(lambda idx: len(idx) * n, args.steps, args.warmup, step_s)
+    sample = (f"{res['queries_per_step']} queries per step over "
+              + (f"all {n} codes" if n_full is None else f"the first {n} codes of a {n_full}-code shard "
+                                                         "(evals/s per (query, code))")
+              + f"; single-core median {res['single_core_ms_per_query']:.1f} ms/query")
+    line = _ref_line(args, world, args.config, cfg, res, kind, sample, "u8" if cfg["b"] == 4 else "f64",
+                     config_dict(args.config, cfg, world, args.n_per_gpu))
     print(json.dumps(line), flush=True)
 
 
@@ -273,43 +353,22 @@ def config_dict(name, cfg, world, n_per_gpu=None):
 
 
 # --------------------------------------------------------------- IVF (cfg3)
-_IVF = {}
-
-
-def _cpu_ivf_query(qi):
+def cpu_baseline_ivf(cfg, books, coarse, sizes, codes, ids, queries, budget_s):
+    """The reference query_ivf (ivf.py:148-196) on a bounded query sample."""
+    kind = _ref_setup(cfg, books, queries=queries, ivf=(coarse, sizes, codes, ids))
     from oracle import pqscan_oracle as O
 
-    d = _IVF
-    O.query_ivf(d["coarse"], d["books"], d["lists_codes"], d["lists_ids"], d["queries"][qi], d["ma"], d["r"])
-    return qi
+    def evals_of(idx):  # exact evaluation count (sizes of the probed lists), outside the timed window
+        cells, _ = O.nearest_k(queries[idx].astype(np.float64), np.asarray(coarse, np.float32).astype(np.float64),
+                               cfg["nprobe"])
+        return float(np.asarray(sizes)[cells].sum())
 
-
-def cpu_baseline_ivf(books, coarse, sizes, codes, ids, queries, ma, r, budget_s):
-    """Oracle query_ivf (ivf.py:148-196) in a fork pool over all host cores."""
-    import multiprocessing as mp
-
-    cores = len(os.sched_getaffinity(0))
-    offs = np.concatenate([[0], np.cumsum(sizes)])
-    _IVF.update(books=books, coarse=coarse, queries=queries, ma=ma, r=r,
-                lists_codes=[codes[offs[c]:offs[c + 1]] for c in range(len(sizes))],
-                lists_ids=[ids[offs[c]:offs[c + 1]] for c in range(len(sizes))])
-    t0 = time.perf_counter()
-    _cpu_ivf_query(0)
-    per_q = time.perf_counter() - t0
-    nq = min(queries.shape[0], max(cores, (int(budget_s / max(per_q, 1e-3)) // cores) * cores))
-    ctx = mp.get_context("fork")
-    with ctx.Pool(cores) as pool:
-        t0 = time.perf_counter()
-        pool.map(_cpu_ivf_query, range(nq), chunksize=1)
-        wall = time.perf_counter() - t0
-    # exact evaluation count of the sampled queries (untimed): sizes of their probed lists
-    from oracle import pqscan_oracle as O
-
-    cells, _ = O.nearest_k(queries[:nq].astype(np.float64), np.asarray(coarse, np.float32).astype(np.float64), ma)
-    evals = float(np.asarray(sizes)[cells].sum())
-    return {"value": evals / wall, "unit": "evals/s", "cores": cores, "kind": "port",
-            "sample": f"{nq} of {queries.shape[0]} queries, nprobe {ma}, full index (oracle query_ivf, fork pool "
-                      f"x{cores}); {evals:.3e} probed codes; single-core {per_q * 1e3:.1f} ms/query"}
+    res = ref_run(evals_of, 1, 0, budget_s)
+    what = "pqscan (the reference, baseline/_ref)" if kind == "reference" else "oracle/pqscan_oracle.py (port)"
+    return {"value": res["value"], "unit": "evals/s", "cores": res["cores"], "kind": kind,
+            "sample": f"{res['queries_per_step']} of {queries.shape[0]} queries, nprobe {cfg['nprobe']}, full index; "
+                      f"{what}, fork pool x{res['cores']}; single-core median "
+                      f"{res['single_core_ms_per_query']:.1f} ms/query"}
 
 
 def make_ivf(args, ctx, dev):
@@ -475,13 +534,34 @@ def run_ivf(args):
         "impl": "ours",
     }
     if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline_ivf(books, coarse.cpu().numpy(), sizes, codes.cpu().numpy(),
-                                                ids.cpu().numpy(), queries, ma, r, args.cpu_sample_s)
+        line["cpu_baseline"] = cpu_baseline_ivf(cfg, books, coarse.cpu().numpy(), sizes, codes.cpu().numpy(),
+                                                ids.cpu().numpy(), queries, args.cpu_sample_s)
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def measured_i8_peak(seconds: float = 3.0):
+    """tcgen05 kind::i8 peak of this GPU, measured live by tools/bin/pqs_peaks
+    (tools/peaks.cu: M=128 N=256 K=32 MMAs back to back, operands resident):
+    a burst figure and a sustained one (back-to-back launches for `seconds`).
+    Falls back to the committed profiles/peaks_r02.json measurement."""
+    exe = os.path.join(ROOT, "tools", "bin", "pqs_peaks")
+    try:
+        out = subprocess.run([exe, "i8", str(seconds)], capture_output=True, text=True, timeout=120)
+        d = json.loads(out.stdout.strip().splitlines()[-1])
+        return {"burst": d["i8_mma"]["tops"], "sustained": d["i8_mma_sustained"]["tops"],
+                "burst_mhz": d["i8_mma"]["sm_mhz"], "source": "measured live (tools/bin/pqs_peaks i8)"}
+    except Exception as e:  # noqa: BLE001
+        try:
+            d = json.load(open(os.path.join(ROOT, "profiles", "peaks_r02.json")))
+            return {"burst": d["i8_mma"]["tops"], "sustained": d.get("i8_mma_sustained", d["i8_mma"])["tops"],
+                    "burst_mhz": d["i8_mma"]["sm_mhz"],
+                    "source": f"profiles/peaks_r02.json (committed measurement; live run failed: {e})"}
+        except Exception:  # noqa: BLE001
+            return None
 
 
 def _ncu_traffic(kernel: str):
@@ -545,6 +625,7 @@ def main():
 
             dist.barrier()
 
+    i8 = measured_i8_peak() if (rank == 0 and cfg["b"] == 4) else None
     for _ in range(args.warmup):
         step_device()
     torch.cuda.synchronize()
@@ -657,9 +738,18 @@ def main():
     except Exception:
         pass
     if engine == 2:
-        # tcgen05 kind::i8 one-hot GEMM: int8 MMA ops actually issued per launch
-        i8_peak = 2.0 * peaks.get("bf16_tflops", 1682.0)  # dense int8 = 2x dense bf16 (nominal 4.5 vs 2.25 P)
+        # tcgen05 kind::i8 one-hot GEMM: int8 MMA ops actually issued per launch,
+        # against the microbenchmarked int8 MMA peak of this GPU: the sustained
+        # figure when the timed region is a long one (> 1 s), else the burst one
         achieved = work / (scan_ms / 1e3) / 1e12
+        regime = "sustained" if total_ms > 1000.0 else "burst"
+        if i8 is not None:
+            i8_peak = i8[regime]
+            peak_source = (f"{i8['source']}: tcgen05.mma kind::i8 M=128 N=256 K=32 back to back, {regime} "
+                           f"(burst {i8['burst']:.0f} / sustained {i8['sustained']:.0f} TOP/s)")
+        else:
+            i8_peak = 2.0 * peaks.get("bf16_tflops", 1660.1)
+            peak_source = "fallback: 2 x MEASURED_PEAKS.json bf16_tflops (pqs_peaks unavailable)"
         roofline = {"bound": "tensor", "achieved": achieved, "peak": i8_peak, "unit": "TOP/s (int8)",
                     "frac": achieved / i8_peak,
                     "traffic": traffic_db.get("scan4tc_kernel", {}).get("bytes"),
@@ -667,8 +757,7 @@ def main():
                     "kernel": "scan4tc_kernel (tcgen05.mma kind::i8, M=128 N=256 K=256 per tile)",
                     "per_unit": "2 x 256 int8 MACs per (query, code) over 256-query groups and 128-code tiles "
                                 f"({work:.3e} ops per launch)",
-                    "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (measured cuBLAS bf16; int8 dense "
-                                   "rate is 2x bf16 on B200) -- derived, not separately measured",
+                    "peak_source": peak_source,
                     "lut_equivalent": lut, "hbm": hbm, "kernel_ms": scan_ms, "share_of_step": scan_ms / ms_per_step}
     else:
         roofline = {"bound": "lut", **lut, "traffic": None,

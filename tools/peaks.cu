@@ -24,6 +24,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <string>
+
 #define CK(x)                                                                              \
   do {                                                                                     \
     cudaError_t e_ = (x);                                                                  \
@@ -294,10 +296,42 @@ static double timed(F launch, Clk* d_clk, double* mhz) {
   return best * 1e-3;
 }
 
-int main() {
+// `pqs_peaks i8 [seconds]`: the int8 MMA peak only -- a burst (best of 5
+// launches of ~20 ms) and a sustained figure (back-to-back launches for the
+// given seconds, default 3, the regime of a kernel timed inside a long step)
+static int i8_only(double seconds) {
+  Clk* d_clk;
+  CK(cudaMalloc(&d_clk, sizeof(Clk)));
+  const int smem = (MM + MN) * 64;
+  const int iters = 40000;
+  double mhz = 0;
+  auto launch = [&]() { mma_peak_kernel<0><<<g_sms, 128, smem>>>(iters, d_clk); };
+  const double s = timed(launch, d_clk, &mhz);
+  const double macs = (double)g_sms * iters * 8 * MM * MN * 32;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  const int nl = (int)(seconds / s) + 1;
+  CK(cudaEventRecord(e0));
+  for (int i = 0; i < nl; ++i) launch();
+  CK(cudaEventRecord(e1));
+  CK(cudaEventSynchronize(e1));
+  float ms;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  Clk c{};
+  CK(cudaMemcpy(&c, d_clk, sizeof(Clk), cudaMemcpyDeviceToHost));
+  const double mhz_last = (double)(c.c1 - c.c0) / (double)(c.t1 - c.t0) * 1e3;
+  printf("{\"i8_mma\": {\"tops\": %.1f, \"sm_mhz\": %.0f, \"ms\": %.3f, \"shape\": \"M128 N256 K32 cta_group::1\"}, "
+         "\"i8_mma_sustained\": {\"tops\": %.1f, \"seconds\": %.2f, \"launches\": %d, \"sm_mhz_last\": %.0f}}\n",
+         2 * macs / s / 1e12, mhz, s * 1e3, 2 * macs * nl / (ms * 1e-3) / 1e12, ms * 1e-3, nl, mhz_last);
+  return 0;
+}
+
+int main(int argc, char** argv) {
   cudaDeviceProp p;
   CK(cudaGetDeviceProperties(&p, 0));
   g_sms = p.multiProcessorCount;
+  if (argc > 1 && std::string(argv[1]) == "i8") return i8_only(argc > 2 ? atof(argv[2]) : 3.0);
   Clk* d_clk;
   uint32_t* sink;
   CK(cudaMalloc(&d_clk, sizeof(Clk)));
