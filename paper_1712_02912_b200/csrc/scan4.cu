@@ -652,6 +652,8 @@ __global__ void gather_rows_u8_kernel(const uint8_t* __restrict__ src, const int
 
 }  // namespace
 
+int tc_query_group();
+int tc_k_per_eval();
 int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const uint8_t* d_theta, int64_t nq,
                     int64_t tile_begin, int64_t tile_end, bool build_b, uint64_t* cand, int* cand_cnt, int64_t cap,
                     int* d_ovf);
@@ -852,7 +854,9 @@ struct QadcRun {
       if (rc == PQS_OK) {
         used_tc = true;
         ctx->last_scan_engine = 2;
-        ctx->last_scan_work = 2.0 * (double)cdiv(nq, 256) * 256.0 * (double)nt128 * 128.0 * 256.0;
+        // int8 MMA ops issued: 2 x K per (query, code) over padded query groups and 128-code tiles
+        const int qg = tc_query_group();
+        ctx->last_scan_work = 2.0 * (double)cdiv(nq, qg) * qg * (double)nt128 * 128.0 * (double)tc_k_per_eval();
       } else if (rc == PQS_ERR_UNSUPPORTED) {
         if (ctx->scan4_engine == 2)
           return set_err(ctx, PQS_ERR_UNSUPPORTED, "tcgen05 Quick ADC scan: unsupported shape (needs m <= 16)");
