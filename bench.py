@@ -196,6 +196,19 @@ def _ref_setup(cfg, books, codes=None, queries=None, ivf=None):
     return kind
 
 
+def _ref_probes(queries, coarse, ma):
+    """The probed cells of a query sample (evaluation accounting, outside the
+    timed window): the reference's own nearest_k (_dist.py:42-67) when it is
+    installed, else the oracle's."""
+    q64 = np.asarray(queries, np.float64)
+    c64 = np.asarray(coarse, np.float32).astype(np.float64)
+    if _REF.get("kind") == "reference":
+        from pqscan._dist import nearest_k
+    else:
+        from oracle.pqscan_oracle import nearest_k
+    return nearest_k(q64, c64, ma)[0]
+
+
 def _ref_query(qi):
     """One reference query (forked worker); returns its wall time."""
     d = _REF
@@ -303,10 +316,9 @@ def run_reference(args):
         coarse_h, codes_h, ids_h = coarse.cpu().numpy(), codes.cpu().numpy(), ids.cpu().numpy()
         del ctx
         kind = _ref_setup(cfg, books, queries=queries, ivf=(coarse_h, sizes, codes_h, ids_h))
-        from oracle import pqscan_oracle as O
 
         def evals_of(idx):  # exact evaluation count: sizes of the probed lists (untimed, after the step)
-            cells, _ = O.nearest_k(queries[idx].astype(np.float64), coarse_h.astype(np.float64), cfg["nprobe"])
+            cells = _ref_probes(queries[idx], coarse_h, cfg["nprobe"])
             return float(np.asarray(sizes)[cells].sum())
 
         res = ref_run(evals_of, args.steps, args.warmup, step_s)
@@ -356,11 +368,9 @@ def config_dict(name, cfg, world, n_per_gpu=None):
 def cpu_baseline_ivf(cfg, books, coarse, sizes, codes, ids, queries, budget_s):
     """The reference query_ivf (ivf.py:148-196) on a bounded query sample."""
     kind = _ref_setup(cfg, books, queries=queries, ivf=(coarse, sizes, codes, ids))
-    from oracle import pqscan_oracle as O
 
     def evals_of(idx):  # exact evaluation count (sizes of the probed lists), outside the timed window
-        cells, _ = O.nearest_k(queries[idx].astype(np.float64), np.asarray(coarse, np.float32).astype(np.float64),
-                               cfg["nprobe"])
+        cells = _ref_probes(queries[idx], coarse, cfg["nprobe"])
         return float(np.asarray(sizes)[cells].sum())
 
     res = ref_run(evals_of, 1, 0, budget_s)
@@ -383,9 +393,11 @@ def make_ivf(args, ctx, dev):
 
 
 def run_ivf(args):
-    """cfg3 (IVFADC): one index per GPU, queries sharded across ranks (each
-    rank searches its own 10k-query batch against a replica of the index:
-    weak scaling, no exchange -- "replicas")."""
+    """cfg3 (IVFADC): the inverted lists are partitioned across the ranks
+    (greedy by length); every rank holds the coarse quantizer,
+    probes all 10k queries and scans its own lists; the per-rank top-100
+    lists are all-gathered and merged (sharded.ShardedSearch.ivf).  The
+    index and the query batch are fixed: strong scaling."""
     import torch
 
     rank, world, local = dist_env()
@@ -405,7 +417,16 @@ def run_ivf(args):
     t_build = time.perf_counter()
     cfg, books, coarse, sizes, codes, ids, queries = make_ivf(args, ctx, dev)
     pq = P.ProductQuantizer(cfg["m"], cfg["b"], cfg["d"], books)
-    ivf = P.DeviceIvf.from_arrays(pq, coarse, sizes, codes, ids, ctx=ctx)
+    from paper_1712_02912_b200.sharded import ShardedSearch
+
+    searcher = ShardedSearch.ivf(pq, coarse, sizes, codes, ids, rank, world, cfg["nprobe"], ctx=ctx)
+    ivf = searcher.ivf_index
+    n_total = int(codes.shape[0])
+    host_index = None
+    if not args.no_cpu_baseline and world == 1:
+        host_index = (codes.cpu().numpy(), ids.cpu().numpy())
+    del codes, ids
+    torch.cuda.empty_cache()
     torch.cuda.synchronize()
     t_build = time.perf_counter() - t_build
     ma, r = cfg["nprobe"], cfg["r"]
@@ -419,7 +440,7 @@ def run_ivf(args):
             dist.barrier()
 
     for _ in range(args.warmup):
-        ivf.search(q_dev, ma, r)
+        searcher.search(q_dev, r)
     torch.cuda.synchronize()
     launches0 = ctx.stat(_lib.STAT_LAUNCHES)
     clocks = ClockSampler(local)
@@ -433,7 +454,7 @@ def run_ivf(args):
     for s in range(args.steps):
         flush.zero_()
         starts[s].record(stream)
-        ivf.search(q_dev, ma, r)
+        searcher.search(q_dev, r)
         ends[s].record(stream)
         scan_ns.append(ctx.stat(_lib.STAT_LAST_SCAN_NS))
         evals.append(ctx.stat(_lib.STAT_LAST_EVALS))
@@ -470,7 +491,12 @@ def run_ivf(args):
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        ivf.search(q_pin, ma, r, out=o_pin)
+        if world == 1:
+            ivf.search(q_pin, ma, r, out=o_pin)
+        else:
+            d_, i_, c_ = searcher.search(torch.from_numpy(q_pin).to(dev, non_blocking=True), r)
+            for dst, src in zip(o_pin, (d_, i_, c_)):
+                torch.from_numpy(dst).copy_(src)
         dt = (time.perf_counter() - t0) * 1e3
         if s >= max(args.warmup, 1):
             e2e.append(dt)
@@ -500,18 +526,18 @@ def run_ivf(args):
     f_mhz = clk.get("sm_mhz") or 1965.0
     lut_peak = sm_count * 32 * f_mhz * 1e6 / 1e9
     lut_rate = evals_step * m / (scan_ms / 1e3) / 1e9
-    hbm_alg = int(codes.shape[0]) * (m + 4)  # list-major: every list's codes + V once per launch
+    hbm_alg = int(ivf_local_n(ivf)) * (m + 4)  # list-major: every list's codes + V once per launch
     hbm_peak = peaks.get("hbm_gbs", 6553.6)
     line = {
         "metric": metric_name("cfg3"), "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32+f64",
         "data": "synthetic (seeded stand-in for the BASELINE config, index built on the GPU; see DESIGN.md)",
         "config": {"workload": "IVFADC K=65536, residual PQ 8x8, nprobe 64", "baseline_config_index": 3,
-                   "N_per_gpu": int(codes.shape[0]), "queries_per_gpu": nq, "K": int(coarse.shape[0]),
+                   "N_total": n_total, "N_per_gpu": int(ivf_local_n(ivf)), "queries": nq, "K": int(coarse.shape[0]),
                    "nprobe": ma, "m": m, "b": cfg["b"], "r": r, "d": cfg["d"],
                    "evals_per_step_per_gpu": evals_step,
-                   "parallelism": f"query-shard replicas x{world}" if world > 1 else "single",
+                   "parallelism": f"inverted lists sharded x{world} (greedy by length)" if world > 1 else "single",
                    "l2": "flushed between timed steps (256 MB write); index 1.6 GB > L2",
                    "index_build_s": t_build},
         "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": queries.nbytes,
@@ -534,13 +560,17 @@ def run_ivf(args):
         "impl": "ours",
     }
     if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline_ivf(cfg, books, coarse.cpu().numpy(), sizes, codes.cpu().numpy(),
-                                                ids.cpu().numpy(), queries, args.cpu_sample_s)
+        line["cpu_baseline"] = cpu_baseline_ivf(cfg, books, coarse.cpu().numpy(), sizes, host_index[0],
+                                                host_index[1], queries, args.cpu_sample_s)
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def ivf_local_n(ivf):
+    return int(ivf.n)
 
 
 def measured_i8_peak(seconds: float = 3.0):
@@ -638,12 +668,23 @@ def main():
     torch.cuda.synchronize()
     clocks.start()
     time.sleep(0.3)
-    for s in range(args.steps):
-        flush.zero_()
-        starts[s].record(stream)
-        step_device()
-        ends[s].record(stream)
-        scan_ns.append(ctx.stat(_lib.STAT_LAST_SCAN_NS))
+    if world == 1:
+        for s in range(args.steps):
+            flush.zero_()
+            starts[s].record(stream)
+            step_device()
+            ends[s].record(stream)
+            scan_ns.append(ctx.stat(_lib.STAT_LAST_SCAN_NS))
+    else:
+        # N > 1: the exchange + merge of step s overlaps the scan of step s+1
+        # (ShardedSearch.search_stream); the K steps are timed as one region
+        # (no per-step L2 flush: the 1 GB shard per GPU exceeds L2 anyway)
+        starts[0].record(stream)
+        for _ in searcher.search_stream((q_dev for _ in range(args.steps)), r):
+            scan_ns.append(ctx.stat(_lib.STAT_LAST_SCAN_NS))
+        ends[0].record(stream)
+        for s in range(1, args.steps):
+            starts[s], ends[s] = ends[0], ends[0]
     cand_max, cand_tot = ctx.stat(_lib.STAT_LAST_MAX_CAND), ctx.stat(_lib.STAT_LAST_CAND_TOTAL)
     torch.cuda.synchronize()
     barrier()

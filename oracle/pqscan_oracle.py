@@ -276,12 +276,13 @@ def sqdist_matrix(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     a = np.asarray(a, dtype=np.float64)
     b = np.asarray(b, dtype=np.float64)
     out = np.empty((a.shape[0], b.shape[0]), dtype=np.float64)
-    for lo in range(0, a.shape[0], 64):
-        d = a[lo:lo + 64, None, :] - b[None, :, :]
+    step = max(1, min(64, (1 << 22) // max(1, b.shape[0] * b.shape[1])))  # bounded temporaries
+    for lo in range(0, a.shape[0], step):
+        d = a[lo:lo + step, None, :] - b[None, :, :]
         acc = np.zeros(d.shape[:2], dtype=np.float64)
         for t in range(d.shape[2]):  # sequential order, as scipy's cdist
             acc += d[:, :, t] * d[:, :, t]
-        out[lo:lo + 64] = acc
+        out[lo:lo + step] = acc
     return out
 
 

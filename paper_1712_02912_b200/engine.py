@@ -324,6 +324,7 @@ class DeviceIvf:
         self.ctx = ctx or default_context()
         self.dq = DeviceQuantizer(pq, self.ctx)
         self.K, self.d = int(coarse.shape[0]), int(coarse.shape[1])
+        self.n = int(np.asarray(sizes).sum())
         if sizes.shape != (self.K,):
             raise ValueError("list_sizes must have one entry per coarse centroid")
         h = ctypes.c_void_p()

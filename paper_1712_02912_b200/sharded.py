@@ -10,6 +10,18 @@ subset of the union of the shard top-r under the same (distance, id) order.
 Quick ADC needs *global* quantization parameters: qmax is the r-th fp64 ADC
 of the first init_count codes of the global list (quickadc.py:130-137), so
 those codes are replicated to every rank (`prefix_codes`).
+
+IVFADC shards the inverted lists: every rank holds the coarse
+quantizer and the residual codebooks (the probes are computed identically
+everywhere) but only its own lists -- assigned greedily by length, largest
+first, to the least-loaded rank -- and returns the exact top-r over the
+probed lists it owns; the same all-gather + (distance, id) merge gives the
+reference's query_ivf result (ivf.py:174-195 merges per-list top-r the same
+way).
+
+`search_stream` overlaps the exchange of one query batch with the scan of the
+next: the all-gather is issued asynchronously, the next batch's scan is
+queued on the compute stream, and only then is the previous batch merged.
 """
 
 from __future__ import annotations
@@ -33,20 +45,65 @@ def all_gather_results(dist, ids, cnt, group=None):
     collective: each rank packs [fp64 distance bits | ids | count] into an
     (nq, 2r + 1) int64 block (the per-step exchange is latency-, not
     bandwidth-bound, so one all-gather instead of three)."""
+    _, finish = all_gather_start(dist, ids, cnt, group)
+    return finish()
+
+
+def all_gather_start(dist, ids, cnt, group=None):
+    """Issue the packed all-gather asynchronously; returns (handle, finish)
+    where finish() waits and unpacks (gd, gi, gc).  CUDA tensors on a gloo
+    group (CPU tests of the device path) are staged through host memory."""
     import torch
     import torch.distributed as dist_
 
     world = dist_.get_world_size(group)
+    dist, ids, cnt = (torch.from_numpy(np.ascontiguousarray(t)) if isinstance(t, np.ndarray) else t
+                      for t in (dist, ids, cnt))
     nq, r = dist.shape
     packed = torch.cat([dist.to(torch.float64).contiguous().view(torch.int64), ids.to(torch.int64),
                         cnt.to(torch.int64).reshape(nq, 1)], dim=1).contiguous()
+    dev = packed.device
+    if packed.is_cuda and dist_.get_backend(group) == "gloo":
+        packed = packed.cpu()
     out = torch.empty((world * nq, packed.shape[1]), dtype=torch.int64, device=packed.device)
-    dist_.all_gather_into_tensor(out, packed, group=group)  # rank blocks concatenated along dim 0
-    out = out.view(world, nq, packed.shape[1])
+    work = dist_.all_gather_into_tensor(out, packed, group=group, async_op=True)  # rank blocks along dim 0
+
+    def finish():
+        work.wait()
+        return _unpack(out.to(dev), world, nq, r, cnt.dtype)
+
+    return work, finish
+
+
+def _unpack(out, world, nq, r, cnt_dtype):
+    out = out.view(world, nq, 2 * r + 1)
+    import torch
+
     gd = out[:, :, :r].contiguous().view(torch.float64)
     gi = out[:, :, r:2 * r].contiguous()
-    gc = out[:, :, 2 * r].to(cnt.dtype).contiguous()
+    gc = out[:, :, 2 * r].to(cnt_dtype).contiguous()
     return gd, gi, gc
+
+
+def partition_lists(sizes, world: int):
+    """Greedy list partition: lists in decreasing size order, each
+    to the rank with the smallest total so far (ties: lowest rank, then the
+    lower list index first).  Returns owner (K,) int64."""
+    sizes = np.asarray(sizes, dtype=np.int64)
+    if world < 1:
+        raise ValueError("bad world")
+    order = np.argsort(-sizes, kind="stable")
+    load = np.zeros(world, dtype=np.int64)
+    owner = np.empty(sizes.shape[0], dtype=np.int64)
+    import heapq
+
+    heap = [(0, g) for g in range(world)]
+    for c in order:
+        ld, g = heapq.heappop(heap)
+        owner[c] = g
+        load[g] = ld + int(sizes[c])
+        heapq.heappush(heap, (int(load[g]), g))
+    return owner
 
 
 class ShardedSearch:
@@ -106,6 +163,56 @@ class ShardedSearch:
         out.db, out.dq = db, dq
         return out
 
+    @classmethod
+    def ivf(cls, pq, coarse, list_sizes, codes, ids, rank: int, world: int, ma: int, ctx=None, group=None):
+        """Device-backed IVF shard: this rank's lists of an index given in
+        cell order (list_sizes host (K,), codes (n, m), ids (n,) -- numpy or
+        CUDA tensors); the other lists are empty here."""
+        import torch
+
+        from .engine import DeviceIvf, merge_topr
+
+        sizes = np.asarray(list_sizes, dtype=np.int64)
+        owner = partition_lists(sizes, world)
+        mine = owner == rank
+        local_sizes = np.where(mine, sizes, 0)
+        if isinstance(codes, np.ndarray):
+            keep = np.repeat(mine, sizes)
+            lc, li = np.ascontiguousarray(codes[keep]), np.ascontiguousarray(ids[keep])
+        else:
+            keep = torch.from_numpy(np.repeat(mine, sizes)).to(codes.device)
+            lc, li = codes[keep].contiguous(), ids[keep].contiguous()
+        div = DeviceIvf.from_arrays(pq, coarse, local_sizes, lc, li, ctx=ctx)
+
+        def local(queries, r):
+            return div.search(queries, ma, r)
+
+        out = cls(local, lambda d, i, c, r: merge_topr(d, i, c, r, ctx=ctx), group)
+        out.ivf_index, out.owner = div, owner
+        return out
+
+    def search_stream(self, batches, r: int):
+        """Global top-r for each query batch of an iterable, the exchange of
+        batch i overlapping the scan of batch i+1 (yields (dist, ids, count)
+        per batch, in order)."""
+        import torch.distributed as dist_
+
+        multi = dist_.is_available() and dist_.is_initialized() and dist_.get_world_size(self.group) > 1
+        pending = None
+        for q in batches:
+            d, i, c = self.local_search(q, r)            # queued on the compute stream
+            if not multi:
+                yield d, i, c
+                continue
+            _, fin = all_gather_start(d, i, c, self.group)
+            if pending is not None:
+                gd, gi, gc = pending()
+                yield self.merge(gd, gi, gc, r)
+            pending = fin
+        if pending is not None:
+            gd, gi, gc = pending()
+            yield self.merge(gd, gi, gc, r)
+
     def search(self, queries, r: int):
         """Global top-r for every query (identical result on every rank)."""
         import torch.distributed as dist_
@@ -117,4 +224,4 @@ class ShardedSearch:
         return self.merge(gd, gi, gc, r)
 
 
-__all__ = ["shard_range", "all_gather_results", "ShardedSearch"]
+__all__ = ["shard_range", "partition_lists", "all_gather_results", "all_gather_start", "ShardedSearch"]

@@ -110,3 +110,17 @@ def test_shard_ranges_cover_exactly():
                 assert b == c and b >= a
             sizes = [b - a for a, b in spans]
             assert max(sizes) - min(sizes) <= 1
+
+
+def test_partition_lists_greedy_balanced():
+    from paper_1712_02912_b200.sharded import partition_lists
+
+    rng = np.random.default_rng(3)
+    sizes = rng.integers(0, 5000, 1000)
+    for world in (1, 2, 3, 8):
+        owner = partition_lists(sizes, world)
+        assert owner.shape == sizes.shape and owner.min() >= 0 and owner.max() < world
+        loads = np.bincount(owner, weights=sizes, minlength=world)
+        assert loads.sum() == sizes.sum()
+        assert loads.max() - loads.min() <= sizes.max()   # LPT bound
+    assert (partition_lists(sizes, 1) == 0).all()
