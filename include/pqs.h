@@ -65,7 +65,8 @@ enum pqs_option {
   PQS_OPT_SAMPLE_DIV = 2,   /* threshold sample = 1/SAMPLE_DIV of the code tiles (default 32) */
   PQS_OPT_FORCE_FALLBACK = 3,/* 1: run the exact dense fallback for every query (testing) */
   PQS_OPT_SCAN4_ENGINE = 4, /* Quick ADC scan: 0 auto (tcgen05 int8 when possible), 1 PRMT, 2 tcgen05 */
-  PQS_OPT_TC_CHUNK_TILES = 5 /* tcgen05 scan: cap on 128-code tiles per launch (0 = automatic; testing) */
+  PQS_OPT_TC_CHUNK_TILES = 5,/* tcgen05 scan: cap on 128-code tiles per launch (0 = automatic; testing) */
+  PQS_OPT_SCAN8_ENGINE = 6  /* float ADC filter: 0 auto (packed two-query words when m <= 64), 1 u16 lane=query, 2 packed */
 };
 
 enum pqs_stat {
@@ -76,7 +77,7 @@ enum pqs_stat {
   PQS_STAT_LAST_SCAN_NS = 5,   /* device time of the last search's main scan kernel (CUDA events) */
   PQS_STAT_LAST_SCAN_LAUNCHES = 6, /* launches of that kernel in the last search */
   PQS_STAT_LAST_CAND_TOTAL = 7,    /* sum over queries of the candidates of the last search */
-  PQS_STAT_LAST_SCAN_ENGINE = 8,   /* 1 PRMT scan4, 2 tcgen05 scan4, 3 scan8, 4 IVF list scan */
+  PQS_STAT_LAST_SCAN_ENGINE = 8,   /* 1 PRMT scan4, 2 tcgen05 scan4, 3 scan8 (u16), 4 IVF list scan, 5 scan8 packed */
   PQS_STAT_LAST_SCAN_WORK = 9,     /* work units of that kernel: tcgen05 -> int8 MMA ops; others -> table lookups */
   PQS_STAT_LAST_RERANK_TOTAL = 10, /* float / IVF: candidates re-scored exactly after the bound tightening (sum over queries) */
   PQS_STAT_LAST_SLOT_EVALS = 11    /* IVF list scan: (slot, code) evaluations incl. idle slots of partly filled 8-query groups */
@@ -236,6 +237,18 @@ int pqs_encode(pqs_ctx* ctx, const pqs_pq* pq, const float* x, int64_t n, const 
                int64_t K, const int64_t* cells, uint8_t* out_codes, int io);
 int pqs_encode_f64(pqs_ctx* ctx, const pqs_pq* pq, const double* x, int64_t n, const float* coarse,
                    int64_t K, const int64_t* cells, uint8_t* out_codes, int io);
+
+/* ---- nearest (_dist.py:24-39), the assignment step of build_ivf (ivf.py:122):
+ * per point the index of its nearest centroid by the fp64 cdist sum, ties to
+ * the lowest index, and that squared distance.  centroids (K, d) float32
+ * (the reference widens them with astype(float64)), points (n, d); out_idx
+ * (n,) int64, out_dist (n,) float64 or NULL.  Runs the probe GEMM (tcgen05
+ * kind::tf32 shortlist with a certified bound) and its exact fp64 re-score,
+ * i.e. nearest_k with k = 1; centroids/points host or device by io.        */
+int pqs_nearest(pqs_ctx* ctx, const float* centroids, int64_t K, int d, const float* points,
+                int64_t n, int64_t* out_idx, double* out_dist, int io);
+int pqs_nearest_f64(pqs_ctx* ctx, const float* centroids, int64_t K, int d, const double* points,
+                    int64_t n, int64_t* out_idx, double* out_dist, int io);
 
 /* ---- sharded merge: top-r of the union of G per-shard top-r lists by
  * (distance, id) -- NeighborSet.push semantics (scan.py:109-118).

@@ -69,7 +69,7 @@ from .derived import (  # noqa: F401
     search_two_pass,
 )
 from .ivf import KERNELS, default_r2, device_index, query_ivf, query_ivf_batch  # noqa: F401
-from .engine import DeviceCodes, DeviceIvf, DeviceQuantizer, merge_topr  # noqa: F401
+from .engine import DeviceCodes, DeviceIvf, DeviceQuantizer, merge_topr, nearest  # noqa: F401
 from ._lib import Context, default_context, load_library  # noqa: F401
 
 __version__ = "0.1.0"

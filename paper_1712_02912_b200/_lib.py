@@ -29,6 +29,7 @@ OPT_SAMPLE_DIV = 2
 OPT_FORCE_FALLBACK = 3
 OPT_SCAN4_ENGINE = 4
 OPT_TC_CHUNK_TILES = 5
+OPT_SCAN8_ENGINE = 6
 STAT_LAUNCHES = 1
 STAT_LAST_MAX_CAND = 2
 STAT_LAST_OVERFLOW = 3
@@ -79,11 +80,12 @@ SIGNATURES = {
     "pqs_fastscan_checked": (_i, [_p, _p, _p, _i64, _i64, _i, _p, _i]),
     "pqs_derived_search": (_i, [_p, _p, _p, _p, _p, _i64, _i, _i64, _p, _p, _p, _i]),
     "pqs_ivf_derived_search": (_i, [_p, _p, _p, _p, _i64, _i, _i, _i64, _p, _p, _p, _i]),
+    "pqs_nearest": (_i, [_p, _p, _i64, _i, _p, _i64, _p, _p, _i]),
     "pqs_merge_topr": (_i, [_p, _i, _p, _p, _p, _i64, _i, _i, _p, _p, _p, _i]),
 }
 # float64 twins of the query-taking entry points (same arguments; queries double*)
 F64_TWINS = ("pqs_compute_tables", "pqs_adc_search", "pqs_qadc_search", "pqs_ivf_probe", "pqs_ivf_search",
-             "pqs_ivf_qadc_search", "pqs_derived_search", "pqs_ivf_derived_search", "pqs_encode")
+             "pqs_ivf_qadc_search", "pqs_derived_search", "pqs_ivf_derived_search", "pqs_encode", "pqs_nearest")
 for _n in F64_TWINS:
     SIGNATURES[_n + "_f64"] = SIGNATURES[_n]
 

@@ -25,6 +25,7 @@ int launch_quantize(pqs_ctx* ctx, double qmin, double qmax, const double* d_v, i
 int ivf_create_impl(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t K, const int64_t* list_sizes,
                     const uint8_t* codes, const int64_t* ids, int io, pqs_ivf** out);
 void ivf_destroy_impl(pqs_ivf* ivf);
+int coarse_index_create(pqs_ctx* ctx, const float* centroids, int64_t K, int d, pqs_ivf** out);
 
 int set_err(pqs_ctx* ctx, int code, const std::string& msg) {
   if (ctx) ctx->err = msg;
@@ -249,6 +250,10 @@ int pqs_ctx_set_option(pqs_ctx* ctx, int option, int64_t value) {
     case PQS_OPT_SCAN4_ENGINE:
       PQS_CHECK(ctx, value >= 0 && value <= 2, "scan4 engine must be 0, 1 or 2");
       ctx->scan4_engine = (int)value;
+      return PQS_OK;
+    case PQS_OPT_SCAN8_ENGINE:
+      PQS_CHECK(ctx, value >= 0 && value <= 2, "scan8 engine must be 0, 1 or 2");
+      ctx->scan8_engine = (int)value;
       return PQS_OK;
     case PQS_OPT_TC_CHUNK_TILES:
       PQS_CHECK(ctx, value >= 0, "chunk must be >= 0");
@@ -764,6 +769,42 @@ int pqs_ivf_probe(pqs_ctx* ctx, const pqs_ivf* ivf, const float* queries, int64_
 int pqs_ivf_probe_f64(pqs_ctx* ctx, const pqs_ivf* ivf, const double* queries, int64_t nq, int ma,
                       int64_t* out_cells, double* out_dist, int io) {
   return ivf_probe_impl(ctx, ivf, queries, 1, nq, ma, out_cells, out_dist, io);
+}
+
+// nearest (_dist.py:24-39): the probe with ma = 1 over a coarse-only handle
+static int nearest_impl(pqs_ctx* ctx, const float* centroids, int64_t K, int d, const void* points, int f64,
+                        int64_t n, int64_t* out_idx, double* out_dist, int io) {
+  if (!ctx || !centroids || !out_idx) return PQS_ERR_INVALID;
+  PQS_TRY(check_io(ctx, io));
+  PQS_CHECK(ctx, n >= 0, "n must be >= 0");
+  PQS_CUDA(ctx, cudaSetDevice(ctx->device));
+  pqs_ivf* iv = nullptr;
+  PQS_TRY(coarse_index_create(ctx, centroids, K, d, &iv));
+  int st = PQS_OK;
+  if (n > 0) {
+    QVec dq;
+    int64_t* dc = nullptr;
+    double* dd = nullptr;
+    st = stage_q(ctx, points, (size_t)n * d, io, f64, &dq);
+    if (st == PQS_OK) st = stage_out(ctx, S_OUT_I, out_idx, (size_t)n, io, &dc);
+    if (st == PQS_OK) st = stage_out(ctx, S_OUT_D, out_dist, (size_t)n, io, &dd);
+    if (st == PQS_OK) st = run_ivf_probe(ctx, iv, dq, n, 1, dc, dd);
+    if (st == PQS_OK) st = copy_out(ctx, out_idx, dc, (size_t)n, io);
+    if (st == PQS_OK) st = copy_out(ctx, out_dist, dd, (size_t)n, io);
+  }
+  // the handle's buffers are read by work queued on the stream: drain it first
+  cudaStreamSynchronize(ctx->stream);
+  ivf_destroy_impl(iv);
+  if (st != PQS_OK) return st;
+  return finish(ctx, io);
+}
+int pqs_nearest(pqs_ctx* ctx, const float* centroids, int64_t K, int d, const float* points, int64_t n,
+                int64_t* out_idx, double* out_dist, int io) {
+  return nearest_impl(ctx, centroids, K, d, points, 0, n, out_idx, out_dist, io);
+}
+int pqs_nearest_f64(pqs_ctx* ctx, const float* centroids, int64_t K, int d, const double* points, int64_t n,
+                    int64_t* out_idx, double* out_dist, int io) {
+  return nearest_impl(ctx, centroids, K, d, points, 1, n, out_idx, out_dist, io);
 }
 
 static int ivf_search_impl(pqs_ctx* ctx, const pqs_ivf* ivf, const void* queries, int f64, int64_t nq, int ma, int r,

@@ -827,6 +827,43 @@ int ivf_create_impl(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t
   return PQS_OK;
 }
 
+// Coarse-only handle (no lists, no residual quantizer): what the probe needs
+// to answer nearest / nearest_k over a centroid set (_dist.py:24-67), used by
+// pqs_nearest for the index build's assignment (ivf.py:122).
+int coarse_index_create(pqs_ctx* ctx, const float* centroids, int64_t K, int d, pqs_ivf** out) {
+  *out = nullptr;
+  PQS_CHECK(ctx, K >= 1 && K < (1ll << 31), "need 1 <= K < 2^31 centroids");
+  PQS_CHECK(ctx, d >= 1, "d must be >= 1");
+  pqs_ivf* iv = new pqs_ivf();
+  iv->K = K;
+  iv->d = d;
+  auto al = [&](void** p, size_t bytes) { return cudaMalloc(p, std::max<size_t>(bytes, 16)) == cudaSuccess; };
+  if (!(al((void**)&iv->coarse, (size_t)K * d * 4) && al((void**)&iv->cnorm, (size_t)K * 8) &&
+        al((void**)&iv->cnormf, (size_t)K * 4) && al((void**)&iv->gnorm, (size_t)K * 4 + 16))) {
+    cudaGetLastError();
+    ivf_destroy_impl(iv);
+    return set_err(ctx, PQS_ERR_NOMEM, "centroid allocation failed");
+  }
+  int st = upload(ctx, iv->coarse, centroids, (size_t)K * d * 4);
+  if (st == PQS_OK) {
+    cnorm_kernel<<<(unsigned)cdiv(K, 256), 256, 0, ctx->stream>>>(iv->coarse, K, d, iv->cnorm, iv->gnorm, iv->cnormf);
+    ctx->launches++;
+    st = probe_build_index(ctx, iv);
+  }
+  std::vector<float> gn(K);
+  if (st == PQS_OK) st = download(ctx, gn.data(), iv->gnorm, (size_t)K * 4);
+  if (st != PQS_OK) {
+    cudaGetLastError();
+    ivf_destroy_impl(iv);
+    return st;
+  }
+  float gm = 0.f;
+  for (float v : gn) gm = std::max(gm, v);
+  iv->gmax = gm;
+  *out = iv;
+  return PQS_OK;
+}
+
 void ivf_destroy_impl(pqs_ivf* iv) {
   if (!iv) return;
   cudaFree(iv->coarse);

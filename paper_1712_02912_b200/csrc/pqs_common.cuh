@@ -91,6 +91,7 @@ struct pqs_ctx {
   int sample_div = 32;
   int force_fallback = 0;
   int scan4_engine = 0;  // 0 auto (tcgen05 when possible), 1 PRMT, 2 tcgen05
+  int scan8_engine = 0;  // 0 auto (packed when m <= 64), 1 u16 lane=query, 2 packed
   int64_t tc_chunk_tiles = 0;  // tcgen05 scan: max 128-code tiles per launch (0 = auto)
   int64_t launches = 0;
   int64_t last_max_cand = 0;

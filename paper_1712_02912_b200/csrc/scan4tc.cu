@@ -38,7 +38,6 @@ constexpr int TC_K = 256;          // one-hot width (16 components x 16 values)
 constexpr int TC_KB = TC_K + 32;   // + one K step carrying the per-query threshold (A: ones, B: -(theta+1))
 constexpr int A32_BYTES = TC_M * TC_K;   // 32 KB: one-hot tile with the threshold folded into B
 constexpr int SS_NA = 3;                 // one-hot tile buffers of the SS filter
-constexpr int64_t SS_TB = 256;           // tiles per block of the SS filter's item order
 constexpr int B_BYTES = TC_N * TC_KB;    // 72 KB per 256-query group
 constexpr int B_ONEHOT_BYTES = TC_N * TC_K;  // its first 64 KB: the quantized tables
 constexpr int LBO_A = (TC_M / 8) * 128;  // byte distance between K-chunks of A (2048)
@@ -105,16 +104,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t total = a.nqg * a.ntiles;
-  // items in tile-block-major order: for each block of SS_TB tiles, every
-  // query group in turn -- a block's codes are read from DRAM once and hit L2
-  // for the other groups (the B tables change every SS_TB items)
-  const int64_t full = a.ntiles / SS_TB, rem = a.ntiles % SS_TB, wfull = full * a.nqg * SS_TB;
-  auto group_of = [&](int64_t w) -> int64_t {
-    return w < wfull ? (w % (a.nqg * SS_TB)) / SS_TB : (w - wfull) / rem;
-  };
-  auto tile_of = [&](int64_t w) -> int64_t {
-    return w < wfull ? (w / (a.nqg * SS_TB)) * SS_TB + w % SS_TB : full * SS_TB + (w - wfull) % rem;
-  };
+  // a CTA range spans <= 2 query groups: (group, tile) of item w without division
+  const int64_t gfirst = ((int64_t)blockIdx.x * total / gridDim.x) / a.ntiles;
+  const int64_t wsplit = (gfirst + 1) * a.ntiles;
+  auto group_of = [&](int64_t w) { return w < wsplit ? gfirst : gfirst + 1; };
+  auto tile_of = [&](int64_t w) { return w < wsplit ? w - gfirst * a.ntiles : w - wsplit; };
   const int64_t w0 = (int64_t)blockIdx.x * total / gridDim.x;
   const int64_t w1 = (int64_t)(blockIdx.x + 1) * total / gridDim.x;
 
@@ -161,7 +155,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
             mbar_expect_tx(&bar_b[bb], (uint32_t)(B_ONEHOT_BYTES + TC_N * 2));
             bulk_g2s(sB, a.bglob + g * (int64_t)B_BYTES, B_ONEHOT_BYTES, &bar_b[bb]);
             bulk_g2s(sAdd + bb * TC_N, a.nadd + g * TC_N, TC_N * 2, &bar_b[bb]);
-            mbar_wait(&bar_b[bb], (uint32_t)((gi >> 1) & 1));
+            mbar_wait(&bar_b[bb], 0);
             cur_g = g;
           }
           const int ab = (int)(it & 1);
@@ -277,7 +271,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) scan4tc_kernel(Scan4TcArgs a) {
         const int64_t g = group_of(w);
         if (g != cur_g) {
           ++gi;
-          mbar_wait(&bar_b[gi & 1], (uint32_t)((gi >> 1) & 1));  // biases of this group are in smem
+          mbar_wait(&bar_b[gi & 1], 0);  // biases of this group are in smem
           cur_g = g;
         }
         const int ab = (int)(it & 1);
@@ -374,7 +368,6 @@ constexpr int LBO_O = (HN / 8) * 128;         // 4096
 constexpr int H_EPI_WARPS = 8;                // 2 per TMEM lane quadrant, 128 code columns each
 constexpr int H_THREADS = (H_EPI_WARPS + 8 + 1) * 32;  // epilogue + 8 producer + 1 MMA warp
 constexpr int H_PAIRS = 64;
-constexpr int H_CNT_PAIRS = 32;               // bin pairs counted by the sample histogram (bins < 64)
 constexpr uint32_t IDESC_H = (2u << 4) | ((uint32_t)(HN >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
 
 struct HistTcArgs {
@@ -514,7 +507,7 @@ __global__ void __launch_bounds__(H_THREADS, 1) scan4tc_hist_kernel(HistTcArgs a
         asm volatile("bar.sync 1, %0;" ::"r"(H_EPI_WARPS * 32));
         const int t = warp * 32 + lane;
         const int64_t q = g * TC_N + t;
-        for (int b = 0; b < H_CNT_PAIRS; ++b) {
+        for (int b = 0; b < H_PAIRS; ++b) {
           const unsigned int v = hist[b * TC_N + t];
           if (v) {
             if (q < a.nq) atomicAdd(a.ghist + q * 128 + 2 * b + 1, v);
@@ -543,15 +536,7 @@ __global__ void __launch_bounds__(H_THREADS, 1) scan4tc_hist_kernel(HistTcArgs a
             TMEM_LD64(tbase + (uint32_t)c0, v);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-            // only bins < 2 * H_CNT_PAIRS are counted: the r-th smallest bin of
-            // the sample is far below (bins saturate at 127 around the
-            // r-th distance of the first init_count codes), and when fewer
-            // than r values fall below, theta4_final's "not reached" answer
-            // 127 (admit everything) is still an upper bound -- most values
-            // skip the shared atomic
-#pragma unroll
-            for (int i = 0; i < 64; ++i)
-              if (v[i] < 2u * H_CNT_PAIRS) atomicAdd(hq + (v[i] >> 1) * TC_N, 1u);
+            for (int i = 0; i < 64; ++i) atomicAdd(hq + (min(v[i], 127u) >> 1) * TC_N, 1u);
           }
           tc_fence_before();
           __syncwarp();
@@ -997,12 +982,10 @@ int launch_scan4_tc(pqs_ctx* ctx, const pqs_db* db, const uint8_t* d_qt, const u
   // every CTA range must span <= 2 query groups (single-buffered B, decode of
   // the staged records) and fit the 17-bit tile-iteration field of a record:
   // long ranges are scanned in chunks of tiles, one launch each
-  // (the SS kernel's tile-block-major item order has no group-span limit; the
-  // TS kernel's ranges must span <= 2 groups)
-  if (!ss && nqg >= nctas_max) return PQS_ERR_UNSUPPORTED;
+  if (nqg >= nctas_max) return PQS_ERR_UNSUPPORTED;
   int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(tile_end - tile_begin, ((1 << 17) - 2) * nctas_max / nqg));
   if (ctx->tc_chunk_tiles > 0) chunk = std::min<int64_t>(chunk, ctx->tc_chunk_tiles);
-  for (int64_t c0 = tile_begin; c0 < tile_end && !ss; c0 += chunk) {
+  for (int64_t c0 = tile_begin; c0 < tile_end; c0 += chunk) {
     const int64_t ntiles = std::min<int64_t>(chunk, tile_end - c0);
     const int64_t total = nqg * ntiles;
     // a CTA range no longer than a group's tile count spans <= 2 groups

@@ -23,6 +23,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "pqs_common.cuh"
@@ -414,6 +416,312 @@ __global__ void __launch_bounds__(SCAN8_THREADS, 1) scan8_kernel(Scan8Args a) {
   flush();
 }
 
+
+// ===================================================================== packed
+// K3p -- the filter pass with two queries per table word.
+//
+// The u16 lane=query kernel above issues ~4.5 instructions per lookup and its
+// LDS.U16 uses half of the 128-byte shared-memory wavefront.  Here one 32-bit
+// word holds the (15-bit) lower-bound entries of two queries, so one LDS.32
+// is 64 lookups and the partial sums of both queries advance with ONE integer
+// add.  Layout of a 32-query group's tables, per component quad Q = j / 4:
+//   word[(Q*k + c) * 64 + (j % 4) * 16 + h] = t'(query h)[j][c] | t'(query h+16)[j][c] << 16
+// i.e. one 256-byte row per entry c.  A quad's 256 rows are exactly 64 KB and
+// are staged at a 64 KB-aligned shared-memory window address, so the address
+// of a lookup is  slot | code << 8 | (j%4)*64 + h*4  -- formed by ONE PRMT
+// that drops the code byte into byte 1 of the lane's base register (no IMAD,
+// no shift).  Half-warp P = lane / 16 takes component parity P: lanes 0-15
+// read sub-slot 2i (banks 0-15 or 16-31 alternating with i), lanes 16-31
+// sub-slot 2i+1 (the other 16 banks) -> every LDS.32 is one conflict-free
+// 128-byte wavefront.  To let one SHFL finish two codes, the upper half-warp
+// walks each code pair in swapped order (acc[e] <-> code e^1): after
+//   tot = acc[e] + shfl_xor(acc[e+1], 16)
+// lanes 0-15 hold the total of code e and lanes 16-31 that of code e+1.
+// Entries are clipped to floor(32767 / m) (a clipped entry is still a lower
+// bound) so a half never carries into its neighbour and bit 15 of each half
+// stays free: (theta | 0x8000) - tot keeps bit 15 set iff tot <= theta, one
+// subtraction tests both queries.  Per 2 lookups: PRMT + LDS.32 + IADD.
+constexpr int CST8P = 8;          // staged candidates per thread and query half
+constexpr int P16_MAX_M = 64;     // clip = floor(32767 / m) >= 511
+constexpr uint32_t P16_TMAX = 32767u;
+constexpr double P16_TARGET = 8191.0;
+
+// one CTA per (query group, padded component): rows read coalesced, transposed
+// through shared memory, written as 64-byte runs of the packed layout
+__global__ void __launch_bounds__(TU16_THREADS) tables_p16_kernel(const float* __restrict__ tables,
+                                                                 const float* __restrict__ off,
+                                                                 const int* __restrict__ ex, int64_t nq, int m, int k,
+                                                                 uint32_t clip, uint32_t* __restrict__ tp) {
+  __shared__ float st[32][257];
+  __shared__ double so[32];
+  __shared__ int se[32];
+  const int mq = ((m + 3) >> 2) << 2;
+  const int64_t qg = blockIdx.x / mq;
+  const int j = (int)(blockIdx.x - qg * mq);
+  uint32_t* dst = tp + ((qg * (mq >> 2) + (j >> 2)) * (int64_t)k) * 64 + (j & 3) * 16;
+  if (j >= m) {  // padding component of the last quad: zero rows
+    for (int i = threadIdx.x; i < 16 * k; i += TU16_THREADS) dst[(int64_t)(i >> 4) * 64 + (i & 15)] = 0u;
+    return;
+  }
+  if (threadIdx.x < 32) {
+    const int64_t q = qg * 32 + threadIdx.x;
+    so[threadIdx.x] = q < nq ? (double)off[q * m + j] : 0.0;
+    se[threadIdx.x] = q < nq ? ex[q] : 0;
+  }
+  for (int i = threadIdx.x; i < 32 * k; i += TU16_THREADS) {
+    const int l = i / k, c = i - l * k;
+    const int64_t q = qg * 32 + l;
+    st[l][c] = q < nq ? tables[(q * m + j) * (int64_t)k + c] : 0.f;
+  }
+  __syncthreads();
+  auto val = [&](int l, int c) -> uint32_t {
+    if (qg * 32 + l >= nq) return 0u;
+    const double f = floor(ldexp((double)st[l][c] - so[l], se[l]));
+    return f >= (double)clip ? clip : (f <= 0.0 ? 0u : (uint32_t)f);
+  };
+  for (int i = threadIdx.x; i < 16 * k; i += TU16_THREADS) {
+    const int h = i & 15, c = i >> 4;
+    dst[(int64_t)c * 64 + h] = val(h, c) | (val(h + 16, c) << 16);
+  }
+}
+
+struct Scan8PArgs {
+  const uint32_t* tp;    // [nqg][nQ][k][64]
+  const uint8_t* codes;  // [ntiles][m][TILE8]
+  int64_t n;
+  int m, k;
+  int64_t nq, nvt, nqg;
+  const uint32_t* theta;  // keep L <= theta[q] (<= P16_TMAX)
+  uint64_t* cand;
+  int* cand_cnt;
+  int64_t cap;
+};
+
+template <int OFF>
+__device__ __forceinline__ uint32_t lds32_off(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(OFF));
+  return v;
+}
+
+template <bool RES>
+__global__ void __launch_bounds__(SCAN8_THREADS, 1) scan8p_kernel(Scan8PArgs a) {
+  extern __shared__ __align__(128) unsigned char smp[];
+  const int m = a.m, k = a.k;
+  const int nQ = (m + 3) >> 2;
+  const uint32_t sb = smem_u32(smp);
+  const uint32_t slot0 = (sb + 65535u) & ~65535u;  // two 64 KB table slots at slot0, slot0 + 64 KB
+  unsigned char* slot_ptr = smp + (slot0 - sb);
+  // low region [sb, slot0): barriers, code buffers, candidate stage
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smp);  // 0/1: stage buffers, 2: resident tables
+  const int crows = RES ? nQ * 4 : 4;
+  const uint32_t code_bytes = (uint32_t)crows * TILE8;
+  uint8_t* code_base = smp + 128;
+  uint32_t* stage = reinterpret_cast<uint32_t*>(code_base + 2 * code_bytes) + threadIdx.x;
+  if (128u + 2u * code_bytes + 2u * CST8P * SCAN8_THREADS * 4u > slot0 - sb) __trap();
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int h = lane & 15, P = lane >> 4;
+  const uint32_t lb = slot0 + (uint32_t)h * 4u + (uint32_t)P * 64u;
+  uint32_t sel[4];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) sel[b] = 0x7604u | ((uint32_t)(b ^ P) << 4);
+
+  // this CTA's balanced range of the linearised (query group, tile) list;
+  // walked with 32-bit (group, tile) cursors
+  const int64_t total = a.nqg * a.nvt;
+  const int64_t w0 = (int64_t)blockIdx.x * total / gridDim.x;
+  const int64_t w1 = (int64_t)(blockIdx.x + 1) * total / gridDim.x;
+  if (w0 >= w1) return;
+  const int nch = RES ? 1 : nQ;
+  const int nvt = (int)a.nvt;
+  const int nw = (int)(w1 - w0);
+  const int S = nw * nch;
+  const int g0 = (int)(w0 / a.nvt), t0 = (int)(w0 - (int64_t)g0 * a.nvt);
+  const uint32_t quad_bytes = (uint32_t)k * 256u;
+
+  auto issue_at = [&](int b, int wi, int ch) {  // wi: index into this CTA's range
+    const int lin = t0 + wi;
+    const int64_t qg = g0 + lin / nvt;
+    const int64_t tile = lin % nvt;
+    if (RES) {
+      mbar_expect_tx(&bars[b], (uint32_t)m * TILE8);
+      bulk_g2s(code_base + b * code_bytes, a.codes + tile * m * (int64_t)TILE8, (uint32_t)m * TILE8, &bars[b]);
+    } else {
+      const int mcur = min(4, m - 4 * ch);
+      mbar_expect_tx(&bars[b], quad_bytes + (uint32_t)mcur * TILE8);
+      bulk_g2s(slot_ptr + b * 65536, a.tp + (qg * nQ + ch) * (int64_t)k * 64, quad_bytes, &bars[b]);
+      bulk_g2s(code_base + b * code_bytes, a.codes + (tile * m + 4 * ch) * (int64_t)TILE8, (uint32_t)mcur * TILE8,
+               &bars[b]);
+    }
+  };
+  auto next_of = [&](int w, int ch, int steps, int& w2, int& ch2) {
+    ch2 = ch + steps;
+    w2 = w;
+    while (ch2 >= nch) {
+      ch2 -= nch;
+      ++w2;
+    }
+  };
+  // code rows of padding components must hold valid codes (their table rows
+  // are zero): clear both buffers once, before any bulk copy lands in them
+  for (uint32_t i = threadIdx.x; i < 2 * code_bytes / 16; i += SCAN8_THREADS)
+    reinterpret_cast<uint4*>(code_base)[i] = make_uint4(0u, 0u, 0u, 0u);
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_init(&bars[2], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    issue_at(0, 0, 0);
+    if (S > 1) {
+      int w2, ch2;
+      next_of(0, 0, 1, w2, ch2);
+      issue_at(1, w2, ch2);
+    }
+  }
+
+  int q0 = -1, cur_qg = -1;  // nq < 2^31
+  uint32_t thg = 0, vmask = 0, tphase = 0;
+  uint32_t ncp = 0;  // staged candidates: query half 0 in byte 0, half 1 in byte 1
+  // append the staged candidates of query half hf to its global list
+  auto flush = [&](int hf) {
+    const int nc = (int)((ncp >> (8 * hf)) & 0xffu);
+    if (nc > 0) {
+      const int64_t q = q0 + 16 * hf;
+      const int pos = atomicAdd(a.cand_cnt + q, nc);
+      const uint32_t* st = stage + hf * CST8P * SCAN8_THREADS;
+      for (int i = 0; i < nc; ++i)
+        if (pos + i < a.cap) a.cand[q * a.cap + pos + i] = (uint64_t)st[i * SCAN8_THREADS];
+      ncp &= ~(0xffu << (8 * hf));
+    }
+  };
+  auto switch_group = [&](int qg) {
+    flush(0);
+    flush(1);
+    q0 = qg * 32 + h;
+    const bool v0 = q0 < a.nq, v1 = q0 + 16 < a.nq;
+    const uint32_t t0 = v0 ? min(a.theta[q0], P16_TMAX) : 0u, t1 = v1 ? min(a.theta[q0 + 16], P16_TMAX) : 0u;
+    thg = t0 | (t1 << 16) | 0x80008000u;
+    vmask = (v0 ? 0x8000u : 0u) | (v1 ? 0x80000000u : 0u);
+    cur_qg = qg;
+  };
+  // one component pair (sub-slots 2*IP and 2*IP+1 of the quad at B) of the warp's 64 codes
+  auto pair_pass = [&](auto ip_tag, uint32_t B, const uint8_t* crow, uint32_t* acc) {
+    constexpr int IP = decltype(ip_tag)::value;
+#pragma unroll
+    for (int v = 0; v < C8 / 16; ++v) {
+      const uint4 cw = *reinterpret_cast<const uint4*>(crow + v * 16);
+      const uint32_t ws[4] = {cw.x, cw.y, cw.z, cw.w};
+#pragma unroll
+      for (int e = 0; e < 16; ++e) acc[v * 16 + e] += lds32_off<IP * 128>(prmt(ws[e >> 2], B, sel[e & 3]));
+    }
+  };
+  // totals of the warp's code pairs and the filter test: the hit bits of a
+  // group of 8 totals shift into one mask word (half 0 in bits 8..15, half 1
+  // in bits 24..31); the rare hits are walked in a compact loop (the kernel
+  // must stay small: a fully unrolled slow path thrashes the instruction cache)
+  auto emit = [&](uint32_t* acc, int64_t c0) {
+    uint32_t M[C8 / 16];
+#pragma unroll
+    for (int g = 0; g < C8 / 16; ++g) M[g] = 0u;
+#pragma unroll
+    for (int e = 0; e < C8; e += 2) {
+      acc[e] += __shfl_xor_sync(0xffffffffu, acc[e + 1], 16);
+      M[e >> 4] = (M[e >> 4] >> 1) | ((thg - acc[e]) & vmask);
+    }
+#pragma unroll
+    for (int g = 0; g < C8 / 16; ++g) {
+      uint32_t mm = M[g];
+      while (mm) {
+        const int p = __ffs((int)mm) - 1;
+        mm &= mm - 1;
+        const int hf = p >> 4;
+        const int64_t code = c0 + g * 16 + 2 * ((p & 15) - 8) + P;
+        if (code < a.n) {
+          const uint32_t nc = (ncp >> (8 * hf)) & 0xffu;
+          stage[(hf * CST8P + nc) * SCAN8_THREADS] = (uint32_t)code;
+          ncp += 1u << (8 * hf);
+          if (nc + 1 == CST8P) flush(hf);
+        }
+      }
+    }
+  };
+
+  uint32_t acc[C8];
+#pragma unroll
+  for (int e = 0; e < C8; ++e) acc[e] = 0u;
+  int s = 0, qg = g0, tile = t0;
+  for (int w = 0; w < nw; ++w) {
+    if (qg != cur_qg) {
+      switch_group(qg);
+      if (RES) {
+        __syncthreads();  // every warp is done with the previous group's tables
+        if (threadIdx.x == 0) {
+          mbar_expect_tx(&bars[2], (uint32_t)nQ * quad_bytes);
+          for (int Q = 0; Q < nQ; ++Q)
+            bulk_g2s(slot_ptr + Q * 65536, a.tp + ((int64_t)qg * nQ + Q) * (int64_t)k * 64, quad_bytes, &bars[2]);
+        }
+        mbar_wait(&bars[2], tphase);
+        tphase ^= 1;
+      }
+    }
+    for (int ch = 0; ch < nch; ++ch, ++s) {
+      const int b = (int)(s & 1);
+      mbar_wait(&bars[b], (uint32_t)((s >> 1) & 1));
+      const uint8_t* cb = code_base + b * code_bytes + warp * C8 + P * TILE8;
+      if (RES) {
+        for (int Q = 0; Q < nQ; ++Q) {
+          const uint32_t B = lb + (uint32_t)Q * 65536u;
+          pair_pass(std::integral_constant<int, 0>{}, B, cb + (4 * Q) * TILE8, acc);
+          if (4 * Q + 2 < m) pair_pass(std::integral_constant<int, 1>{}, B, cb + (4 * Q + 2) * TILE8, acc);
+        }
+      } else {
+        const uint32_t B = lb + (uint32_t)b * 65536u;
+        pair_pass(std::integral_constant<int, 0>{}, B, cb, acc);
+        if (4 * ch + 2 < m) pair_pass(std::integral_constant<int, 1>{}, B, cb + 2 * TILE8, acc);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0 && s + 2 < S) {
+        int w2, ch2;
+        next_of(w, ch, 2, w2, ch2);
+        issue_at(b, w2, ch2);
+      }
+    }
+    emit(acc, (int64_t)tile * TILE8 + warp * C8);
+#pragma unroll
+    for (int e = 0; e < C8; ++e) acc[e] = 0u;
+    if (++tile == nvt) {
+      tile = 0;
+      ++qg;
+    }
+  }
+  flush(0);
+  flush(1);
+}
+
+int launch_scan8p(pqs_ctx* ctx, Scan8PArgs a) {
+  const int nQ = (a.m + 3) / 4;
+  const bool res = nQ <= 2;
+  const int smem = 227 * 1024;
+  auto kern = res ? scan8p_kernel<true> : scan8p_kernel<false>;
+  static uint64_t attr_set[2] = {0, 0};  // per device
+  if (!((attr_set[res] >> (ctx->device & 63)) & 1)) {
+    PQS_CUDA(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set[res] |= 1ull << (ctx->device & 63);
+  }
+  a.nqg = cdiv(a.nq, 32);
+  const int64_t total = a.nqg * a.nvt;
+  if (total <= 0) return PQS_OK;
+  const int64_t nctas = std::min<int64_t>(total, (int64_t)ctx->sm_count);
+  kern<<<(unsigned)nctas, SCAN8_THREADS, smem, ctx->stream>>>(a);
+  PQS_LAUNCHED(ctx);
+  return PQS_OK;
+}
+
 constexpr int RESIDENT_BUDGET = 160 * 1024;
 
 template <int MODE>
@@ -449,7 +757,7 @@ int launch_scan8(pqs_ctx* ctx, Scan8Args a) {
 // scale e1 puts D' near 2^16 * max(1, m/8); theta = floor(D' * 2^e1).
 __global__ void theta8_kernel(const uint32_t* __restrict__ sample, int64_t ns, int r, int m,
                               const int* __restrict__ e0, const double* __restrict__ slack, int* __restrict__ e1,
-                              uint32_t* __restrict__ theta) {
+                              uint32_t* __restrict__ theta, double target, uint32_t tmax) {
   __shared__ unsigned int hist[256];
   __shared__ unsigned int s_prefix, s_k, s_valid, s_vmax;
   const int64_t q = blockIdx.x;
@@ -476,7 +784,7 @@ __global__ void theta8_kernel(const uint32_t* __restrict__ sample, int64_t ns, i
   if (s_valid < (unsigned)r) {
     if (threadIdx.x == 0) {
       e1[q] = e0[q];
-      theta[q] = 0xFFFFFFFEu;
+      theta[q] = tmax;
     }
     return;
   }
@@ -520,7 +828,6 @@ __global__ void theta8_kernel(const uint32_t* __restrict__ sample, int64_t ns, i
   }
   if (threadIdx.x == 0) {
     const double Dp = ldexp((double)s_prefix + (double)m, -e0[q]) + slack[q];
-    const double target = 65536.0 * (m > 8 ? m / 8.0 : 1.0);
     int e = e0[q];
     if (Dp > 0.0) {
       e = (int)floor(log2(target / Dp));
@@ -528,7 +835,7 @@ __global__ void theta8_kernel(const uint32_t* __restrict__ sample, int64_t ns, i
     }
     const double th = floor(ldexp(Dp, e) * (1.0 + 1e-12));
     e1[q] = e;
-    theta[q] = th >= 4294967294.0 ? 0xFFFFFFFEu : (uint32_t)th;
+    theta[q] = th >= (double)tmax ? tmax : (uint32_t)th;
   }
 }
 
@@ -588,7 +895,13 @@ int run_adc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t 
   PQS_TRY(scratch(ctx, S_QMINMAX, (size_t)nq * 2, &e0));
   e1 = e0 + nq;
   PQS_TRY(scratch(ctx, S_PREFIX, (size_t)nq, &slack));
-  PQS_TRY(scratch(ctx, S_TABLES_T, (size_t)(cdiv(nq, 32) * 32 * m * k), &tt));
+  // the filter pass runs the packed two-queries-per-word kernel (K3p) when the
+  // entries keep >= 9 bits (m <= 64); PQS_OPT_SCAN8_ENGINE = 1 keeps the u16 kernel
+  if (ctx->scan8_engine == 2 && m > P16_MAX_M)
+    return set_err(ctx, PQS_ERR_UNSUPPORTED, "packed scan8 engine takes m <= 64");
+  const bool packed = ctx->scan8_engine != 1 && m <= P16_MAX_M;
+  const int mq = ((m + 3) / 4) * 4;
+  PQS_TRY(scratch(ctx, S_TABLES_T, (size_t)(cdiv(nq, 32) * 32 * (packed ? mq : m) * k), &tt));
   PQS_TRY(scratch(ctx, S_THETA, (size_t)nq, &theta));
   tables_u16_stats_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(d_tables, nq, m, k, off, e0, slack);
   PQS_LAUNCHED(ctx);
@@ -599,8 +912,13 @@ int run_adc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t 
   const int64_t cap = std::min<int64_t>(ctx->cand_cap, n);
   const int64_t r_eff = std::min<int64_t>(r, n);
   if (n <= cap) {
-    fill_u32_kernel<<<(unsigned)cdiv(nq, 256), 256, 0, ctx->stream>>>(theta, nq, 0xFFFFFFFEu);
+    fill_u32_kernel<<<(unsigned)cdiv(nq, 256), 256, 0, ctx->stream>>>(theta, nq, packed ? P16_TMAX : 0xFFFFFFFEu);
     PQS_LAUNCHED(ctx);
+    if (packed) {
+      tables_p16_kernel<<<(unsigned)(cdiv(nq, 32) * mq), TU16_THREADS, 0, ctx->stream>>>(
+          d_tables, off, e0, nq, m, k, P16_TMAX / (uint32_t)m, reinterpret_cast<uint32_t*>(tt));
+      PQS_LAUNCHED(ctx);
+    }
   } else {
     int64_t st = std::max<int64_t>(cdiv(db->ntiles, ctx->sample_div), cdiv(16 * r_eff, TILE8));
     st = std::min<int64_t>(st, db->ntiles);
@@ -621,10 +939,16 @@ int run_adc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t 
     a.out = sample;
     a.ld = ns;
     PQS_TRY(launch_scan8<MODE8_DENSE>(ctx, a));
-    theta8_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(sample, ns, (int)r_eff, m, e0, slack, e1, theta);
+    theta8_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(
+        sample, ns, (int)r_eff, m, e0, slack, e1, theta, packed ? P16_TARGET : 65536.0 * (m > 8 ? m / 8.0 : 1.0),
+        packed ? P16_TMAX : 0xFFFFFFFEu);
     PQS_LAUNCHED(ctx);
     // rebuild the tables at the filter scale e1
-    tables_u16_t_kernel<<<(unsigned)(cdiv(nq, 32) * m), TU16_THREADS, 0, ctx->stream>>>(d_tables, off, e1, nq, m, k, tt);
+    if (packed)
+      tables_p16_kernel<<<(unsigned)(cdiv(nq, 32) * mq), TU16_THREADS, 0, ctx->stream>>>(
+          d_tables, off, e1, nq, m, k, P16_TMAX / (uint32_t)m, reinterpret_cast<uint32_t*>(tt));
+    else
+      tables_u16_t_kernel<<<(unsigned)(cdiv(nq, 32) * m), TU16_THREADS, 0, ctx->stream>>>(d_tables, off, e1, nq, m, k, tt);
     PQS_LAUNCHED(ctx);
   }
 
@@ -633,7 +957,26 @@ int run_adc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t 
   PQS_TRY(scratch(ctx, S_CAND, (size_t)(nq * cap), &cand));
   PQS_TRY(scratch(ctx, S_CAND_CNT, (size_t)nq, &cnt));
   PQS_CUDA(ctx, cudaMemsetAsync(cnt, 0, sizeof(int) * nq, ctx->stream));
-  {
+  if (packed) {
+    Scan8PArgs a{};
+    a.tp = reinterpret_cast<const uint32_t*>(tt);
+    a.codes = db->codes8;
+    a.n = n;
+    a.m = m;
+    a.k = k;
+    a.nq = nq;
+    a.nvt = db->ntiles;
+    a.theta = theta;
+    a.cand = cand;
+    a.cand_cnt = cnt;
+    a.cap = cap;
+    PQS_TRY(scan_timer_begin(ctx));
+    PQS_TRY(launch_scan8p(ctx, a));
+    PQS_TRY(scan_timer_end(ctx));
+    ctx->last_scan_launches = 1;
+    ctx->last_scan_engine = 5;
+    ctx->last_scan_work = (double)nq * (double)n * (double)m;
+  } else {
     Scan8Args a{};
     a.tt = tt;
     a.codes = db->codes8;

@@ -238,9 +238,9 @@ def kmeans_device(x, k: int, iters: int, seed: int, chunk: int = 8192):
 
 
 def assign_device(x, c, chunk: int = 8192):
-    """Nearest centroid per row by ||c||^2 - 2<x, c> with a TF32 GEMM (BASELINE
-    cfg3: "assignment as an fp32/tf32 GEMM"); index build only -- the search's
-    probes use the exact path (pqs_ivf_probe)."""
+    """Nearest centroid per row by ||c||^2 - 2<x, c> with a TF32 GEMM: only the
+    Lloyd iterations of the coarse k-means (training, out of scope) use it;
+    the index build's assignment is the exact `nearest` (pqs_nearest)."""
     import torch
 
     prev = torch.backends.cuda.matmul.allow_tf32
@@ -259,13 +259,17 @@ def assign_device(x, c, chunk: int = 8192):
 def make_ivf_device(name: str, dq_factory, seed: int = 1712, n: int | None = None, K: int | None = None,
                     nq: int | None = None, coarse_iters: int = 8, device="cuda", chunk: int = 1 << 22):
     """cfg3-style IVFADC index built on the GPU:
-    coarse k-means on a device sample, TF32 assignment of every row, residual
+    coarse k-means on a device sample, exact assignment of every row
+    (nearest, _dist.py:24-39 / ivf.py:122: pqs_nearest = tcgen05 tf32 probe
+    GEMM shortlist + fp64 re-score, ties to the lowest index), residual
     PQ trained on the host from a residual sample (ivf.py:120-134 recipe),
     exact residual encode on the device (encode kernel), lists in cell order
     (stable, ids ascending inside a list as build_ivf's flatnonzero).
     Returns (books, coarse CUDA (K, d), list_sizes host (K,), codes CUDA (n, m),
     ids CUDA (n,), host queries)."""
     import torch
+
+    from .engine import nearest
 
     cfg = CONFIGS[name]
     n = cfg["N"] if n is None else n
@@ -278,7 +282,7 @@ def make_ivf_device(name: str, dq_factory, seed: int = 1712, n: int | None = Non
     cells = torch.empty(n, dtype=torch.int64, device=device)
     for a in range(0, n, chunk):
         b = min(n, a + chunk)
-        cells[a:b] = assign_device(device_rows(cfg, seed, a, b, stream=1, device=device), coarse)
+        cells[a:b] = nearest(device_rows(cfg, seed, a, b, stream=1, device=device), coarse)[0]
     # residual PQ from a residual sample (100 * 2^b rows, as build_ivf)
     nt = min(n, 100 * (1 << cfg["b"]))
     xt = device_rows(cfg, seed, 0, nt, stream=1, device=device)

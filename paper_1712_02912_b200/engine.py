@@ -104,6 +104,33 @@ def _host_f32(a, ndim, what):
     return a
 
 
+def nearest(points, centroids, ctx=None):
+    """nearest (_dist.py:24-39), the assignment step of build_ivf (ivf.py:122):
+    per point (index of its nearest centroid, squared distance to it) by the
+    fp64 cdist sum, ties to the lowest index -- pqs_nearest: the tcgen05 tf32
+    probe GEMM's certified shortlist, re-scored exactly in fp64.  points (n, d)
+    float32 / float64, host array or CUDA tensor; centroids (K, d) float32 on
+    the same side.  Returns (idx int64 (n,), dist float64 (n,))."""
+    ctx = ctx or default_context()
+    x, f64 = _queries(points, 2, "points")
+    if _is_device(x):
+        if not _is_device(centroids) or str(centroids.dtype) != "torch.float32" or centroids.dim() != 2:
+            raise ValueError("centroids must be a 2-D float32 CUDA tensor when the points are on the device")
+        c = centroids.contiguous()
+    else:
+        c = np.ascontiguousarray(centroids, dtype=np.float32)
+        if c.ndim != 2:
+            raise ValueError("centroids must be 2-D")
+    if tuple(c.shape)[1] != x.shape[1]:
+        raise ValueError("points and centroids must have the same dimension")
+    n = x.shape[0]
+    idx = _empty((n,), np.int64, x)
+    dist = _empty((n,), np.float64, x)
+    ctx.check(_fn(ctx, "pqs_nearest", f64)(ctx.handle, ptr(c), c.shape[0], c.shape[1], ptr(x), n, ptr(idx),
+                                            ptr(dist), _io(ctx, x, idx)), "nearest")
+    return idx, dist
+
+
 class DeviceQuantizer:
     """pqs_pq: device copy of a ProductQuantizer's codebooks (no rotation)."""
 
