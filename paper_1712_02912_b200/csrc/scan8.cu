@@ -54,6 +54,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -445,6 +448,7 @@ constexpr int CST8P = 8;          // staged candidates per thread and query half
 constexpr int P16_MAX_M = 64;     // clip = floor(32767 / m) >= 511
 constexpr uint32_t P16_TMAX = 32767u;
 constexpr double P16_TARGET = 8191.0;
+constexpr int P16_RUN = 4;        // streamed tables: tiles per run of one query group
 
 // one CTA per (query group, padded component): rows read coalesced, transposed
 // through shared memory, written as 64-byte runs of the packed layout
@@ -513,12 +517,19 @@ __global__ void __launch_bounds__(SCAN8_THREADS, 1) scan8p_kernel(Scan8PArgs a) 
   const uint32_t slot0 = (sb + 65535u) & ~65535u;  // two 64 KB table slots at slot0, slot0 + 64 KB
   unsigned char* slot_ptr = smp + (slot0 - sb);
   // low region [sb, slot0): barriers, code buffers, candidate stage
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smp);  // 0/1: stage buffers, 2: resident tables
+  // stage buffers: NB code buffers (+ the two table slots when the tables
+  // stream).  full[b]: the bulk copies of a stage landed; empty[b]: all W8
+  // warps are done with it (no block-wide barrier per stage: a warp delayed by
+  // its candidate path does not hold the others back)
+  constexpr int NB = RES ? 3 : 2;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smp);
+  uint64_t* empty = full + NB;
+  uint64_t* tabbar = empty + NB;  // resident tables
   const int crows = RES ? nQ * 4 : 4;
   const uint32_t code_bytes = (uint32_t)crows * TILE8;
   uint8_t* code_base = smp + 128;
-  uint32_t* stage = reinterpret_cast<uint32_t*>(code_base + 2 * code_bytes) + threadIdx.x;
-  if (128u + 2u * code_bytes + 2u * CST8P * SCAN8_THREADS * 4u > slot0 - sb) __trap();
+  uint32_t* stage = reinterpret_cast<uint32_t*>(code_base + NB * code_bytes) + threadIdx.x;
+  if (128u + NB * code_bytes + 2u * CST8P * SCAN8_THREADS * 4u > slot0 - sb) __trap();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int h = lane & 15, P = lane >> 4;
@@ -527,62 +538,79 @@ __global__ void __launch_bounds__(SCAN8_THREADS, 1) scan8p_kernel(Scan8PArgs a) 
 #pragma unroll
   for (int b = 0; b < 4; ++b) sel[b] = 0x7604u | ((uint32_t)(b ^ P) << 4);
 
-  // this CTA's balanced range of the linearised (query group, tile) list;
-  // walked with 32-bit (group, tile) cursors
+  // items = (query group, tile) pairs.  Resident tables: a balanced contiguous
+  // range of the group-major list (tables reloaded at a group change only).
+  // Streamed tables (every item streams its quads anyway): runs of P16_RUN
+  // consecutive tiles of one group, runs in tile-major order, CTA i takes runs
+  // i, i + grid, ... -- at any time the CTAs share a few tile blocks, so each
+  // code tile comes from DRAM once and the (small) tables cycle through L2.
+  // Runs of the last tile block are padded with empty items (tile >= nvt).
   const int64_t total = a.nqg * a.nvt;
-  const int64_t w0 = (int64_t)blockIdx.x * total / gridDim.x;
-  const int64_t w1 = (int64_t)(blockIdx.x + 1) * total / gridDim.x;
-  if (w0 >= w1) return;
   const int nch = RES ? 1 : nQ;
-  const int nvt = (int)a.nvt;
-  const int nw = (int)(w1 - w0);
+  const int nvt = (int)a.nvt, nqg = (int)a.nqg;
+  int nw, g0 = 0, t0 = 0;
+  if (RES) {
+    const int64_t w0 = (int64_t)blockIdx.x * total / gridDim.x;
+    const int64_t w1 = (int64_t)(blockIdx.x + 1) * total / gridDim.x;
+    nw = (int)(w1 - w0);
+    g0 = (int)(w0 / a.nvt);
+    t0 = (int)(w0 - (int64_t)g0 * a.nvt);
+  } else {
+    const int64_t nruns = (int64_t)((nvt + P16_RUN - 1) / P16_RUN) * nqg;
+    nw = (int)((nruns - blockIdx.x + gridDim.x - 1) / gridDim.x) * P16_RUN;
+  }
+  if (nw <= 0) return;
   const int S = nw * nch;
-  const int g0 = (int)(w0 / a.nvt), t0 = (int)(w0 - (int64_t)g0 * a.nvt);
+  auto item = [&](int wi, int& qg, int& tile) {  // wi: index into this CTA's items
+    if (RES) {
+      const int lin = t0 + wi;
+      qg = g0 + lin / nvt;
+      tile = lin % nvt;
+    } else {
+      const int64_t rw = (int64_t)blockIdx.x + (int64_t)(wi / P16_RUN) * gridDim.x;
+      const int tb = (int)(rw / nqg);
+      qg = (int)(rw - (int64_t)tb * nqg);
+      tile = tb * P16_RUN + wi % P16_RUN;
+    }
+  };
   const uint32_t quad_bytes = (uint32_t)k * 256u;
 
-  auto issue_at = [&](int b, int wi, int ch) {  // wi: index into this CTA's range
-    const int lin = t0 + wi;
-    const int64_t qg = g0 + lin / nvt;
-    const int64_t tile = lin % nvt;
+  auto issue_at = [&](int b, int wi, int ch) {
+    int qgi, tli;
+    item(wi, qgi, tli);
+    const int64_t qg = qgi, tile = tli;
+    if (!RES && tli >= nvt) {  // padding item: complete the phase with no bytes
+      mbar_expect_tx(&full[b], 0u);
+      return;
+    }
     if (RES) {
-      mbar_expect_tx(&bars[b], (uint32_t)m * TILE8);
-      bulk_g2s(code_base + b * code_bytes, a.codes + tile * m * (int64_t)TILE8, (uint32_t)m * TILE8, &bars[b]);
+      mbar_expect_tx(&full[b], (uint32_t)m * TILE8);
+      bulk_g2s(code_base + b * code_bytes, a.codes + tile * m * (int64_t)TILE8, (uint32_t)m * TILE8, &full[b]);
     } else {
       const int mcur = min(4, m - 4 * ch);
-      mbar_expect_tx(&bars[b], quad_bytes + (uint32_t)mcur * TILE8);
-      bulk_g2s(slot_ptr + b * 65536, a.tp + (qg * nQ + ch) * (int64_t)k * 64, quad_bytes, &bars[b]);
+      mbar_expect_tx(&full[b], quad_bytes + (uint32_t)mcur * TILE8);
+      bulk_g2s(slot_ptr + b * 65536, a.tp + (qg * nQ + ch) * (int64_t)k * 64, quad_bytes, &full[b]);
       bulk_g2s(code_base + b * code_bytes, a.codes + (tile * m + 4 * ch) * (int64_t)TILE8, (uint32_t)mcur * TILE8,
-               &bars[b]);
+               &full[b]);
     }
   };
-  auto next_of = [&](int w, int ch, int steps, int& w2, int& ch2) {
-    ch2 = ch + steps;
-    w2 = w;
-    while (ch2 >= nch) {
-      ch2 -= nch;
-      ++w2;
-    }
-  };
+  auto issue_stage = [&](int st) { issue_at(st % NB, st / nch, st % nch); };
   // code rows of padding components must hold valid codes (their table rows
   // are zero): clear both buffers once, before any bulk copy lands in them
-  for (uint32_t i = threadIdx.x; i < 2 * code_bytes / 16; i += SCAN8_THREADS)
+  for (uint32_t i = threadIdx.x; i < NB * code_bytes / 16; i += SCAN8_THREADS)
     reinterpret_cast<uint4*>(code_base)[i] = make_uint4(0u, 0u, 0u, 0u);
   if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    mbar_init(&bars[2], 1);
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], W8);
+    }
+    mbar_init(tabbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
-  if (threadIdx.x == 0) {
-    issue_at(0, 0, 0);
-    if (S > 1) {
-      int w2, ch2;
-      next_of(0, 0, 1, w2, ch2);
-      issue_at(1, w2, ch2);
-    }
-  }
+  if (threadIdx.x == 0)
+    for (int st = 0; st < NB - 1 && st < S; ++st) issue_stage(st);
 
   int q0 = -1, cur_qg = -1;  // nq < 2^31
   uint32_t thg = 0, vmask = 0, tphase = 0;
@@ -654,26 +682,39 @@ __global__ void __launch_bounds__(SCAN8_THREADS, 1) scan8p_kernel(Scan8PArgs a) 
   uint32_t acc[C8];
 #pragma unroll
   for (int e = 0; e < C8; ++e) acc[e] = 0u;
-  int s = 0, qg = g0, tile = t0;
+  int s = 0;
   for (int w = 0; w < nw; ++w) {
+    int qg, tile;
+    item(w, qg, tile);
     if (qg != cur_qg) {
       switch_group(qg);
       if (RES) {
         __syncthreads();  // every warp is done with the previous group's tables
         if (threadIdx.x == 0) {
-          mbar_expect_tx(&bars[2], (uint32_t)nQ * quad_bytes);
+          mbar_expect_tx(tabbar, (uint32_t)nQ * quad_bytes);
           for (int Q = 0; Q < nQ; ++Q)
-            bulk_g2s(slot_ptr + Q * 65536, a.tp + ((int64_t)qg * nQ + Q) * (int64_t)k * 64, quad_bytes, &bars[2]);
+            bulk_g2s(slot_ptr + Q * 65536, a.tp + ((int64_t)qg * nQ + Q) * (int64_t)k * 64, quad_bytes, tabbar);
         }
-        mbar_wait(&bars[2], tphase);
+        mbar_wait(tabbar, tphase);
         tphase ^= 1;
       }
     }
     for (int ch = 0; ch < nch; ++ch, ++s) {
-      const int b = (int)(s & 1);
-      mbar_wait(&bars[b], (uint32_t)((s >> 1) & 1));
+      const int b = s % NB;
+      // warp 0 keeps NB - 1 stages in flight: stage s + NB - 1 reuses the
+      // buffer of stage s - 1, once every warp has released it
+      if (warp == 0 && s + NB - 1 < S) {
+        if (lane == 0) {
+          if (s >= 1) mbar_wait(&empty[(s - 1) % NB], (uint32_t)(((s - 1) / NB) & 1));
+          issue_stage(s + NB - 1);
+        }
+        __syncwarp();
+      }
+      mbar_wait(&full[b], (uint32_t)((s / NB) & 1));
       const uint8_t* cb = code_base + b * code_bytes + warp * C8 + P * TILE8;
-      if (RES) {
+      if (!RES && tile >= nvt) {
+        // padding item: nothing to scan
+      } else if (RES) {
         for (int Q = 0; Q < nQ; ++Q) {
           const uint32_t B = lb + (uint32_t)Q * 65536u;
           pair_pass(std::integral_constant<int, 0>{}, B, cb + (4 * Q) * TILE8, acc);
@@ -684,19 +725,13 @@ __global__ void __launch_bounds__(SCAN8_THREADS, 1) scan8p_kernel(Scan8PArgs a) 
         pair_pass(std::integral_constant<int, 0>{}, B, cb, acc);
         if (4 * ch + 2 < m) pair_pass(std::integral_constant<int, 1>{}, B, cb + 2 * TILE8, acc);
       }
-      __syncthreads();
-      if (threadIdx.x == 0 && s + 2 < S) {
-        int w2, ch2;
-        next_of(w, ch, 2, w2, ch2);
-        issue_at(b, w2, ch2);
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[b]);
     }
-    emit(acc, (int64_t)tile * TILE8 + warp * C8);
+    if (RES || tile < nvt) {
+      emit(acc, (int64_t)tile * TILE8 + warp * C8);
 #pragma unroll
-    for (int e = 0; e < C8; ++e) acc[e] = 0u;
-    if (++tile == nvt) {
-      tile = 0;
-      ++qg;
+      for (int e = 0; e < C8; ++e) acc[e] = 0u;
     }
   }
   flush(0);

@@ -3,5 +3,5 @@
 # this library's kernels (cold-cache, serialised: use for shares, not absolutes)
 out=$1; shift
 ncu --metrics gpu__time_duration.sum --clock-control none \
-    -k 'regex:cand8|tables_u16|scan4|scan8|select|theta|qadc|tables_exact|bucket|build_b|build_bias|fill_u|gather|ivf|probe|utables|pair_|merge|dense_adc|cnorm|v_kernel' \
+    -k 'regex:cand8|tables_u16|tables_p16|scan4|scan8|select|theta|qadc|tables_exact|bucket|build_b|build_bias|fill_u|gather|ivf|probe|utables|pair_|merge|dense_adc|cnorm|v_kernel' \
     --csv --log-file "$out" python bench.py "$@" > /dev/null 2>&1
