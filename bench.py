@@ -451,6 +451,7 @@ def run_ivf(args):
     torch.cuda.synchronize()
     clocks.start()
     time.sleep(0.3)
+    torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" profiles the steps only
     for s in range(args.steps):
         flush.zero_()
         starts[s].record(stream)
@@ -459,6 +460,7 @@ def run_ivf(args):
         scan_ns.append(ctx.stat(_lib.STAT_LAST_SCAN_NS))
         evals.append(ctx.stat(_lib.STAT_LAST_EVALS))
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     barrier()
     clk = clocks.stop()
     launches = ctx.stat(_lib.STAT_LAUNCHES) - launches0
@@ -526,7 +528,11 @@ def run_ivf(args):
     f_mhz = clk.get("sm_mhz") or 1965.0
     lut_peak = sm_count * 32 * f_mhz * 1e6 / 1e9
     lut_rate = evals_step * m / (scan_ms / 1e3) / 1e9
-    hbm_alg = int(ivf_local_n(ivf)) * (m + 4)  # list-major: every list's codes + V once per launch
+    engine = ctx.stat(_lib.STAT_LAST_SCAN_ENGINE)
+    packed = engine == 6
+    # list-major: every list's codes (+ V for the float scan, + the list's W table for the packed one) once
+    hbm_alg = int(ivf_local_n(ivf)) * (m + (0 if packed else 4)) + (int(coarse.shape[0]) * m * 256 * 4 if packed else 0)
+    lut_bound = (2.0 if packed else 1.0) * lut_peak
     hbm_peak = peaks.get("hbm_gbs", 6553.6)
     line = {
         "metric": metric_name("cfg3"), "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
@@ -548,12 +554,17 @@ def run_ivf(args):
                        "list_scan_slot_utilization": (ctx.stat(_lib.STAT_LAST_EVALS) /
                                                       max(1, ctx.stat(_lib.STAT_LAST_SLOT_EVALS)))},
         "clocks": clk,
-        "roofline": {"bound": "lut", "achieved": lut_rate, "peak": lut_peak, "unit": "Glookup/s",
-                     "frac": lut_rate / lut_peak, "traffic": _ncu_traffic("ivf_list_kernel"),
-                     "traffic_note": "DRAM bytes of one list-scan launch from the committed ncu capture (profiles/r01_ivf_cfg3.md); the excess over the algorithmic bytes is the per-(list, query) staging of the 8 KB query tables",
-                     "kernel": "ivf_list_kernel (list-major, smem LUT)",
+        "roofline": {"bound": "lut", "achieved": lut_rate, "peak": lut_bound, "unit": "Glookup/s",
+                     "frac": lut_rate / lut_bound,
+                     "traffic": _ncu_traffic("ivf_list16_kernel" if packed else "ivf_list_kernel"),
+                     "traffic_note": "DRAM bytes of one list-scan launch from the committed ncu capture (profiles/)",
+                     "kernel": ("ivf_list16_kernel (list-major, packed two-query words, tables built per (list, 16 queries))"
+                                if packed else "ivf_list_kernel (list-major, smem LUT)"),
                      "per_unit": f"{m} table lookups per probed (query, code); {evals_step:.3e} per launch",
-                     "peak_source": f"shared-memory LUT rate {sm_count} SM x 32 lookups/clk x {f_mhz:.0f} MHz",
+                     "peak_source": (f"shared-memory wavefront rate {sm_count} SM x 64 lookups/clk (two queries per "
+                                     f"32-bit word) x {f_mhz:.0f} MHz" if packed else
+                                     f"shared-memory LUT rate {sm_count} SM x 32 lookups/clk x {f_mhz:.0f} MHz"),
+                     "north_star_lut_frac": lut_rate / lut_peak,
                      "hbm": {"algorithmic_bytes": hbm_alg, "achieved_GBs": hbm_alg / (scan_ms / 1e3) / 1e9,
                              "peak_GBs": hbm_peak, "frac": hbm_alg / (scan_ms / 1e3) / 1e9 / hbm_peak},
                      "kernel_ms": scan_ms, "share_of_step": scan_ms / ms_per_step},
@@ -669,12 +680,15 @@ def main():
     clocks.start()
     time.sleep(0.3)
     if world == 1:
+        torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" profiles the steps only
         for s in range(args.steps):
             flush.zero_()
             starts[s].record(stream)
             step_device()
             ends[s].record(stream)
             scan_ns.append(ctx.stat(_lib.STAT_LAST_SCAN_NS))
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_pop()
     else:
         # N > 1: the exchange + merge of step s overlaps the scan of step s+1
         # (ShardedSearch.search_stream); the K steps are timed as one region
@@ -800,6 +814,21 @@ def main():
                                 f"({work:.3e} ops per launch)",
                     "peak_source": peak_source,
                     "lut_equivalent": lut, "hbm": hbm, "kernel_ms": scan_ms, "share_of_step": scan_ms / ms_per_step}
+    elif engine == 5:
+        # packed float filter: one 32-bit word carries two queries' entries, so a
+        # conflict-free LDS.32 is 64 lookups per 128-byte wavefront: the bound is
+        # the shared-memory wavefront rate (1 / clk / SM) x 64, twice the
+        # north-star LUT rate (kept beside it)
+        roofline = {"bound": "lut", "achieved": lut_rate, "peak": 2.0 * lut_peak, "unit": "Glookup/s",
+                    "frac": lut_rate / (2.0 * lut_peak),
+                    "per_unit": lut["per_unit"],
+                    "peak_source": f"shared-memory wavefront rate {sm_count} SM x 1 wavefront/clk x 64 lookups "
+                                   f"(two queries per 32-bit word) x {f_mhz:.0f} MHz",
+                    "north_star_lut": lut,
+                    "traffic": traffic_db.get("scan8p_kernel_" + args.config, {}).get("bytes"),
+                    "traffic_note": "DRAM bytes of one filter launch from the committed ncu capture (profiles/r02_scan8p_*.md)",
+                    "kernel": "scan8p_kernel (packed two-query words, PRMT-formed addresses, smem LUT)",
+                    "hbm": hbm, "kernel_ms": scan_ms, "share_of_step": scan_ms / ms_per_step}
     else:
         roofline = {"bound": "lut", **lut, "traffic": None,
                     "kernel": {1: "scan4_kernel<16,FILTER> (PRMT register LUT)", 3: "scan8_kernel (smem LUT)"}.get(

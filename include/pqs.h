@@ -66,7 +66,8 @@ enum pqs_option {
   PQS_OPT_FORCE_FALLBACK = 3,/* 1: run the exact dense fallback for every query (testing) */
   PQS_OPT_SCAN4_ENGINE = 4, /* Quick ADC scan: 0 auto (tcgen05 int8 when possible), 1 PRMT, 2 tcgen05 */
   PQS_OPT_TC_CHUNK_TILES = 5,/* tcgen05 scan: cap on 128-code tiles per launch (0 = automatic; testing) */
-  PQS_OPT_SCAN8_ENGINE = 6  /* float ADC filter: 0 auto (packed two-query words when m <= 64), 1 u16 lane=query, 2 packed */
+  PQS_OPT_SCAN8_ENGINE = 6, /* float ADC filter: 0 auto (packed two-query words when m <= 64), 1 u16 lane=query, 2 packed */
+  PQS_OPT_IVF_ENGINE = 7    /* IVF 'adc' list scan: 0 auto (packed integer pre-filter when m = 8, k = 256), 1 float, 2 packed */
 };
 
 enum pqs_stat {
@@ -77,7 +78,7 @@ enum pqs_stat {
   PQS_STAT_LAST_SCAN_NS = 5,   /* device time of the last search's main scan kernel (CUDA events) */
   PQS_STAT_LAST_SCAN_LAUNCHES = 6, /* launches of that kernel in the last search */
   PQS_STAT_LAST_CAND_TOTAL = 7,    /* sum over queries of the candidates of the last search */
-  PQS_STAT_LAST_SCAN_ENGINE = 8,   /* 1 PRMT scan4, 2 tcgen05 scan4, 3 scan8 (u16), 4 IVF list scan, 5 scan8 packed */
+  PQS_STAT_LAST_SCAN_ENGINE = 8,   /* 1 PRMT scan4, 2 tcgen05 scan4, 3 scan8 (u16), 4 IVF list scan (float), 5 scan8 packed, 6 IVF list scan (packed) */
   PQS_STAT_LAST_SCAN_WORK = 9,     /* work units of that kernel: tcgen05 -> int8 MMA ops; others -> table lookups */
   PQS_STAT_LAST_RERANK_TOTAL = 10, /* float / IVF: candidates re-scored exactly after the bound tightening (sum over queries) */
   PQS_STAT_LAST_SLOT_EVALS = 11    /* IVF list scan: (slot, code) evaluations incl. idle slots of partly filled 8-query groups */

@@ -30,6 +30,7 @@ OPT_FORCE_FALLBACK = 3
 OPT_SCAN4_ENGINE = 4
 OPT_TC_CHUNK_TILES = 5
 OPT_SCAN8_ENGINE = 6
+OPT_IVF_ENGINE = 7
 STAT_LAUNCHES = 1
 STAT_LAST_MAX_CAND = 2
 STAT_LAST_OVERFLOW = 3

@@ -255,6 +255,10 @@ int pqs_ctx_set_option(pqs_ctx* ctx, int option, int64_t value) {
       PQS_CHECK(ctx, value >= 0 && value <= 2, "scan8 engine must be 0, 1 or 2");
       ctx->scan8_engine = (int)value;
       return PQS_OK;
+    case PQS_OPT_IVF_ENGINE:
+      PQS_CHECK(ctx, value >= 0 && value <= 2, "ivf engine must be 0, 1 or 2");
+      ctx->ivf_engine = (int)value;
+      return PQS_OK;
     case PQS_OPT_TC_CHUNK_TILES:
       PQS_CHECK(ctx, value >= 0, "chunk must be >= 0");
       ctx->tc_chunk_tiles = value;

@@ -28,6 +28,7 @@
 
 #include "pqs_common.cuh"
 #include "select_dev.cuh"
+#include "tc_common.cuh"
 
 namespace {
 
@@ -328,7 +329,7 @@ __global__ void scan_kernel(const int* __restrict__ in, int64_t K, int64_t* __re
 
 __global__ void pair_fill_kernel(const int64_t* __restrict__ cells, const double* __restrict__ pdist, int64_t nq, int ma,
                                  const int64_t* __restrict__ starts, int* __restrict__ fill, int* __restrict__ pq,
-                                 float* __restrict__ pa) {
+                                 float* __restrict__ pa, int* __restrict__ pcell) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nq * ma) return;
   const int64_t c = cells[i];
@@ -337,6 +338,7 @@ __global__ void pair_fill_kernel(const int64_t* __restrict__ cells, const double
   const int64_t o = starts[c] + slot;
   pq[o] = (int)(i / ma);
   pa[o] = (float)pdist[i];
+  pcell[o] = (int)c;
 }
 
 // One CTA per inverted list (two resident per SM); the queries probing it are
@@ -376,6 +378,11 @@ __device__ __forceinline__ void cp_async4_stream(void* smem, const void* gmem, u
                : "memory");
 }
 
+__device__ __forceinline__ uint32_t prmt_b(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
 __device__ __forceinline__ float2 lds_f32x2(uint32_t addr) {
   float2 v;
   asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
@@ -567,6 +574,481 @@ __global__ void __launch_bounds__(LIST_THREADS, 2) ivf_list_kernel(
 }
 
 
+
+// ------------------------------------------------------------------ K8p
+// Packed list scan (m = 8, k = 256): an integer version of the list-major
+// scan with two queries per table word, as in scan8.cu (K3p).  Per (list c,
+// pass of 8 probing queries) the CTA builds the residual tables of the pass
+// in shared memory,
+//   T[j][e] = U_q[j][e] + W_c[j][e] + a_qj        (a_qj = ||q_j - c_j||^2)
+//           = ||(q - c)_j - C_j[e]||^2 >= 0       (W_c[j][e] = 2 <c_j, C_j[e]>)
+// -- no cancellation is left for the scan (the entries are true sub-space
+// distances), so they quantise to 12-bit integers t' = min(4095, floor(s_q T))
+// at a per-query power-of-two scale s_q that puts the query's threshold near
+// 4080.  Word (e, j, h) = t'(slot h) | t'(slot h + 4) << 16 sits at byte
+// e * 256 + par * 128 + j * 16 + h * 4 (par = pass parity: the two halves of a
+// 256-byte row hold alternate passes), so one PRMT builds the offset (code
+// byte into byte 1).  An octet of lanes (4 lanes x 2 slots) evaluates one
+// code; the eight octets of a warp walk the components in rotated order
+// (component (t + o) mod 8 at step t): one warp-wide LDS.32 reads eight
+// disjoint 4-bank windows -- conflict-free, 64 lookups per wavefront, and a
+// pass of 8 slots wastes no lanes on lists probed by few queries.
+// Every code with L <= Tint_q becomes a candidate with the filter distance
+// L / s_q, certified within aerr2_q of the reference distance (see
+// ivf_qparams_kernel): the scan reads no per-code V, no fp32 tables and
+// needs no fp32 re-filter.
+constexpr int L8_Q = 8;
+constexpr int L8_CH = 3072;    // codes per staged chunk
+constexpr uint32_t L8_CLIP = 4095u;
+constexpr double L8_TARGET = 4080.0;
+
+// W[c][e * m + j] = 2 <c_j, C_j[e]> (fp64 -> fp32) and max |W|
+__global__ void ivf_w_kernel(const float* __restrict__ coarse, const float* __restrict__ books, int m, int k, int dsub,
+                             float* __restrict__ W, float* __restrict__ wmax) {
+  const int64_t c = blockIdx.x;
+  const int d = m * dsub;
+  float mx = 0.f;
+  for (int i = threadIdx.x; i < m * k; i += blockDim.x) {
+    const int e = i / m, j = i - e * m;
+    const float* cb = books + ((int64_t)j * k + e) * dsub;
+    const float* g = coarse + c * d + j * dsub;
+    double s = 0.0;
+    for (int t = 0; t < dsub; ++t) s += (double)g[t] * (double)cb[t];
+    const float w = (float)(2.0 * s);
+    W[c * (int64_t)m * k + i] = w;
+    mx = fmaxf(mx, fabsf(w));
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(reinterpret_cast<int*>(wmax), __float_as_int(mx));
+}
+
+// Per query: scale s_q = 2^e, integer threshold Tint_q and the certified error
+// aerr2_q of the packed scan's filter distance L / s_q.
+//  * theta_q >= (r-th smallest reference distance d_ref over the probed lists)
+//    + aerr_q (ivf_theta_kernel), so every code the search can return has
+//    D <= theta' = (theta + aerr)(1 + 4u): D is the exact sum of the exact
+//    sub-space distances, d_ref the sum of their float32 roundings.
+//  * one table entry: T32 = fl(fl(U32 + W32) + a32) with |U32 - U| <= u |U|,
+//    |W32 - W| <= u |W|, |a32 - a| <= u a, so |T32 - T| <= epsT = 1.5 x 3u
+//    (usum + wmax + amax) (|U| <= usum = sum_j max_e |U|, a <= max probe
+//    distance).  The builder stores t' with  s max(T32, 0) - 2 < t' <=
+//    s max(T32, 0)  unless it clips at 4095 (floor, minus one more on a
+//    round-to-even tie of the magic-number conversion).
+//  * hence  L <= s (D + m epsT)  for every code, and  s D <= L + 2 m + s m
+//    epsT  for every code without a clipped entry.  Tint = floor(s theta') +
+//    m + 2 < 4095 keeps every returnable code and rejects every clipped one,
+//    so all candidates obey |L / s - d_ref| <= aerr2 = 2 m / s + m epsT + 4u
+//    theta'.
+// theta = +inf (sample shorter than r): s = 0 -- every probed code is kept.
+__global__ void ivf_qparams_kernel(const float* __restrict__ U, const double* __restrict__ pdist,
+                                   const float* __restrict__ theta, const float* __restrict__ aerr,
+                                   const float* __restrict__ wmax, int64_t nq, int ma, int m, int k,
+                                   float* __restrict__ qscale, uint32_t* __restrict__ qtint,
+                                   float* __restrict__ aerr2) {
+  const int64_t q = blockIdx.x;
+  __shared__ double part[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double s = 0.0;
+  for (int j = warp; j < m; j += nw) {
+    float mx = 0.f;
+    for (int i = lane; i < k; i += 32) mx = fmaxf(mx, fabsf(U[(q * k + i) * (int64_t)m + j]));
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    s += (double)mx;
+  }
+  if (lane == 0) part[warp] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double usum = 0.0;
+    for (int i = 0; i < nw; ++i) usum += part[i];
+    double amax = 0.0;
+    for (int p = 0; p < ma; ++p) amax = fmax(amax, pdist[q * ma + p]);
+    const double u = 5.9604644775390625e-08;
+    const double epsT = 1.5 * u * 3.0 * (usum + (double)wmax[0] + amax);
+    const float th = theta[q];
+    if (!(th < __int_as_float(0x7f800000))) {
+      qscale[q] = 0.f;
+      qtint[q] = L8_CLIP - 1u;
+      aerr2[q] = __int_as_float(0x7f800000);
+    } else {
+      const double tp = ((double)th + (double)aerr[q]) * (1.0 + 4.0 * u) + (double)m * epsT;
+      int e = 0;
+      if (tp > 0.0) e = (int)floor(log2(L8_TARGET / tp));
+      e = max(-100, min(100, e));
+      qscale[q] = (float)ldexp(1.0, e);
+      const double t = (tp > 0.0 ? floor(ldexp(tp, e)) : 0.0) + (double)m + 2.0;
+      qtint[q] = t >= (double)(L8_CLIP - 1u) ? L8_CLIP - 1u : (uint32_t)t;
+      const double a2 = ldexp(2.0 * (double)m, -e) + (double)m * epsT + 4.0 * u * tp;
+      float f = (float)a2;
+      if ((double)f < a2) f = nextafterf(f, __int_as_float(0x7f800000));
+      aerr2[q] = f;
+    }
+  }
+}
+
+// Per (query, probe) pair in list order: the query's scale and threshold and
+// the scaled sub-space terms a_qj * s_q of the pair (fp64 -> fp32)
+__global__ void ivf_pair_params_kernel(const int* __restrict__ pq, const int* __restrict__ pcell,
+                                       const int64_t* __restrict__ npairs_p, QVec queries, const float* __restrict__ coarse, int d, int dsub,
+                                       const float* __restrict__ qscale, const uint32_t* __restrict__ qtint,
+                                       float* __restrict__ ps, uint32_t* __restrict__ pt, float* __restrict__ pas) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t g = i >> 3;
+  const int j = (int)(i & 7);
+  if (g >= *npairs_p) return;  // pairs of cells this index does not hold (-1) are not in the lists
+  const int q = pq[g];
+  const float sc = qscale[q];
+  const float* c = coarse + (int64_t)pcell[g] * d + j * dsub;
+  const int64_t qo = (int64_t)q * d + j * dsub;
+  double acc = 0.0;
+  for (int t = 0; t < dsub; ++t) {
+    const double df = queries.at(qo + t) - (double)c[t];
+    acc += df * df;
+  }
+  pas[i] = (float)acc * sc;
+  if (j == 0) {
+    ps[g] = sc;
+    pt[g] = qtint[q];
+  }
+}
+
+// one descriptor per list in scan order: the producer warps prefetch it
+struct ListDesc {
+  int c;          // cell
+  int np;         // probing pairs
+  int64_t p0;     // first pair
+  int64_t b;      // first code
+  int64_t n;      // codes
+};
+__global__ void ivf_desc_kernel(const int* __restrict__ order, const int64_t* __restrict__ starts,
+                                const int64_t* __restrict__ offsets, int64_t K, ListDesc* __restrict__ desc) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= K) return;
+  const int64_t c = order ? order[i] : i;
+  ListDesc d;
+  d.c = (int)c;
+  d.p0 = starts[c];
+  d.np = (int)(starts[c + 1] - starts[c]);
+  d.b = offsets[c];
+  d.n = offsets[c + 1] - offsets[c];
+  desc[i] = d;
+}
+
+struct List8Args {
+  const float* U;         // [nq][k * m] (entry-major, component fastest)
+  const float* W;         // [K][k * m]
+  const ListDesc* desc;   // (K,) lists in scan order
+  int64_t K;
+  const int* pq;          // pair -> query
+  const float* ps;        // pair -> scale
+  const uint32_t* pt;     // pair -> integer threshold
+  const float* pas;       // pair -> a_qj * s_q (8 per pair)
+  const uint8_t* codes;   // (n, 8) row-major, list order
+  uint64_t* cand;         // per query: list << 32 | position
+  float* cand_apx;        // per query: L / s_q
+  int* cand_cnt;
+  int64_t cap;
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem)
+               : "memory");
+}
+
+// Persistent, warp-specialised: L8_PW producer warps fetch the list
+// descriptors (CTA i takes lists i, i + grid, ... of the scan order, the next
+// descriptor / W table / pass parameters prefetched in registers), stage the
+// code chunks (cp.async) and build the packed tables of pass p + 1 while
+// L8_CW consumer warps scan pass p.  Stages (one code chunk each, two
+// buffers) and the two table halves are handed over with full / empty
+// mbarriers; the candidate path is per consumer warp (own stage, no block
+// barrier anywhere in the steady state).
+constexpr int L8_PW = 8, L8_CW = 16;
+constexpr int L8_PT = L8_PW * 32;
+constexpr int L8_THREADS = (L8_PW + L8_CW) * 32;
+constexpr int L8_WST = 96;     // staged candidates per consumer warp
+
+struct L8Stage {   // what the consumers need to scan one chunk
+  int nc;          // codes in the chunk; < 0: no more work
+  uint32_t loff0;  // list offset of its first code
+  int par;         // table half
+  int last;        // last chunk of the pass: flush, release the table half
+  int ns;          // live slots
+  int c;           // cell
+  int64_t b;       // list base position
+  int q[L8_Q];
+  float inv[L8_Q];
+  uint32_t t[L8_Q];
+};
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+__global__ void __launch_bounds__(L8_THREADS, 1) ivf_list8_kernel(List8Args a) {
+  constexpr int M = 8, KK = 256, MK = M * KK;
+  extern __shared__ __align__(256) unsigned char l8[];
+  // the 64 KB table slot sits at a 64 KB-aligned shared-window address, so a
+  // lookup address is one PRMT of the code byte into byte 1 of the lane's
+  // base (no add); the code chunks and candidate stages fill the region
+  // below it, the list table the region above
+  const uint32_t sb = (uint32_t)__cvta_generic_to_shared(l8);
+  const uint32_t slot_w = (sb + 65535u) & ~65535u;  // window address of the slot
+  unsigned char* slot = l8 + (slot_w - sb);                              // 64 KB: packed tables, two interleaved halves
+  float* sW = reinterpret_cast<float*>(slot + 65536);                    // [MK] list table (producers only)
+  uint2* scode = reinterpret_cast<uint2*>(l8);                           // [2][L8_CH] code rows
+  uint64_t* wst = reinterpret_cast<uint64_t*>(scode + 2 * L8_CH);        // [L8_CW][L8_WST] candidate records
+  if (2u * L8_CH * 8u + L8_CW * L8_WST * 8u > slot_w - sb) __trap();
+  __shared__ L8Stage sinfo[2];
+  __shared__ __align__(8) uint64_t st_full[2], st_empty[2], tab_empty[2];
+  __shared__ int pp_q[L8_Q], s_wcnt[L8_CW];
+  __shared__ float pp_s[L8_Q], pp_as[L8_Q][M];
+  __shared__ uint32_t pp_t[L8_Q];
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&st_full[i], 1);
+      tc::mbar_init(&st_empty[i], L8_CW);
+      tc::mbar_init(&tab_empty[i], L8_CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp < L8_PW) {
+    // =============================== producers ===============================
+    const int ptid = threadIdx.x;
+    const int bj = lane & 7, be = lane >> 3;
+    int sidx = 0, pc = 0;  // stage and pass counters (buffer = & 1)
+    // registers holding the next list's descriptor and W slice
+    ListDesc nd;
+    float wreg[MK / L8_PT];
+    int64_t li = blockIdx.x;
+    auto fetch_list = [&](int64_t l) {
+      if (l < a.K) {
+        nd = a.desc[l];
+        if (nd.np > 0 && nd.n > 0) {
+#pragma unroll
+          for (int i = 0; i < MK / L8_PT; ++i) wreg[i] = __ldg(a.W + (int64_t)nd.c * MK + ptid + i * L8_PT);
+        }
+      }
+    };
+    fetch_list(li);
+    for (; li < a.K; li += gridDim.x) {
+      const ListDesc d = nd;
+      const bool live = d.np > 0 && d.n > 0;
+      if (live) {
+        named_bar_sync(1, L8_PT);  // the previous list's builds are done with sW
+#pragma unroll
+        for (int i = 0; i < MK / L8_PT; ++i) sW[ptid + i * L8_PT] = wreg[i];
+      }
+      fetch_list(li + gridDim.x);  // in flight during this list
+      if (!live) continue;
+      // pass parameters: thread t < 8 -> (q, s, tint) of slot t; threads 32..95 -> a_qj * s_q
+      int rq = 0;
+      float rs = 0.f, ras = 0.f;
+      uint32_t rt = 0;
+      auto fetch_pass = [&](int g0, int ns) {
+        if (ptid < L8_Q) {
+          const bool ok = ptid < ns;
+          rq = ok ? a.pq[d.p0 + g0 + ptid] : 0;
+          rs = ok ? a.ps[d.p0 + g0 + ptid] : 0.f;
+          rt = ok ? a.pt[d.p0 + g0 + ptid] : 0u;
+        } else if (ptid >= 32 && ptid < 32 + L8_Q * M) {
+          const int t = ptid - 32;
+          ras = (t >> 3) < ns ? a.pas[(d.p0 + g0) * M + t] : 0.f;
+        }
+      };
+      fetch_pass(0, min(L8_Q, d.np));
+      for (int g0 = 0; g0 < d.np; g0 += L8_Q, ++pc) {
+        const int ns = min(L8_Q, d.np - g0);
+        const int par = pc & 1;
+        named_bar_sync(1, L8_PT);  // previous pass's build has read pp_*, sW is written
+        if (ptid < L8_Q) {
+          pp_q[ptid] = rq;
+          pp_s[ptid] = rs;
+          pp_t[ptid] = rt;
+        } else if (ptid >= 32 && ptid < 32 + L8_Q * M) {
+          pp_as[(ptid - 32) >> 3][(ptid - 32) & 7] = ras;
+        }
+        named_bar_sync(1, L8_PT);
+        if (g0 + L8_Q < d.np) fetch_pass(g0 + L8_Q, min(L8_Q, d.np - g0 - L8_Q));  // next pass, in flight
+        bool built = false;
+        for (int64_t cb = 0; cb < d.n; cb += L8_CH, ++sidx) {
+          const int nc = (int)min((int64_t)L8_CH, d.n - cb);
+          const int buf = sidx & 1;
+          tc::mbar_wait(&st_empty[buf], (uint32_t)(((sidx >> 1) & 1) ^ 1));
+          {
+            const uint2* src = reinterpret_cast<const uint2*>(a.codes) + d.b + cb;
+            uint2* dst = scode + buf * L8_CH;
+            for (int i = ptid; i < nc; i += L8_PT) cp_async8(dst + i, src + i);
+          }
+          if (!built) {
+            built = true;
+            tc::mbar_wait(&tab_empty[par], (uint32_t)(((pc >> 1) & 1) ^ 1));
+            // ---- table build: 8 coalesced loads (one per slot), 4 packed words, one STS.128
+            float as[L8_Q], sc[L8_Q];
+            uint32_t up[L8_Q];  // word offsets into U (nq * 2048 < 2^32, checked by the launcher)
+#pragma unroll
+            for (int i = 0; i < L8_Q; ++i) {
+              as[i] = pp_as[i][bj];
+              sc[i] = pp_s[i];
+              up[i] = (uint32_t)pp_q[i] * (uint32_t)MK + (uint32_t)bj;
+            }
+#pragma unroll 2
+            for (int e0 = warp * 4 + be; e0 < KK; e0 += 4 * L8_PW) {
+              const float wv = sW[e0 * M + bj];
+              float uv[L8_Q];
+#pragma unroll
+              for (int i = 0; i < L8_Q; ++i) uv[i] = __ldg(a.U + (up[i] + (uint32_t)(e0 * M)));
+              uint32_t tq[L8_Q];
+#pragma unroll
+              for (int i = 0; i < L8_Q; ++i) {
+                float x = fmaf(uv[i] + wv, sc[i], as[i]);
+                x = fminf(fmaxf(x, 0.5f), (float)L8_CLIP + 0.5f);
+                tq[i] = __float_as_uint(x + 8388607.5f) & 0xFFFFu;  // floor(x), or floor(x) - 1 on a rounding tie
+              }
+              uint4 w4;
+              w4.x = tq[0] | (tq[4] << 16);
+              w4.y = tq[1] | (tq[5] << 16);
+              w4.z = tq[2] | (tq[6] << 16);
+              w4.w = tq[3] | (tq[7] << 16);
+              *reinterpret_cast<uint4*>(slot + e0 * 256 + par * 128 + bj * 16) = w4;
+            }
+          }
+          cp_async_wait_all();
+          if (ptid == 0) {
+            L8Stage& si = sinfo[buf];
+            si.nc = nc;
+            si.loff0 = (uint32_t)cb;
+            si.par = par;
+            si.last = cb + L8_CH >= d.n ? 1 : 0;
+            si.ns = ns;
+            si.c = d.c;
+            si.b = d.b;
+          }
+          if (ptid < L8_Q) {
+            L8Stage& si = sinfo[buf];
+            si.q[ptid] = pp_q[ptid];
+            si.inv[ptid] = pp_s[ptid] > 0.f ? 1.0f / pp_s[ptid] : 0.f;  // exact: a power of two
+            si.t[ptid] = pp_t[ptid];
+          }
+          named_bar_sync(1, L8_PT);  // tables, codes and the stage record are written
+          if (ptid == 0) tc::mbar_arrive(&st_full[buf]);
+        }
+      }
+    }
+    // no more work
+    {
+      const int buf = sidx & 1;
+      tc::mbar_wait(&st_empty[buf], (uint32_t)(((sidx >> 1) & 1) ^ 1));
+      if (ptid == 0) {
+        sinfo[buf].nc = -1;
+        tc::mbar_arrive(&st_full[buf]);
+      }
+    }
+  } else {
+    // =============================== consumers ===============================
+    const int cw = warp - L8_PW;
+    const int o = lane >> 2, h = lane & 3;
+    const int rsh = 8 * (o & 3);
+    const bool rswap = (o & 4) != 0;
+    uint64_t* mst = wst + cw * L8_WST;  // this warp's candidate stage
+    int* mcnt = &s_wcnt[cw];            // its fill count (shared atomics of the hitting lanes)
+    if (lane == 0) *mcnt = 0;
+    __syncwarp();
+    for (int sidx = 0;; ++sidx) {
+      const int buf = sidx & 1;
+      tc::mbar_wait(&st_full[buf], (uint32_t)((sidx >> 1) & 1));
+      const L8Stage& si = sinfo[buf];
+      const int nc = si.nc;
+      if (nc < 0) break;
+      const int ns = si.ns;
+      const uint32_t par = (uint32_t)si.par * 128u;
+      const bool v0 = h < ns, v1 = h + 4 < ns;
+      const uint32_t thg = (v0 ? si.t[h] : 0u) | ((v1 ? si.t[h + 4] : 0u) << 16) | 0x80008000u;
+      const uint32_t vmask = (v0 ? 0x8000u : 0u) | (v1 ? 0x80000000u : 0u);
+      const uint32_t loff0 = si.loff0;
+      // candidate record (list offset | L << 32 | slot << 48) -> the query's list
+      auto append = [&](uint64_t rcd) {
+        const int sl = (int)(rcd >> 48);
+        const int qs = si.q[sl];
+        const int gp = atomicAdd(a.cand_cnt + qs, 1);
+        if (gp < a.cap) {
+          a.cand[(int64_t)qs * a.cap + gp] = ((uint64_t)(uint32_t)si.c << 32) | (uint64_t)(uint32_t)(si.b + (uint32_t)rcd);
+          a.cand_apx[(int64_t)qs * a.cap + gp] = (float)((uint32_t)(rcd >> 32) & 0x7FFFu) * si.inv[sl];
+        }
+      };
+      auto flush = [&]() {
+        __syncwarp();
+        const int n = min(*reinterpret_cast<volatile int*>(mcnt), L8_WST);
+        for (int i = lane; i < n; i += 32) {
+          const uint64_t rcd = mst[i];
+          if (rcd != ~0ull) append(rcd);
+        }
+        __syncwarp();
+        if (lane == 0) *mcnt = 0;
+        __syncwarp();
+      };
+      uint32_t lbase[M];
+#pragma unroll
+      for (int t = 0; t < M; ++t) lbase[t] = slot_w + par + (uint32_t)(((t + o) & 7) * 16 + h * 4);
+      const uint2* sc = scode + buf * L8_CH;
+      // four codes per lane and step: 4 code rows and 32 lookups in flight
+      constexpr int ILP = 4, STEP = 8 * L8_CW;
+      for (int ib = cw * 8; ib < nc; ib += ILP * STEP) {  // warp-uniform trip count
+        const int i0 = ib + o;
+        if (*reinterpret_cast<volatile int*>(mcnt) > L8_WST / 2) flush();  // warp-uniform: only this warp changes it
+        uint32_t acc[ILP];
+        uint2 cwd[ILP];
+#pragma unroll
+        for (int u = 0; u < ILP; ++u) cwd[u] = sc[min(i0 + u * STEP, nc - 1)];
+#pragma unroll
+        for (int u = 0; u < ILP; ++u) {
+          const uint32_t x = rswap ? cwd[u].y : cwd[u].x, y = rswap ? cwd[u].x : cwd[u].y;
+          const uint32_t r0 = __funnelshift_r(x, y, rsh), r1 = __funnelshift_r(y, x, rsh);
+          uint32_t s = 0u;
+#pragma unroll
+          for (int t = 0; t < M; ++t) {
+            uint32_t v;
+            asm volatile("ld.shared.u32 %0, [%1];"
+                         : "=r"(v)
+                         : "r"(prmt_b(t < 4 ? r0 : r1, lbase[t], 0x7604u | ((uint32_t)(t & 3) << 4))));
+            s += v;
+          }
+          acc[u] = s;
+        }
+#pragma unroll
+        for (int u = 0; u < ILP; ++u) {
+          const int i = i0 + u * STEP;
+          const uint32_t hit = i < nc ? (thg - acc[u]) & vmask : 0u;
+          if (hit) {  // rare per lane; kept tiny
+            const uint32_t two = hit & (hit << 16);
+            const int sp = atomicAdd(mcnt, two ? 2 : 1);
+            const uint32_t loff = loff0 + (uint32_t)i;
+            const uint32_t m0 = (acc[u] & 0x7FFFu) | ((uint32_t)h << 16);              // L | slot << 16
+            const uint32_t m1 = ((acc[u] >> 16) & 0x7FFFu) | ((uint32_t)(h + 4) << 16);
+            uint2* m2 = reinterpret_cast<uint2*>(mst);
+            if (sp + 2 <= L8_WST) {
+              m2[sp] = make_uint2(loff, (hit & 0x8000u) ? m0 : m1);
+              if (two) m2[sp + 1] = make_uint2(loff, m1);
+            } else {  // stage full: direct append (a skipped last slot is marked)
+              if (sp == L8_WST - 1) mst[sp] = ~0ull;
+              if (hit & 0x8000u) append((uint64_t)loff | ((uint64_t)m0 << 32));
+              if (hit & 0x80000000u) append((uint64_t)loff | ((uint64_t)m1 << 32));
+            }
+          }
+        }
+      }
+      if (si.last) {
+        flush();  // reads the stage record: before the release below
+        if (lane == 0) tc::mbar_arrive(&tab_empty[si.par]);
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&st_empty[buf]);
+    }
+  }
+}
 
 // After the list scan: every probed code with filter distance <= theta is a
 // candidate, and theta >= the r-th smallest filter distance, so the r-th
@@ -797,6 +1279,20 @@ int ivf_create_impl(pqs_ctx* ctx, const pqs_pq* pq, const float* coarse, int64_t
   v_kernel<<<(unsigned)K, 256, 0, ctx->stream>>>(iv->coarse, iv->books, iv->offsets, iv->codes, iv->m, iv->k, iv->dsub,
                                                  d, iv->vtab, iv->vmax);
   PQS_LAUNCHED(ctx);
+  // W tables of the packed list scan (m = 8, k = 256): K x 8 KB
+  static const int use_w = getenv("PQS_IVF_W") ? atoi(getenv("PQS_IVF_W")) : 1;
+  if (use_w && iv->m == 8 && iv->k == 256) {
+    if (cudaMalloc(&iv->wtab, (size_t)K * iv->m * iv->k * 4) == cudaSuccess && cudaMalloc(&iv->wmax, 16) == cudaSuccess) {
+      PQS_CUDA(ctx, cudaMemsetAsync(iv->wmax, 0, 16, ctx->stream));
+      ivf_w_kernel<<<(unsigned)K, 256, 0, ctx->stream>>>(iv->coarse, iv->books, iv->m, iv->k, iv->dsub, iv->wtab,
+                                                        iv->wmax);
+      PQS_LAUNCHED(ctx);
+    } else {  // no room: the float list scan needs no W
+      cudaGetLastError();
+      if (iv->wtab) cudaFree(iv->wtab);
+      iv->wtab = nullptr;
+    }
+  }
   PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   // list scan order: cells grouped by their nearest of P = sqrt(K) pivot cells
   // (PQS_LIST_ORDER=0 keeps cell order)
@@ -877,6 +1373,8 @@ void ivf_destroy_impl(pqs_ivf* iv) {
   cudaFree(iv->vtab);
   cudaFree(iv->vmax);
   if (iv->list_order) cudaFree(iv->list_order);
+  if (iv->wtab) cudaFree(iv->wtab);
+  if (iv->wmax) cudaFree(iv->wmax);
   if (iv->probe_b) cudaFree(iv->probe_b);
   delete iv;
 }
@@ -925,15 +1423,16 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, 
   float* pa = nullptr;
   PQS_TRY(scratch(ctx, S_IVF_WORK2, (size_t)(K + 1), &lcnt));
   PQS_TRY(scratch(ctx, S_IVF_WORK3, (size_t)(K + 1), &starts));
-  PQS_TRY(scratch(ctx, S_MISC, (size_t)(nq * ma) * 2, &pq_));
+  PQS_TRY(scratch(ctx, S_MISC, (size_t)(nq * ma) * 3, &pq_));
   pa = (float*)(pq_ + nq * ma);
+  int* pcell = pq_ + 2 * nq * ma;
   PQS_CUDA(ctx, cudaMemsetAsync(lcnt, 0, sizeof(int) * (K + 1), ctx->stream));
   pair_count_kernel<<<(unsigned)cdiv(nq * ma, 256), 256, 0, ctx->stream>>>(cells, nq * ma, lcnt);
   PQS_LAUNCHED(ctx);
   scan_kernel<<<1, 1024, 0, ctx->stream>>>(lcnt, K, starts);
   PQS_LAUNCHED(ctx);
   PQS_CUDA(ctx, cudaMemsetAsync(lcnt, 0, sizeof(int) * (K + 1), ctx->stream));
-  pair_fill_kernel<<<(unsigned)cdiv(nq * ma, 256), 256, 0, ctx->stream>>>(cells, pdist, nq, ma, starts, lcnt, pq_, pa);
+  pair_fill_kernel<<<(unsigned)cdiv(nq * ma, 256), 256, 0, ctx->stream>>>(cells, pdist, nq, ma, starts, lcnt, pq_, pa, pcell);
   PQS_LAUNCHED(ctx);
   // list-major filtered scan
   const int64_t cap = ctx->cand_cap;
@@ -949,20 +1448,69 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, 
   PQS_CHECK(ctx, lsm <= 220 * 1024, "IVF list scan: m * k too large for the shared-memory tables");
   auto list_kernel = (m == 8 && k == 256) ? ivf_list_kernel<8, 256> : ivf_list_kernel<0, 0>;
   PQS_CUDA(ctx, cudaFuncSetAttribute(list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
-  PQS_TRY(scan_timer_begin(ctx));
-  list_kernel<<<(unsigned)K, LIST_THREADS, lsm, ctx->stream>>>(U, starts, pq_, pa, iv->offsets, iv->codes, iv->vtab,
-                                                              m, k, theta, cand, capx, cnt, cap, iv->list_order);
-  PQS_LAUNCHED(ctx);
-  PQS_TRY(scan_timer_end(ctx));
-  ctx->last_scan_launches = 1;
-  ctx->last_scan_engine = 4;
+  if (ctx->ivf_engine == 2 && !iv->wtab)
+    return set_err(ctx, PQS_ERR_UNSUPPORTED, "packed IVF list scan needs m = 8, k = 256 (W tables)");
+  const bool packed = ctx->ivf_engine != 1 && iv->wtab != nullptr && nq < (1ll << 21);
+  const float* aerr_ct = aerr;  // error bound of the candidates' filter distances (ivf_cand_theta_kernel)
+  if (packed) {
+    // integer list scan (K8p): candidates carry L / s_q, certified within aerr2
+    float* qscale = nullptr;
+    PQS_TRY(scratch(ctx, S_QT_WORK, (size_t)nq * 3 + (size_t)(nq * ma) * 10, &qscale));
+    uint32_t* qtint = reinterpret_cast<uint32_t*>(qscale + nq);
+    float* aerr2 = qscale + 2 * nq;
+    float* ps = qscale + 3 * nq;
+    uint32_t* pt = reinterpret_cast<uint32_t*>(ps + nq * ma);
+    float* pas = ps + 2 * nq * ma;
+    ivf_qparams_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(U, pdist, theta, aerr, iv->wmax, nq, ma, m, k, qscale,
+                                                             qtint, aerr2);
+    PQS_LAUNCHED(ctx);
+    ivf_pair_params_kernel<<<(unsigned)cdiv(nq * ma * 8, 256), 256, 0, ctx->stream>>>(
+        pq_, pcell, starts + K, d_queries, iv->coarse, iv->d, iv->dsub, qscale, qtint, ps, pt, pas);
+    PQS_LAUNCHED(ctx);
+    ListDesc* desc = nullptr;
+    PQS_TRY(scratch(ctx, S_TC_REC, (size_t)K, &desc));
+    ivf_desc_kernel<<<(unsigned)cdiv(K, 256), 256, 0, ctx->stream>>>(iv->list_order, starts, iv->offsets, K, desc);
+    PQS_LAUNCHED(ctx);
+    List8Args la{};
+    la.U = U;
+    la.W = iv->wtab;
+    la.desc = desc;
+    la.K = K;
+    la.pq = pq_;
+    la.ps = ps;
+    la.pt = pt;
+    la.pas = pas;
+    la.codes = iv->codes;
+    la.cand = cand;
+    la.cand_apx = capx;
+    la.cand_cnt = cnt;
+    la.cap = cap;
+    const size_t l8sm = 65536 /* below the aligned slot */ + 65536 + (size_t)m * k * 4;
+    PQS_CUDA(ctx, cudaFuncSetAttribute(ivf_list8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l8sm));
+    PQS_TRY(scan_timer_begin(ctx));
+    ivf_list8_kernel<<<(unsigned)std::min<int64_t>(K, ctx->sm_count), L8_THREADS, l8sm, ctx->stream>>>(la);
+    PQS_LAUNCHED(ctx);
+    PQS_TRY(scan_timer_end(ctx));
+    ctx->last_scan_launches = 1;
+    ctx->last_scan_engine = 6;
+    aerr_ct = aerr2;
+  }
+  if (!packed) {
+    PQS_TRY(scan_timer_begin(ctx));
+    list_kernel<<<(unsigned)K, LIST_THREADS, lsm, ctx->stream>>>(U, starts, pq_, pa, iv->offsets, iv->codes, iv->vtab,
+                                                                m, k, theta, cand, capx, cnt, cap, iv->list_order);
+    PQS_LAUNCHED(ctx);
+    PQS_TRY(scan_timer_end(ctx));
+    ctx->last_scan_launches = 1;
+    ctx->last_scan_engine = 4;
+  }
   // tighten to the candidates within 2 aerr of the r-th filter distance,
   // exact rerank (keys in place in cand2, ids into cand) + select
   uint64_t* cand2 = nullptr;
   int* cnt2 = nullptr;
   PQS_TRY(scratch(ctx, S_PIDS, (size_t)(nq * cap), &cand2));
   PQS_TRY(scratch(ctx, S_IVF_CNT2, (size_t)nq, &cnt2));
-  ivf_cand_theta_kernel<<<(unsigned)nq, CT_THREADS, 0, ctx->stream>>>(cand, capx, cnt, cap, r, aerr, cand2, cnt2);
+  ivf_cand_theta_kernel<<<(unsigned)nq, CT_THREADS, 0, ctx->stream>>>(cand, capx, cnt, cap, r, aerr_ct, cand2, cnt2);
   PQS_LAUNCHED(ctx);
   int64_t* pids = reinterpret_cast<int64_t*>(cand);
   auto rerank = [&](uint64_t* cd, const int* cc, int64_t cp, QVec qs, int64_t nqr, int64_t* pi) -> int {

@@ -92,6 +92,7 @@ struct pqs_ctx {
   int force_fallback = 0;
   int scan4_engine = 0;  // 0 auto (tcgen05 when possible), 1 PRMT, 2 tcgen05
   int scan8_engine = 0;  // 0 auto (packed when m <= 64), 1 u16 lane=query, 2 packed
+  int ivf_engine = 0;    // 0 auto (packed list scan when the index has W tables), 1 float list scan, 2 packed
   int64_t tc_chunk_tiles = 0;  // tcgen05 scan: max 128-code tiles per launch (0 = auto)
   int64_t launches = 0;
   int64_t last_max_cand = 0;
@@ -168,6 +169,8 @@ struct pqs_ivf {
   int64_t* ids = nullptr;         // (n,)
   int64_t max_list = 0;
   int* list_order = nullptr;      // (K,) list-scan order (cells grouped by nearest pivot) or null
+  float* wtab = nullptr;          // (K, k*m) W_c[e*m + j] = 2 <c_j, C_j[e]> (packed list scan, m = 8, k = 256) or null
+  float* wmax = nullptr;          // (1,) max |W|
   // probe GEMM (probe.cu): canonical tf32 B tiles of (-2c, ||c||^2 hi, lo),
   // 256 cells per tile, dpad = d + 2 rounded up to 8 (0: d + 2 > 256, exact probes)
   float* probe_b = nullptr;
