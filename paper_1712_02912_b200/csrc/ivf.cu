@@ -296,6 +296,30 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
   }
 }
 
+// per query: codes in its probed lists (the r_eff of the overflow check and the
+// evaluation count); per launch: slot evaluations of the list scan including
+// the idle slots of partly filled 8-query passes
+__global__ void ivf_probed_kernel(const int64_t* __restrict__ cells, const int64_t* __restrict__ offsets, int64_t nq,
+                                  int ma, int64_t* __restrict__ tot) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  int64_t t = 0;
+  for (int p = 0; p < ma; ++p) {
+    const int64_t c = cells[q * ma + p];
+    if (c >= 0) t += offsets[c + 1] - offsets[c];
+  }
+  tot[q] = t;
+}
+__global__ void ivf_slot_evals_kernel(const int* __restrict__ lcnt, const int64_t* __restrict__ offsets, int64_t K,
+                                      int lq, unsigned long long* __restrict__ out) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  unsigned long long v = 0;
+  if (c < K) v = (unsigned long long)(offsets[c + 1] - offsets[c]) * (unsigned long long)lq *
+                 (unsigned long long)((lcnt[c] + lq - 1) / lq);
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, v);
+}
+
 __global__ void pair_count_kernel(const int64_t* __restrict__ cells, int64_t npairs, int* __restrict__ cnt) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < npairs && cells[i] >= 0) atomicAdd(cnt + cells[i], 1);
@@ -637,8 +661,8 @@ __global__ void ivf_w_kernel(const float* __restrict__ coarse, const float* __re
 //  * hence  L <= s (D + m epsT)  for every code, and  s D <= L + 2 m + s m
 //    epsT  for every code without a clipped entry.  Tint = floor(s theta') +
 //    m + 2 < 4095 keeps every returnable code and rejects every clipped one,
-//    so all candidates obey |L / s - d_ref| <= aerr2 = 2 m / s + m epsT + 4u
-//    theta'.
+//    so all candidates obey |(L + m) / s - d_ref| <= aerr2 = m / s + m epsT +
+//    4u theta' (the candidates carry the centred estimate (L + m) / s).
 // theta = +inf (sample shorter than r): s = 0 -- every probed code is kept.
 __global__ void ivf_qparams_kernel(const float* __restrict__ U, const double* __restrict__ pdist,
                                    const float* __restrict__ theta, const float* __restrict__ aerr,
@@ -677,7 +701,8 @@ __global__ void ivf_qparams_kernel(const float* __restrict__ U, const double* __
       qscale[q] = (float)ldexp(1.0, e);
       const double t = (tp > 0.0 ? floor(ldexp(tp, e)) : 0.0) + (double)m + 2.0;
       qtint[q] = t >= (double)(L8_CLIP - 1u) ? L8_CLIP - 1u : (uint32_t)t;
-      const double a2 = ldexp(2.0 * (double)m, -e) + (double)m * epsT + 4.0 * u * tp;
+      // the candidates carry (L + m) / s: |(L + m) / s - D| <= m / s + m epsT
+      const double a2 = ldexp((double)m, -e) + (double)m * epsT + 4.0 * u * tp;
       float f = (float)a2;
       if ((double)f < a2) f = nextafterf(f, __int_as_float(0x7f800000));
       aerr2[q] = f;
@@ -749,6 +774,10 @@ struct List8Args {
   int64_t cap;
 };
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem)
                : "memory");
@@ -795,14 +824,15 @@ __global__ void __launch_bounds__(L8_THREADS, 1) ivf_list8_kernel(List8Args a) {
   const uint32_t slot_w = (sb + 65535u) & ~65535u;  // window address of the slot
   unsigned char* slot = l8 + (slot_w - sb);                              // 64 KB: packed tables, two interleaved halves
   float* sW = reinterpret_cast<float*>(slot + 65536);                    // [MK] list table (producers only)
+  float* raw = sW + MK;                                                  // [L8_Q][MK] the pass's U tables (producers only)
   uint2* scode = reinterpret_cast<uint2*>(l8);                           // [2][L8_CH] code rows
   uint64_t* wst = reinterpret_cast<uint64_t*>(scode + 2 * L8_CH);        // [L8_CW][L8_WST] candidate records
   if (2u * L8_CH * 8u + L8_CW * L8_WST * 8u > slot_w - sb) __trap();
   __shared__ L8Stage sinfo[2];
   __shared__ __align__(8) uint64_t st_full[2], st_empty[2], tab_empty[2];
-  __shared__ int pp_q[L8_Q], s_wcnt[L8_CW];
-  __shared__ float pp_s[L8_Q], pp_as[L8_Q][M];
-  __shared__ uint32_t pp_t[L8_Q];
+  __shared__ int pp_q[2][L8_Q], s_wcnt[L8_CW];
+  __shared__ float pp_s[2][L8_Q], pp_as[2][L8_Q][M];
+  __shared__ uint32_t pp_t[2][L8_Q];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
@@ -817,106 +847,147 @@ __global__ void __launch_bounds__(L8_THREADS, 1) ivf_list8_kernel(List8Args a) {
 
   if (warp < L8_PW) {
     // =============================== producers ===============================
+    // Everything a pass needs from global memory is requested one pass ahead:
+    // the next list's descriptor and W slice and the next pass's parameters
+    // travel in registers, the next pass's eight raw U tables (64 KB) in a
+    // cp.async group that lands during the current build -- the build itself
+    // reads shared memory only.
     const int ptid = threadIdx.x;
     const int bj = lane & 7, be = lane >> 3;
     int sidx = 0, pc = 0;  // stage and pass counters (buffer = & 1)
-    // registers holding the next list's descriptor and W slice
+    for (int i = ptid; i < L8_Q * MK / 4; i += L8_PT) reinterpret_cast<float4*>(raw)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    // list cursor: `d` current, `nd` / wreg the prefetched next live list
     ListDesc nd;
+    nd.np = 0;
+    nd.n = 0;
     float wreg[MK / L8_PT];
-    int64_t li = blockIdx.x;
-    auto fetch_list = [&](int64_t l) {
-      if (l < a.K) {
-        nd = a.desc[l];
-        if (nd.np > 0 && nd.n > 0) {
-#pragma unroll
-          for (int i = 0; i < MK / L8_PT; ++i) wreg[i] = __ldg(a.W + (int64_t)nd.c * MK + ptid + i * L8_PT);
+    int64_t nli = (int64_t)blockIdx.x - gridDim.x;
+    bool more = true;
+    auto fetch_list = [&]() {  // advance to the next list with work (descriptor + W slice into registers)
+      for (;;) {
+        nli += gridDim.x;
+        if (nli >= a.K) {
+          more = false;
+          return;
         }
+        nd = a.desc[nli];
+        if (nd.np > 0 && nd.n > 0) break;
+      }
+#pragma unroll
+      for (int i = 0; i < MK / L8_PT; ++i) wreg[i] = __ldg(a.W + (int64_t)nd.c * MK + ptid + i * L8_PT);
+    };
+    // pass parameters in registers: thread t < 8 -> (q, s, tint) of slot t; threads 32..95 -> a_qj * s_q
+    int rq = 0;
+    float rs = 0.f, ras = 0.f;
+    uint32_t rt = 0;
+    auto fetch_pass = [&](const ListDesc& dd, int g0) {
+      const int ns = min(L8_Q, dd.np - g0);
+      if (ptid < L8_Q) {
+        const bool ok = ptid < ns;
+        rq = ok ? a.pq[dd.p0 + g0 + ptid] : 0;
+        rs = ok ? a.ps[dd.p0 + g0 + ptid] : 0.f;
+        rt = ok ? a.pt[dd.p0 + g0 + ptid] : 0u;
+      } else if (ptid >= 32 && ptid < 32 + L8_Q * M) {
+        const int t = ptid - 32;
+        ras = (t >> 3) < ns ? a.pas[(dd.p0 + g0) * M + t] : 0.f;
       }
     };
-    fetch_list(li);
-    for (; li < a.K; li += gridDim.x) {
-      const ListDesc d = nd;
-      const bool live = d.np > 0 && d.n > 0;
-      if (live) {
-        named_bar_sync(1, L8_PT);  // the previous list's builds are done with sW
-#pragma unroll
-        for (int i = 0; i < MK / L8_PT; ++i) sW[ptid + i * L8_PT] = wreg[i];
+    auto store_pass = [&](int pb) {
+      if (ptid < L8_Q) {
+        pp_q[pb][ptid] = rq;
+        pp_s[pb][ptid] = rs;
+        pp_t[pb][ptid] = rt;
+      } else if (ptid >= 32 && ptid < 32 + L8_Q * M) {
+        pp_as[pb][(ptid - 32) >> 3][(ptid - 32) & 7] = ras;
       }
-      fetch_list(li + gridDim.x);  // in flight during this list
-      if (!live) continue;
-      // pass parameters: thread t < 8 -> (q, s, tint) of slot t; threads 32..95 -> a_qj * s_q
-      int rq = 0;
-      float rs = 0.f, ras = 0.f;
-      uint32_t rt = 0;
-      auto fetch_pass = [&](int g0, int ns) {
-        if (ptid < L8_Q) {
-          const bool ok = ptid < ns;
-          rq = ok ? a.pq[d.p0 + g0 + ptid] : 0;
-          rs = ok ? a.ps[d.p0 + g0 + ptid] : 0.f;
-          rt = ok ? a.pt[d.p0 + g0 + ptid] : 0u;
-        } else if (ptid >= 32 && ptid < 32 + L8_Q * M) {
-          const int t = ptid - 32;
-          ras = (t >> 3) < ns ? a.pas[(d.p0 + g0) * M + t] : 0.f;
-        }
-      };
-      fetch_pass(0, min(L8_Q, d.np));
-      for (int g0 = 0; g0 < d.np; g0 += L8_Q, ++pc) {
+    };
+    auto issue_raw = [&](int pb, int ns) {  // one commit group per call (every thread commits)
+      for (int idx = ptid; idx < ns * (MK / 4); idx += L8_PT) {
+        const int sl = idx / (MK / 4), w4 = idx - sl * (MK / 4);
+        cp_async16(raw + sl * MK + w4 * 4, a.U + (int64_t)pp_q[pb][sl] * MK + w4 * 4);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    fetch_list();
+    if (more) {
+      ListDesc d = nd;
+      int g0 = 0;
+      bool new_list = true;
+      fetch_pass(d, 0);
+      store_pass(0);
+      named_bar_sync(1, L8_PT);
+      issue_raw(0, min(L8_Q, d.np));
+      for (;;) {  // one iteration per pass
         const int ns = min(L8_Q, d.np - g0);
-        const int par = pc & 1;
-        named_bar_sync(1, L8_PT);  // previous pass's build has read pp_*, sW is written
-        if (ptid < L8_Q) {
-          pp_q[ptid] = rq;
-          pp_s[ptid] = rs;
-          pp_t[ptid] = rt;
-        } else if (ptid >= 32 && ptid < 32 + L8_Q * M) {
-          pp_as[(ptid - 32) >> 3][(ptid - 32) & 7] = ras;
+        const int par = pc & 1, pb = pc & 1;
+        if (new_list) {
+          named_bar_sync(1, L8_PT);  // the previous list's builds are done with sW
+#pragma unroll
+          for (int i = 0; i < MK / L8_PT; ++i) sW[ptid + i * L8_PT] = wreg[i];
+          fetch_list();  // the list after this one: in flight during this list
+          new_list = false;
         }
-        named_bar_sync(1, L8_PT);
-        if (g0 + L8_Q < d.np) fetch_pass(g0 + L8_Q, min(L8_Q, d.np - g0 - L8_Q));  // next pass, in flight
+        // the pass after this one
+        const bool last_pass = g0 + L8_Q >= d.np;
+        const bool have_next = !last_pass || more;
+        const ListDesc dn = last_pass ? nd : d;
+        const int gn = last_pass ? 0 : g0 + L8_Q;
+        if (have_next) fetch_pass(dn, gn);
         bool built = false;
         for (int64_t cb = 0; cb < d.n; cb += L8_CH, ++sidx) {
           const int nc = (int)min((int64_t)L8_CH, d.n - cb);
           const int buf = sidx & 1;
-          tc::mbar_wait(&st_empty[buf], (uint32_t)(((sidx >> 1) & 1) ^ 1));
+          if (ptid == 0) tc::mbar_wait(&st_empty[buf], (uint32_t)(((sidx >> 1) & 1) ^ 1));
+          named_bar_sync(1, L8_PT);  // one thread polls, the others park on the hardware barrier
           {
             const uint2* src = reinterpret_cast<const uint2*>(a.codes) + d.b + cb;
             uint2* dst = scode + buf * L8_CH;
             for (int i = ptid; i < nc; i += L8_PT) cp_async8(dst + i, src + i);
+            asm volatile("cp.async.commit_group;" ::: "memory");
           }
           if (!built) {
             built = true;
-            tc::mbar_wait(&tab_empty[par], (uint32_t)(((pc >> 1) & 1) ^ 1));
-            // ---- table build: 8 coalesced loads (one per slot), 4 packed words, one STS.128
-            float as[L8_Q], sc[L8_Q];
-            uint32_t up[L8_Q];  // word offsets into U (nq * 2048 < 2^32, checked by the launcher)
-#pragma unroll
-            for (int i = 0; i < L8_Q; ++i) {
-              as[i] = pp_as[i][bj];
-              sc[i] = pp_s[i];
-              up[i] = (uint32_t)pp_q[i] * (uint32_t)MK + (uint32_t)bj;
-            }
-#pragma unroll 2
-            for (int e0 = warp * 4 + be; e0 < KK; e0 += 4 * L8_PW) {
-              const float wv = sW[e0 * M + bj];
-              float uv[L8_Q];
-#pragma unroll
-              for (int i = 0; i < L8_Q; ++i) uv[i] = __ldg(a.U + (up[i] + (uint32_t)(e0 * M)));
-              uint32_t tq[L8_Q];
+            if (ptid == 0) tc::mbar_wait(&tab_empty[par], (uint32_t)(((pc >> 1) & 1) ^ 1));
+            asm volatile("cp.async.wait_group 1;" ::: "memory");  // this pass's raw tables (the codes may still fly)
+            named_bar_sync(1, L8_PT);
+            // ---- table build from shared memory: 8 loads (one per slot), 4 packed words, one STS.128
+            {
+              float as[L8_Q], sc[L8_Q];
 #pragma unroll
               for (int i = 0; i < L8_Q; ++i) {
-                float x = fmaf(uv[i] + wv, sc[i], as[i]);
-                x = fminf(fmaxf(x, 0.5f), (float)L8_CLIP + 0.5f);
-                tq[i] = __float_as_uint(x + 8388607.5f) & 0xFFFFu;  // floor(x), or floor(x) - 1 on a rounding tie
+                as[i] = pp_as[pb][i][bj];
+                sc[i] = pp_s[pb][i];
               }
-              uint4 w4;
-              w4.x = tq[0] | (tq[4] << 16);
-              w4.y = tq[1] | (tq[5] << 16);
-              w4.z = tq[2] | (tq[6] << 16);
-              w4.w = tq[3] | (tq[7] << 16);
-              *reinterpret_cast<uint4*>(slot + e0 * 256 + par * 128 + bj * 16) = w4;
+#pragma unroll 2
+              for (int e0 = warp * 4 + be; e0 < KK; e0 += 4 * L8_PW) {
+                const float wv = sW[e0 * M + bj];
+                uint32_t tq[L8_Q];
+#pragma unroll
+                for (int i = 0; i < L8_Q; ++i) {
+                  float x = fmaf(raw[i * MK + e0 * M + bj] + wv, sc[i], as[i]);
+                  x = fminf(fmaxf(x, 0.5f), (float)L8_CLIP + 0.5f);
+                  tq[i] = __float_as_uint(x + 8388607.5f) & 0xFFFFu;  // floor(x), or floor(x) - 1 on a rounding tie
+                }
+                uint4 w4;
+                w4.x = tq[0] | (tq[4] << 16);
+                w4.y = tq[1] | (tq[5] << 16);
+                w4.z = tq[2] | (tq[6] << 16);
+                w4.w = tq[3] | (tq[7] << 16);
+                *reinterpret_cast<uint4*>(slot + e0 * 256 + par * 128 + bj * 16) = w4;
+              }
             }
+            named_bar_sync(1, L8_PT);  // every thread is done with raw and pp[pb ^ 1]'s previous user
+            if (have_next) {
+              store_pass(pb ^ 1);
+              named_bar_sync(1, L8_PT);
+              issue_raw(pb ^ 1, min(L8_Q, dn.np - gn));
+            } else {
+              asm volatile("cp.async.commit_group;" ::: "memory");  // keep the group count in step
+            }
+            asm volatile("cp.async.wait_group 1;" ::: "memory");  // the code chunk (older than the raw group)
+          } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
           }
-          cp_async_wait_all();
           if (ptid == 0) {
             L8Stage& si = sinfo[buf];
             si.nc = nc;
@@ -929,12 +1000,21 @@ __global__ void __launch_bounds__(L8_THREADS, 1) ivf_list8_kernel(List8Args a) {
           }
           if (ptid < L8_Q) {
             L8Stage& si = sinfo[buf];
-            si.q[ptid] = pp_q[ptid];
-            si.inv[ptid] = pp_s[ptid] > 0.f ? 1.0f / pp_s[ptid] : 0.f;  // exact: a power of two
-            si.t[ptid] = pp_t[ptid];
+            si.q[ptid] = pp_q[pb][ptid];
+            si.inv[ptid] = pp_s[pb][ptid] > 0.f ? 1.0f / pp_s[pb][ptid] : 0.f;  // exact: a power of two
+            si.t[ptid] = pp_t[pb][ptid];
           }
           named_bar_sync(1, L8_PT);  // tables, codes and the stage record are written
           if (ptid == 0) tc::mbar_arrive(&st_full[buf]);
+        }
+        ++pc;
+        if (!have_next) break;
+        if (last_pass) {
+          d = dn;
+          g0 = 0;
+          new_list = true;
+        } else {
+          g0 += L8_Q;
         }
       }
     }
@@ -949,8 +1029,14 @@ __global__ void __launch_bounds__(L8_THREADS, 1) ivf_list8_kernel(List8Args a) {
     }
   } else {
     // =============================== consumers ===============================
+    // A duet of lanes evaluates one code: lane h2 of the duet reads the two
+    // adjacent words (slots 2 h2 | 2 h2 + 4 and 2 h2 + 1 | 2 h2 + 5) of a
+    // table row with one LDS.64 -- one address PRMT and two adds per four
+    // lookups.  The 16 duets of a warp take 16 codes; duets d and d + 8 share
+    // a component window (rotation (t + d) mod 8), which a 64-bit access
+    // spends as its second wavefront anyway.
     const int cw = warp - L8_PW;
-    const int o = lane >> 2, h = lane & 3;
+    const int o = lane >> 1, h2 = lane & 1;
     const int rsh = 8 * (o & 3);
     const bool rswap = (o & 4) != 0;
     uint64_t* mst = wst + cw * L8_WST;  // this warp's candidate stage
@@ -965,9 +1051,12 @@ __global__ void __launch_bounds__(L8_THREADS, 1) ivf_list8_kernel(List8Args a) {
       if (nc < 0) break;
       const int ns = si.ns;
       const uint32_t par = (uint32_t)si.par * 128u;
-      const bool v0 = h < ns, v1 = h + 4 < ns;
-      const uint32_t thg = (v0 ? si.t[h] : 0u) | ((v1 ? si.t[h + 4] : 0u) << 16) | 0x80008000u;
-      const uint32_t vmask = (v0 ? 0x8000u : 0u) | (v1 ? 0x80000000u : 0u);
+      // accumulator A: slots 2 h2 (low half) and 2 h2 + 4 (high); B: 2 h2 + 1 and 2 h2 + 5
+      const int sA = 2 * h2, sB = 2 * h2 + 1;
+      const uint32_t thA = (sA < ns ? si.t[sA] : 0u) | ((sA + 4 < ns ? si.t[sA + 4] : 0u) << 16) | 0x80008000u;
+      const uint32_t thB = (sB < ns ? si.t[sB] : 0u) | ((sB + 4 < ns ? si.t[sB + 4] : 0u) << 16) | 0x80008000u;
+      const uint32_t vmA = (sA < ns ? 0x8000u : 0u) | (sA + 4 < ns ? 0x80000000u : 0u);
+      const uint32_t vmB = (sB < ns ? 0x8000u : 0u) | (sB + 4 < ns ? 0x80000000u : 0u);
       const uint32_t loff0 = si.loff0;
       // candidate record (list offset | L << 32 | slot << 48) -> the query's list
       auto append = [&](uint64_t rcd) {
@@ -976,7 +1065,8 @@ __global__ void __launch_bounds__(L8_THREADS, 1) ivf_list8_kernel(List8Args a) {
         const int gp = atomicAdd(a.cand_cnt + qs, 1);
         if (gp < a.cap) {
           a.cand[(int64_t)qs * a.cap + gp] = ((uint64_t)(uint32_t)si.c << 32) | (uint64_t)(uint32_t)(si.b + (uint32_t)rcd);
-          a.cand_apx[(int64_t)qs * a.cap + gp] = (float)((uint32_t)(rcd >> 32) & 0x7FFFu) * si.inv[sl];
+          // centred estimate: s D lies in [L - s m epsT, L + 2 m + s m epsT]
+          a.cand_apx[(int64_t)qs * a.cap + gp] = (float)(((uint32_t)(rcd >> 32) & 0x7FFFu) + 8u) * si.inv[sl];
         }
       };
       auto flush = [&]() {
@@ -990,16 +1080,31 @@ __global__ void __launch_bounds__(L8_THREADS, 1) ivf_list8_kernel(List8Args a) {
         if (lane == 0) *mcnt = 0;
         __syncwarp();
       };
+      // one packed sum -> its (at most two) candidates
+      auto emit = [&](uint32_t hit, uint32_t acc, int slo, uint32_t loff) {
+        const uint32_t two = hit & (hit << 16);
+        const int sp = atomicAdd(mcnt, two ? 2 : 1);
+        const uint32_t m0 = (acc & 0x7FFFu) | ((uint32_t)slo << 16);  // L | slot << 16
+        const uint32_t m1 = ((acc >> 16) & 0x7FFFu) | ((uint32_t)(slo + 4) << 16);
+        uint2* m2 = reinterpret_cast<uint2*>(mst);
+        if (sp + 2 <= L8_WST) {
+          m2[sp] = make_uint2(loff, (hit & 0x8000u) ? m0 : m1);
+          if (two) m2[sp + 1] = make_uint2(loff, m1);
+        } else {  // stage full: direct append (a skipped last slot is marked)
+          if (sp == L8_WST - 1) mst[sp] = ~0ull;
+          if (hit & 0x8000u) append((uint64_t)loff | ((uint64_t)m0 << 32));
+          if (hit & 0x80000000u) append((uint64_t)loff | ((uint64_t)m1 << 32));
+        }
+      };
       uint32_t lbase[M];
 #pragma unroll
-      for (int t = 0; t < M; ++t) lbase[t] = slot_w + par + (uint32_t)(((t + o) & 7) * 16 + h * 4);
+      for (int t = 0; t < M; ++t) lbase[t] = slot_w + par + (uint32_t)(((t + o) & 7) * 16 + h2 * 8);
       const uint2* sc = scode + buf * L8_CH;
-      // four codes per lane and step: 4 code rows and 32 lookups in flight
-      constexpr int ILP = 4, STEP = 8 * L8_CW;
-      for (int ib = cw * 8; ib < nc; ib += ILP * STEP) {  // warp-uniform trip count
+      constexpr int ILP = 2, STEP = 16 * L8_CW;
+      for (int ib = cw * 16; ib < nc; ib += ILP * STEP) {  // warp-uniform trip count
         const int i0 = ib + o;
         if (*reinterpret_cast<volatile int*>(mcnt) > L8_WST / 2) flush();  // warp-uniform: only this warp changes it
-        uint32_t acc[ILP];
+        uint32_t accA[ILP], accB[ILP];
         uint2 cwd[ILP];
 #pragma unroll
         for (int u = 0; u < ILP; ++u) cwd[u] = sc[min(i0 + u * STEP, nc - 1)];
@@ -1007,36 +1112,28 @@ __global__ void __launch_bounds__(L8_THREADS, 1) ivf_list8_kernel(List8Args a) {
         for (int u = 0; u < ILP; ++u) {
           const uint32_t x = rswap ? cwd[u].y : cwd[u].x, y = rswap ? cwd[u].x : cwd[u].y;
           const uint32_t r0 = __funnelshift_r(x, y, rsh), r1 = __funnelshift_r(y, x, rsh);
-          uint32_t s = 0u;
+          uint32_t sa = 0u, sb2 = 0u;
 #pragma unroll
           for (int t = 0; t < M; ++t) {
-            uint32_t v;
-            asm volatile("ld.shared.u32 %0, [%1];"
-                         : "=r"(v)
+            uint32_t va, vb;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                         : "=r"(va), "=r"(vb)
                          : "r"(prmt_b(t < 4 ? r0 : r1, lbase[t], 0x7604u | ((uint32_t)(t & 3) << 4))));
-            s += v;
+            sa += va;
+            sb2 += vb;
           }
-          acc[u] = s;
+          accA[u] = sa;
+          accB[u] = sb2;
         }
 #pragma unroll
         for (int u = 0; u < ILP; ++u) {
           const int i = i0 + u * STEP;
-          const uint32_t hit = i < nc ? (thg - acc[u]) & vmask : 0u;
-          if (hit) {  // rare per lane; kept tiny
-            const uint32_t two = hit & (hit << 16);
-            const int sp = atomicAdd(mcnt, two ? 2 : 1);
+          const uint32_t hitA = i < nc ? (thA - accA[u]) & vmA : 0u;
+          const uint32_t hitB = i < nc ? (thB - accB[u]) & vmB : 0u;
+          if (hitA | hitB) {  // rare per lane; kept small
             const uint32_t loff = loff0 + (uint32_t)i;
-            const uint32_t m0 = (acc[u] & 0x7FFFu) | ((uint32_t)h << 16);              // L | slot << 16
-            const uint32_t m1 = ((acc[u] >> 16) & 0x7FFFu) | ((uint32_t)(h + 4) << 16);
-            uint2* m2 = reinterpret_cast<uint2*>(mst);
-            if (sp + 2 <= L8_WST) {
-              m2[sp] = make_uint2(loff, (hit & 0x8000u) ? m0 : m1);
-              if (two) m2[sp + 1] = make_uint2(loff, m1);
-            } else {  // stage full: direct append (a skipped last slot is marked)
-              if (sp == L8_WST - 1) mst[sp] = ~0ull;
-              if (hit & 0x8000u) append((uint64_t)loff | ((uint64_t)m0 << 32));
-              if (hit & 0x80000000u) append((uint64_t)loff | ((uint64_t)m1 << 32));
-            }
+            if (hitA) emit(hitA, accA[u], sA, loff);
+            if (hitB) emit(hitB, accB[u], sB, loff);
           }
         }
       }
@@ -1485,7 +1582,7 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, 
     la.cand_apx = capx;
     la.cand_cnt = cnt;
     la.cap = cap;
-    const size_t l8sm = 65536 /* below the aligned slot */ + 65536 + (size_t)m * k * 4;
+    const size_t l8sm = 65536 /* below the aligned slot */ + 65536 + (size_t)m * k * 4 * (1 + L8_Q);
     PQS_CUDA(ctx, cudaFuncSetAttribute(ivf_list8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)l8sm));
     PQS_TRY(scan_timer_begin(ctx));
     ivf_list8_kernel<<<(unsigned)std::min<int64_t>(K, ctx->sm_count), L8_THREADS, l8sm, ctx->stream>>>(la);
@@ -1540,22 +1637,38 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, 
   s.gids = gi;
   s.gcap = cap;
   PQS_TRY(launch_select(ctx, s));
-  // overflow / sanity check against the exact probed totals
-  std::vector<int> hcnt(nq), hcnt2(nq);
-  PQS_CUDA(ctx, cudaMemcpyAsync(hcnt2.data(), cnt2, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
-  std::vector<int64_t> hcells(nq * ma);
-  PQS_CUDA(ctx, cudaMemcpyAsync(hcnt.data(), cnt, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
-  PQS_CUDA(ctx, cudaMemcpyAsync(hcells.data(), cells, sizeof(int64_t) * nq * ma, cudaMemcpyDeviceToHost, ctx->stream));
+  // overflow / sanity check against the exact probed totals; the totals and
+  // the statistics are reduced on the device and land in one pinned buffer
+  int64_t* d_tot = nullptr;
+  PQS_TRY(scratch(ctx, S_IVF_WORK, (size_t)nq + 1, &d_tot));
+  ivf_probed_kernel<<<(unsigned)cdiv(nq, 256), 256, 0, ctx->stream>>>(cells, iv->offsets, nq, ma, d_tot);
+  PQS_LAUNCHED(ctx);
+  PQS_CUDA(ctx, cudaMemsetAsync(d_tot + nq, 0, 8, ctx->stream));
+  ivf_slot_evals_kernel<<<(unsigned)cdiv(K, 256), 256, 0, ctx->stream>>>(
+      lcnt, iv->offsets, K, LQ, reinterpret_cast<unsigned long long*>(d_tot + nq));
+  PQS_LAUNCHED(ctx);
+  const int64_t need = 4 * nq + 2;
+  if (ctx->h_cnt_cap < need) {
+    if (ctx->h_cnt) {
+      PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+      cudaFreeHost(ctx->h_cnt);
+      ctx->h_cnt = nullptr;
+    }
+    PQS_CUDA(ctx, cudaHostAlloc((void**)&ctx->h_cnt, sizeof(int) * (size_t)need, cudaHostAllocDefault));
+    ctx->h_cnt_cap = need;
+  }
+  int* hcnt = ctx->h_cnt;
+  int* hcnt2 = ctx->h_cnt + nq;
+  int64_t* htot = reinterpret_cast<int64_t*>(ctx->h_cnt + 2 * nq);
+  PQS_CUDA(ctx, cudaMemcpyAsync(hcnt2, cnt2, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
+  PQS_CUDA(ctx, cudaMemcpyAsync(hcnt, cnt, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
+  PQS_CUDA(ctx, cudaMemcpyAsync(htot, d_tot, sizeof(int64_t) * (nq + 1), cudaMemcpyDeviceToHost, ctx->stream));
   PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   PQS_TRY(scan_timer_collect(ctx));
   std::vector<int> over;
   int64_t mx = 0, ctot = 0, total_evals = 0, worst_total = 0;
   for (int64_t q = 0; q < nq; ++q) {
-    int64_t tot = 0;
-    for (int p = 0; p < ma; ++p) {
-      const int64_t c = hcells[q * ma + p];
-      if (c >= 0) tot += iv->h_offsets[c + 1] - iv->h_offsets[c];
-    }
+    const int64_t tot = htot[q];
     total_evals += tot;
     mx = std::max<int64_t>(mx, hcnt[q]);
     ctot += hcnt[q];
@@ -1571,14 +1684,7 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, 
   }
   ctx->last_evals = total_evals;
   ctx->last_scan_work = (double)total_evals * (double)m;
-  {
-    std::vector<int> pc((size_t)K, 0);
-    for (int64_t c : hcells)
-      if (c >= 0) ++pc[(size_t)c];
-    int64_t se = 0;
-    for (int64_t c = 0; c < K; ++c) se += (iv->h_offsets[c + 1] - iv->h_offsets[c]) * (int64_t)LQ * ((pc[c] + LQ - 1) / LQ);
-    ctx->last_slot_evals = se;
-  }
+  ctx->last_slot_evals = htot[nq];
   ctx->last_max_cand = mx;
   ctx->last_cand_total = ctot;
   {
