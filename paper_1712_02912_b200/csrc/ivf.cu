@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
   float* su = (float*)tsm;                                   // [m][k] (lanes read random entries of one row)
   unsigned int* keys = (unsigned int*)(su + (size_t)m * k);  // [ma*spl]
   __shared__ unsigned int hist[256];
-  __shared__ unsigned int s_prefix, s_k, s_valid, s_kmin, s_kmax;
+  __shared__ unsigned int s_prefix, s_k, s_valid, s_kmin, s_kmax, s_cnt2;
   const int64_t q = blockIdx.x;
   for (int i = threadIdx.x; i < m * k; i += blockDim.x) {
     const int e = i / m, j = i - e * m;
@@ -198,16 +198,33 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
   }
   __syncthreads();
   const int ns = ma * spl;
+  // list bases / lengths / probe distances of the ma probes: one dependent
+  // load chain per probe (not per sample), so the sample loop below issues
+  // independent loads only
+  int64_t* s_b = reinterpret_cast<int64_t*>(keys + ns + (ns & 1));  // [ma]
+  int* s_len = reinterpret_cast<int*>(s_b + ma);                    // [ma]
+  float* s_pd = reinterpret_cast<float*>(s_len + ma);               // [ma]
+  for (int p = threadIdx.x; p < ma; p += blockDim.x) {
+    const int64_t c = cells[q * ma + p];
+    int64_t b = 0, e = 0;
+    if (c >= 0) {
+      b = offsets[c];
+      e = offsets[c + 1];
+    }
+    s_b[p] = b;
+    s_len[p] = (int)min((int64_t)spl, e - b);
+    s_pd[p] = (float)pdist[q * ma + p];
+  }
+  __syncthreads();
   unsigned int valid = 0, kmin = 0xFFFFFFFFu, kmax = 0u;
+#pragma unroll 4
   for (int s2 = threadIdx.x; s2 < ns; s2 += blockDim.x) {
     const int p = s2 / spl, i = s2 - p * spl;
-    const int64_t c = cells[q * ma + p];
     unsigned int key = 0xFFFFFFFFu;
-    if (c >= 0) {
-      const int64_t b = offsets[c], e = offsets[c + 1];
-      if (b + i < e) {
-        const int64_t pos = b + i;
-        float acc = (float)pdist[q * ma + p] + V[pos];
+    {
+      if (i < s_len[p]) {
+        const int64_t pos = s_b[p] + i;
+        float acc = s_pd[p] + V[pos];
         if (m == 8) {  // one 8-byte load per sampled code
           const uint2 cw = *reinterpret_cast<const uint2*>(codes + pos * 8);
 #pragma unroll
@@ -243,51 +260,101 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
   // sign/exponent bits: a fixed 24-bit first shift would pile them into a
   // few hot bins); the common high bits seed the prefix
   const unsigned kdiff = s_kmin ^ s_kmax;
-  int top = kdiff ? 32 - __clz((int)kdiff) : 0;
-  if (threadIdx.x == 0) s_prefix = top >= 32 ? 0u : (s_kmin >> top) << top;
-  __syncthreads();
-  for (; top > 0;) {
-    const int width = top < 8 ? top : 8, shift = top - width;
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+  const int top0 = kdiff ? 32 - __clz((int)kdiff) : 0;
+  const unsigned prefix0 = top0 >= 32 ? 0u : (s_kmin >> top0) << top0;
+  // k-th smallest (0-based) of the valid keys arr[i * stride], i < n: MSD radix
+  // select, 8-bit digits, shared histogram; result in s_prefix
+  auto radix_kth = [&](const unsigned int* arr, int n, int stride, unsigned kth) {
     __syncthreads();
-    const unsigned prefix = s_prefix;
-    for (int i = threadIdx.x; i < ns; i += blockDim.x) {
-      const unsigned key = keys[i];
-      if (key == 0xFFFFFFFFu) continue;
-      const bool match = top >= 32 ? true : ((key ^ prefix) >> top) == 0;
-      if (match) atomicAdd(&hist[(key >> shift) & ((1u << width) - 1u)], 1u);
+    if (threadIdx.x == 0) {
+      s_prefix = prefix0;
+      s_k = kth;
     }
     __syncthreads();
-    if (threadIdx.x < 32) {  // lane-parallel digit search: each lane owns 8 bins
-      const int lane = threadIdx.x;
-      unsigned int s8 = 0;
-#pragma unroll
-      for (int bb = 0; bb < 8; ++bb) s8 += hist[lane * 8 + bb];
-      unsigned int incl = s8;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
+    for (int top = top0; top > 0;) {
+      const int width = top < 8 ? top : 8, shift = top - width;
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      const unsigned prefix = s_prefix;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const unsigned key = arr[i * stride];
+        if (key == 0xFFFFFFFFu) continue;
+        const bool match = top >= 32 ? true : ((key ^ prefix) >> top) == 0;
+        if (match) atomicAdd(&hist[(key >> shift) & ((1u << width) - 1u)], 1u);
       }
-      const unsigned int kk = s_k, excl = incl - s8;
-      if (kk >= excl && kk < incl) {
-        unsigned int cc = excl;
-        int d = lane * 8;
-        for (int bb = 0; bb < 8; ++bb) {
-          const unsigned int h = hist[lane * 8 + bb];
-          if (kk < cc + h) {
-            d = lane * 8 + bb;
-            break;
-          }
-          cc += h;
+      __syncthreads();
+      if (threadIdx.x < 32) {  // lane-parallel digit search: each lane owns 8 bins
+        const int lane = threadIdx.x;
+        unsigned int s8 = 0;
+#pragma unroll
+        for (int bb = 0; bb < 8; ++bb) s8 += hist[lane * 8 + bb];
+        unsigned int incl = s8;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
         }
-        s_k = kk - cc;
-        s_prefix = prefix | ((unsigned)d << shift);
+        const unsigned int kk = s_k, excl = incl - s8;
+        if (kk >= excl && kk < incl) {
+          unsigned int cc = excl;
+          int d = lane * 8;
+          for (int bb = 0; bb < 8; ++bb) {
+            const unsigned int h = hist[lane * 8 + bb];
+            if (kk < cc + h) {
+              d = lane * 8 + bb;
+              break;
+            }
+            cc += h;
+          }
+          s_k = kk - cc;
+          s_prefix = prefix | ((unsigned)d << shift);
+        }
+      }
+      __syncthreads();
+      top = shift;
+    }
+  };
+  // The r-th smallest of ~16k keys is a low quantile: take a pivot from a
+  // strided subsample (rank ~3 r scaled to the subsample), compact the keys
+  // below it (a few hundred) and select among those; the full-array select
+  // runs only if the pivot missed (fewer than r keys below it, or too many).
+  constexpr int SUB = 1024;
+  const unsigned int SMALL = (unsigned)min(2048, m * k);  // the compacted keys reuse the table area
+  bool done = false;
+  if (ns >= 4 * SUB && (int)s_valid >= 8 * r) {
+    const int stride = ns / SUB;
+    // valid keys of the subsample (slots past a list's end hold 0xFFFFFFFF)
+    if (threadIdx.x == 0) s_cnt2 = 0;
+    __syncthreads();
+    unsigned int sv = 0;
+    for (int i = threadIdx.x; i < SUB; i += blockDim.x) sv += keys[i * stride] != 0xFFFFFFFFu;
+    atomicAdd(&s_cnt2, sv);
+    __syncthreads();
+    const unsigned int subv = s_cnt2;
+    const unsigned int want = (unsigned)((3ull * (unsigned)r * subv + s_valid - 1) / s_valid) + 8u;  // rank in the subsample
+    if (want < subv) {
+      radix_kth(keys, SUB, stride, want);
+      const unsigned int pivot = s_prefix;
+      __syncthreads();
+      if (threadIdx.x == 0) s_cnt2 = 0;
+      __syncthreads();
+      unsigned int* small = reinterpret_cast<unsigned int*>(su);  // the tables are not needed any more
+      for (int i = threadIdx.x; i < ns; i += blockDim.x) {
+        const unsigned key = keys[i];
+        if (key <= pivot) {
+          const unsigned int p = atomicAdd(&s_cnt2, 1u);
+          if (p < SMALL) small[p] = key;
+        }
+      }
+      __syncthreads();
+      const unsigned int nsm = s_cnt2;
+      if (nsm >= (unsigned)r && nsm <= SMALL) {
+        radix_kth(small, (int)nsm, 1, (unsigned)(r - 1));
+        done = true;
       }
     }
-    __syncthreads();
-    top = shift;
   }
+  if (!done) radix_kth(keys, ns, 1, (unsigned)(r - 1));
   if (threadIdx.x == 0) {
     const double t = (double)fkey_inv(s_prefix) + 2.0 * (double)aerr[q];
     float f = (float)t;
@@ -1507,7 +1574,7 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, 
   float* theta = nullptr;
   PQS_TRY(scratch(ctx, S_THETA, (size_t)nq * 4, (uint8_t**)&theta));
   const size_t usm = (size_t)m * k * 4;
-  const size_t tsm = usm + (size_t)ma * spl * 4;
+  const size_t tsm = usm + (size_t)ma * spl * 4 + 8 + (size_t)ma * 16;
   PQS_CHECK(ctx, tsm <= 200 * 1024, "IVF threshold sample: m * k too large");
   PQS_CUDA(ctx, cudaFuncSetAttribute(ivf_theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
   ivf_theta_kernel<<<(unsigned)nq, THETA_THREADS, tsm, ctx->stream>>>(U, cells, pdist, iv->offsets, iv->codes,
