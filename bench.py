@@ -559,9 +559,9 @@ def run_ivf(args):
         "clocks": clk,
         "roofline": {"bound": "lut", "achieved": lut_rate, "peak": lut_bound, "unit": "Glookup/s",
                      "frac": lut_rate / lut_bound,
-                     "traffic": _ncu_traffic("ivf_list16_kernel" if packed else "ivf_list_kernel"),
+                     "traffic": _ncu_traffic("ivf_list8_kernel" if packed else "ivf_list_kernel"),
                      "traffic_note": "DRAM bytes of one list-scan launch from the committed ncu capture (profiles/)",
-                     "kernel": ("ivf_list16_kernel (list-major, packed two-query words, tables built per (list, 16 queries))"
+                     "kernel": ("ivf_list8_kernel (list-major, integer residual tables built per (list, 8 queries), two queries per word)"
                                 if packed else "ivf_list_kernel (list-major, smem LUT)"),
                      "per_unit": f"{m} table lookups per probed (query, code); {evals_step:.3e} per launch",
                      "peak_source": (f"shared-memory wavefront rate {sm_count} SM x 64 lookups/clk (two queries per "
@@ -811,8 +811,10 @@ def main():
             peak_source = "fallback: 2 x MEASURED_PEAKS.json bf16_tflops (pqs_peaks unavailable)"
         roofline = {"bound": "tensor", "achieved": achieved, "peak": i8_peak, "unit": "TOP/s (int8)",
                     "frac": achieved / i8_peak,
-                    "traffic": traffic_db.get("scan4tc_kernel", {}).get("bytes"),
-                    "traffic_note": "DRAM bytes of the filter launches of one search from the committed ncu capture (profiles/r01_final_cfg1.md)",
+                    "traffic": traffic_db.get("scan4tc_kernel_" + args.config, {}).get("bytes"),
+                    "traffic_note": "DRAM bytes (read + write) of the filter launches of one search from the committed "
+                                    "ncu --set full capture of this config ("
+                                    + str(traffic_db.get("scan4tc_kernel_" + args.config, {}).get("capture")) + ")",
                     "kernel": "scan4tc_kernel (tcgen05.mma kind::i8, M=128 N=256 K=256 per tile)",
                     "per_unit": "2 x 256 int8 MACs per (query, code) over 256-query groups and 128-code tiles "
                                 f"({work:.3e} ops per launch)",
