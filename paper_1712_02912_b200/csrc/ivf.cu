@@ -177,8 +177,9 @@ constexpr int THETA_SAMPLE_CAP = 16384;
 
 __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
     const float* __restrict__ U, const int64_t* __restrict__ cells, const double* __restrict__ pdist,
-    const int64_t* __restrict__ offsets, const uint8_t* __restrict__ codes, const float* __restrict__ V, int ma,
-    int spl, int m, int k, int r, const float* __restrict__ aerr, float* __restrict__ theta) {
+    const int64_t* __restrict__ offsets, const uint8_t* __restrict__ codes, const float* __restrict__ V, int ma_row,
+    int ma, int spl, int m, int k, int r, const float* __restrict__ aerr, float* __restrict__ theta) {
+  // ma_row: probes per query (row stride of cells / pdist); ma: the nearest probes that are sampled
   extern __shared__ __align__(16) unsigned char tsm[];
   float* su = (float*)tsm;                                   // [m][k] (lanes read random entries of one row)
   unsigned int* keys = (unsigned int*)(su + (size_t)m * k);  // [ma*spl]
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
   int* s_len = reinterpret_cast<int*>(s_b + ma);                    // [ma]
   float* s_pd = reinterpret_cast<float*>(s_len + ma);               // [ma]
   for (int p = threadIdx.x; p < ma; p += blockDim.x) {
-    const int64_t c = cells[q * ma + p];
+    const int64_t c = cells[q * ma_row + p];
     int64_t b = 0, e = 0;
     if (c >= 0) {
       b = offsets[c];
@@ -213,7 +214,7 @@ __global__ void __launch_bounds__(THETA_THREADS) ivf_theta_kernel(
     }
     s_b[p] = b;
     s_len[p] = (int)min((int64_t)spl, e - b);
-    s_pd[p] = (float)pdist[q * ma + p];
+    s_pd[p] = (float)pdist[q * ma_row + p];
   }
   __syncthreads();
   unsigned int valid = 0, kmin = 0xFFFFFFFFu, kmax = 0u;
@@ -1311,10 +1312,12 @@ __global__ void __launch_bounds__(CT_THREADS) ivf_cand_theta_kernel(const uint64
 // j0, j0 + 8, ...), the ordered j-sum by shuffles; grid (query, slice).
 constexpr int RERANK_THREADS = 256;
 
+template <int DSUB>  // compile-time sub-space dimension (all loads of a sub-space in flight), 0: runtime
 __global__ void __launch_bounds__(RERANK_THREADS, 4) ivf_rerank_kernel(
     uint64_t* __restrict__ cand, const int* __restrict__ cand_cnt, int64_t cap, const int64_t* __restrict__ ids,
     QVec queries, const float* __restrict__ coarse, const float* __restrict__ books,
-    const uint8_t* __restrict__ codes, int m, int k, int d, int dsub, int64_t* __restrict__ pids) {
+    const uint8_t* __restrict__ codes, int m, int k, int d, int dsub_rt, int64_t* __restrict__ pids) {
+  const int dsub = DSUB > 0 ? DSUB : dsub_rt;
   const int64_t q = blockIdx.x;
   const int64_t M = min((int64_t)cand_cnt[q], cap);
   uint64_t* cq = cand + q * cap;
@@ -1338,11 +1341,33 @@ __global__ void __launch_bounds__(RERANK_THREADS, 4) ivf_rerank_kernel(
       if (valid && j < m) {
         const float* cb = books + ((int64_t)j * k + code[j]) * dsub;
         double t = 0.0;
-        for (int s2 = 0; s2 < dsub; ++s2) {
-          const int dd = j * dsub + s2;
-          const double rr = __dsub_rn(qv.at(dd), (double)__ldg(g + dd));
-          const double df = __dsub_rn(rr, (double)__ldg(cb + s2));
-          t = __dadd_rn(t, __dmul_rn(df, df));
+        if constexpr (DSUB > 0 && DSUB % 4 == 0) {
+          // the sub-space's coordinates of the centroid and the codeword as
+          // 16-byte loads, all issued before the ordered fp64 sum
+          float gv[DSUB], cv[DSUB];
+          double qd[DSUB];
+#pragma unroll
+          for (int s4 = 0; s4 < DSUB / 4; ++s4) {
+            const float4 a4 = __ldg(reinterpret_cast<const float4*>(g + j * DSUB) + s4);
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(cb) + s4);
+            gv[4 * s4] = a4.x, gv[4 * s4 + 1] = a4.y, gv[4 * s4 + 2] = a4.z, gv[4 * s4 + 3] = a4.w;
+            cv[4 * s4] = b4.x, cv[4 * s4 + 1] = b4.y, cv[4 * s4 + 2] = b4.z, cv[4 * s4 + 3] = b4.w;
+          }
+#pragma unroll
+          for (int s2 = 0; s2 < DSUB; ++s2) qd[s2] = qv.at(j * DSUB + s2);
+#pragma unroll
+          for (int s2 = 0; s2 < DSUB; ++s2) {
+            const double rr = __dsub_rn(qd[s2], (double)gv[s2]);
+            const double df = __dsub_rn(rr, (double)cv[s2]);
+            t = __dadd_rn(t, __dmul_rn(df, df));
+          }
+        } else {
+          for (int s2 = 0; s2 < dsub; ++s2) {
+            const int dd = j * dsub + s2;
+            const double rr = __dsub_rn(qv.at(dd), (double)__ldg(g + dd));
+            const double df = __dsub_rn(rr, (double)__ldg(cb + s2));
+            t = __dadd_rn(t, __dmul_rn(df, df));
+          }
         }
         tf = __double2float_rn(t);
       }
@@ -1570,15 +1595,29 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, 
   // threshold from the sample (the first spl codes of every probed list)
   static const int theta_cap = getenv("PQS_THETA_CAP") ? std::min(THETA_SAMPLE_CAP, atoi(getenv("PQS_THETA_CAP")))
                                                         : THETA_SAMPLE_CAP;  // tuning experiments
-  const int spl = std::min(256, std::max(1, theta_cap / std::max(ma, 1)));
+  // The sample: the first spl codes of the mas NEAREST probed lists.  Any >= r
+  // probed codes give a valid threshold (an upper bound of the r-th smallest
+  // distance); the nearest lists hold most of the true neighbours, so their
+  // r-th smallest is tighter than that of a sample spread over all ma lists
+  // (cfg3: 1742 -> fewer candidates per query) and the reads are longer runs.
+  // mas: enough of them for ~32 r sampled codes at the average list length,
+  // at least 8 (PQS_THETA_PROBES / PQS_THETA_SPL override, tuning experiments);
+  // cfg3 sweep (probes x codes -> ms/step): 64x256 8.60, 32x512 8.38, 16x1024
+  // 8.28, 8x2048 8.20, 8x1024 7.96.
+  static const int theta_probes = getenv("PQS_THETA_PROBES") ? std::max(1, atoi(getenv("PQS_THETA_PROBES"))) : 0;
+  static const int theta_spl = getenv("PQS_THETA_SPL") ? std::max(1, atoi(getenv("PQS_THETA_SPL"))) : 1024;
+  const int64_t avg_list = std::max<int64_t>(1, iv->n / std::max<int64_t>(1, K));
+  const int64_t per_list = std::min<int64_t>(theta_spl, avg_list);
+  const int mas = std::min<int64_t>(ma, theta_probes > 0 ? theta_probes : std::max<int64_t>(8, cdiv(32 * (int64_t)r, per_list)));
+  const int spl = std::min(theta_spl, std::max(1, theta_cap / std::max(mas, 1)));
   float* theta = nullptr;
   PQS_TRY(scratch(ctx, S_THETA, (size_t)nq * 4, (uint8_t**)&theta));
   const size_t usm = (size_t)m * k * 4;
-  const size_t tsm = usm + (size_t)ma * spl * 4 + 8 + (size_t)ma * 16;
+  const size_t tsm = usm + (size_t)mas * spl * 4 + 8 + (size_t)mas * 16;
   PQS_CHECK(ctx, tsm <= 200 * 1024, "IVF threshold sample: m * k too large");
   PQS_CUDA(ctx, cudaFuncSetAttribute(ivf_theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
   ivf_theta_kernel<<<(unsigned)nq, THETA_THREADS, tsm, ctx->stream>>>(U, cells, pdist, iv->offsets, iv->codes,
-                                                                     iv->vtab, ma, spl, m, k, r, aerr, theta);
+                                                                     iv->vtab, ma, mas, spl, m, k, r, aerr, theta);
   PQS_LAUNCHED(ctx);
   // bucket (query, probe) pairs by list
   int* lcnt = nullptr;
@@ -1679,8 +1718,11 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, 
   int64_t* pids = reinterpret_cast<int64_t*>(cand);
   auto rerank = [&](uint64_t* cd, const int* cc, int64_t cp, QVec qs, int64_t nqr, int64_t* pi) -> int {
     dim3 rg((unsigned)nqr, 8);
-    ivf_rerank_kernel<<<rg, RERANK_THREADS, 0, ctx->stream>>>(cd, cc, cp, iv->ids, qs, iv->coarse, iv->books,
-                                                              iv->codes, m, k, iv->d, iv->dsub, pi);
+    // float4 loads need 16-byte aligned sub-vectors: dsub % 4 == 0 (cudaMalloc'd bases)
+    auto rk = iv->dsub == 16 ? ivf_rerank_kernel<16> : iv->dsub == 8 ? ivf_rerank_kernel<8>
+              : iv->dsub == 4 ? ivf_rerank_kernel<4> : ivf_rerank_kernel<0>;
+    rk<<<rg, RERANK_THREADS, 0, ctx->stream>>>(cd, cc, cp, iv->ids, qs, iv->coarse, iv->books, iv->codes, m, k, iv->d,
+                                               iv->dsub, pi);
     PQS_LAUNCHED(ctx);
     return PQS_OK;
   };
