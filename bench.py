@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--cpu-sample-s", type=float, default=20.0, help="CPU work budget of the baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--engine", type=int, default=0, help="Quick ADC scan engine: 0 auto, 1 PRMT, 2 tcgen05")
+    ap.add_argument("--tc-chunk-tiles", type=int, default=0, help="tcgen05 Quick ADC scan: 128-code tiles per launch (0: library default)")
     ap.add_argument("--scan8-engine", type=int, default=0, help="float ADC filter: 0 auto (packed), 1 u16 lane=query, 2 packed")
     ap.add_argument("--ivf-engine", type=int, default=0, help="IVF list scan: 0 auto (packed), 1 float, 2 packed")
     ap.add_argument("--sample-div", type=int, default=0, help="threshold sample = 1/N of the tiles (0: library default)")
@@ -646,6 +647,8 @@ def main():
     ctx.set_stream(stream.cuda_stream)
     ctx.set_option(_lib.OPT_SCAN4_ENGINE, args.engine)
     ctx.set_option(_lib.OPT_SCAN8_ENGINE, args.scan8_engine)
+    if args.tc_chunk_tiles:
+        ctx.set_option(_lib.OPT_TC_CHUNK_TILES, args.tc_chunk_tiles)
     if args.sample_div:
         ctx.set_option(_lib.OPT_SAMPLE_DIV, args.sample_div)
     pq = P.ProductQuantizer(cfg["m"], cfg["b"], cfg["d"], books)
