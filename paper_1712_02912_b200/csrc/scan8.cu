@@ -495,6 +495,7 @@ struct Scan8PArgs {
   int64_t n;
   int m, k;
   int64_t nq, nvt, nqg;
+  int64_t tile0;          // first tile of this launch (nvt tiles from there)
   const uint32_t* theta;  // keep L <= theta[q] (<= P16_TMAX)
   uint64_t* cand;
   int* cand_cnt;
@@ -578,7 +579,7 @@ __global__ void __launch_bounds__(SCAN8_THREADS, 1) scan8p_kernel(Scan8PArgs a) 
   auto issue_at = [&](int b, int wi, int ch) {
     int qgi, tli;
     item(wi, qgi, tli);
-    const int64_t qg = qgi, tile = tli;
+    const int64_t qg = qgi, tile = tli + a.tile0;
     if (!RES && tli >= nvt) {  // padding item: complete the phase with no bytes
       mbar_expect_tx(&full[b], 0u);
       return;
@@ -729,7 +730,7 @@ __global__ void __launch_bounds__(SCAN8_THREADS, 1) scan8p_kernel(Scan8PArgs a) 
       if (lane == 0) mbar_arrive(&empty[b]);
     }
     if (RES || tile < nvt) {
-      emit(acc, (int64_t)tile * TILE8 + warp * C8);
+      emit(acc, ((int64_t)tile + a.tile0) * TILE8 + warp * C8);
 #pragma unroll
       for (int e = 0; e < C8; ++e) acc[e] = 0u;
     }
@@ -805,6 +806,7 @@ __global__ void theta8_kernel(const uint32_t* __restrict__ sample, int64_t ns, i
   }
   __syncthreads();
   unsigned int valid = 0, vmax = 0;
+#pragma unroll 4
   for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
     const uint32_t v = row[i];
     if (v != 0xFFFFFFFFu) {
@@ -825,42 +827,93 @@ __global__ void theta8_kernel(const uint32_t* __restrict__ sample, int64_t ns, i
   }
   // MSD radix select over the significant bits only: the first digit is the
   // top 8 bits below the largest value's leading one (all 256 bins in use,
-  // no hot-bin atomics), then 8-bit digits down to bit 0
-  for (int top = 32 - __clz((int)s_vmax); top > 0;) {
-    const int width = top < 8 ? top : 8, shift = top - width;
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+  // no hot-bin atomics), then 8-bit digits down to bit 0.  k-th smallest
+  // (0-based) of the valid values arr[i * stride], i < n; result in s_prefix
+  const int top0 = 32 - __clz((int)s_vmax);
+  auto radix_kth = [&](const uint32_t* arr, int64_t n, int64_t stride, unsigned kth) {
     __syncthreads();
-    const unsigned prefix = s_prefix;
-    for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
-      const uint32_t v = row[i];
-      if (v == 0xFFFFFFFFu) continue;
-      const bool match = top >= 32 ? true : ((v ^ prefix) >> top) == 0;
-      if (match) atomicAdd(&hist[(v >> shift) & ((1u << width) - 1u)], 1u);
+    if (threadIdx.x == 0) {
+      s_prefix = 0;
+      s_k = kth;
     }
     __syncthreads();
-    if (threadIdx.x < 32) {  // warp-parallel digit search: lane l owns bins 8l..8l+7
-      const int lane = threadIdx.x;
-      unsigned h8[8], s8 = 0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) s8 += (h8[u] = hist[8 * lane + u]);
-      unsigned incl = s8;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
+    for (int top = top0; top > 0;) {
+      const int width = top < 8 ? top : 8, shift = top - width;
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+      __syncthreads();
+      const unsigned prefix = s_prefix;
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t v = arr[i * stride];
+        if (v == 0xFFFFFFFFu) continue;
+        const bool match = top >= 32 ? true : ((v ^ prefix) >> top) == 0;
+        if (match) atomicAdd(&hist[(v >> shift) & ((1u << width) - 1u)], 1u);
       }
-      const unsigned kk = s_k, excl = incl - s8;
-      if (kk >= excl && kk < incl) {
-        unsigned c = excl;
-        int u = 0;
-        while (kk >= c + h8[u]) c += h8[u++];
-        s_k = kk - c;
-        s_prefix = prefix | ((unsigned)(8 * lane + u) << shift);
+      __syncthreads();
+      if (threadIdx.x < 32) {  // warp-parallel digit search: lane l owns bins 8l..8l+7
+        const int lane = threadIdx.x;
+        unsigned h8[8], s8 = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s8 += (h8[u] = hist[8 * lane + u]);
+        unsigned incl = s8;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const unsigned kk = s_k, excl = incl - s8;
+        if (kk >= excl && kk < incl) {
+          unsigned c = excl;
+          int u = 0;
+          while (kk >= c + h8[u]) c += h8[u++];
+          s_k = kk - c;
+          s_prefix = prefix | ((unsigned)(8 * lane + u) << shift);
+        }
+      }
+      __syncthreads();
+      top = shift;
+    }
+  };
+  // The r-th smallest of a few 10^4 sums is a low quantile: a pivot from a
+  // strided subsample (rank ~3 r scaled to it), the values below it compacted
+  // into shared memory (a few hundred), the select among those -- two passes
+  // over the sample instead of five.  The full-array select runs only when
+  // the pivot missed.
+  constexpr int SUB = 1024, SMALL = 2048;
+  __shared__ uint32_t small[SMALL];
+  __shared__ unsigned int s_cnt2;
+  bool done = false;
+  if (ns >= 8 * SUB && (int64_t)s_valid >= 8ll * r) {
+    const int64_t stride = ns / SUB;
+    if (threadIdx.x == 0) s_cnt2 = 0;
+    __syncthreads();
+    unsigned int sv = 0;
+    for (int i = threadIdx.x; i < SUB; i += blockDim.x) sv += row[i * stride] != 0xFFFFFFFFu;
+    atomicAdd(&s_cnt2, sv);
+    __syncthreads();
+    const unsigned int subv = s_cnt2;
+    const unsigned int want = (unsigned)((3ull * (unsigned)r * subv + s_valid - 1) / s_valid) + 8u;
+    if (want < subv) {
+      radix_kth(row, SUB, stride, want);
+      const uint32_t pivot = s_prefix;
+      __syncthreads();
+      if (threadIdx.x == 0) s_cnt2 = 0;
+      __syncthreads();
+      for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
+        const uint32_t v = row[i];
+        if (v <= pivot) {
+          const unsigned int p = atomicAdd(&s_cnt2, 1u);
+          if (p < SMALL) small[p] = v;
+        }
+      }
+      __syncthreads();
+      const unsigned int nsm = s_cnt2;
+      if (nsm >= (unsigned)r && nsm <= SMALL) {
+        radix_kth(small, nsm, 1, (unsigned)(r - 1));
+        done = true;
       }
     }
-    __syncthreads();
-    top = shift;
   }
+  if (!done) radix_kth(row, ns, 1, (unsigned)(r - 1));
   if (threadIdx.x == 0) {
     const double Dp = ldexp((double)s_prefix + (double)m, -e0[q]) + slack[q];
     int e = e0[q];
@@ -872,6 +925,24 @@ __global__ void theta8_kernel(const uint32_t* __restrict__ sample, int64_t ns, i
     e1[q] = e;
     theta[q] = th >= (double)tmax ? tmax : (uint32_t)th;
   }
+}
+
+// Second threshold of the packed filter: the exact r-th smallest distance D2
+// among the candidates of the first tiles (select_kernel's output) bounds the
+// r-th smallest overall, so the remaining tiles are filtered with
+// floor(2^e1 (D2 - O + slack)) -- the same certified form as theta8_kernel's,
+// from an exact distance instead of a sampled lower bound.
+__global__ void theta8_refine_kernel(const double* __restrict__ topd, const int32_t* __restrict__ topc, int64_t nq,
+                                     int r, int m, const float* __restrict__ off, const double* __restrict__ slack,
+                                     const int* __restrict__ e1, uint32_t* __restrict__ theta) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= nq || topc[q] < r) return;
+  double O = 0.0;
+  for (int j = 0; j < m; ++j) O += (double)off[q * m + j];
+  const double Dp = (topd[q * r + r - 1] - O) + slack[q];
+  if (!(Dp >= 0.0)) return;
+  const double th = floor(ldexp(Dp, e1[q]) * (1.0 + 1e-12)) + 1.0;
+  if (th < (double)theta[q]) theta[q] = (uint32_t)th;
 }
 
 __global__ void fill_u32_kernel(uint32_t* p, int64_t n, uint32_t v) {
@@ -935,6 +1006,14 @@ int run_adc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t 
   if (ctx->scan8_engine == 2 && m > P16_MAX_M)
     return set_err(ctx, PQS_ERR_UNSUPPORTED, "packed scan8 engine takes m <= 64");
   const bool packed = ctx->scan8_engine != 1 && m <= P16_MAX_M;
+  // threshold scale of the packed filter: entries clip at floor(32767 / m).  For
+  // m <= 8 the threshold stays below the clip value, so a code with a clipped
+  // entry can never pass (no false candidates from clipping; cfg0: 3836 ->
+  // fewer candidates per query); for larger m that would leave too few bits
+  // (m = 64: clip 511), so the threshold sits at 8191 = 16 clip / m x the
+  // average entry of a threshold-distance code
+  static const double tgt_env = getenv("PQS_P16_TARGET") ? atof(getenv("PQS_P16_TARGET")) : 0.0;  // tuning
+  const double p16_target = tgt_env > 0.0 ? tgt_env : (m <= 8 ? std::min(P16_TARGET, (double)(P16_TMAX / (uint32_t)m) - 1.0) : P16_TARGET);
   const int mq = ((m + 3) / 4) * 4;
   PQS_TRY(scratch(ctx, S_TABLES_T, (size_t)(cdiv(nq, 32) * 32 * (packed ? mq : m) * k), &tt));
   PQS_TRY(scratch(ctx, S_THETA, (size_t)nq, &theta));
@@ -975,7 +1054,7 @@ int run_adc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t 
     a.ld = ns;
     PQS_TRY(launch_scan8<MODE8_DENSE>(ctx, a));
     theta8_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(
-        sample, ns, (int)r_eff, m, e0, slack, e1, theta, packed ? P16_TARGET : 65536.0 * (m > 8 ? m / 8.0 : 1.0),
+        sample, ns, (int)r_eff, m, e0, slack, e1, theta, packed ? p16_target : 65536.0 * (m > 8 ? m / 8.0 : 1.0),
         packed ? P16_TMAX : 0xFFFFFFFEu);
     PQS_LAUNCHED(ctx);
     // rebuild the tables at the filter scale e1
@@ -1005,10 +1084,51 @@ int run_adc_topr(pqs_ctx* ctx, const pqs_db* db, const float* d_tables, int64_t 
     a.cand = cand;
     a.cand_cnt = cnt;
     a.cap = cap;
+    // Two steps when the list is long: the first 1/8 of the tiles with the
+    // sampled threshold, then the exact r-th distance among their candidates
+    // (one small select) tightens the threshold for the other 7/8 -- about 3x
+    // fewer candidates for the exact re-score and the final select.
+    static const int t1div = getenv("PQS_ADC_T1_DIV") ? std::max(2, atoi(getenv("PQS_ADC_T1_DIV"))) : 8;  // tuning
+    const int64_t t1 = (n > cap && db->ntiles >= 64 && r_eff == r) ? std::max<int64_t>(1, db->ntiles / t1div) : 0;
     PQS_TRY(scan_timer_begin(ctx));
+    if (t1 > 0) {
+      a.nvt = t1;
+      a.tile0 = 0;
+      PQS_TRY(launch_scan8p(ctx, a));
+      uint64_t* gk1 = nullptr;
+      int64_t* gi1 = nullptr;
+      PQS_TRY(scratch(ctx, S_KEYS, (size_t)(nq * cap), &gk1));
+      PQS_TRY(scratch(ctx, S_IDS, (size_t)(nq * cap), &gi1));
+      SelArgs s1{};
+      s1.src = SEL_CAND_ADC;
+      s1.nq = nq;
+      s1.r = r;
+      s1.cand = cand;
+      s1.cand_cnt = cnt;
+      s1.cap = cap;
+      s1.ids = db->ids;
+      s1.id_base = db->id_base;
+      s1.tables = d_tables;
+      s1.codes8 = db->codes8;
+      s1.codes_rm = db->codes_rm;
+      s1.m = m;
+      s1.k = k;
+      s1.out_d = d_dist;  // scratch here: the final select overwrites them
+      s1.out_i = d_ids;
+      s1.out_c = d_count;
+      s1.gkeys = gk1;
+      s1.gids = gi1;
+      s1.gcap = cap;
+      PQS_TRY(launch_select(ctx, s1));
+      theta8_refine_kernel<<<(unsigned)cdiv(nq, 128), 128, 0, ctx->stream>>>(d_dist, d_count, nq, r, m, off, slack, e1,
+                                                                            theta);
+      PQS_LAUNCHED(ctx);
+      a.nvt = db->ntiles - t1;
+      a.tile0 = t1;
+    }
     PQS_TRY(launch_scan8p(ctx, a));
     PQS_TRY(scan_timer_end(ctx));
-    ctx->last_scan_launches = 1;
+    ctx->last_scan_launches = t1 > 0 ? 2 : 1;
     ctx->last_scan_engine = 5;
     ctx->last_scan_work = (double)nq * (double)n * (double)m;
   } else {
