@@ -561,7 +561,7 @@ def run_ivf(args):
         "roofline": {"bound": "lut", "achieved": lut_rate, "peak": lut_bound, "unit": "Glookup/s",
                      "frac": lut_rate / lut_bound,
                      "traffic": _ncu_traffic("ivf_list8_kernel" if packed else "ivf_list_kernel"),
-                     "traffic_note": "DRAM bytes of one list-scan launch from the committed ncu capture (profiles/)",
+                     "traffic_note": _traffic_note(_ncu_entry("ivf_list8_kernel" if packed else "ivf_list_kernel")),
                      "kernel": ("ivf_list8_kernel (list-major, integer residual tables built per (list, 8 queries), two queries per word)"
                                 if packed else "ivf_list_kernel (list-major, smem LUT)"),
                      "per_unit": f"{m} table lookups per probed (query, code); {evals_step:.3e} per launch",
@@ -607,6 +607,20 @@ def measured_i8_peak(seconds: float = 3.0):
                     "source": f"profiles/peaks_r02.json (committed measurement; live run failed: {e})"}
         except Exception:  # noqa: BLE001
             return None
+
+
+def _ncu_entry(kernel: str):
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+def _traffic_note(entry):
+    """dram__bytes_read.sum + dram__bytes_write.sum of ONE launch of the kernel, from the committed ncu capture."""
+    if not entry:
+        return "no ncu capture committed for this kernel / config"
+    return (f"DRAM read + write bytes of one launch, ncu --set full ({entry.get('capture')}): " + entry.get("note", "")).strip()
 
 
 def _ncu_traffic(kernel: str):
@@ -815,9 +829,7 @@ def main():
         roofline = {"bound": "tensor", "achieved": achieved, "peak": i8_peak, "unit": "TOP/s (int8)",
                     "frac": achieved / i8_peak,
                     "traffic": traffic_db.get("scan4tc_kernel_" + args.config, {}).get("bytes"),
-                    "traffic_note": "DRAM bytes (read + write) of the filter launches of one search from the committed "
-                                    "ncu --set full capture of this config ("
-                                    + str(traffic_db.get("scan4tc_kernel_" + args.config, {}).get("capture")) + ")",
+                    "traffic_note": _traffic_note(traffic_db.get("scan4tc_kernel_" + args.config)),
                     "kernel": "scan4tc_kernel (tcgen05.mma kind::i8, M=128 N=256 K=256 per tile)",
                     "per_unit": "2 x 256 int8 MACs per (query, code) over 256-query groups and 128-code tiles "
                                 f"({work:.3e} ops per launch)",
@@ -835,7 +847,7 @@ def main():
                                    f"(two queries per 32-bit word) x {f_mhz:.0f} MHz",
                     "north_star_lut": lut,
                     "traffic": traffic_db.get("scan8p_kernel_" + args.config, {}).get("bytes"),
-                    "traffic_note": "DRAM bytes of one filter launch from the committed ncu capture (profiles/r02_scan8p_*.md)",
+                    "traffic_note": _traffic_note(traffic_db.get("scan8p_kernel_" + args.config)),
                     "kernel": "scan8p_kernel (packed two-query words, PRMT-formed addresses, smem LUT)",
                     "hbm": hbm, "kernel_ms": scan_ms, "share_of_step": scan_ms / ms_per_step}
     else:

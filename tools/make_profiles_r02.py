@@ -104,7 +104,8 @@ def main():
                     launches.summarise(lst) + "\n```\n"
             shutil.copy(lst, os.path.join(OUT, f"r02_final_launches_{name.split('_')[-1]}.csv"))
         open(os.path.join(OUT, f"r02_final_{name}.md"), "w").write(text)
-        traffic[key] = {"bytes": nbytes, "round": 2, "capture": f"profiles/r02_final_{name}.md"}
+        traffic[key] = {"bytes": nbytes, "round": 2, "capture": f"profiles/r02_final_{name}.md",
+                        "note": TRAFFIC_NOTES.get(name, "")}
         print(name, nbytes)
     lst = os.path.join(SRC, f"{TAG}_launches_cfg1.csv")
     if os.path.exists(lst):
@@ -113,6 +114,15 @@ def main():
 
 
 NOTES = {}
+TRAFFIC_NOTES = {
+    "scan4tc_cfg4": "one main-range launch = 1/60 of the search (16,208 tiles: 16.6 MB of codes + 40 groups x 72 KB of tables "
+                    "= 19.5 MB algorithmic); the search's ~61 filter launches read ~1.2 GB for 1.0 GB of codes",
+    "scan8p_cfg0": "the second filter launch (7/8 of the tiles: 7 MB of codes + 4 MB of packed tables algorithmic)",
+    "scan8p_cfg2": "the second filter launch (7/8 of the tiles: 56 MB of codes + 32 MB of packed tables algorithmic, plus "
+                   "the candidate writes)",
+    "list8_cfg3": "the one list-scan launch of a search: 0.8 GB of codes + 0.5 GB of per-list W tables algorithmic, plus U "
+                  "tables that miss L2 and the candidate writes",
+}
 if __name__ == "__main__":
     np = os.path.join(ROOT, "tools", "profile_notes_r02.json")
     if os.path.exists(np):
