@@ -897,7 +897,7 @@ __global__ void __launch_bounds__(L8_THREADS, 1) ivf_list8_kernel(List8Args a) {
   uint64_t* wst = reinterpret_cast<uint64_t*>(scode + 2 * L8_CH);        // [L8_CW][L8_WST] candidate records
   if (2u * L8_CH * 8u + L8_CW * L8_WST * 8u > slot_w - sb) __trap();
   __shared__ L8Stage sinfo[2];
-  __shared__ __align__(8) uint64_t st_full[2], st_empty[2], tab_empty[2];
+  __shared__ __align__(8) uint64_t st_full[2], st_empty[2], tab_empty[2], raw_full;
   __shared__ int pp_q[2][L8_Q], s_wcnt[L8_CW];
   __shared__ float pp_s[2][L8_Q], pp_as[2][L8_Q][M];
   __shared__ uint32_t pp_t[2][L8_Q];
@@ -909,6 +909,7 @@ __global__ void __launch_bounds__(L8_THREADS, 1) ivf_list8_kernel(List8Args a) {
       tc::mbar_init(&st_empty[i], L8_CW);
       tc::mbar_init(&tab_empty[i], L8_CW);
     }
+    tc::mbar_init(&raw_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -918,12 +919,13 @@ __global__ void __launch_bounds__(L8_THREADS, 1) ivf_list8_kernel(List8Args a) {
     // Everything a pass needs from global memory is requested one pass ahead:
     // the next list's descriptor and W slice and the next pass's parameters
     // travel in registers, the next pass's eight raw U tables (64 KB) in a
-    // cp.async group that lands during the current build -- the build itself
-    // reads shared memory only.
+    // TMA bulk copies (one 8 KB copy per slot) that land during the current
+    // build -- the build itself reads shared memory only.
     const int ptid = threadIdx.x;
     const int bj = lane & 7, be = lane >> 3;
     int sidx = 0, pc = 0;  // stage and pass counters (buffer = & 1)
     for (int i = ptid; i < L8_Q * MK / 4; i += L8_PT) reinterpret_cast<float4*>(raw)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the zero fill is ordered before the bulk copies
     // list cursor: `d` current, `nd` / wreg the prefetched next live list
     ListDesc nd;
     nd.np = 0;
@@ -969,12 +971,12 @@ __global__ void __launch_bounds__(L8_THREADS, 1) ivf_list8_kernel(List8Args a) {
         pp_as[pb][(ptid - 32) >> 3][(ptid - 32) & 7] = ras;
       }
     };
-    auto issue_raw = [&](int pb, int ns) {  // one commit group per call (every thread commits)
-      for (int idx = ptid; idx < ns * (MK / 4); idx += L8_PT) {
-        const int sl = idx / (MK / 4), w4 = idx - sl * (MK / 4);
-        cp_async16(raw + sl * MK + w4 * 4, a.U + (int64_t)pp_q[pb][sl] * MK + w4 * 4);
+    auto issue_raw = [&](int pb, int ns) {  // one 8 KB bulk copy (TMA) per live slot, completing on raw_full
+      if (ptid == 0) {
+        tc::mbar_expect_tx(&raw_full, (uint32_t)ns * MK * 4u);
+        for (int sl = 0; sl < ns; ++sl)
+          tc::bulk_g2s(raw + sl * MK, a.U + (int64_t)pp_q[pb][sl] * MK, MK * 4u, &raw_full);
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");
     };
     fetch_list();
     if (more) {
@@ -1015,9 +1017,12 @@ __global__ void __launch_bounds__(L8_THREADS, 1) ivf_list8_kernel(List8Args a) {
           }
           if (!built) {
             built = true;
-            if (ptid == 0) tc::mbar_wait(&tab_empty[par], (uint32_t)(((pc >> 1) & 1) ^ 1));
-            asm volatile("cp.async.wait_group 1;" ::: "memory");  // this pass's raw tables (the codes may still fly)
+            if (ptid == 0) {
+              tc::mbar_wait(&tab_empty[par], (uint32_t)(((pc >> 1) & 1) ^ 1));
+              tc::mbar_wait(&raw_full, (uint32_t)(pc & 1));  // this pass's raw tables landed
+            }
             named_bar_sync(1, L8_PT);
+            tc::mbar_wait(&raw_full, (uint32_t)(pc & 1));  // passes at once: every reader observes the phase itself
             // ---- table build from shared memory: 8 loads (one per slot), 4 packed words, one STS.128
             {
               float as[L8_Q], sc[L8_Q];
@@ -1034,13 +1039,13 @@ __global__ void __launch_bounds__(L8_THREADS, 1) ivf_list8_kernel(List8Args a) {
                 for (int i = 0; i < L8_Q; ++i) {
                   float x = fmaf(raw[i * MK + e0 * M + bj] + wv, sc[i], as[i]);
                   x = fminf(fmaxf(x, 0.5f), (float)L8_CLIP + 0.5f);
-                  tq[i] = __float_as_uint(x + 8388607.5f) & 0xFFFFu;  // floor(x), or floor(x) - 1 on a rounding tie
+                  tq[i] = __float_as_uint(x + 8388607.5f);  // low 16 bits: floor(x), or floor(x) - 1 on a rounding tie
                 }
-                uint4 w4;
-                w4.x = tq[0] | (tq[4] << 16);
-                w4.y = tq[1] | (tq[5] << 16);
-                w4.z = tq[2] | (tq[6] << 16);
-                w4.w = tq[3] | (tq[7] << 16);
+                uint4 w4;  // one PRMT packs the low halves of two slots' words
+                w4.x = __byte_perm(tq[0], tq[4], 0x5410);
+                w4.y = __byte_perm(tq[1], tq[5], 0x5410);
+                w4.z = __byte_perm(tq[2], tq[6], 0x5410);
+                w4.w = __byte_perm(tq[3], tq[7], 0x5410);
                 *reinterpret_cast<uint4*>(slot + e0 * 256 + par * 128 + bj * 16) = w4;
               }
             }
@@ -1049,13 +1054,9 @@ __global__ void __launch_bounds__(L8_THREADS, 1) ivf_list8_kernel(List8Args a) {
               store_pass(pb ^ 1);
               named_bar_sync(1, L8_PT);
               issue_raw(pb ^ 1, min(L8_Q, dn.np - gn));
-            } else {
-              asm volatile("cp.async.commit_group;" ::: "memory");  // keep the group count in step
             }
-            asm volatile("cp.async.wait_group 1;" ::: "memory");  // the code chunk (older than the raw group)
-          } else {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
           }
+          asm volatile("cp.async.wait_group 0;" ::: "memory");  // the code chunk
           if (ptid == 0) {
             L8Stage& si = sinfo[buf];
             si.nc = nc;
