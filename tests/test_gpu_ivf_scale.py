@@ -135,3 +135,45 @@ def test_packed_list_scan_small_index_all_kept():
         assert cc[qi] == len(od)
         np.testing.assert_array_equal(dd[qi, :cc[qi]], od)
         np.testing.assert_array_equal(ii[qi, :cc[qi]], oi)
+
+
+def test_packed_list_scan_long_lists_many_passes():
+    """Few, long lists probed by many queries: every list spans several staged
+    code chunks (> 3072 codes) and takes many 8-query passes (double-buffered
+    table halves, raw-table prefetch across passes and lists); packed engine ==
+    float engine for all queries and == oracle on a sample."""
+    from paper_1712_02912_b200 import _lib
+
+    rng = np.random.default_rng(21)
+    d, K, n, nq = 32, 12, 150_000, 200
+    centers = rng.uniform(0, 100, (K, d)).astype(np.float32)
+    lab = rng.integers(0, K, n)
+    x = (centers[lab] + rng.normal(0, 6, (n, d))).astype(np.float32)
+    coarse = centers + rng.normal(0, 1, (K, d)).astype(np.float32)
+    assign, _ = P.nearest(x, coarse)
+    books = rng.normal(0, 5, (8, 256, 4)).astype(np.float32)
+    pq = P.ProductQuantizer(8, 8, d, books)
+    res = (x.astype(np.float64) - coarse[assign].astype(np.float64)).astype(np.float32)
+    codes = P.DeviceQuantizer(pq).encode(res)
+    codes = np.asarray(codes)
+    lists_c = [codes[assign == c] for c in range(K)]
+    lists_i = [np.flatnonzero(assign == c).astype(np.int64) for c in range(K)]
+    assert max(len(l) for l in lists_c) > 2 * 3072
+    qs = (x[rng.integers(0, n, nq)] + rng.normal(0, 2, (nq, d))).astype(np.float32)
+    idx = P.IvfIndex(coarse, pq, [P.CodeList(a, b) for a, b in zip(lists_c, lists_i)])
+    out = {}
+    for eng in (1, 2):
+        ctx = P.Context(0)
+        ctx.set_option(_lib.OPT_IVF_ENGINE, eng)
+        ivf = P.DeviceIvf(idx, ctx=ctx)
+        out[eng] = ivf.search(qs, 4, 100)
+        assert ctx.stat(_lib.STAT_LAST_SCAN_ENGINE) == (4 if eng == 1 else 6)
+        assert ctx.stat(_lib.STAT_LAST_OVERFLOW) == 0
+    for a, b in zip(out[1], out[2]):
+        np.testing.assert_array_equal(a, b)
+    dd, ii, cc = out[2]
+    for qi in range(0, nq, 37):
+        od, oi = O.query_ivf(coarse, books, lists_c, lists_i, qs[qi], 4, 100)
+        assert cc[qi] == len(od)
+        np.testing.assert_array_equal(dd[qi, :cc[qi]], od)
+        np.testing.assert_array_equal(ii[qi, :cc[qi]], oi)
