@@ -17,8 +17,8 @@ for c in cfg4 cfg1 cfg0 cfg2 cfg3; do
   timeout 600 bash tools/launchlist.sh gpurun_out/${R}_launches_$c.csv --config $c --steps 1 --warmup 1 --no-cpu-baseline
 done
 SKIP=5 timeout 600 bash tools/prof.sh scan4tc_kernel ${R}_scan4tc_cfg4 --config cfg4   # a main-range launch (the first is the prefix)
-timeout 600 bash tools/prof.sh scan8p ${R}_scan8p_cfg0 --config cfg0
-timeout 600 bash tools/prof.sh scan8p ${R}_scan8p_cfg2 --config cfg2
+SKIP=1 timeout 600 bash tools/prof.sh scan8p ${R}_scan8p_cfg0 --config cfg0   # the second filter launch (7/8 of the tiles)
+SKIP=1 timeout 600 bash tools/prof.sh scan8p ${R}_scan8p_cfg2 --config cfg2
 timeout 600 bash tools/prof.sh ivf_list8 ${R}_list8_cfg3 --config cfg3
 tail -n 3 gpurun_out/${R}_gputests.log gpurun_out/${R}_smoke.log
 for f in gpurun_out/${R}_bench_*.log; do echo $f; tail -n 1 $f | cut -c1-400; done
