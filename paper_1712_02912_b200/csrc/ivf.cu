@@ -421,16 +421,27 @@ __global__ void scan_kernel(const int* __restrict__ in, int64_t K, int64_t* __re
 
 __global__ void pair_fill_kernel(const int64_t* __restrict__ cells, const double* __restrict__ pdist, int64_t nq, int ma,
                                  const int64_t* __restrict__ starts, int* __restrict__ fill, int* __restrict__ pq,
-                                 float* __restrict__ pa, int* __restrict__ pcell) {
+                                 float* __restrict__ pa, int* __restrict__ pcell, const float* __restrict__ sub8,
+                                 const float* __restrict__ qscale, const uint32_t* __restrict__ qtint,
+                                 float* __restrict__ ps, uint32_t* __restrict__ pt, float* __restrict__ pas) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= nq * ma) return;
   const int64_t c = cells[i];
   if (c < 0) return;
   const int slot = atomicAdd(fill + c, 1);
   const int64_t o = starts[c] + slot;
-  pq[o] = (int)(i / ma);
+  const int q = (int)(i / ma);
+  pq[o] = q;
   pa[o] = (float)pdist[i];
   pcell[o] = (int)c;
+  if (sub8) {  // packed list scan: the pair's scale, threshold and scaled sub-space terms a_qj * s_q
+    const float sc = qscale[q];
+    ps[o] = sc;
+    pt[o] = qtint[q];
+    const float4 a0 = *reinterpret_cast<const float4*>(sub8 + i * 8), a1 = *reinterpret_cast<const float4*>(sub8 + i * 8 + 4);
+    *reinterpret_cast<float4*>(pas + o * 8) = make_float4(a0.x * sc, a0.y * sc, a0.z * sc, a0.w * sc);
+    *reinterpret_cast<float4*>(pas + o * 8 + 4) = make_float4(a1.x * sc, a1.y * sc, a1.z * sc, a1.w * sc);
+  }
 }
 
 // One CTA per inverted list (two resident per SM); the queries probing it are
@@ -775,32 +786,6 @@ __global__ void ivf_qparams_kernel(const float* __restrict__ U, const double* __
       if ((double)f < a2) f = nextafterf(f, __int_as_float(0x7f800000));
       aerr2[q] = f;
     }
-  }
-}
-
-// Per (query, probe) pair in list order: the query's scale and threshold and
-// the scaled sub-space terms a_qj * s_q of the pair (fp64 -> fp32)
-__global__ void ivf_pair_params_kernel(const int* __restrict__ pq, const int* __restrict__ pcell,
-                                       const int64_t* __restrict__ npairs_p, QVec queries, const float* __restrict__ coarse, int d, int dsub,
-                                       const float* __restrict__ qscale, const uint32_t* __restrict__ qtint,
-                                       float* __restrict__ ps, uint32_t* __restrict__ pt, float* __restrict__ pas) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t g = i >> 3;
-  const int j = (int)(i & 7);
-  if (g >= *npairs_p) return;  // pairs of cells this index does not hold (-1) are not in the lists
-  const int q = pq[g];
-  const float sc = qscale[q];
-  const float* c = coarse + (int64_t)pcell[g] * d + j * dsub;
-  const int64_t qo = (int64_t)q * d + j * dsub;
-  double acc = 0.0;
-  for (int t = 0; t < dsub; ++t) {
-    const double df = queries.at(qo + t) - (double)c[t];
-    acc += df * df;
-  }
-  pas[i] = (float)acc * sc;
-  if (j == 0) {
-    ps[g] = sc;
-    pt[g] = qtint[q];
   }
 }
 
@@ -1578,7 +1563,32 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, 
   double* pdist = nullptr;
   PQS_TRY(scratch(ctx, S_PROBE, (size_t)(nq * ma), &cells));
   PQS_TRY(scratch(ctx, S_PROBE_D, (size_t)(nq * ma), &pdist));
-  PQS_TRY(run_ivf_probe(ctx, iv, d_queries, nq, ma, cells, pdist));
+  // PQS_IVF_TIMING=1: device time of each phase of the search (CUDA events on
+  // the context stream, printed to stderr after the search) -- the in-pipeline,
+  // warm-cache counterpart of the serialised ncu launch list
+  static const bool phase_timing = getenv("PQS_IVF_TIMING") != nullptr;
+  struct Phase {
+    const char* name;
+    cudaEvent_t ev;
+  };
+  std::vector<Phase> phases;
+  auto mark = [&](const char* name) {
+    if (!phase_timing) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, ctx->stream);
+    phases.push_back({name, e});
+  };
+  mark("start");
+  // packed list scan: the probe's exact re-score also emits the sub-space terms
+  // a_qj = ||q_j - c_j||^2 of the selected cells (no separate pass over the pairs)
+  if (ctx->ivf_engine == 2 && !iv->wtab)
+    return set_err(ctx, PQS_ERR_UNSUPPORTED, "packed IVF list scan needs m = 8, k = 256 (W tables)");
+  const bool packed = ctx->ivf_engine != 1 && iv->wtab != nullptr && nq < (1ll << 21);
+  float* sub8 = nullptr;
+  if (packed) PQS_TRY(scratch(ctx, S_TC_B, (size_t)(nq * ma) * 8, &sub8));
+  PQS_TRY(run_ivf_probe(ctx, iv, d_queries, nq, ma, cells, pdist, sub8, packed ? m : 0));
+  mark("probe");
   // per-query tables + bound
   float* U = nullptr;
   float* aerr = nullptr;
@@ -1617,9 +1627,28 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, 
   const size_t tsm = usm + (size_t)mas * spl * 4 + 8 + (size_t)mas * 16;
   PQS_CHECK(ctx, tsm <= 200 * 1024, "IVF threshold sample: m * k too large");
   PQS_CUDA(ctx, cudaFuncSetAttribute(ivf_theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+  mark("utables+bound");
   ivf_theta_kernel<<<(unsigned)nq, THETA_THREADS, tsm, ctx->stream>>>(U, cells, pdist, iv->offsets, iv->codes,
                                                                      iv->vtab, ma, mas, spl, m, k, r, aerr, theta);
   PQS_LAUNCHED(ctx);
+  mark("theta sample");
+  // packed list scan: per-query scale / integer threshold / error bound, then the
+  // pair kernels below also lay out the per-pair parameters
+  float* qscale = nullptr;
+  uint32_t* qtint = nullptr;
+  float *aerr2 = nullptr, *ps = nullptr, *pas = nullptr;
+  uint32_t* pt = nullptr;
+  if (packed) {
+    PQS_TRY(scratch(ctx, S_QT_WORK, (size_t)nq * 3 + (size_t)(nq * ma) * 10 + 8, &qscale));
+    qtint = reinterpret_cast<uint32_t*>(qscale + nq);
+    aerr2 = qscale + 2 * nq;
+    ps = qscale + 3 * nq + ((4 - (3 * nq) % 4) % 4);  // 16-byte aligned rows for the float4 stores of pas
+    pt = reinterpret_cast<uint32_t*>(ps + nq * ma);
+    pas = ps + 2 * nq * ma + ((4 - (2 * nq * ma) % 4) % 4);
+    ivf_qparams_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(U, pdist, theta, aerr, iv->wmax, nq, ma, m, k, qscale,
+                                                             qtint, aerr2);
+    PQS_LAUNCHED(ctx);
+  }
   // bucket (query, probe) pairs by list
   int* lcnt = nullptr;
   int64_t* starts = nullptr;
@@ -1636,7 +1665,8 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, 
   scan_kernel<<<1, 1024, 0, ctx->stream>>>(lcnt, K, starts);
   PQS_LAUNCHED(ctx);
   PQS_CUDA(ctx, cudaMemsetAsync(lcnt, 0, sizeof(int) * (K + 1), ctx->stream));
-  pair_fill_kernel<<<(unsigned)cdiv(nq * ma, 256), 256, 0, ctx->stream>>>(cells, pdist, nq, ma, starts, lcnt, pq_, pa, pcell);
+  pair_fill_kernel<<<(unsigned)cdiv(nq * ma, 256), 256, 0, ctx->stream>>>(cells, pdist, nq, ma, starts, lcnt, pq_, pa, pcell,
+                                                                          sub8, qscale, qtint, ps, pt, pas);
   PQS_LAUNCHED(ctx);
   // list-major filtered scan
   const int64_t cap = ctx->cand_cap;
@@ -1652,25 +1682,9 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, 
   PQS_CHECK(ctx, lsm <= 220 * 1024, "IVF list scan: m * k too large for the shared-memory tables");
   auto list_kernel = (m == 8 && k == 256) ? ivf_list_kernel<8, 256> : ivf_list_kernel<0, 0>;
   PQS_CUDA(ctx, cudaFuncSetAttribute(list_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
-  if (ctx->ivf_engine == 2 && !iv->wtab)
-    return set_err(ctx, PQS_ERR_UNSUPPORTED, "packed IVF list scan needs m = 8, k = 256 (W tables)");
-  const bool packed = ctx->ivf_engine != 1 && iv->wtab != nullptr && nq < (1ll << 21);
   const float* aerr_ct = aerr;  // error bound of the candidates' filter distances (ivf_cand_theta_kernel)
   if (packed) {
     // integer list scan (K8p): candidates carry L / s_q, certified within aerr2
-    float* qscale = nullptr;
-    PQS_TRY(scratch(ctx, S_QT_WORK, (size_t)nq * 3 + (size_t)(nq * ma) * 10, &qscale));
-    uint32_t* qtint = reinterpret_cast<uint32_t*>(qscale + nq);
-    float* aerr2 = qscale + 2 * nq;
-    float* ps = qscale + 3 * nq;
-    uint32_t* pt = reinterpret_cast<uint32_t*>(ps + nq * ma);
-    float* pas = ps + 2 * nq * ma;
-    ivf_qparams_kernel<<<(unsigned)nq, 256, 0, ctx->stream>>>(U, pdist, theta, aerr, iv->wmax, nq, ma, m, k, qscale,
-                                                             qtint, aerr2);
-    PQS_LAUNCHED(ctx);
-    ivf_pair_params_kernel<<<(unsigned)cdiv(nq * ma * 8, 256), 256, 0, ctx->stream>>>(
-        pq_, pcell, starts + K, d_queries, iv->coarse, iv->d, iv->dsub, qscale, qtint, ps, pt, pas);
-    PQS_LAUNCHED(ctx);
     ListDesc* desc = nullptr;
     PQS_TRY(scratch(ctx, S_TC_REC, (size_t)K, &desc));
     ivf_desc_kernel<<<(unsigned)cdiv(K, 256), 256, 0, ctx->stream>>>(iv->list_order, starts, iv->offsets, K, desc);
@@ -1714,8 +1728,10 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, 
   int* cnt2 = nullptr;
   PQS_TRY(scratch(ctx, S_PIDS, (size_t)(nq * cap), &cand2));
   PQS_TRY(scratch(ctx, S_IVF_CNT2, (size_t)nq, &cnt2));
+  mark("pairs+params+list scan");
   ivf_cand_theta_kernel<<<(unsigned)nq, CT_THREADS, 0, ctx->stream>>>(cand, capx, cnt, cap, r, aerr_ct, cand2, cnt2);
   PQS_LAUNCHED(ctx);
+  mark("cand tighten");
   int64_t* pids = reinterpret_cast<int64_t*>(cand);
   auto rerank = [&](uint64_t* cd, const int* cc, int64_t cp, QVec qs, int64_t nqr, int64_t* pi) -> int {
     dim3 rg((unsigned)nqr, 8);
@@ -1728,6 +1744,7 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, 
     return PQS_OK;
   };
   PQS_TRY(rerank(cand2, cnt2, cap, d_queries, nq, pids));
+  mark("exact rerank");
   uint64_t* gk = nullptr;
   int64_t* gi = nullptr;
   PQS_TRY(scratch(ctx, S_KEYS, (size_t)(nq * cap), &gk));
@@ -1747,6 +1764,7 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, 
   s.gids = gi;
   s.gcap = cap;
   PQS_TRY(launch_select(ctx, s));
+  mark("select");
   // overflow / sanity check against the exact probed totals; the totals and
   // the statistics are reduced on the device and land in one pinned buffer
   int64_t* d_tot = nullptr;
@@ -1773,8 +1791,17 @@ int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, 
   PQS_CUDA(ctx, cudaMemcpyAsync(hcnt2, cnt2, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
   PQS_CUDA(ctx, cudaMemcpyAsync(hcnt, cnt, sizeof(int) * nq, cudaMemcpyDeviceToHost, ctx->stream));
   PQS_CUDA(ctx, cudaMemcpyAsync(htot, d_tot, sizeof(int64_t) * (nq + 1), cudaMemcpyDeviceToHost, ctx->stream));
+  mark("stats");
   PQS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   PQS_TRY(scan_timer_collect(ctx));
+  if (phase_timing) {
+    for (size_t i = 1; i < phases.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, phases[i - 1].ev, phases[i].ev);
+      fprintf(stderr, "pqs ivf phase %-24s %8.3f ms\n", phases[i].name, ms);
+    }
+    for (auto& ph : phases) cudaEventDestroy(ph.ev);
+  }
   std::vector<int> over;
   int64_t mx = 0, ctot = 0, total_evals = 0, worst_total = 0;
   for (int64_t q = 0; q < nq; ++q) {

@@ -351,8 +351,9 @@ struct SelArgs {
 };
 int launch_select(pqs_ctx* ctx, const SelArgs& a);
 // ivf.cu
+// d_sub (optional): (nq, ma, nsub) float32 ||q_j - c_j||^2 per sub-space of the selected cells
 int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* ivf, QVec d_queries, int64_t nq, int ma,
-                  int64_t* d_cells, double* d_dist);
+                  int64_t* d_cells, double* d_dist, float* d_sub = nullptr, int nsub = 0);
 int run_ivf_search(pqs_ctx* ctx, const pqs_ivf* ivf, QVec d_queries, int64_t nq, int ma,
                    int r, double* d_dist, int64_t* d_ids, int32_t* d_count);
 // fastscan.cu

@@ -434,6 +434,8 @@ struct ProbeFinalArgs {
   int64_t* gids;
   int64_t* out_cells;    // (nq, ma)
   double* out_dist;
+  float* out_sub;        // optional (nq, ma, nsub): ||q_j - c_j||^2 per sub-space of the selected cells
+  int nsub;
 };
 
 // exact fp64 squared distance, scipy cdist order (sequential over t).  The
@@ -557,6 +559,52 @@ __global__ void __launch_bounds__(PF_THREADS) probe_final_kernel(ProbeFinalArgs 
     a.out_cells[q * ma + p] = p < r_eff ? oi[p] : -1;
     if (a.out_dist) a.out_dist[q * ma + p] = p < r_eff ? dkey_inv(ok[p]) : __longlong_as_double(0x7FF0000000000000ll);
   }
+  if (a.out_sub) {  // sub-space terms of the selected cells (the packed IVF scan's a_qj), fp64 -> fp32
+    const int dsub = a.d / a.nsub;
+    const int lps = dsub >> 2;  // lanes per sub-space when a lane takes 4 coordinates
+    if ((dsub & 3) == 0 && lps <= 32 && (lps & (lps - 1)) == 0 && (a.d & 3) == 0) {
+      // a warp per selected cell: coalesced 16-byte loads of the centroid row,
+      // 4 coordinates per lane, the sub-space sums by a shuffle tree
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      constexpr int UN = 4;  // cells in flight per warp
+      for (int base = 0; base < a.d; base += 128) {
+        const int t = base + lane * 4;
+        for (int p0 = warp * UN; p0 < ma; p0 += nw * UN) {
+          float4 gv[UN];
+#pragma unroll
+          for (int u = 0; u < UN; ++u) {
+            const int p = p0 + u;
+            gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (p < r_eff && t < a.d) gv[u] = __ldg(reinterpret_cast<const float4*>(a.coarse + oi[p] * a.d + t));
+          }
+#pragma unroll
+          for (int u = 0; u < UN; ++u) {
+            const int p = p0 + u;
+            double s = 0.0;
+            if (p < r_eff && t < a.d) {
+              const double d0 = qx[t] - (double)gv[u].x, d1 = qx[t + 1] - (double)gv[u].y,
+                           d2 = qx[t + 2] - (double)gv[u].z, d3 = qx[t + 3] - (double)gv[u].w;
+              s = (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+            }
+            for (int o = lps >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (p < ma && (lane & (lps - 1)) == 0 && t < a.d) a.out_sub[(q * ma + p) * a.nsub + t / dsub] = (float)s;
+          }
+        }
+      }
+    } else
+    for (int idx = threadIdx.x; idx < ma * a.nsub; idx += blockDim.x) {
+      const int p = idx / a.nsub, j = idx - p * a.nsub;
+      double s = 0.0;
+      if (p < r_eff) {
+        const float* g = a.coarse + oi[p] * a.d + j * dsub;
+        for (int t = 0; t < dsub; ++t) {
+          const double df = qx[j * dsub + t] - (double)__ldg(g + t);
+          s += df * df;
+        }
+      }
+      a.out_sub[(q * ma + p) * a.nsub + j] = (float)s;
+    }
+  }
 }
 
 }  // namespace
@@ -580,7 +628,7 @@ int probe_build_index(pqs_ctx* ctx, pqs_ivf* iv) {
 }
 
 int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, int ma, int64_t* d_cells,
-                  double* d_dist) {
+                  double* d_dist, float* d_sub, int nsub) {
   const int64_t K = iv->K;
   const int d = iv->d;
   int P = 1;
@@ -639,6 +687,8 @@ int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, i
     f.q0 = q0;
     f.out_cells = d_cells;
     f.out_dist = d_dist;
+    f.out_sub = (d_sub && nsub > 0 && d % nsub == 0) ? d_sub : nullptr;
+    f.nsub = nsub;
     if (tc_path) {
       const int64_t nblocks = cdiv(nb, PM);
       probe_build_a_kernel<<<(unsigned)cdiv(nblocks * PM * (dpad / 4), 256), 256, 0, ctx->stream>>>(qb, nb, d, dpad,
