@@ -642,7 +642,10 @@ int run_ivf_probe(pqs_ctx* ctx, const pqs_ivf* iv, QVec d_queries, int64_t nq, i
   PQS_CHECK(ctx, fsmem <= 200 * 1024, "probe: d too large for the shared-memory query stage");
   PQS_CUDA(ctx, cudaFuncSetAttribute(probe_final_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
   // query batches of QB (multiple of PM): candidate rows QB x cap
-  const int64_t QB = std::min<int64_t>(cdiv(nq, PM) * PM, 8192);
+  // balanced batches of at most 12,288 queries (10,000 queries run as ONE batch: a short tail batch would run the
+  // GEMM over all K cells with a few query blocks only)
+  const int64_t nbatch = std::max<int64_t>(1, cdiv(nq, 12288));
+  const int64_t QB = cdiv(cdiv(nq, nbatch), PM) * PM;
   double* eps = nullptr;
   PQS_TRY(scratch(ctx, S_AERR, (size_t)QB * 2, (float**)&eps));
   uint64_t* cand = nullptr;
